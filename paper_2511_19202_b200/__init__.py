@@ -1,0 +1,27 @@
+"""B200-native instanced 3DGS renderer with neural occlusion culling.
+
+Drop-in for the reference ``splatcull`` render path (arXiv 2511.19202
+desk-scale package): same public names (reference sc/__init__.py:3-29) plus
+the SPEC-level scene / visibility-MLP API, computed by hand-written sm_100a
+kernels in ``libsplatcull_b200.so`` (see include/splatcull_b200.h).
+Importing the package needs no GPU; rendering does, and raises without one.
+"""
+
+from .asset import (Asset, Gaussian, asset_hash, compute_sampling_distances, logit, prepare, prune, recenter,
+                    sigmoid, validate_asset)
+from .camera import Camera, diag_to_fov_y, fov_y_to_diag, train_focal
+from .nn import Mlp, VisibilityModel, encode_features, forward, init_mlp, make_model
+from .raster import RenderOutput, compute_metrics_pair, psnr, render, ssim
+from .scene import (ComposedScene, FrameStats, InstanceTransform, Renderer, RenderOptions, local_inputs,
+                    render_composed)
+
+__all__ = [
+    "Asset", "Gaussian", "Camera", "RenderOutput", "asset_hash", "compute_metrics_pair",
+    "compute_sampling_distances", "prepare", "prune", "recenter", "render", "sigmoid", "logit",
+    "validate_asset", "diag_to_fov_y", "fov_y_to_diag", "train_focal", "psnr", "ssim",
+    "Mlp", "VisibilityModel", "init_mlp", "make_model", "forward", "encode_features",
+    "ComposedScene", "InstanceTransform", "FrameStats", "RenderOptions", "Renderer", "render_composed",
+    "local_inputs",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,308 @@
+// C ABI of libsplatcull_b200.so: argument checks, workspace carving and the
+// per-frame stage orchestration.  See include/splatcull_b200.h.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace sc {
+cudaError_t launch_count_used(const float *cmax, const unsigned long long *n_dev, int64_t n_max,
+                              sc_frame_stats *stats, cudaStream_t st);
+}
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+extern "C" void sc_note_launch(void) { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static int fail(int code, const char *fmt, const char *detail = "")
+{
+    char buf[512];
+    snprintf(buf, sizeof(buf), fmt, detail);
+    g_last_error = buf;
+    return code;
+}
+
+static int cuda_status(cudaError_t e, const char *where)
+{
+    if (e == cudaSuccess) return SC_OK;
+    char buf[512];
+    snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(e));
+    g_last_error = buf;
+    return SC_ERR_CUDA;
+}
+
+#define SC_TRY(expr, where)                                  \
+    do {                                                     \
+        int _rc = cuda_status((expr), where);                \
+        if (_rc != SC_OK) return _rc;                        \
+    } while (0)
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {
+    size_t inst, chunk_state, ctr, surv, splats, key_a, key_b, val_a, val_b, depth64, rect, ecount, ekey_a, ekey_b,
+        eval_a, eval_b, tile_off, hist, scan_part, total;
+    int64_t max_chunks, nblk_max, n_tiles;
+    int n_tx, n_ty;
+};
+
+Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int32_t w, int32_t h)
+{
+    Layout L{};
+    L.n_tx = (w + sc::kTile - 1) / sc::kTile;
+    L.n_ty = (h + sc::kTile - 1) / sc::kTile;
+    L.n_tiles = (int64_t)L.n_tx * L.n_ty;
+    L.max_chunks = max_pairs / sc::kChunk + n_inst + 1;
+    const int64_t big = std::max<int64_t>(std::max<int64_t>(capS, capE), 1);
+    L.nblk_max = (big + sc::kRadixTile - 1) / sc::kRadixTile;
+    const int64_t part = std::max<int64_t>((256 * L.nblk_max + sc::kScanTile - 1) / sc::kScanTile,
+                                           (big + sc::kScanTile - 1) / sc::kScanTile) + 1;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + std::max<size_t>(bytes, 1));
+        return o;
+    };
+    L.inst = take(sizeof(sc::InstFrame) * (size_t)std::max<int64_t>(n_inst, 1));
+    L.chunk_state = take(sizeof(unsigned long long) * (size_t)L.max_chunks);
+    L.ctr = take(sizeof(sc::Counters));
+    L.surv = take(sizeof(sc_survivor) * (size_t)capS);
+    L.splats = take(sizeof(sc_splat) * (size_t)capS);
+    L.key_a = take(4 * (size_t)capS);
+    L.key_b = take(4 * (size_t)capS);
+    L.val_a = take(4 * (size_t)capS);
+    L.val_b = take(4 * (size_t)capS);
+    L.depth64 = take(8 * (size_t)capS);
+    L.rect = take(8 * (size_t)capS);
+    L.ecount = take(4 * (size_t)capS);
+    L.ekey_a = take(4 * (size_t)capE);
+    L.ekey_b = take(4 * (size_t)capE);
+    L.eval_a = take(4 * (size_t)capE);
+    L.eval_b = take(4 * (size_t)capE);
+    L.tile_off = take(4 * (size_t)(L.n_tiles + 1));
+    L.hist = take(4 * (size_t)(256 * L.nblk_max));
+    L.scan_part = take(4 * (size_t)part);
+    L.total = off;
+    return L;
+}
+
+int carve(const sc_workspace *ws, int32_t w, int32_t h, sc::Ws &out)
+{
+    if (!ws || !ws->base) return fail(SC_ERR_INVALID, "workspace is NULL%s");
+    if (ws->cap_survivors < 0 || ws->cap_entries < 0 || ws->cap_survivors > 0xFFFFFFF0ll ||
+        ws->cap_entries > 0xFFFFFFF0ll)
+        return fail(SC_ERR_INVALID, "workspace capacities out of range%s");
+    Layout L = layout(ws->n_instances, ws->max_pairs, ws->cap_survivors, ws->cap_entries, w, h);
+    if (ws->bytes < L.total) return fail(SC_ERR_INVALID, "workspace too small for these capacities%s");
+    char *b = static_cast<char *>(ws->base);
+    out.inst = reinterpret_cast<sc::InstFrame *>(b + L.inst);
+    out.chunk_state = reinterpret_cast<unsigned long long *>(b + L.chunk_state);
+    out.ctr = reinterpret_cast<sc::Counters *>(b + L.ctr);
+    out.surv = reinterpret_cast<sc_survivor *>(b + L.surv);
+    out.splats = reinterpret_cast<sc_splat *>(b + L.splats);
+    out.key_a = reinterpret_cast<uint32_t *>(b + L.key_a);
+    out.key_b = reinterpret_cast<uint32_t *>(b + L.key_b);
+    out.val_a = reinterpret_cast<uint32_t *>(b + L.val_a);
+    out.val_b = reinterpret_cast<uint32_t *>(b + L.val_b);
+    out.depth64 = reinterpret_cast<double *>(b + L.depth64);
+    out.rect = reinterpret_cast<ushort4 *>(b + L.rect);
+    out.ecount = reinterpret_cast<uint32_t *>(b + L.ecount);
+    out.ekey_a = reinterpret_cast<uint32_t *>(b + L.ekey_a);
+    out.ekey_b = reinterpret_cast<uint32_t *>(b + L.ekey_b);
+    out.eval_a = reinterpret_cast<uint32_t *>(b + L.eval_a);
+    out.eval_b = reinterpret_cast<uint32_t *>(b + L.eval_b);
+    out.tile_off = reinterpret_cast<uint32_t *>(b + L.tile_off);
+    out.hist = reinterpret_cast<uint32_t *>(b + L.hist);
+    out.scan_part = reinterpret_cast<uint32_t *>(b + L.scan_part);
+    out.capS = ws->cap_survivors;
+    out.capE = ws->cap_entries;
+    out.max_chunks = L.max_chunks;
+    out.nblk_max = L.nblk_max;
+    out.n_tiles = L.n_tiles;
+    out.n_tx = L.n_tx;
+    out.n_ty = L.n_ty;
+    return SC_OK;
+}
+
+int check_camera(const sc_camera *cam)
+{
+    if (!cam) return fail(SC_ERR_INVALID, "camera is NULL%s");
+    if (cam->width <= 0 || cam->height <= 0 || cam->width > 32000 || cam->height > 32000)
+        return fail(SC_ERR_INVALID, "camera size out of range%s");
+    if (!(cam->focal > 0.0)) return fail(SC_ERR_INVALID, "camera focal must be positive%s");
+    return SC_OK;
+}
+
+int check_opts(const sc_opts *o)
+{
+    if (!o) return fail(SC_ERR_INVALID, "opts is NULL%s");
+    if (o->tile_size != sc::kTile) return fail(SC_ERR_UNSUPPORTED, "tile_size must be 16%s");
+    if (o->frustum_mode < SC_FRUSTUM_MARGIN || o->frustum_mode > SC_FRUSTUM_OFF)
+        return fail(SC_ERR_INVALID, "unknown frustum_mode%s");
+    return SC_OK;
+}
+
+int check_scene(const sc_scene *s)
+{
+    if (!s) return fail(SC_ERR_INVALID, "scene is NULL%s");
+    if (s->n_instances < 0 || s->n_gauss < 0 || s->n_assets < 0) return fail(SC_ERR_INVALID, "negative scene sizes%s");
+    if (s->n_instances > 0 && (!s->instances || !s->assets))
+        return fail(SC_ERR_INVALID, "scene tables are NULL%s");
+    if (s->n_gauss > 0 && (!s->mean_opa || !s->quat || !s->scale_smax || !s->sh))
+        return fail(SC_ERR_INVALID, "scene gaussian arrays are NULL%s");
+    if (s->sh_stride < 3) return fail(SC_ERR_INVALID, "sh_stride must be >= 3%s");
+    return SC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sc_abi_version(void) { return SC_ABI_VERSION; }
+const char *sc_last_error(void) { return g_last_error.c_str(); }
+int64_t sc_kernel_launches(void) { return (int64_t)g_launches.load(); }
+
+size_t sc_workspace_bytes(int64_t n_instances, int64_t max_pairs, int64_t cap_survivors, int64_t cap_entries,
+                          int32_t width, int32_t height, int32_t tile_size)
+{
+    if (tile_size != sc::kTile || width <= 0 || height <= 0 || cap_survivors < 0 || cap_entries < 0) return 0;
+    return layout(n_instances, max_pairs, cap_survivors, cap_entries, width, height).total;
+}
+
+int sc_cull_mlp(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts, const sc_workspace *ws,
+                sc_survivor *survivors, int64_t cap_survivors, sc_frame_stats *stats, void *stream)
+{
+    int rc;
+    if ((rc = check_scene(scene)) || (rc = check_camera(cam)) || (rc = check_opts(opts))) return rc;
+    if (!stats) return fail(SC_ERR_INVALID, "stats is NULL%s");
+    sc::Ws w;
+    if ((rc = carve(ws, cam->width, cam->height, w))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
+    SC_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(sc::Counters), st), "memset counters");
+    SC_TRY(sc::launch_prep(*scene, *cam, *opts, w, stats, st), "prep");
+    SC_TRY(sc::launch_cull(*scene, *cam, *opts, w, survivors ? survivors : w.surv,
+                           survivors ? cap_survivors : w.capS, stats, st),
+           "cull");
+    return SC_OK;
+}
+
+int sc_project(const sc_scene *scene, const sc_survivor *survivors, int64_t n, const sc_camera *cam,
+               const sc_opts *opts, sc_splat *splats, double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags,
+               sc_frame_stats *stats, void *stream)
+{
+    int rc;
+    if ((rc = check_scene(scene)) || (rc = check_camera(cam)) || (rc = check_opts(opts))) return rc;
+    if (n < 0 || (n > 0 && (!survivors || !splats))) return fail(SC_ERR_INVALID, "bad survivor / splat buffers%s");
+    if (!stats) return fail(SC_ERR_INVALID, "stats is NULL%s");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
+    SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, nullptr, nullptr, nullptr, nullptr,
+                              dbg_f64, dbg_rect, dbg_flags, stats, nullptr, st),
+           "project");
+    return SC_OK;
+}
+
+static int run_bin(const sc_scene *scene, const sc_survivor *surv, const unsigned long long *n_dev, int64_t n_max,
+                   const sc_camera *cam, const sc_opts *opts, sc::Ws &w, sc_splat *splats, sc_frame_stats *stats,
+                   uint32_t **order, uint32_t **entries, cudaStream_t st)
+{
+    SC_TRY(sc::launch_project(*scene, surv, n_dev, n_max, *cam, *opts, splats, w.key_a, w.val_a, w.depth64, w.rect,
+                              nullptr, nullptr, nullptr, stats, &w.ctr->passed, st),
+           "project");
+    SC_TRY(sc::launch_bin(w, n_dev, n_max, *cam, stats, order, entries, st), "bin/sort");
+    return SC_OK;
+}
+
+int sc_bin_sort(const sc_scene *scene, const sc_survivor *survivors, int64_t n, const sc_camera *cam,
+                const sc_opts *opts, const sc_workspace *ws, sc_splat *splats, uint32_t *entry_idx,
+                uint32_t *tile_offsets, uint32_t *order_idx, sc_frame_stats *stats, void *stream)
+{
+    int rc;
+    if ((rc = check_scene(scene)) || (rc = check_camera(cam)) || (rc = check_opts(opts))) return rc;
+    if (!stats || !splats) return fail(SC_ERR_INVALID, "stats / splats are NULL%s");
+    sc::Ws w;
+    if ((rc = carve(ws, cam->width, cam->height, w))) return rc;
+    if (n > w.capS) return fail(SC_ERR_INVALID, "n exceeds workspace cap_survivors%s");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
+    SC_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(sc::Counters), st), "memset counters");
+    uint32_t *order = nullptr, *entries = nullptr;
+    if ((rc = run_bin(scene, survivors, nullptr, n, cam, opts, w, splats, stats, &order, &entries, st))) return rc;
+    if (order_idx && n > 0) SC_TRY(cudaMemcpyAsync(order_idx, order, 4 * (size_t)n, cudaMemcpyDeviceToDevice, st), "copy order");
+    if (entry_idx && w.capE > 0)
+        SC_TRY(cudaMemcpyAsync(entry_idx, entries, 4 * (size_t)w.capE, cudaMemcpyDeviceToDevice, st), "copy entries");
+    if (tile_offsets)
+        SC_TRY(cudaMemcpyAsync(tile_offsets, w.tile_off, 4 * (size_t)(w.n_tiles + 1), cudaMemcpyDeviceToDevice, st),
+               "copy tile offsets");
+    return SC_OK;
+}
+
+int sc_blend(const sc_splat *splats, int64_t n_splats, const uint32_t *entry_idx, const uint32_t *tile_offsets,
+             const sc_camera *cam, const sc_opts *opts, const sc_frame_out *out, void *stream)
+{
+    int rc;
+    if ((rc = check_camera(cam)) || (rc = check_opts(opts))) return rc;
+    if (!out || !out->image || !out->trans || !tile_offsets) return fail(SC_ERR_INVALID, "output buffers are NULL%s");
+    if (opts->record_contributions && (!out->contrib_max || !out->contrib_sum))
+        return fail(SC_ERR_INVALID, "record_contributions needs contrib_max and contrib_sum%s");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (opts->record_contributions && n_splats > 0)
+        SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)n_splats, st), "memset contrib_max");
+    SC_TRY(sc::launch_blend(splats, entry_idx, tile_offsets, *cam, *opts, *out, n_splats, st), "blend");
+    return SC_OK;
+}
+
+int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts, const sc_workspace *ws,
+                       const sc_frame_out *out, void *stream)
+{
+    int rc;
+    if ((rc = check_scene(scene)) || (rc = check_camera(cam)) || (rc = check_opts(opts))) return rc;
+    if (!out || !out->image || !out->trans || !out->stats) return fail(SC_ERR_INVALID, "output buffers are NULL%s");
+    if (opts->record_contributions && (!out->contrib_max || !out->contrib_sum))
+        return fail(SC_ERR_INVALID, "record_contributions needs contrib_max and contrib_sum%s");
+    sc::Ws w;
+    if ((rc = carve(ws, cam->width, cam->height, w))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    sc_frame_stats *stats = out->stats;
+    SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
+    SC_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(sc::Counters), st), "memset counters");
+    SC_TRY(sc::launch_prep(*scene, *cam, *opts, w, stats, st), "prep");
+    SC_TRY(sc::launch_cull(*scene, *cam, *opts, w, w.surv, w.capS, stats, st), "cull");
+    uint32_t *order = nullptr, *entries = nullptr;
+    if ((rc = run_bin(scene, w.surv, &w.ctr->survivors, w.capS, cam, opts, w, w.splats, stats, &order, &entries, st)))
+        return rc;
+    if (opts->record_contributions && w.capS > 0)
+        SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
+    SC_TRY(sc::launch_blend(w.splats, entries, w.tile_off, *cam, *opts, *out, w.capS, st), "blend");
+    if (opts->record_contributions)
+        SC_TRY(sc::launch_count_used(out->contrib_max, &w.ctr->survivors, w.capS, stats, st), "count used");
+    if (out->survivors && w.capS > 0)
+        SC_TRY(cudaMemcpyAsync(out->survivors, w.surv, sizeof(sc_survivor) * (size_t)w.capS, cudaMemcpyDeviceToDevice,
+                               st),
+               "copy survivors");
+    return SC_OK;
+}
+
+int sc_vis_mlp_forward(const sc_vis_weights *w, const float *x, int64_t n, float *logits, void *stream)
+{
+    if (n < 0 || (n > 0 && (!w || !x || !logits))) return fail(SC_ERR_INVALID, "bad MLP forward arguments%s");
+    SC_TRY(sc::launch_vis_mlp(w, x, n, logits, static_cast<cudaStream_t>(stream)), "vis mlp");
+    return SC_OK;
+}
+
+int sc_encode_features(const float *params, const float *x, int64_t n, uint16_t *features, void *stream)
+{
+    if (n < 0 || (n > 0 && (!params || !x || !features))) return fail(SC_ERR_INVALID, "bad feature arguments%s");
+    SC_TRY(sc::launch_encode_features(params, x, n, features, static_cast<cudaStream_t>(stream)), "features");
+    return SC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// Shared device helpers and internal layouts for libsplatcull_b200.so (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "splatcull_b200.h"
+
+namespace sc {
+
+constexpr int kTile = 16;              // pixel tile edge (the oracle's tile_size)
+constexpr int kCullThreads = 128;      // one MLP row per thread (tcgen05 M = 128)
+constexpr int kCullTilesPerChunk = 8;  // chunk = 1024 (instance, gaussian) pairs
+constexpr int kChunk = kCullThreads * kCullTilesPerChunk;
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;   // 4096 keys per block
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kBlendThreads = 256;
+
+// Per-frame, per-instance state written by the prep kernel.
+struct InstFrame {
+    double corr;          // (f_train / focal) / s   (Eq. 2)
+    float fwd_local[3];   // R^T camera forward
+    int32_t visible;      // survived the bounding-sphere cull
+    uint32_t chunk_begin; // exclusive prefix of chunk counts
+    uint32_t n_chunks;
+};
+
+// Internal counters block (device), zeroed per frame together with the stats.
+struct Counters {
+    unsigned long long chunk_ticket;   // dynamic chunk assignment for the cull kernel
+    unsigned long long total_chunks;
+    unsigned long long survivors;      // = stats.survivors (u64 copy for kernels)
+    unsigned long long passed;
+    unsigned long long entries;
+    unsigned long long entries_eff;    // entries, or 0 when they overflow the workspace
+    unsigned long long pad[2];
+};
+
+// Workspace carve-out (all offsets 256-byte aligned), see api.cu:carve().
+struct Ws {
+    InstFrame *inst;                 // [n_instances]
+    unsigned long long *chunk_state; // [max_chunks] decoupled look-back
+    Counters *ctr;
+    sc_survivor *surv;               // [capS]
+    sc_splat *splats;                // [capS]
+    uint32_t *key_a, *key_b;         // [capS]
+    uint32_t *val_a, *val_b;         // [capS]
+    double *depth64;                 // [capS]
+    ushort4 *rect;                   // [capS]  tx0, tx1, ty0, ty1
+    uint32_t *ecount;                // [capS]  tile count -> exclusive offsets
+    uint32_t *ekey_a, *ekey_b;       // [capE]
+    uint32_t *eval_a, *eval_b;       // [capE]
+    uint32_t *tile_off;              // [n_tiles + 1]
+    uint32_t *hist;                  // radix histograms [256 * nblk_max]
+    uint32_t *scan_part;             // scan partials
+    int64_t capS, capE, max_chunks, nblk_max, n_tiles;
+    int n_tx, n_ty;
+};
+
+// ------------------------------------------------------------------------
+// float64 helpers.  TUs that include the bit-exact f64 paths are compiled
+// with -fmad=false, so plain operators give unfused IEEE mul/add exactly as
+// the reference's numba kernels (fastmath=False, no contraction).
+// ------------------------------------------------------------------------
+
+// B2 instancing: mean' = s (R m) + t in f64, rounded to f32 (Asset dtype).
+__device__ __forceinline__ float3 inst_mean(const sc_instance_rec &in, float mx, float my, float mz)
+{
+    double m0 = mx, m1 = my, m2 = mz;
+    double v0 = in.R[0] * m0 + in.R[1] * m1 + in.R[2] * m2;
+    double v1 = in.R[3] * m0 + in.R[4] * m1 + in.R[5] * m2;
+    double v2 = in.R[6] * m0 + in.R[7] * m1 + in.R[8] * m2;
+    return make_float3(__double2float_rn(in.s * v0 + in.t[0]), __double2float_rn(in.s * v1 + in.t[1]),
+                       __double2float_rn(in.s * v2 + in.t[2]));
+}
+
+// q' = q_i (x) q (Hamilton product, wxyz), f64 -> f32.
+__device__ __forceinline__ float4 inst_quat(const sc_instance_rec &in, float4 q)
+{
+    double w1 = in.q[0], x1 = in.q[1], y1 = in.q[2], z1 = in.q[3];
+    double w2 = q.x, x2 = q.y, y2 = q.z, z2 = q.w;
+    return make_float4(__double2float_rn(w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2),
+                       __double2float_rn(w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2),
+                       __double2float_rn(w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2),
+                       __double2float_rn(w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2));
+}
+
+// camera-space position of a world point, same association as the reference
+// projection (sc/_kernels.py:35-43)
+__device__ __forceinline__ void cam_xyz(const sc_camera &c, double m0, double m1, double m2, double &tx,
+                                        double &ty, double &tz)
+{
+    const double *R = c.rot;
+    tx = R[0] * (m0 - c.pos[0]) + R[1] * (m1 - c.pos[1]) + R[2] * (m2 - c.pos[2]);
+    ty = R[3] * (m0 - c.pos[0]) + R[4] * (m1 - c.pos[1]) + R[5] * (m2 - c.pos[2]);
+    tz = R[6] * (m0 - c.pos[0]) + R[7] * (m1 - c.pos[1]) + R[8] * (m2 - c.pos[2]);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// order-preserving float -> uint32 radix key
+__device__ __forceinline__ uint32_t float_key(float f)
+{
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+}  // namespace sc
+
+// launch bookkeeping (api.cu)
+extern "C" void sc_note_launch(void);
+#define SC_LAUNCH(kernel, grid, block, smem, stream, ...)                                    \
+    do {                                                                                      \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                           \
+        sc_note_launch();                                                                     \
+    } while (0)
+
+// internal launchers (host)
+namespace sc {
+cudaError_t launch_prep(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
+                        sc_frame_stats *stats, cudaStream_t st);
+cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
+                        sc_survivor *out, int64_t cap, sc_frame_stats *stats, cudaStream_t st);
+cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
+                           int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
+                           uint32_t *keys, uint32_t *vals, double *depth64, ushort4 *rect, double *dbg_f64,
+                           int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats,
+                           unsigned long long *passed_ctr, cudaStream_t st);
+cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
+                       sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out, cudaStream_t st);
+cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
+                         const sc_camera &cam, const sc_opts &opts, const sc_frame_out &out,
+                         int64_t n_splats, cudaStream_t st);
+cudaError_t launch_vis_mlp(const sc_vis_weights *w, const float *x, int64_t n, float *logits,
+                           cudaStream_t st);
+cudaError_t launch_encode_features(const float *params, const float *x, int64_t n, uint16_t *feat,
+                                   cudaStream_t st);
+}  // namespace sc

@@ -1,0 +1,429 @@
+// Stages (a) + (b): per-instance bounding-sphere cull, per-(instance, gaussian)
+// frustum test, d_near gate and the fused tcgen05 visibility MLP, with an
+// order-preserving (decoupled look-back) compaction of survivors.
+//
+// Compiled with -fmad=false: the frustum / gate arithmetic is float64 and must
+// reproduce the oracle (oracle/sc_oracle.c:orc_scene_cull) bit for bit.
+//
+// Reference semantics: SPEC.md:344-361 (local_inputs, render_composed steps
+// 1-2), SPEC.md:378-379 (margin, below-d_near rule), PAPER.md:186-204 (Eq. 2).
+#include <algorithm>
+
+#include "tc05.cuh"
+
+namespace sc {
+
+// ---------------------------------------------------------------------------
+// Per-instance prep: Eq. 2 factor, local camera forward, conservative
+// bounding-sphere test and the chunk prefix.  One CTA of 1024 threads.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc_opts opts, Ws ws,
+                                               sc_frame_stats *stats)
+{
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_running;
+    __shared__ unsigned long long s_pairs, s_vis;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) {
+        s_running = 0;
+        s_pairs = 0;
+        s_vis = 0;
+    }
+    __syncthreads();
+    const double f = cam.focal;
+    const double cxp = (double)(cam.width - 1) / 2.0, cyp = (double)(cam.height - 1) / 2.0;
+    const double TW = (double)(kTile * ((cam.width + kTile - 1) / kTile));
+    const double TH = (double)(kTile * ((cam.height + kTile - 1) / kTile));
+    for (int64_t base = 0; base < scene.n_instances; base += 1024) {
+        const int64_t i = base + tid;
+        uint32_t nch = 0;
+        if (i < scene.n_instances) {
+            const sc_instance_rec &in = scene.instances[i];
+            const sc_asset_rec &a = scene.assets[in.asset];
+            InstFrame fr;
+            fr.corr = (a.model >= 0) ? (a.f_train / cam.focal) / in.s : 0.0;
+            for (int k = 0; k < 3; k++)
+                fr.fwd_local[k] = (float)(in.R[k] * cam.rot[6] + in.R[3 + k] * cam.rot[7] + in.R[6 + k] * cam.rot[8]);
+            int vis = a.count > 0;
+            if (opts.frustum_mode != SC_FRUSTUM_OFF && vis) {
+                // sphere around the instance covering every instanced mean, with slack
+                // for the f32 rounding of instanced means
+                double tmax = fmax(fabs(in.t[0]), fmax(fabs(in.t[1]), fabs(in.t[2])));
+                double rho = in.s * a.bound_local * (1.0 + 1e-6) + 1e-6 * (2.0 * tmax + in.s * a.bound_local) + 1e-9;
+                double cx, cy, cz;
+                cam_xyz(cam, in.t[0], in.t[1], in.t[2], cx, cy, cz);
+                if (cz + rho <= cam.near_) vis = 0;
+                double mg = 0.0, pad = 0.0, xlo = 0.0, xhi = (double)(cam.width - 1), ylo = 0.0,
+                       yhi = (double)(cam.height - 1);
+                if (opts.frustum_mode == SC_FRUSTUM_MARGIN) {
+                    mg = 3.0 * f * opts.frustum_G * in.s * a.sigma_max * (1.0 + 1e-6);
+                    pad = 3.0;
+                    xhi = TW;
+                    yhi = TH;
+                }
+                // low side:  f t + (c + pad - lo) z + mg >= 0 must be reachable
+                double kl = cxp + pad - xlo;
+                if (f * cx + kl * cz + mg + rho * sqrt(f * f + kl * kl) < 0.0) vis = 0;
+                double kh = cxp - pad - xhi;
+                if (f * cx + kh * cz - mg - rho * sqrt(f * f + kh * kh) > 0.0) vis = 0;
+                kl = cyp + pad - ylo;
+                if (f * cy + kl * cz + mg + rho * sqrt(f * f + kl * kl) < 0.0) vis = 0;
+                kh = cyp - pad - yhi;
+                if (f * cy + kh * cz - mg - rho * sqrt(f * f + kh * kh) > 0.0) vis = 0;
+            }
+            fr.visible = vis;
+            nch = vis ? (uint32_t)((a.count + kChunk - 1) / kChunk) : 0u;
+            fr.n_chunks = nch;
+            fr.chunk_begin = 0;
+            ws.inst[i] = fr;
+            if (vis) {
+                atomicAdd(&s_pairs, (unsigned long long)a.count);
+                atomicAdd(&s_vis, 1ull);
+            }
+        }
+        // block exclusive scan of nch
+        uint32_t x = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = s_warp[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            s_warp[lane] = w;
+        }
+        __syncthreads();
+        const uint32_t excl = s_running + (wid ? s_warp[wid - 1] : 0u) + x - nch;
+        if (i < scene.n_instances) ws.inst[i].chunk_begin = excl;
+        __syncthreads();
+        if (tid == 0) s_running += s_warp[31];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        ws.ctr->total_chunks = s_running;
+        ws.ctr->chunk_ticket = 0;
+        stats->instances_visible = (int64_t)s_vis;
+        stats->pairs_tested = (int64_t)s_pairs;
+    }
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+constexpr unsigned long long kFlagAgg = 1ull << 32, kFlagPre = 2ull << 32;
+
+// ---------------------------------------------------------------------------
+// Cull + MLP.  Persistent CTAs of 128 threads take chunks of kChunk pairs of
+// one instance from an atomic ticket (so look-back never waits on an
+// unscheduled chunk).  Each 128-pair tile: thread = pair; f64 frustum test on
+// the f32-rounded instanced mean (B2/B3), Eq. 2 gate in f64, 16 fp16 inputs
+// into the smem A tile, tcgen05 MLP, survivor ballot into an smem list kept
+// in pair order.  The chunk's list is placed after its predecessors'.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera cam, sc_opts opts, Ws ws,
+                                                       sc_survivor *out, long long cap, sc_frame_stats *stats)
+{
+    __shared__ MlpSmem sm;
+    __shared__ sc_instance_rec s_in;
+    __shared__ sc_asset_rec s_as;
+    __shared__ InstFrame s_fr;
+    __shared__ sc_survivor s_surv[kChunk];
+    __shared__ uint32_t s_wcnt[kCullThreads / 32];
+    __shared__ uint32_t s_chunk, s_inst, s_prefix;
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    mlp_setup(sm, tid);
+    uint32_t phase = 0;
+    int loaded_model = -1;
+    unsigned long long n_pass = 0, n_query = 0, n_cull = 0;
+    const unsigned long long total = ws.ctr->total_chunks;
+    const double cxp = (double)(cam.width - 1) / 2.0, cyp = (double)(cam.height - 1) / 2.0;
+    const double TW = (double)(kTile * ((cam.width + kTile - 1) / kTile));
+    const double TH = (double)(kTile * ((cam.height + kTile - 1) / kTile));
+
+    for (;;) {
+        if (tid == 0) s_chunk = (uint32_t)atomicAdd(&ws.ctr->chunk_ticket, 1ull);
+        __syncthreads();
+        const uint32_t chunk = s_chunk;
+        if (chunk >= total) break;
+        if (tid == 0) {
+            // last instance with chunk_begin <= chunk
+            int64_t lo = 0, hi = scene.n_instances;
+            while (hi - lo > 1) {
+                int64_t mid = (lo + hi) >> 1;
+                if (ws.inst[mid].chunk_begin <= chunk) lo = mid; else hi = mid;
+            }
+            s_inst = (uint32_t)lo;
+            s_in = scene.instances[lo];
+            s_as = scene.assets[s_in.asset];
+            s_fr = ws.inst[lo];
+        }
+        __syncthreads();
+        const int model = (opts.use_mlp && s_as.model >= 0) ? s_as.model : -1;
+        if (model >= 0 && model != loaded_model) {
+            mlp_load_weights(sm, scene.vis_weights + model, tid, kCullThreads);
+            loaded_model = model;
+            __syncthreads();
+        }
+        const int64_t j0 = (int64_t)(chunk - s_fr.chunk_begin) * kChunk;
+        const int64_t j1 = min(j0 + (int64_t)kChunk, s_as.count);
+        const uint32_t inst_id = s_inst;
+        uint32_t n_c = 0;   // survivors of this chunk so far (uniform)
+
+        for (int t = 0; t < kCullTilesPerChunk; t++) {
+            const int64_t jt = j0 + (int64_t)t * kCullThreads;
+            if (jt >= j1) break;
+            const int64_t j = jt + tid;
+            const bool active = j < j1;
+            bool pass = false, queried = false;
+            uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
+            if (active) {
+                const int64_t g = s_as.offset + j;
+                const float4 mo = __ldg(reinterpret_cast<const float4 *>(scene.mean_opa) + g);
+                const float smax = __ldg(scene.scale_smax + 4 * g + 3);
+                const float3 mw = inst_mean(s_in, mo.x, mo.y, mo.z);
+                const double m0 = mw.x, m1 = mw.y, m2 = mw.z;
+                if (opts.frustum_mode == SC_FRUSTUM_OFF) {
+                    pass = true;
+                } else {
+                    double tx, ty, tz;
+                    cam_xyz(cam, m0, m1, m2, tx, ty, tz);
+                    if (tz > cam.near_) {
+                        const double mx = cam.focal * (tx / tz) + cxp;
+                        const double my = cam.focal * (ty / tz) + cyp;
+                        if (opts.frustum_mode == SC_FRUSTUM_STRICT) {
+                            pass = mx >= 0.0 && mx <= (double)(cam.width - 1) && my >= 0.0 &&
+                                   my <= (double)(cam.height - 1);
+                        } else {
+                            const double sigma_w = s_in.s * (double)smax;
+                            const double rb = 3.0 * (cam.focal / tz) * sigma_w * opts.frustum_G + 3.0;
+                            pass = (mx + rb >= 0.0) && (mx - rb < TW) && (my + rb >= 0.0) && (my - rb < TH);
+                        }
+                    }
+                }
+                if (pass && model >= 0) {
+                    const double dx = m0 - cam.pos[0], dy = m1 - cam.pos[1], dz = m2 - cam.pos[2];
+                    const double d_r = sqrt(dx * dx + dy * dy + dz * dz);
+                    const double d_t = d_r * s_fr.corr;
+                    if (d_t >= s_as.d_near) {
+                        queried = true;
+                        const double inv = 1.0 / d_r;
+                        const double *R = s_in.R;
+                        const float dl0 = (float)((R[0] * dx + R[3] * dy + R[6] * dz) * inv);
+                        const float dl1 = (float)((R[1] * dx + R[4] * dy + R[7] * dz) * inv);
+                        const float dl2 = (float)((R[2] * dx + R[5] * dy + R[8] * dz) * inv);
+                        double dn = 2.0 * (d_t - s_as.d_near) / (s_as.d_far - s_as.d_near) - 1.0;
+                        dn = dn < -1.0 ? -1.0 : (dn > 1.0 ? 1.0 : dn);
+                        const float ims = (float)s_as.inv_mean_scale;
+                        lo = make_uint4(pack_h2(mo.x * ims, mo.y * ims), pack_h2(mo.z * ims, dl0),
+                                        pack_h2(dl1, dl2), pack_h2((float)dn, s_fr.fwd_local[0]));
+                        const uint4 feat = __ldg(reinterpret_cast<const uint4 *>(scene.features) + g);
+                        hi = make_uint4(pack_h2(s_fr.fwd_local[1], s_fr.fwd_local[2]), feat.x, feat.y, feat.z);
+                    }
+                }
+            }
+            bool keep = pass;
+            if (model >= 0) {
+                mlp_store_row(sm, tid, lo, hi);
+                if (__syncthreads_or(queried)) {
+                    const float logit = mlp_tile(sm, tid, phase);
+                    if (queried && !(logit >= s_as.logit_threshold)) keep = false;
+                }
+            }
+            n_pass += pass;
+            n_query += queried;
+            n_cull += (pass && !keep);
+            // ordered compaction into s_surv
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) s_wcnt[wid] = __popc(bal);
+            __syncthreads();
+            uint32_t off = n_c;
+            for (int w = 0; w < wid; w++) off += s_wcnt[w];
+            if (keep) {
+                sc_survivor sv;
+                sv.inst = inst_id;
+                sv.gid = (uint32_t)j;
+                s_surv[off + __popc(bal & lanemask_lt())] = sv;
+            }
+            uint32_t tot = 0;
+            for (int w = 0; w < kCullThreads / 32; w++) tot += s_wcnt[w];
+            n_c += tot;
+            __syncthreads();
+        }
+
+        // decoupled look-back over chunk aggregates
+        if (tid == 0) {
+            unsigned long long *st = ws.chunk_state;
+            uint32_t prefix = 0;
+            if (chunk == 0) {
+                atomicExch(&st[0], kFlagPre | n_c);
+            } else {
+                atomicExch(&st[chunk], kFlagAgg | n_c);
+                int64_t k = (int64_t)chunk - 1;
+                for (;;) {
+                    const unsigned long long v = ld_relaxed(&st[k]);
+                    const unsigned long long flag = v & (3ull << 32);
+                    if (flag == 0) continue;
+                    prefix += (uint32_t)v;
+                    if (flag == kFlagPre) break;
+                    k--;
+                }
+                atomicExch(&st[chunk], kFlagPre | (unsigned long long)(prefix + n_c));
+            }
+            s_prefix = prefix;
+            if (chunk == total - 1) {
+                stats->survivors = (int64_t)prefix + n_c;
+                ws.ctr->survivors = (unsigned long long)prefix + n_c;
+                if ((long long)prefix + n_c > cap) atomicOr((unsigned long long *)&stats->overflow, 1ull);
+            }
+        }
+        __syncthreads();
+        const uint32_t prefix = s_prefix;
+        for (uint32_t k = tid; k < n_c; k += kCullThreads) {
+            const long long pos = (long long)prefix + k;
+            if (pos < cap) out[pos] = s_surv[k];
+        }
+    }
+    // stats
+    for (int o = 16; o > 0; o >>= 1) {
+        n_pass += __shfl_down_sync(0xffffffffu, n_pass, o);
+        n_query += __shfl_down_sync(0xffffffffu, n_query, o);
+        n_cull += __shfl_down_sync(0xffffffffu, n_cull, o);
+    }
+    if (lane == 0) {
+        if (n_pass) atomicAdd((unsigned long long *)&stats->frustum_passed, n_pass);
+        if (n_query) atomicAdd((unsigned long long *)&stats->mlp_queried, n_query);
+        if (n_cull) atomicAdd((unsigned long long *)&stats->mlp_culled, n_cull);
+    }
+    mlp_teardown(sm, tid);
+}
+
+// ---------------------------------------------------------------------------
+// Batched forward on materialised fp32 inputs (config-4 sweep, nn.forward).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_vis_forward(const sc_vis_weights *w, const float *x, int64_t n,
+                                                     float *logits)
+{
+    __shared__ MlpSmem sm;
+    const int tid = threadIdx.x;
+    mlp_setup(sm, tid);
+    mlp_load_weights(sm, w, tid, 128);
+    __syncthreads();
+    uint32_t phase = 0;
+    const int64_t n_tiles = (n + 127) / 128;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t r = tile * 128 + tid;
+        uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
+        if (r < n) {
+            const float4 *row = reinterpret_cast<const float4 *>(x + r * 16);
+            const float4 a = __ldg(row), b = __ldg(row + 1), c = __ldg(row + 2), d = __ldg(row + 3);
+            lo = make_uint4(pack_h2(a.x, a.y), pack_h2(a.z, a.w), pack_h2(b.x, b.y), pack_h2(b.z, b.w));
+            hi = make_uint4(pack_h2(c.x, c.y), pack_h2(c.z, c.w), pack_h2(d.x, d.y), pack_h2(d.z, d.w));
+        }
+        mlp_store_row(sm, tid, lo, hi);
+        const float lg = mlp_tile(sm, tid, phase);
+        if (r < n) logits[r] = lg;
+    }
+    mlp_teardown(sm, tid);
+}
+
+// ---------------------------------------------------------------------------
+// Feature MLP 14 -> 32 -> 32 -> 6 (once per asset, off the frame path).
+// fp32 CUDA cores; output fp16 [n][8].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_encode_features(const float *params, const float *x, int64_t n,
+                                                         uint16_t *feat)
+{
+    constexpr int P = 14 * 32 + 32 + 32 * 32 + 32 + 6 * 32 + 6;
+    __shared__ float sp[P];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sp[i] = params[i];
+    __syncthreads();
+    const float *W1 = sp, *b1 = W1 + 14 * 32, *W2 = b1 + 32, *b2 = W2 + 32 * 32, *W3 = b2 + 32, *b3 = W3 + 6 * 32;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        float in[14], h1[32], h2[32];
+        for (int k = 0; k < 14; k++) in[k] = x[r * 14 + k];
+        for (int o = 0; o < 32; o++) {
+            float a = 0.f;
+            for (int k = 0; k < 14; k++) a += W1[o * 14 + k] * in[k];
+            h1[o] = fmaxf(a + b1[o], 0.f);
+        }
+        for (int o = 0; o < 32; o++) {
+            float a = 0.f;
+            for (int k = 0; k < 32; k++) a += W2[o * 32 + k] * h1[k];
+            h2[o] = fmaxf(a + b2[o], 0.f);
+        }
+        uint32_t outw[4];
+        float y[8];
+        for (int o = 0; o < 6; o++) {
+            float a = 0.f;
+            for (int k = 0; k < 32; k++) a += W3[o * 32 + k] * h2[k];
+            y[o] = a + b3[o];
+        }
+        y[6] = y[7] = 0.f;
+        for (int e = 0; e < 4; e++) outw[e] = pack_h2(y[2 * e], y[2 * e + 1]);
+        reinterpret_cast<uint4 *>(feat)[r] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static int sm_count()
+{
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+cudaError_t launch_prep(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
+                        sc_frame_stats *stats, cudaStream_t st)
+{
+    SC_LAUNCH(k_prep, 1, 1024, 0, st, scene, cam, opts, ws, stats);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
+                        sc_survivor *out, int64_t cap, sc_frame_stats *stats, cudaStream_t st)
+{
+    cudaError_t e = cudaMemsetAsync(ws.chunk_state, 0, sizeof(unsigned long long) * (size_t)ws.max_chunks, st);
+    if (e != cudaSuccess) return e;
+    const int grid = sm_count() * 4;
+    SC_LAUNCH(k_cull, grid, kCullThreads, 0, st, scene, cam, opts, ws, out, (long long)cap, stats);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vis_mlp(const sc_vis_weights *w, const float *x, int64_t n, float *logits, cudaStream_t st)
+{
+    if (n <= 0) return cudaSuccess;
+    const int64_t tiles = (n + 127) / 128;
+    const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 8);
+    SC_LAUNCH(k_vis_forward, grid, 128, 0, st, w, x, n, logits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encode_features(const float *params, const float *x, int64_t n, uint16_t *feat,
+                                   cudaStream_t st)
+{
+    if (n <= 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+    SC_LAUNCH(k_encode_features, grid, 256, 0, st, params, x, n, feat);
+    return cudaGetLastError();
+}
+
+}  // namespace sc

@@ -1,0 +1,251 @@
+// Stage (c): instanced projection + SH colour + opacity, on survivors only.
+//
+// Compiled with -fmad=false.  Per survivor the kernel instantiates the
+// Gaussian (B2: f64 -> f32, never stored), then follows the reference
+// projection (sc/_kernels.py:35-133) operation by operation in float64, the
+// radius clip and tile rectangle (sc/raster.py:289-316) and SH colour
+// (sc/raster.py:198-226), and emits the 48-byte blend record, the depth sort
+// key and the tile rectangle.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sc {
+
+__constant__ double kShC0 = 0.28209479177387814;
+__constant__ double kShC1 = 0.4886025119029199;
+__constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                -1.0925484305920792, 0.5462742152960396};
+__constant__ double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
+                                -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
+
+__device__ __forceinline__ int16_t clamp16(double v)
+{
+    return (int16_t)(v < -1.0 ? -1.0 : (v > 32767.0 ? 32767.0 : v));
+}
+
+__device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+__global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_survivor *surv,
+                                                 const unsigned long long *n_dev, int64_t n_host, sc_camera cam,
+                                                 sc_opts opts, sc_splat *splats, uint32_t *keys, uint32_t *vals,
+                                                 double *depth64, ushort4 *rect, double *dbg_f64, int32_t *dbg_rect,
+                                                 uint8_t *dbg_flags, sc_frame_stats *stats,
+                                                 unsigned long long *passed_ctr)
+{
+    const int64_t n = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
+    const double lim_x = 1.3 * cam.tan_x, lim_y = 1.3 * cam.tan_y;
+    const double focal = cam.focal;
+    const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
+    const double log_min_alpha = log(1.0 / 255.0);
+    unsigned long long n_passed = 0, n_skipped = 0;
+
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const sc_survivor sv = surv[k];
+        const sc_instance_rec &in = scene.instances[sv.inst];
+        const sc_asset_rec &as = scene.assets[in.asset];
+        const int64_t g = as.offset + sv.gid;
+        const float4 mo = __ldg(reinterpret_cast<const float4 *>(scene.mean_opa) + g);
+        const float4 q4 = __ldg(reinterpret_cast<const float4 *>(scene.quat) + g);
+        const float4 ls4 = __ldg(reinterpret_cast<const float4 *>(scene.scale_smax) + g);
+
+        // --- instancing (B2), exactly as the oracle's orc_instantiate ---
+        const float3 mw = inst_mean(in, mo.x, mo.y, mo.z);
+        const float4 qw = inst_quat(in, q4);
+        const float ls0 = __double2float_rn((double)ls4.x + in.ln_s);
+        const float ls1 = __double2float_rn((double)ls4.y + in.ln_s);
+        const float ls2 = __double2float_rn((double)ls4.z + in.ln_s);
+
+        // --- projection (sc/_kernels.py:35-133) ---
+        const double m0 = mw.x, m1 = mw.y, m2 = mw.z;
+        double tx, ty, tz;
+        cam_xyz(cam, m0, m1, m2, tx, ty, tz);
+        bool valid = false;
+        double mx = 0.0, my = 0.0, ca = 0.0, cb = 0.0, cc = 0.0, radius = 0.0, det = 0.0;
+        if (tz > cam.near_) {
+            const double txz = tx / tz, tyz = ty / tz;
+            const double ctxz = fmin(fmax(txz, -lim_x), lim_x);
+            const double ctyz = fmin(fmax(tyz, -lim_y), lim_y);
+            const double *R = cam.rot;
+            const double fz = focal / tz;
+            const double j00 = fz * R[0] - fz * ctxz * R[6];
+            const double j01 = fz * R[1] - fz * ctxz * R[7];
+            const double j02 = fz * R[2] - fz * ctxz * R[8];
+            const double j10 = fz * R[3] - fz * ctyz * R[6];
+            const double j11 = fz * R[4] - fz * ctyz * R[7];
+            const double j12 = fz * R[5] - fz * ctyz * R[8];
+
+            const double q0 = qw.x, q1 = qw.y, q2 = qw.z, q3 = qw.w;
+            const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+            const double w = q0 / qn, x = q1 / qn, y = q2 / qn, z = q3 / qn;
+            const double r00 = 1.0 - 2.0 * (y * y + z * z);
+            const double r01 = 2.0 * (x * y - w * z);
+            const double r02 = 2.0 * (x * z + w * y);
+            const double r10 = 2.0 * (x * y + w * z);
+            const double r11 = 1.0 - 2.0 * (x * x + z * z);
+            const double r12 = 2.0 * (y * z - w * x);
+            const double r20 = 2.0 * (x * z - w * y);
+            const double r21 = 2.0 * (y * z + w * x);
+            const double r22 = 1.0 - 2.0 * (x * x + y * y);
+            const double s0 = exp(2.0 * (double)ls0);
+            const double s1 = exp(2.0 * (double)ls1);
+            const double s2 = exp(2.0 * (double)ls2);
+            const double g00 = r00 * r00 * s0 + r01 * r01 * s1 + r02 * r02 * s2;
+            const double g01 = r00 * r10 * s0 + r01 * r11 * s1 + r02 * r12 * s2;
+            const double g02 = r00 * r20 * s0 + r01 * r21 * s1 + r02 * r22 * s2;
+            const double g11 = r10 * r10 * s0 + r11 * r11 * s1 + r12 * r12 * s2;
+            const double g12 = r10 * r20 * s0 + r11 * r21 * s1 + r12 * r22 * s2;
+            const double g22 = r20 * r20 * s0 + r21 * r21 * s1 + r22 * r22 * s2;
+            const double u0 = j00 * g00 + j01 * g01 + j02 * g02;
+            const double u1 = j00 * g01 + j01 * g11 + j02 * g12;
+            const double u2 = j00 * g02 + j01 * g12 + j02 * g22;
+            const double v0 = j10 * g00 + j11 * g01 + j12 * g02;
+            const double v1 = j10 * g01 + j11 * g11 + j12 * g12;
+            const double v2 = j10 * g02 + j11 * g12 + j12 * g22;
+            const double a = u0 * j00 + u1 * j01 + u2 * j02 + opts.dilation;
+            const double b = u0 * j10 + u1 * j11 + u2 * j12;
+            const double c = v0 * j10 + v1 * j11 + v2 * j12 + opts.dilation;
+            mx = focal * txz + (double)(cam.width - 1) / 2.0;
+            my = focal * tyz + (double)(cam.height - 1) / 2.0;
+            det = a * c - b * b;
+            if (det <= 1e-12) {
+                n_skipped++;
+            } else {
+                ca = c / det;
+                cb = -b / det;
+                cc = a / det;
+                const double mid = 0.5 * (a + c);
+                const double disc = mid * mid - det;
+                const double lam = mid + sqrt(disc > 0.0 ? disc : 0.0);
+                radius = ceil(3.0 * sqrt(lam));
+                valid = radius > 0.0;
+                if (valid && opts.radius_clip > 0.0 && det < opts.radius_clip) valid = false;
+            }
+        }
+        // --- tile rectangle (sc/raster.py:307-314) ---
+        int tx0 = 0, tx1 = 0, ty0 = 0, ty1 = 0;
+        bool passed = false;
+        if (valid) {
+            tx0 = (int)clampd(floor((mx - radius) / (double)kTile), 0.0, (double)n_tx);
+            tx1 = (int)clampd(floor((mx + radius) / (double)kTile) + 1.0, 0.0, (double)n_tx);
+            ty0 = (int)clampd(floor((my - radius) / (double)kTile), 0.0, (double)n_ty);
+            ty1 = (int)clampd(floor((my + radius) / (double)kTile) + 1.0, 0.0, (double)n_ty);
+            passed = tx1 > tx0 && ty1 > ty0;
+        }
+        n_passed += passed;
+
+        // --- colour (sc/raster.py:198-226) and opacity (sc/asset.py:44-51) ---
+        int deg = as.sh_degree;
+        if (opts.sh_degree_eval >= 0 && opts.sh_degree_eval < deg) deg = opts.sh_degree_eval;
+        const float *shp = scene.sh + g * (int64_t)scene.sh_stride;
+        double col[3];
+        for (int ch = 0; ch < 3; ch++) col[ch] = kShC0 * (double)__ldg(shp + ch);
+        if (deg >= 1) {
+            double dx = m0 - cam.pos[0], dy = m1 - cam.pos[1], dz = m2 - cam.pos[2];
+            const double nrm = sqrt(dx * dx + dy * dy + dz * dz);
+            dx /= nrm;
+            dy /= nrm;
+            dz /= nrm;
+            for (int ch = 0; ch < 3; ch++) {
+                const double s1 = __ldg(shp + 3 + ch), s2 = __ldg(shp + 6 + ch), s3 = __ldg(shp + 9 + ch);
+                col[ch] = col[ch] - kShC1 * dy * s1 + kShC1 * dz * s2 - kShC1 * dx * s3;
+            }
+            if (deg >= 2) {
+                const double xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yz = dy * dz, xz = dx * dz;
+                for (int ch = 0; ch < 3; ch++) {
+                    const float *c = shp + ch;
+                    col[ch] = col[ch] + kShC2[0] * xy * (double)c[12] + kShC2[1] * yz * (double)c[15] +
+                              kShC2[2] * (2.0 * zz - xx - yy) * (double)c[18] + kShC2[3] * xz * (double)c[21] +
+                              kShC2[4] * (xx - yy) * (double)c[24];
+                }
+                if (deg >= 3) {
+                    for (int ch = 0; ch < 3; ch++) {
+                        const float *c = shp + ch;
+                        col[ch] = col[ch] + kShC3[0] * dy * (3.0 * xx - yy) * (double)c[27] +
+                                  kShC3[1] * xy * dz * (double)c[30] +
+                                  kShC3[2] * dy * (4.0 * zz - xx - yy) * (double)c[33] +
+                                  kShC3[3] * dz * (2.0 * zz - 3.0 * xx - 3.0 * yy) * (double)c[36] +
+                                  kShC3[4] * dx * (4.0 * zz - xx - yy) * (double)c[39] +
+                                  kShC3[5] * dz * (xx - yy) * (double)c[42] +
+                                  kShC3[6] * dx * (xx - 3.0 * yy) * (double)c[45];
+                    }
+                }
+            }
+        }
+        const double xl = (double)mo.w;
+        double op;
+        if (xl >= 0.0) {
+            op = 1.0 / (1.0 + exp(-xl));
+        } else {
+            const double e = exp(xl);
+            op = e / (1.0 + e);
+        }
+        const double log_op = log(op > 1e-300 ? op : 1e-300);
+
+        sc_splat sp;
+        sp.mx = (float)mx;
+        sp.my = (float)my;
+        sp.half_a = (float)(0.5 * ca);
+        sp.b = (float)cb;
+        sp.half_c = (float)(0.5 * cc);
+        sp.opacity = (float)op;
+        sp.p_min = (float)(log_min_alpha - log_op);
+        for (int ch = 0; ch < 3; ch++) sp.rgb[ch] = (float)clampd(col[ch] + 0.5, 0.0, 1.0);
+        if (passed && !(op < 1.0 / 255.0)) {
+            sp.win[0] = clamp16(floor(mx - radius));
+            sp.win[1] = clamp16(floor(mx + radius) + 1.0);
+            sp.win[2] = clamp16(floor(my - radius));
+            sp.win[3] = clamp16(floor(my + radius) + 1.0);
+        } else {   // skipped by the blend (reference: `op < min_alpha: continue`)
+            sp.win[0] = 1;
+            sp.win[1] = 0;
+            sp.win[2] = 1;
+            sp.win[3] = 0;
+        }
+        splats[k] = sp;
+        if (keys) {
+            keys[k] = passed ? float_key((float)tz) : 0xFFFFFFFFu;
+            vals[k] = (uint32_t)k;
+            depth64[k] = tz;
+            rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0,
+                                   (unsigned short)ty1);
+        }
+        if (dbg_f64) {
+            double *d = dbg_f64 + 8 * k;
+            d[0] = mx; d[1] = my; d[2] = ca; d[3] = cb; d[4] = cc; d[5] = tz; d[6] = radius; d[7] = det;
+        }
+        if (dbg_rect) {
+            dbg_rect[4 * k] = tx0; dbg_rect[4 * k + 1] = tx1; dbg_rect[4 * k + 2] = ty0; dbg_rect[4 * k + 3] = ty1;
+        }
+        if (dbg_flags) dbg_flags[k] = (uint8_t)((valid ? 1 : 0) | (passed ? 2 : 0));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        n_passed += __shfl_down_sync(0xffffffffu, n_passed, o);
+        n_skipped += __shfl_down_sync(0xffffffffu, n_skipped, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (n_passed) {
+            atomicAdd((unsigned long long *)&stats->passed, n_passed);
+            if (passed_ctr) atomicAdd(passed_ctr, n_passed);
+        }
+        if (n_skipped) atomicAdd((unsigned long long *)&stats->skipped, n_skipped);
+    }
+}
+
+cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
+                           int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
+                           uint32_t *keys, uint32_t *vals, double *depth64, ushort4 *rect, double *dbg_f64,
+                           int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats,
+                           unsigned long long *passed_ctr, cudaStream_t st)
+{
+    if (n_max <= 0) return cudaSuccess;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 8);
+    SC_LAUNCH(k_project, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, keys, vals, depth64,
+              rect, dbg_f64, dbg_rect, dbg_flags, stats, passed_ctr);
+    return cudaGetLastError();
+}
+
+}  // namespace sc

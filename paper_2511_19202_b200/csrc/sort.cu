@@ -1,0 +1,395 @@
+// Stage (d): (depth, index) order of the passed splats and tile binning.
+//
+// Reference: argsort(depth, kind="stable") over passed splats
+// (sc/raster.py:319) followed by the counting sort bin_tiles
+// (sc/_kernels.py:137-165).  B200 version, all on device, no host sync:
+//   1. stable LSD radix sort (4 x 8 bits) of the f32 depth keys of all
+//      survivors (non-passed keys are 0xFFFFFFFF and sink to the end); the
+//      input is in survivor order, so equal keys stay index-ordered;
+//   2. tie-fix: runs of equal f32 keys are re-ordered by (f64 depth, index),
+//      which makes the order identical to the reference's f64 argsort;
+//   3. per-splat tile counts -> exclusive scan -> entry emission
+//      (tile id, survivor index) in depth order;
+//   4. stable LSD radix sort of the entries by tile id (2 x 8 bits), i.e.
+//      the reference's stable counting sort by tile;
+//   5. tile offsets (the reference's `counts` array).
+// Every kernel reads its element count from device memory, so the whole
+// frame stays asynchronous (and CUDA-graph capturable).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sc {
+
+// ---------------------------------------------------------------------------
+// generic exclusive scan of uint32 (3 phases), n read from device or host
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t dev_count(const unsigned long long *n_dev, int64_t n_host)
+{
+    return n_dev ? std::min<int64_t>((int64_t)*n_dev, n_host) : n_host;
+}
+
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t *s_warp, uint32_t &total)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = THREADS / 32;
+    uint32_t v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) s_warp[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < NW ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < NW) s_warp[lane] = w;
+    }
+    __syncthreads();
+    total = s_warp[NW - 1];
+    const uint32_t r = (wid ? s_warp[wid - 1] : 0u) + v - x;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *in, const unsigned long long *n_dev,
+                                                              int64_t n_host, uint32_t *part)
+{
+    __shared__ uint32_t s_warp[32];
+    const int64_t n = dev_count(n_dev, n_host);
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    uint32_t sum = 0;
+    if (base < n) {
+        for (int j = 0; j < kScanItems; j++) {
+            const int64_t i = base + (int64_t)j * kScanThreads + threadIdx.x;
+            if (i < n) sum += in[i];
+        }
+    }
+    uint32_t total;
+    block_excl_scan<kScanThreads>(sum, s_warp, total);
+    if (threadIdx.x == 0) part[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of the block partials, total -> *total_out
+__global__ void __launch_bounds__(1024) k_scan_partials(uint32_t *part, int64_t nblk, unsigned long long *total_out,
+                                                        int64_t *stat_out)
+{
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_run;
+    if (threadIdx.x == 0) s_run = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nblk; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        const uint32_t x = i < nblk ? part[i] : 0u;
+        uint32_t total;
+        const uint32_t e = block_excl_scan<1024>(x, s_warp, total);
+        if (i < nblk) part[i] = s_run + e;
+        __syncthreads();
+        if (threadIdx.x == 0) s_run += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (total_out) *total_out = s_run;
+        if (stat_out) *stat_out = (int64_t)s_run;
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t *in, uint32_t *out,
+                                                            const unsigned long long *n_dev, int64_t n_host,
+                                                            const uint32_t *part)
+{
+    __shared__ uint32_t s_warp[32];
+    const int64_t n = dev_count(n_dev, n_host);
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    if (base >= n) return;
+    // blocked arrangement: thread t owns items [base + t*16, base + t*16 + 16)
+    uint32_t v[kScanItems];
+    uint32_t sum = 0;
+    const int64_t my = base + (int64_t)threadIdx.x * kScanItems;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        const int64_t i = my + j;
+        v[j] = i < n ? in[i] : 0u;
+        sum += v[j];
+    }
+    uint32_t total;
+    uint32_t run = block_excl_scan<kScanThreads>(sum, s_warp, total) + part[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        const int64_t i = my + j;
+        if (i < n) out[i] = run;
+        run += v[j];
+    }
+}
+
+static cudaError_t scan_excl(const uint32_t *in, uint32_t *out, const unsigned long long *n_dev, int64_t n_max,
+                             uint32_t *part, unsigned long long *total_out, int64_t *stat_out, cudaStream_t st)
+{
+    const int64_t nblk = std::max<int64_t>(1, (n_max + kScanTile - 1) / kScanTile);
+    SC_LAUNCH(k_scan_reduce, (int)nblk, kScanThreads, 0, st, in, n_dev, n_max, part);
+    SC_LAUNCH(k_scan_partials, 1, 1024, 0, st, part, nblk, total_out, stat_out);
+    SC_LAUNCH(k_scan_down, (int)nblk, kScanThreads, 0, st, in, out, n_dev, n_max, part);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// LSD radix sort pass (8-bit digit), reduce-then-scan, stable.
+// hist layout: digit-major [256][nblk] so one exclusive scan yields every
+// (digit, block) scatter base.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t *keys, const unsigned long long *n_dev,
+                                                              int64_t n_host, int shift, uint32_t *hist,
+                                                              int64_t nblk)
+{
+    __shared__ uint32_t h[256];
+    const int64_t n = dev_count(n_dev, n_host);
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+    if (base < n) {
+#pragma unroll 4
+        for (int j = 0; j < kRadixItems; j++) {
+            const int64_t i = base + (int64_t)j * kRadixThreads + threadIdx.x;
+            if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xFFu], 1u);
+        }
+    }
+    __syncthreads();
+    hist[(int64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t *keys_in, const uint32_t *vals_in,
+                                                                 uint32_t *keys_out, uint32_t *vals_out,
+                                                                 const unsigned long long *n_dev, int64_t n_host,
+                                                                 int shift, const uint32_t *hist_scanned,
+                                                                 int64_t nblk)
+{
+    __shared__ uint32_t s_keys[kRadixTile];
+    __shared__ uint32_t s_vals[kRadixTile];
+    __shared__ uint32_t s_wcnt[kRadixThreads / 32][256];
+    __shared__ uint32_t s_dstart[256];   // block-local start of each digit
+    __shared__ uint32_t s_gbase[256];    // global scatter base of each digit
+    __shared__ uint32_t s_run[256];      // running count per digit over rounds
+    __shared__ uint32_t s_warp[32];
+    const int64_t n = dev_count(n_dev, n_host);
+    const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+    if (base >= n) return;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int cnt = (int)std::min<int64_t>(kRadixTile, n - base);
+
+    uint32_t k[kRadixItems], v[kRadixItems];
+#pragma unroll
+    for (int j = 0; j < kRadixItems; j++) {
+        const int i = j * kRadixThreads + tid;
+        k[j] = i < cnt ? keys_in[base + i] : 0u;
+        v[j] = i < cnt ? vals_in[base + i] : 0u;
+    }
+    // block-local digit histogram -> digit starts
+    s_run[tid] = 0;
+    for (int w = 0; w < kRadixThreads / 32; w++) s_wcnt[w][tid] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRadixItems; j++) {
+        const int i = j * kRadixThreads + tid;
+        if (i < cnt) atomicAdd(&s_run[(k[j] >> shift) & 0xFFu], 1u);
+    }
+    __syncthreads();
+    {
+        uint32_t total;
+        const uint32_t c = s_run[tid];
+        const uint32_t e = block_excl_scan<kRadixThreads>(c, s_warp, total);
+        s_dstart[tid] = e;
+        s_gbase[tid] = hist_scanned[(int64_t)tid * nblk + blockIdx.x];
+        s_run[tid] = 0;
+    }
+    __syncthreads();
+    // stable ranking, one round per 256 consecutive items
+#pragma unroll 1
+    for (int j = 0; j < kRadixItems; j++) {
+        const int i = j * kRadixThreads + tid;
+        const bool ok = i < cnt;
+        const uint32_t d = ok ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane;   // unique dummy digit
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & lanemask_lt());
+        if (ok && rank == 0) s_wcnt[wid][d] = __popc(peers);
+        __syncthreads();
+        {   // per digit: exclusive prefix over warps, then advance the running count
+            uint32_t run = s_run[tid];
+#pragma unroll
+            for (int w = 0; w < kRadixThreads / 32; w++) {
+                const uint32_t c = s_wcnt[w][tid];
+                s_wcnt[w][tid] = run;
+                run += c;
+            }
+            s_run[tid] = run;
+        }
+        __syncthreads();
+        if (ok) {
+            const uint32_t pos = s_dstart[d] + s_wcnt[wid][d] + rank;
+            s_keys[pos] = k[j];
+            s_vals[pos] = v[j];
+        }
+        __syncthreads();
+        for (int w = 0; w < kRadixThreads / 32; w++) s_wcnt[w][tid] = 0;
+        __syncthreads();
+    }
+    // coalesced write-out: consecutive positions of one digit are contiguous in the output
+    for (int i = tid; i < cnt; i += kRadixThreads) {
+        const uint32_t key = s_keys[i];
+        const uint32_t d = (key >> shift) & 0xFFu;
+        const uint32_t dst = s_gbase[d] + (uint32_t)i - s_dstart[d];
+        keys_out[dst] = key;
+        vals_out[dst] = s_vals[i];
+    }
+}
+
+// Sorts (keys, vals) in place-ish over `bits` low bits; result ends in the
+// buffer pointed to by *keys_res / *vals_res (ping-pong).
+static cudaError_t radix_sort(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, const unsigned long long *n_dev,
+                              int64_t n_max, int bits, uint32_t *hist, uint32_t *part, uint32_t **keys_res,
+                              uint32_t **vals_res, cudaStream_t st)
+{
+    const int64_t nblk = std::max<int64_t>(1, (n_max + kRadixTile - 1) / kRadixTile);
+    uint32_t *ki = ka, *vi = va, *ko = kb, *vo = vb;
+    for (int shift = 0; shift < bits; shift += 8) {
+        SC_LAUNCH(k_radix_hist, (int)nblk, kRadixThreads, 0, st, ki, n_dev, n_max, shift, hist, nblk);
+        cudaError_t e = scan_excl(hist, hist, nullptr, 256 * nblk, part, nullptr, nullptr, st);
+        if (e != cudaSuccess) return e;
+        SC_LAUNCH(k_radix_scatter, (int)nblk, kRadixThreads, 0, st, ki, vi, ko, vo, n_dev, n_max, shift, hist, nblk);
+        std::swap(ki, ko);
+        std::swap(vi, vo);
+    }
+    *keys_res = ki;
+    *vals_res = vi;
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// tie-fix: equal f32 keys -> order by (f64 depth, survivor index)
+// ---------------------------------------------------------------------------
+__global__ void k_tiefix(const uint32_t *keys, uint32_t *vals, const double *depth64, const unsigned long long *n_dev,
+                        int64_t n_host, sc_frame_stats *stats)
+{
+    const int64_t n = dev_count(n_dev, n_host);
+    unsigned long long longest = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t key = keys[i];
+        if (i > 0 && keys[i - 1] == key) continue;          // not a run head
+        if (i + 1 >= n || keys[i + 1] != key) continue;     // run of length 1
+        int64_t e = i + 1;
+        while (e < n && keys[e] == key) e++;
+        longest = std::max<unsigned long long>(longest, (unsigned long long)(e - i));
+        // insertion sort on (depth64[v], v); linear when already ordered
+        for (int64_t a = i + 1; a < e; a++) {
+            const uint32_t va = vals[a];
+            const double da = depth64[va];
+            int64_t b = a - 1;
+            while (b >= i) {
+                const uint32_t vb = vals[b];
+                const double db = depth64[vb];
+                if (db < da || (db == da && vb < va)) break;
+                vals[b + 1] = vb;
+                b--;
+            }
+            vals[b + 1] = va;
+        }
+    }
+    if (longest) atomicMax((unsigned long long *)&stats->max_tie_run, longest);
+}
+
+// ---------------------------------------------------------------------------
+// entries: per passed splat (depth order) count, scan, emit (tile, survivor)
+// ---------------------------------------------------------------------------
+__global__ void k_entry_count(const uint32_t *order, const ushort4 *rect, const unsigned long long *n_dev,
+                              int64_t n_host, uint32_t *cnt)
+{
+    const int64_t n = dev_count(n_dev, n_host);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const ushort4 r = rect[order[k]];
+        cnt[k] = (uint32_t)(r.y - r.x) * (uint32_t)(r.w - r.z);
+    }
+}
+
+__global__ void k_entry_emit(const uint32_t *order, const ushort4 *rect, const uint32_t *off,
+                             const unsigned long long *n_dev, int64_t n_host, int n_tx, uint32_t *ekey,
+                             uint32_t *eval, const unsigned long long *e_total, unsigned long long *e_eff, int64_t cap_e,
+                             sc_frame_stats *stats)
+{
+    const int64_t n = dev_count(n_dev, n_host);
+    const bool over = (int64_t)*e_total > cap_e;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *e_eff = over ? 0ull : *e_total;
+        if (over) atomicOr((unsigned long long *)&stats->overflow, 2ull);
+    }
+    if (over) return;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t sv = order[k];
+        const ushort4 r = rect[sv];
+        uint32_t o = off[k];
+        for (int y = r.z; y < r.w; y++)
+            for (int x = r.x; x < r.y; x++) {
+                ekey[o] = (uint32_t)(y * n_tx + x);
+                eval[o] = sv;
+                o++;
+            }
+    }
+}
+
+// tile_off[t] = first entry index with tile >= t, for t in [0, n_tiles]
+__global__ void k_tile_offsets(const uint32_t *ekey, const unsigned long long *e_dev, int64_t cap_e, int64_t n_tiles,
+                               uint32_t *tile_off)
+{
+    const int64_t E = std::min<int64_t>((int64_t)*e_dev, cap_e);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= E; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev = i > 0 ? (int64_t)ekey[i - 1] : -1;
+        const int64_t cur = i < E ? (int64_t)ekey[i] : n_tiles;
+        for (int64_t t = prev + 1; t <= cur; t++) tile_off[t] = (uint32_t)i;
+    }
+}
+
+static int grid_for(int64_t n, int threads)
+{
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)nsm * 16));
+}
+
+// n_dev: survivor count (device).  Inputs: ws.key_a / val_a / depth64 / rect
+// from the projection.  Outputs: order (passed survivors by (depth, index)),
+// entries (survivor index per entry, tile-major), ws.tile_off, stats.entries.
+cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
+                       sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out, cudaStream_t st)
+{
+    cudaError_t e;
+    uint32_t *keys_s = nullptr, *order = nullptr;
+    e = radix_sort(ws.key_a, ws.val_a, ws.key_b, ws.val_b, n_dev, n_max, 32, ws.hist, ws.scan_part, &keys_s, &order,
+                   st);
+    if (e != cudaSuccess) return e;
+    const unsigned long long *p_dev = &ws.ctr->passed;   // passed splats lead the sorted order
+    SC_LAUNCH(k_tiefix, grid_for(n_max, 256), 256, 0, st, keys_s, order, ws.depth64, p_dev, n_max, stats);
+    SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, ws.ecount);
+    e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, &stats->entries, st);
+    if (e != cudaSuccess) return e;
+    SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, ws.rect, ws.ecount, p_dev, n_max, ws.n_tx,
+              ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
+    int bits = 0;
+    while ((1ll << bits) < ws.n_tiles) bits += 8;
+    uint32_t *ek = nullptr, *ev = nullptr;
+    if (bits == 0) bits = 8;
+    e = radix_sort(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, bits, ws.hist,
+                   ws.scan_part, &ek, &ev, st);
+    if (e != cudaSuccess) return e;
+    SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE, ws.n_tiles,
+              ws.tile_off);
+    *order_out = order;
+    *entries_out = ev;
+    return cudaGetLastError();
+}
+
+}  // namespace sc

@@ -1,0 +1,113 @@
+"""Drop-in ``render`` (reference sc/raster.py:240-339) on the B200 path.
+
+``render(asset, cam, **opts)`` is the single-identity-instance, no-cull,
+no-MLP case of the composed-scene pipeline: the same sm_100a projection /
+sort / blend kernels, with ``frustum="off"`` so the splat set is exactly the
+reference's.  Images come back as float32 numpy arrays (the device blends in
+fp32; tolerance in tests/test_gpu_parity.py).  PSNR / SSIM follow
+sc/raster.py:346-399 (host, numpy/scipy: these are parity metrics, not part
+of the frame path).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .camera import Camera  # noqa: F401  (re-export, reference raster.Camera)
+
+MIN_ALPHA = 1.0 / 255.0
+STOP_TRANSMITTANCE = 1.0 / 255.0
+COV_DILATION = 0.3
+DET_EPS = 1e-12
+PSNR_SENTINEL = 99.0
+
+
+@dataclass
+class RenderOutput:
+    """Same fields as the reference RenderOutput (sc/raster.py:229-237)."""
+
+    image: np.ndarray                      # (H, W, 3) float32, background composited
+    final_transmittance: np.ndarray        # (H, W) float32
+    contribution_max: np.ndarray | None    # (n,) max alpha*T over pixels, per (survivor) splat
+    contribution_sum: np.ndarray | None    # (H, W)
+    used_count: int | None
+    passed_count: int
+    skipped_count: int
+
+
+def render(asset, cam, *, sh_degree_eval: int | None = None, record_contributions: bool = False,
+           radius_clip: float | None = None, tile_size: int = 16,
+           stop_transmittance: float = STOP_TRANSMITTANCE, background=(1.0, 1.0, 1.0),
+           dilation: float = COV_DILATION) -> RenderOutput:
+    """Rasterize one asset on the GPU (reference signature, sc/raster.py:240-251)."""
+    from .scene import ComposedScene, InstanceTransform, Renderer, RenderOptions
+
+    if tile_size != 16:
+        raise ValueError("tile_size must be 16 (the reference's default; tile size changes the image)")
+    if len(asset) == 0:
+        h, w = int(cam.height), int(cam.width)
+        bg = np.asarray(background, dtype=np.float32)
+        return RenderOutput(np.broadcast_to(bg, (h, w, 3)).copy(), np.ones((h, w), np.float32),
+                            np.zeros(0, np.float32) if record_contributions else None,
+                            np.zeros((h, w), np.float32) if record_contributions else None,
+                            0 if record_contributions else None, 0, 0)
+    scene = ComposedScene()
+    scene.add_asset(asset)
+    scene.add_instance(0, InstanceTransform.identity())
+    opts = RenderOptions(sh_degree_eval=sh_degree_eval, record_contributions=record_contributions,
+                         radius_clip=radius_clip, tile_size=tile_size, stop_transmittance=stop_transmittance,
+                         background=tuple(background), dilation=dilation, use_mlp=False, frustum="off")
+    out, _stats = Renderer(scene).render(cam, opts)
+    return out
+
+
+def psnr(a, b) -> float:
+    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    if mse <= 0.0:
+        return PSNR_SENTINEL
+    return min(PSNR_SENTINEL, -10.0 * math.log10(mse))
+
+
+def psnr_uncapped(a, b) -> float:
+    mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return math.inf if mse <= 0.0 else -10.0 * math.log10(mse)
+
+
+def ssim(a, b) -> float:
+    """Mean SSIM: 11x11 Gaussian window, sigma 1.5, per channel, border-cropped."""
+    from scipy.ndimage import correlate1d
+
+    x0 = np.asarray(a, dtype=np.float64)
+    y0 = np.asarray(b, dtype=np.float64)
+    if x0.ndim == 2:
+        x0, y0 = x0[:, :, None], y0[:, :, None]
+    r = 5
+    t = np.arange(-r, r + 1, dtype=np.float64)
+    k = np.exp(-0.5 * t * t / 2.25)
+    k /= k.sum()
+    c1, c2 = 1e-4, 9e-4
+
+    def smooth(img):
+        return correlate1d(correlate1d(img, k, axis=0, mode="nearest"), k, axis=1, mode="nearest")
+
+    out = []
+    for ch in range(x0.shape[2]):
+        x, y = x0[:, :, ch], y0[:, :, ch]
+        mx, my = smooth(x), smooth(y)
+        sxx = smooth(x * x) - mx * mx
+        syy = smooth(y * y) - my * my
+        sxy = smooth(x * y) - mx * my
+        m = ((2 * mx * my + c1) * (2 * sxy + c2)) / ((mx * mx + my * my + c1) * (sxx + syy + c2))
+        out.append(float(m[r:-r, r:-r].mean()))
+    return float(np.mean(out))
+
+
+def compute_metrics_pair(a, b) -> tuple[float, float]:
+    a = np.asarray(a)
+    b = np.asarray(b)
+    if a.shape != b.shape:
+        raise ValueError(f"image shapes differ: {a.shape} vs {b.shape}")
+    return psnr(a, b), ssim(a, b)

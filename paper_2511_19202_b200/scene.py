@@ -1,0 +1,526 @@
+"""Composed scenes and the instanced, occlusion-culled render path.
+
+The reference package does not ship its ``scene`` module; this implements
+SPEC.md:325-389 (InstanceTransform, ComposedScene, FrameStats, local_inputs,
+render_composed) with every per-frame stage on the B200:
+
+    sc_render_composed (libsplatcull_b200.so)
+      prep     per-instance Eq. 2 factor + bounding-sphere cull
+      cull     per-(instance, gaussian) frustum test, d_near gate, tcgen05 MLP,
+               order-preserving survivor compaction           stages (a)+(b)
+      project  instancing + EWA projection + SH on survivors  stage (c)
+      bin      depth radix sort + tie-fix + tile binning      stage (d)
+      blend    per-tile front-to-back compositing             stage (e)
+
+Assets are stored once (struct-of-arrays in HBM) with a list of similarity
+transforms; culled Gaussians are never instantiated in HBM.  The host only
+passes the camera per frame and reads back the image and the counters.
+
+Pinned restatement decisions (shared with oracle/scene_ref.py):
+flat order (asset, instance, gaussian); instanced mean s R m + t in f64 then
+f32; q' = q_i (x) q; log_s' = log_s + ln s; frustum = conservative superset
+of what the rasterizer passes (``frustum="margin"``) or mean-in-image
+(``"strict"``); gate d_t = |c - m'| (f_t / f_r) / s >= d_near; keep iff
+logit >= logit(threshold).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .asset import Asset
+from .nn import VisibilityModel, feature_inputs
+
+FRUSTUM_MODES = {"margin": nat.SC_FRUSTUM_MARGIN, "strict": nat.SC_FRUSTUM_STRICT, "off": nat.SC_FRUSTUM_OFF}
+
+
+@dataclass
+class InstanceTransform:
+    """Similarity transform: x' = s R(q) x + t."""
+
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    rotation: np.ndarray = field(default_factory=lambda: np.array([1.0, 0.0, 0.0, 0.0]))  # (w, x, y, z)
+    scale: float = 1.0
+
+    def __post_init__(self):
+        self.translation = np.asarray(self.translation, dtype=np.float64).reshape(3)
+        self.rotation = np.asarray(self.rotation, dtype=np.float64).reshape(4)
+        self.scale = float(self.scale)
+        if not (self.scale > 0.0 and math.isfinite(self.scale)):
+            raise ValueError(f"instance scale must be > 0, got {self.scale}")
+        if not np.isfinite(self.translation).all() or not np.isfinite(self.rotation).all():
+            raise ValueError("non-finite instance transform")
+        n = float(np.sqrt((self.rotation ** 2).sum()))
+        if abs(n - 1.0) > 1e-6:
+            raise ValueError(f"instance rotation must be a unit quaternion (norm {n})")
+
+    @classmethod
+    def identity(cls) -> "InstanceTransform":
+        return cls()
+
+
+def instance_frame(tr: InstanceTransform) -> tuple[list[float], list[float], float, float]:
+    """(R row-major, normalised q, s, ln s) with plain float64 scalar math.
+
+    R follows the reference quaternion formula (sc/raster.py:111-126).
+    """
+    w, x, y, z = (float(v) for v in tr.rotation)
+    n = math.sqrt(w * w + x * x + y * y + z * z)
+    w, x, y, z = w / n, x / n, y / n, z / n
+    R = [1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+         2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
+         2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)]
+    return R, [w, x, y, z], float(tr.scale), math.log(float(tr.scale))
+
+
+@dataclass
+class SceneAsset:
+    asset: Asset
+    model: VisibilityModel | None = None
+
+
+class ComposedScene:
+    """Assets stored once, each with a list of instance transforms."""
+
+    def __init__(self):
+        self.assets: list[SceneAsset] = []
+        self.instances: list[list[InstanceTransform]] = []
+        self._version = 0
+        self._device = None
+
+    def add_asset(self, asset: Asset, model: VisibilityModel | None = None) -> int:
+        if len(asset) == 0:
+            raise ValueError("cannot add an empty asset")
+        if model is not None and model.asset_hash is not None:
+            from .asset import asset_hash
+            if asset_hash(asset) != model.asset_hash:
+                raise ValueError("visibility model was trained for a different asset (hash mismatch)")
+        self.assets.append(SceneAsset(asset, model))
+        self.instances.append([])
+        self._touch()
+        return len(self.assets) - 1
+
+    def add_instance(self, asset_id: int, transform: InstanceTransform | None = None) -> None:
+        if not (0 <= asset_id < len(self.assets)):
+            raise ValueError(f"unknown asset id {asset_id}")
+        self.instances[asset_id].append(transform if transform is not None else InstanceTransform())
+        self._touch()
+
+    def set_model(self, asset_id: int, model: VisibilityModel | None) -> None:
+        self.assets[asset_id].model = model
+        self._touch()
+
+    def _touch(self):
+        self._version += 1
+        self._device = None
+
+    @property
+    def n_instances(self) -> int:
+        return sum(len(v) for v in self.instances)
+
+    @property
+    def n_instantiated(self) -> int:
+        """Gaussians if every instance were flattened."""
+        return sum(len(a.asset) * len(v) for a, v in zip(self.assets, self.instances))
+
+    def flat_instances(self):
+        """(asset index, transform) in flat order (asset-major)."""
+        for a, lst in enumerate(self.instances):
+            for tr in lst:
+                yield a, tr
+
+
+@dataclass
+class FrameStats:
+    """Per-frame counters plus device-side extras."""
+
+    frustum_passed: int
+    mlp_culled: int
+    instantiated: int
+    used: int | None
+    mem_bytes_instantiated: int
+    render_ms: float
+    mlp_ms: float
+    preprocess_ms: float
+    mlp_queried: int = 0
+    instances_visible: int = 0
+    pairs_tested: int = 0
+    passed: int = 0
+    skipped: int = 0
+    entries: int = 0
+    max_tie_run: int = 0
+
+
+@dataclass
+class RenderOptions:
+    """render() keywords (sc/raster.py:240-251) plus the scene-path switches."""
+
+    sh_degree_eval: int | None = None
+    record_contributions: bool = False
+    radius_clip: float | None = None
+    tile_size: int = 16
+    stop_transmittance: float = 1.0 / 255.0
+    background: tuple = (1.0, 1.0, 1.0)
+    dilation: float = 0.3
+    use_mlp: bool = True
+    frustum: str = "margin"
+
+    def struct(self, cam) -> nat.ScOpts:
+        if self.tile_size != 16:
+            raise ValueError("tile_size must be 16 (the oracle's tile semantics; see DESIGN.md)")
+        if self.frustum not in FRUSTUM_MODES:
+            raise ValueError(f"frustum must be one of {sorted(FRUSTUM_MODES)}")
+        o = nat.ScOpts()
+        o.tile_size = 16
+        o.sh_degree_eval = -1 if self.sh_degree_eval is None else int(self.sh_degree_eval)
+        o.record_contributions = 1 if self.record_contributions else 0
+        o.use_mlp = 1 if self.use_mlp else 0
+        o.frustum_mode = FRUSTUM_MODES[self.frustum]
+        o.radius_clip = float(self.radius_clip) if self.radius_clip is not None else 0.0
+        o.stop_transmittance = float(self.stop_transmittance)
+        o.background[:] = [float(v) for v in self.background]
+        o.dilation = float(self.dilation)
+        o.frustum_G = frustum_G(cam)
+        return o
+
+
+def frustum_G(cam) -> float:
+    """Bound on |J W| in units of f/z for the clamped Jacobian."""
+    tx, ty = cam.tan_half_fov
+    return math.sqrt(1.0 + 1.69 * (tx * tx + ty * ty)) * 1.00001
+
+
+def sigma_max(asset: Asset) -> np.ndarray:
+    """Per-gaussian largest std-dev exp(max log_scale), f32 (frustum margin input)."""
+    return np.exp(asset.log_scales.max(axis=1).astype(np.float64)).astype(np.float32)
+
+
+def vis_weights_struct(model: VisibilityModel) -> nat.ScVisWeights:
+    w = nat.ScVisWeights()
+    W1, W2, W3 = model.vis_mlp.weights
+    b1, b2, b3 = model.vis_mlp.biases
+    if W1.shape != (32, 16) or W2.shape != (32, 32) or W3.shape != (1, 32):
+        raise ValueError(f"device MLP supports 16->32->32->1 only, got {model.vis_mlp.widths}")
+    w.w1[:] = W1.astype(np.float16).view(np.uint16).reshape(-1).tolist()
+    w.w2[:] = W2.astype(np.float16).view(np.uint16).reshape(-1).tolist()
+    w.b1[:] = b1.astype(np.float32).tolist()
+    w.b2[:] = b2.astype(np.float32).tolist()
+    w.w3[:] = W3.reshape(-1).astype(np.float32).tolist()
+    w.b3 = float(b3[0])
+    return w
+
+
+def feature_params(model: VisibilityModel) -> np.ndarray:
+    m = model.feature_mlp
+    parts = []
+    for W, b in zip(m.weights, m.biases):
+        parts += [W.astype(np.float32).reshape(-1), b.astype(np.float32).reshape(-1)]
+    p = np.concatenate(parts)
+    if m.widths != (14, 32, 32, 6):
+        raise ValueError(f"device feature MLP supports 14->32->32->6 only, got {m.widths}")
+    return p
+
+
+class DeviceScene:
+    """The scene in HBM: concatenated gaussian SoA + asset / instance / weight tables."""
+
+    def __init__(self, scene: ComposedScene, device=None):
+        import torch
+
+        nat.load()
+        self.device = torch.device(device or "cuda")
+        assets = scene.assets
+        if not assets:
+            raise ValueError("scene has no assets")
+        counts = [len(a.asset) for a in assets]
+        offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        n = int(offsets[-1])
+        max_deg = max(a.asset.sh_degree for a in assets)
+        sh_stride = 3 * (max_deg + 1) ** 2
+        mean_opa = np.empty((n, 4), np.float32)
+        quat = np.empty((n, 4), np.float32)
+        scale_smax = np.empty((n, 4), np.float32)
+        sh = np.zeros((n, sh_stride), np.float32)
+        arecs = (nat.ScAssetRec * len(assets))()
+        models: list[VisibilityModel] = []
+        feat_jobs = []
+        for i, sa in enumerate(assets):
+            a = sa.asset
+            lo, hi = int(offsets[i]), int(offsets[i + 1])
+            mean_opa[lo:hi, :3] = a.means
+            mean_opa[lo:hi, 3] = a.opacity_logits
+            quat[lo:hi] = a.rotations
+            scale_smax[lo:hi, :3] = a.log_scales
+            smax = sigma_max(a)
+            scale_smax[lo:hi, 3] = smax
+            k = 3 * (a.sh_degree + 1) ** 2
+            sh[lo:hi, :k] = a.sh_coeffs.reshape(hi - lo, k)
+            r = arecs[i]
+            r.offset, r.count = lo, hi - lo
+            r.bound_local = float(np.sqrt((a.means.astype(np.float64) ** 2).sum(axis=1)).max())
+            r.sigma_max = float(smax.astype(np.float64).max())
+            r.sh_degree = a.sh_degree
+            m = sa.model
+            if m is not None:
+                r.model = len(models)
+                models.append(m)
+                r.d_near, r.d_far = float(m.d_near), float(m.d_far)
+                r.inv_mean_scale = 1.0 / float(m.mean_scale)
+                r.f_train = float(m.f_train)
+                r.logit_threshold = float(m.logit_threshold)
+                feat_jobs.append((lo, hi, m, a))
+            else:
+                r.model = -1
+                r.d_near = float(a.d_near) if a.d_near is not None else 0.0
+                r.d_far = float(a.d_far) if a.d_far is not None else 1.0
+                r.inv_mean_scale = 1.0
+                r.f_train = 0.0
+                r.logit_threshold = 0.0
+        flat = list(scene.flat_instances())
+        irecs = (nat.ScInstanceRec * max(1, len(flat)))()
+        for k, (ai, tr) in enumerate(flat):
+            R, q, s, ln_s = instance_frame(tr)
+            rec = irecs[k]
+            rec.R[:] = R
+            rec.t[:] = [float(v) for v in tr.translation]
+            rec.q[:] = q
+            rec.s, rec.ln_s = s, ln_s
+            rec.asset = ai
+        wrecs = (nat.ScVisWeights * max(1, len(models)))()
+        for k, m in enumerate(models):
+            wrecs[k] = vis_weights_struct(m)
+
+        dev = self.device
+        T = torch.from_numpy
+        self.mean_opa = T(mean_opa).to(dev)
+        self.quat = T(quat).to(dev)
+        self.scale_smax = T(scale_smax).to(dev)
+        self.sh = T(sh).to(dev)
+        self.features = torch.zeros((max(n, 1), 8), dtype=torch.float16, device=dev)
+        self.assets_t = nat.struct_tensor(arecs, dev)
+        self.instances_t = nat.struct_tensor(irecs, dev)
+        self.weights_t = nat.struct_tensor(wrecs, dev)
+        self.n_gauss, self.n_instances, self.n_models = n, len(flat), len(models)
+        self.max_pairs = int(sum(counts[ai] for ai, _ in flat))
+        self.sh_stride = sh_stride
+        self.asset_offsets = offsets
+        self.inst_asset = np.array([ai for ai, _ in flat], dtype=np.int64)
+        self.scene_version = scene._version
+        for lo, hi, m, a in feat_jobs:
+            self.features[lo:hi] = encode_features_device(m, a, dev)
+        self.struct = nat.ScScene()
+        s = self.struct
+        s.mean_opa, s.quat, s.scale_smax = nat.ptr(self.mean_opa), nat.ptr(self.quat), nat.ptr(self.scale_smax)
+        s.sh, s.features = nat.ptr(self.sh), nat.ptr(self.features)
+        s.n_gauss, s.sh_stride, s.n_assets = n, sh_stride, len(assets)
+        s.assets, s.instances, s.n_instances = nat.ptr(self.assets_t), nat.ptr(self.instances_t), len(flat)
+        s.vis_weights, s.n_models = nat.ptr(self.weights_t), len(models)
+        self.payload_bytes = [44 + 12 * (a.asset.sh_degree + 1) ** 2 for a in assets]
+
+
+def encode_features_device(model: VisibilityModel, asset: Asset, device) -> "torch.Tensor":
+    """nn.encode_features on the GPU: (n, 8) fp16 (6 used)."""
+    import torch
+
+    lib = nat.load()
+    x = torch.from_numpy(feature_inputs(asset, model.mean_scale)).to(device)
+    p = torch.from_numpy(feature_params(model)).to(device)
+    out = torch.empty((len(asset), 8), dtype=torch.float16, device=device)
+    nat.check(lib.sc_encode_features(nat.ptr(p), nat.ptr(x), len(asset), nat.ptr(out), nat.stream_handle()),
+              "sc_encode_features")
+    return out
+
+
+class Workspace:
+    """Device workspace sized from the previous frame's counts (grows on overflow)."""
+
+    def __init__(self, dscene: DeviceScene, width: int, height: int, cap_s: int | None = None,
+                 cap_e: int | None = None):
+        self.dscene, self.width, self.height = dscene, int(width), int(height)
+        mp = max(1, dscene.max_pairs)
+        self.cap_s = int(cap_s if cap_s is not None else min(mp, 1 << 24))
+        self.cap_e = int(cap_e if cap_e is not None else max(4 * self.cap_s, 1 << 16))
+        self._alloc()
+
+    def _alloc(self):
+        import torch
+
+        lib = nat.load()
+        nbytes = lib.sc_workspace_bytes(self.dscene.n_instances, self.dscene.max_pairs, self.cap_s, self.cap_e,
+                                        self.width, self.height, 16)
+        if nbytes == 0:
+            raise ValueError("invalid workspace request")
+        self.buf = torch.empty(int(nbytes), dtype=torch.uint8, device=self.dscene.device)
+        self.struct = nat.ScWorkspace()
+        w = self.struct
+        w.base, w.bytes = nat.ptr(self.buf), int(nbytes)
+        w.n_instances, w.max_pairs = self.dscene.n_instances, self.dscene.max_pairs
+        w.cap_survivors, w.cap_entries = self.cap_s, self.cap_e
+
+    def grow(self, need_s: int, need_e: int) -> None:
+        self.cap_s = max(self.cap_s, int(need_s * 1.15) + 1024)
+        self.cap_e = max(self.cap_e, int(need_e * 1.15) + 4096)
+        self.buf = None
+        self._alloc()
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.buf.numel())
+
+
+@dataclass
+class DeviceFrame:
+    """A rendered frame still on the device (torch tensors)."""
+
+    image: "torch.Tensor"          # (H, W, 3) f32
+    trans: "torch.Tensor"          # (H, W) f32
+    stats_raw: "torch.Tensor"      # sc_frame_stats bytes
+    contrib_sum: "torch.Tensor | None" = None
+    contrib_max: "torch.Tensor | None" = None
+    survivors: "torch.Tensor | None" = None
+
+
+class Renderer:
+    """Renders frames of one ComposedScene on one GPU."""
+
+    def __init__(self, scene: ComposedScene, device=None):
+        self.scene = scene
+        self.dscene = DeviceScene(scene, device)
+        self.workspaces: dict[tuple[int, int], Workspace] = {}
+
+    def workspace(self, cam) -> Workspace:
+        key = (int(cam.width), int(cam.height))
+        if key not in self.workspaces:
+            self.workspaces[key] = Workspace(self.dscene, *key)
+        return self.workspaces[key]
+
+    def render_device(self, cam, opts: RenderOptions | None = None, out: DeviceFrame | None = None,
+                      return_survivors: bool = False) -> DeviceFrame:
+        """Enqueue one frame on the current stream; no host synchronisation."""
+        import torch
+
+        opts = opts or RenderOptions()
+        lib = nat.load()
+        ws = self.workspace(cam)
+        dev = self.dscene.device
+        h, w = int(cam.height), int(cam.width)
+        if out is None or out.image.shape != (h, w, 3):
+            out = DeviceFrame(torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                              torch.empty((h, w), dtype=torch.float32, device=dev),
+                              torch.empty(nat.STATS_BYTES, dtype=torch.uint8, device=dev))
+        if opts.record_contributions:
+            if out.contrib_sum is None or out.contrib_sum.shape != (h, w):
+                out.contrib_sum = torch.empty((h, w), dtype=torch.float32, device=dev)
+            if out.contrib_max is None or out.contrib_max.numel() != ws.cap_s:
+                out.contrib_max = torch.empty(ws.cap_s, dtype=torch.float32, device=dev)
+        if return_survivors and (out.survivors is None or out.survivors.shape[0] != ws.cap_s):
+            out.survivors = torch.empty((ws.cap_s, 2), dtype=torch.int32, device=dev)
+        fo = nat.ScFrameOut()
+        fo.image, fo.trans, fo.stats = nat.ptr(out.image), nat.ptr(out.trans), nat.ptr(out.stats_raw)
+        fo.contrib_sum = nat.ptr(out.contrib_sum) if opts.record_contributions else 0
+        fo.contrib_max = nat.ptr(out.contrib_max) if opts.record_contributions else 0
+        fo.survivors = nat.ptr(out.survivors) if return_survivors else 0
+        camc = nat.camera_struct(cam)
+        optc = opts.struct(cam)
+        nat.check(lib.sc_render_composed(ctypes.byref(self.dscene.struct), ctypes.byref(camc), ctypes.byref(optc),
+                                         ctypes.byref(ws.struct), ctypes.byref(fo), nat.stream_handle()),
+                  "sc_render_composed")
+        return out
+
+    def render(self, cam, opts: RenderOptions | None = None, return_survivors: bool = False,
+               to_host: bool = True):
+        """One frame -> (RenderOutput, FrameStats); regrows the workspace on overflow."""
+        import torch
+
+        from .raster import RenderOutput
+
+        opts = opts or RenderOptions()
+        for _attempt in range(4):
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            frame = self.render_device(cam, opts, return_survivors=return_survivors)
+            ev1.record()
+            st = nat.stats_dict(frame.stats_raw.cpu().numpy())
+            if not st["overflow"]:
+                break
+            self.workspace(cam).grow(st["survivors"], st["entries"])
+        else:
+            raise nat.NativeError("workspace overflow persists after regrowing")
+        render_ms = float(ev0.elapsed_time(ev1))
+        n_s = st["survivors"]
+        payload = self._payload_bytes_per_survivor(n_s, frame, return_survivors)
+        stats = FrameStats(frustum_passed=st["frustum_passed"], mlp_culled=st["mlp_culled"], instantiated=n_s,
+                           used=st["used"] if opts.record_contributions else None,
+                           mem_bytes_instantiated=payload, render_ms=render_ms, mlp_ms=float("nan"),
+                           preprocess_ms=float("nan"), mlp_queried=st["mlp_queried"],
+                           instances_visible=st["instances_visible"], pairs_tested=st["pairs_tested"],
+                           passed=st["passed"], skipped=st["skipped"], entries=st["entries"],
+                           max_tie_run=st["max_tie_run"])
+        if not to_host:
+            return frame, stats
+        out = RenderOutput(
+            image=frame.image.cpu().numpy(),
+            final_transmittance=frame.trans.cpu().numpy(),
+            contribution_max=frame.contrib_max[:n_s].cpu().numpy() if opts.record_contributions else None,
+            contribution_sum=frame.contrib_sum.cpu().numpy() if opts.record_contributions else None,
+            used_count=st["used"] if opts.record_contributions else None,
+            passed_count=st["passed"], skipped_count=st["skipped"])
+        if return_survivors:
+            out.survivors = frame.survivors[:n_s].cpu().numpy().astype(np.int64)
+        return out, stats
+
+    def _payload_bytes_per_survivor(self, n_s, frame, have_surv):
+        # instantiated x per-gaussian Asset payload (56 B at SH degree 0)
+        pb = self.dscene.payload_bytes
+        if len(set(pb)) == 1:
+            return int(n_s) * pb[0]
+        if have_surv and frame.survivors is not None:
+            inst = frame.survivors[:n_s, 0].cpu().numpy()
+            per = np.array(pb)[self.dscene.inst_asset[inst]]
+            return int(per.sum())
+        return int(n_s) * int(np.mean(pb))
+
+
+def render_composed(scene: ComposedScene, cam, opts: RenderOptions | None = None, **kw):
+    """-> (RenderOutput, FrameStats).  The device scene is cached on ``scene``."""
+    r = scene._device
+    if r is None or r.dscene.scene_version != scene._version:
+        r = Renderer(scene)
+        scene._device = r
+    if kw:
+        opts = RenderOptions(**kw) if opts is None else opts
+    return r.render(cam, opts)
+
+
+def local_inputs(g_index: int, asset: Asset, inst: InstanceTransform, cam, model: VisibilityModel,
+                 features: np.ndarray | None = None) -> np.ndarray:
+    """The 16 visibility-MLP inputs of one (gaussian, instance) pair, host f64.
+
+    [mean / r (3), local direction camera->gaussian (3), normalised corrected
+    distance (1), local camera forward (3), feature (6)].  Inspection helper;
+    the device builds the same vector inside the fused cull kernel.
+    """
+    R, _q, s, _ln = instance_frame(inst)
+    Rm = np.array(R).reshape(3, 3)
+    m = asset.means[g_index].astype(np.float64)
+    mw = np.array([np.float32(s * (Rm[k, 0] * m[0] + Rm[k, 1] * m[1] + Rm[k, 2] * m[2]) + inst.translation[k])
+                   for k in range(3)], dtype=np.float64)
+    d = mw - cam.position
+    d_r = math.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2])
+    corr = (model.f_train / cam.focal) / s
+    d_t = d_r * corr
+    x = np.empty(16)
+    x[0:3] = m / model.mean_scale
+    x[3:6] = Rm.T @ d / d_r
+    x[6] = min(1.0, max(-1.0, 2.0 * (d_t - model.d_near) / (model.d_far - model.d_near) - 1.0))
+    x[7:10] = Rm.T @ cam.rotation[2]
+    if features is None:
+        features = model.feature_mlp.forward_host(feature_inputs(asset, model.mean_scale)[g_index:g_index + 1])[0]
+    x[10:16] = np.asarray(features, dtype=np.float64)[:6]
+    return x

@@ -1,0 +1,278 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tolerances:
+  * projection depth / mean2d / radius / tile rect / valid: bit-exact
+    (f64, no FMA); conic: rtol 1e-12 (CUDA exp vs glibc exp ulp);
+  * (depth, index) order, entry_idx, tile offsets: bit-exact;
+  * image (fp32 device blend vs f64 oracle, same entries): max-abs <= 5e-3,
+    uncapped PSNR >= 80 dB;
+  * MLP decisions: equal except where |logit_ref| < LOGIT_MARGIN (fp16 inputs
+    and weights, fp32 accumulate);
+  * whole pipeline with each side's own survivors: PSNR >= 45 dB.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import raster_ref as rr
+from oracle import scene_ref as sr
+
+pytestmark = pytest.mark.gpu
+
+IMG_MAX_ABS = 5e-3
+IMG_PSNR = 80.0
+LOGIT_MARGIN = 0.01
+
+
+def _single_scene(asset):
+    from paper_2511_19202_b200.scene import ComposedScene, DeviceScene, InstanceTransform
+
+    sc = ComposedScene()
+    sc.add_asset(asset)
+    sc.add_instance(0, InstanceTransform())
+    return sc, DeviceScene(sc)
+
+
+def _opts(**kw):
+    from paper_2511_19202_b200.scene import RenderOptions
+
+    o = RenderOptions(use_mlp=False, frustum="off")
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def test_projection_bit_exact(golden):
+    from paper_2511_19202_b200 import stages
+
+    name, asset, cam, opts, z = golden
+    _sc, ds = _single_scene(asset)
+    n = len(asset)
+    p = stages.project(ds, np.zeros(n, np.int64), np.arange(n), cam, _opts(**opts))
+    np.testing.assert_array_equal(p["depth"], z["depth"])
+    vz = z["depth"] > cam.near
+    np.testing.assert_array_equal(p["mean2d"][vz], z["mean2d"][vz])
+    np.testing.assert_array_equal(p["radius"], z["radius"])
+    np.testing.assert_allclose(p["conic"], z["conic"], rtol=1e-12, atol=0)
+    np.testing.assert_array_equal(p["valid"], z["valid"])
+    passed = p["passed"]
+    ref_passed = np.zeros(n, bool)
+    ref_passed[z["order_idx"]] = True
+    np.testing.assert_array_equal(passed, ref_passed)
+    for k, key in enumerate(("tx0", "tx1", "ty0", "ty1")):
+        np.testing.assert_array_equal(p["rect"][passed, k], z[key][passed], err_msg=key)
+    assert p["stats"]["skipped"] == int(z["n_skipped"])
+
+
+def test_bin_sort_bit_exact(golden):
+    from paper_2511_19202_b200 import stages
+
+    name, asset, cam, opts, z = golden
+    _sc, ds = _single_scene(asset)
+    n = len(asset)
+    b = stages.bin_sort(ds, np.zeros(n, np.int64), np.arange(n), cam, _opts(**opts))
+    np.testing.assert_array_equal(b["order_idx"], z["order_idx"])
+    np.testing.assert_array_equal(b["entry_idx"], z["entry_idx"])
+    np.testing.assert_array_equal(b["counts"], z["counts"])
+    assert b["stats"]["entries"] == z["entry_idx"].size
+
+
+def _image_close(img, ref):
+    d = np.abs(np.asarray(img, np.float64) - ref)
+    mse = float((d ** 2).mean())
+    p = math.inf if mse == 0 else -10 * math.log10(mse)
+    assert d.max() <= IMG_MAX_ABS, f"max-abs {d.max()}"
+    assert p >= IMG_PSNR, f"PSNR {p}"
+    return d.max(), p
+
+
+def test_blend_with_reference_entries(golden):
+    from paper_2511_19202_b200 import stages
+
+    name, asset, cam, opts, z = golden
+    _sc, ds = _single_scene(asset)
+    n = len(asset)
+    o = _opts(**opts)
+    p = stages.project(ds, np.zeros(n, np.int64), np.arange(n), cam, o)
+    res = stages.blend(p["splats"], z["entry_idx"], z["counts"], cam, o, n_splats=n)
+    _image_close(res["image"], z["image"])
+    _image_close(res["trans"], z["final_transmittance"])
+    if opts.get("record_contributions"):
+        np.testing.assert_allclose(res["contrib_max"], z["contribution_max"], atol=IMG_MAX_ABS)
+
+
+def test_render_dropin_vs_reference(golden):
+    import paper_2511_19202_b200 as sc
+
+    name, asset, cam, opts, z = golden
+    out = sc.render(asset, cam, **opts)
+    _image_close(out.image, z["image"])
+    _image_close(out.final_transmittance, z["final_transmittance"])
+    assert out.passed_count == int(z["passed_count"])
+    assert out.skipped_count == int(z["skipped_count"])
+    if opts.get("record_contributions"):
+        np.testing.assert_allclose(out.contribution_max, z["contribution_max"], atol=IMG_MAX_ABS)
+        assert abs(out.used_count - int(z["used_count"])) <= max(2, int(0.002 * len(asset)))
+
+
+def test_mlp_forward_vs_f64():
+    from paper_2511_19202_b200 import nn, synth
+    from paper_2511_19202_b200.asset import prepare
+    from paper_2511_19202_b200.workloads import calibrated_model
+
+    a = prepare(synth.make_shell(500, seed=3))
+    m = calibrated_model(a, seed=3)
+    x = np.random.default_rng(0).uniform(-1, 1, size=(200_003, 16)).astype(np.float32)
+    got = nn.forward(m, x)[:, 0]
+    ref = sr.mlp_forward(m.vis_mlp, x.astype(np.float64))[:, 0]
+    diff = np.abs(got - ref)
+    flips = (got >= 0) != (ref >= 0)
+    assert np.all(np.abs(ref[flips]) < LOGIT_MARGIN), f"decision flip at |logit| {np.abs(ref[flips]).max()}"
+    assert diff.max() < 0.05, diff.max()
+    assert 0.5 < (ref >= 0).mean() < 0.8
+
+
+def _oracle_tables(scene):
+    return sr.SceneTables(scene)
+
+
+def _multi_scene(with_model):
+    from paper_2511_19202_b200 import synth
+    from paper_2511_19202_b200.asset import prepare
+    from paper_2511_19202_b200.scene import ComposedScene, InstanceTransform
+    from paper_2511_19202_b200.workloads import calibrated_model, random_unit_quats
+
+    rng = np.random.default_rng(7)
+    sc = ComposedScene()
+    a0 = prepare(synth.make_shell(3000, seed=1))
+    a1 = prepare(synth.make_random_cloud(2000, seed=2))
+    sc.add_asset(a0, calibrated_model(a0, 1) if with_model else None)
+    sc.add_asset(a1, calibrated_model(a1, 2) if with_model else None)
+    q = random_unit_quats(rng, 7)
+    for k in range(4):
+        sc.add_instance(0, InstanceTransform([3.0 * k - 4.5, 0.5 * k, 0.2], q[k], 0.7 + 0.3 * k))
+    for k in range(3):
+        sc.add_instance(1, InstanceTransform([3.0 * k - 3.0, 3.0, -0.5], q[4 + k], 1.5 - 0.3 * k))
+    return sc
+
+
+CAMS = [([0.0, -14.0, 4.0], [0, 1.0, 0], 45, 320, 240), ([-2.0, -4.0, 1.0], [0, 2.0, 0], 70, 200, 150),
+        ([9.0, 6.0, 2.0], [0, 1.0, 0], 40, 256, 256)]
+
+
+@pytest.mark.parametrize("cam_i", range(len(CAMS)))
+@pytest.mark.parametrize("frustum", ["margin", "strict"])
+def test_cull_bit_exact_without_model(cam_i, frustum):
+    from paper_2511_19202_b200 import stages
+    from paper_2511_19202_b200.scene import DeviceScene, RenderOptions
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=False)
+    cam = look_at(*CAMS[cam_i])
+    ds = DeviceScene(sc)
+    surv, st = stages.cull_mlp(ds, cam, RenderOptions(frustum=frustum))
+    c = sr.cull(_oracle_tables(sc), cam, frustum=frustum)
+    s = surv.cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(s[:, 0], c.surv_inst)
+    np.testing.assert_array_equal(s[:, 1], c.surv_gid)
+    assert st["frustum_passed"] == int(np.count_nonzero(c.flags & 1))
+
+
+@pytest.mark.parametrize("cam_i", range(len(CAMS)))
+def test_cull_mlp_decisions(cam_i):
+    from paper_2511_19202_b200 import stages
+    from paper_2511_19202_b200.scene import DeviceScene, RenderOptions
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    cam = look_at(*CAMS[cam_i])
+    ds = DeviceScene(sc)
+    surv, st = stages.cull_mlp(ds, cam, RenderOptions())
+    c = sr.cull(_oracle_tables(sc), cam)
+    gpu = np.zeros(c.keep.size, bool)
+    s = surv.cpu().numpy().astype(np.int64)
+    flat = sr.SceneTables(sc).pair_offset[s[:, 0]] + s[:, 1]
+    gpu[flat] = True
+    # survivors stay in flat order
+    assert np.all(np.diff(flat) > 0)
+    ref = c.keep.astype(bool)
+    bad = np.flatnonzero(gpu != ref)
+    if bad.size:
+        assert np.all(c.flags[bad] & 2), "non-MLP decision differs"
+        assert np.abs(c.logit[bad]).max() < LOGIT_MARGIN, np.abs(c.logit[bad]).max()
+    assert st["mlp_queried"] == int(np.count_nonzero(c.flags & 2))
+    assert st["frustum_passed"] == int(np.count_nonzero(c.flags & 1))
+
+
+@pytest.mark.parametrize("cam_i", range(len(CAMS)))
+def test_composed_pipeline_vs_oracle(cam_i):
+    import paper_2511_19202_b200 as pkg
+    from paper_2511_19202_b200 import stages
+    from paper_2511_19202_b200.scene import DeviceScene, RenderOptions
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    cam = look_at(*CAMS[cam_i])
+    ref = sr.render_composed(sc, cam)
+    out, stats = pkg.render_composed(sc, cam)
+    d = np.abs(out.image - ref.out.image)
+    assert rr.psnr(out.image, ref.out.image, cap=None) >= 45.0
+    assert stats.frustum_passed == ref.stats["frustum_passed"]
+    # identical survivors injected -> order/bins bit-exact, image within blend tolerance
+    ds = DeviceScene(sc)
+    b = stages.bin_sort(ds, ref.cull.surv_inst, ref.cull.surv_gid, cam, RenderOptions())
+    np.testing.assert_array_equal(b["order_idx"], ref.stages.order_idx)
+    np.testing.assert_array_equal(b["entry_idx"], ref.stages.entry_idx)
+    np.testing.assert_array_equal(b["counts"], ref.stages.counts)
+    res = stages.blend(b["splats"], b["entry_idx"], b["counts"], cam, RenderOptions(),
+                       n_splats=len(ref.cull.surv_inst))
+    _image_close(res["image"], ref.out.image)
+    assert d.max() <= 1.0
+
+
+def test_zero_culling_equivalence():
+    """no models -> instanced render == flattened render, bit for bit."""
+    import paper_2511_19202_b200 as pkg
+    from paper_2511_19202_b200.asset import Asset
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=False)
+    cam = look_at(*CAMS[0])
+    out, _ = pkg.render_composed(sc, cam)
+    tabs = sr.SceneTables(sc)
+    n_pairs = int(tabs.pair_offset[-1])
+    counts = np.diff(tabs.pair_offset)
+    inst = np.repeat(np.arange(len(counts)), counts)
+    gid = np.arange(n_pairs) - np.repeat(tabs.pair_offset[:-1], counts)
+    m, ls, q, op, sh, deg = sr.instantiate(tabs, cam, inst, gid)
+    flat = Asset(m, ls, q, op, sh, deg)
+    ref = pkg.render(flat, cam)
+    np.testing.assert_array_equal(out.image, ref.image)
+    np.testing.assert_array_equal(out.final_transmittance, ref.final_transmittance)
+
+
+def test_deterministic():
+    import paper_2511_19202_b200 as pkg
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    cam = look_at(*CAMS[2])
+    a, _ = pkg.render_composed(sc, cam)
+    b, _ = pkg.render_composed(sc, cam)
+    np.testing.assert_array_equal(a.image, b.image)
+
+
+def test_config1_vs_oracle():
+    """BASELINE config 1: 10K cloud, 1 instance, random-init MLP, 256^2."""
+    import paper_2511_19202_b200 as pkg
+    from paper_2511_19202_b200.workloads import config1
+
+    wl = config1()
+    cam = wl.cameras[0]
+    ref = sr.render_composed(wl.scene, cam)
+    out, stats = pkg.render_composed(wl.scene, cam)
+    assert stats.frustum_passed == ref.stats["frustum_passed"]
+    assert abs(stats.mlp_culled - ref.stats["mlp_culled"]) <= max(3, int(1e-3 * stats.mlp_queried))
+    assert rr.psnr(out.image, ref.out.image, cap=None) >= 45.0

@@ -487,15 +487,23 @@ class Renderer:
         return int(n_s) * int(np.mean(pb))
 
 
-def render_composed(scene: ComposedScene, cam, opts: RenderOptions | None = None, **kw):
-    """-> (RenderOutput, FrameStats).  The device scene is cached on ``scene``."""
+def render_composed(scene: ComposedScene, cam, opts: RenderOptions | None = None, *,
+                    return_survivors: bool = False, **kw):
+    """-> (RenderOutput, FrameStats).  The device scene is cached on ``scene``.
+
+    Keyword options (``record_contributions=...``, ``frustum=...`` ...) build a
+    RenderOptions when ``opts`` is not given.  ``return_survivors`` adds
+    ``out.survivors`` (S, 2) [flat instance index, gaussian index].
+    """
     r = scene._device
     if r is None or r.dscene.scene_version != scene._version:
         r = Renderer(scene)
         scene._device = r
     if kw:
-        opts = RenderOptions(**kw) if opts is None else opts
-    return r.render(cam, opts)
+        if opts is not None:
+            raise ValueError("pass either opts or keyword options, not both")
+        opts = RenderOptions(**kw)
+    return r.render(cam, opts, return_survivors=return_survivors)
 
 
 def local_inputs(g_index: int, asset: Asset, inst: InstanceTransform, cam, model: VisibilityModel,

@@ -192,7 +192,15 @@ typedef struct sc_frame_out {
     float *contrib_max;          /* [cap_survivors] f32 or NULL (record mode) */
     sc_frame_stats *stats;       /* device */
     sc_survivor *survivors;      /* optional device copy-out [cap_survivors] or NULL */
+    /* optional stage timing: cudaEvent_t handles (host array), recorded on the
+     * stream at [0] frame start, [1] after cull+MLP, [2] after projection,
+     * [3] after sort/binning, [4] after blend.  NULL to skip. */
+    void *const *stage_events;
+    int32_t n_stage_events;
+    int32_t reserved0;
 } sc_frame_out;
+
+#define SC_STAGE_EVENTS 5
 
 typedef struct sc_workspace {
     void *base;                  /* device, sc_workspace_bytes() bytes */

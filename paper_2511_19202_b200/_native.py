@@ -80,7 +80,11 @@ class ScSplat(ctypes.Structure):
 
 class ScFrameOut(ctypes.Structure):
     _fields_ = [("image", P), ("trans", P), ("contrib_sum", P), ("contrib_max", P), ("stats", P),
-                ("survivors", P)]
+                ("survivors", P), ("stage_events", P), ("n_stage_events", c_i32), ("reserved0", c_i32)]
+
+
+N_STAGE_EVENTS = 5
+STAGE_NAMES = ("cull_mlp", "project", "sort_bin", "blend")
 
 
 class ScWorkspace(ctypes.Structure):

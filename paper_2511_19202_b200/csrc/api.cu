@@ -215,7 +215,7 @@ static int run_bin(const sc_scene *scene, const sc_survivor *surv, const unsigne
                    uint32_t **order, uint32_t **entries, cudaStream_t st)
 {
     SC_TRY(sc::launch_project(*scene, surv, n_dev, n_max, *cam, *opts, splats, w.key_a, w.val_a, w.depth64, w.rect,
-                              nullptr, nullptr, nullptr, stats, &w.ctr->passed, st),
+                              nullptr, nullptr, nullptr, stats, w.ctr, st),
            "project");
     SC_TRY(sc::launch_bin(w, n_dev, n_max, *cam, stats, order, entries, st), "bin/sort");
     return SC_OK;
@@ -272,16 +272,28 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
     if ((rc = carve(ws, cam->width, cam->height, w))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     sc_frame_stats *stats = out->stats;
+    auto mark = [&](int i) -> cudaError_t {
+        if (out->stage_events && i < out->n_stage_events && out->stage_events[i])
+            return cudaEventRecord(static_cast<cudaEvent_t>(out->stage_events[i]), st);
+        return cudaSuccess;
+    };
+    SC_TRY(mark(0), "event");
     SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
     SC_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(sc::Counters), st), "memset counters");
     SC_TRY(sc::launch_prep(*scene, *cam, *opts, w, stats, st), "prep");
     SC_TRY(sc::launch_cull(*scene, *cam, *opts, w, w.surv, w.capS, stats, st), "cull");
+    SC_TRY(mark(1), "event");
+    SC_TRY(sc::launch_project(*scene, w.surv, &w.ctr->survivors, w.capS, *cam, *opts, w.splats, w.key_a, w.val_a,
+                              w.depth64, w.rect, nullptr, nullptr, nullptr, stats, w.ctr, st),
+           "project");
+    SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;
-    if ((rc = run_bin(scene, w.surv, &w.ctr->survivors, w.capS, cam, opts, w, w.splats, stats, &order, &entries, st)))
-        return rc;
+    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, stats, &order, &entries, st), "bin/sort");
+    SC_TRY(mark(3), "event");
     if (opts->record_contributions && w.capS > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
     SC_TRY(sc::launch_blend(w.splats, entries, w.tile_off, *cam, *opts, *out, w.capS, st), "blend");
+    SC_TRY(mark(4), "event");
     if (opts->record_contributions)
         SC_TRY(sc::launch_count_used(out->contrib_max, &w.ctr->survivors, w.capS, stats, st), "count used");
     if (out->survivors && w.capS > 0)

@@ -2,30 +2,45 @@
 //
 // Reference: composite_tiles (sc/_kernels.py:190-275) + finish()
 // (sc/raster.py:267-282).  One CTA per 16x16 tile, one thread per pixel,
-// each warp owning an 8x4 pixel block.  Splat records of the tile's entries
-// are staged through shared memory in batches of 256 (one coalesced 48-byte
-// record per thread); each warp then ballots the batch against its pixel
-// block so it only walks the entries whose exact f64 pixel window
-// (sc_splat.win, computed by the projection) touches it.  Pixels retire
-// after compositing once T < stop_transmittance (A8 step 7), warps stop when
-// all 32 pixels retired and the CTA stops loading batches when every warp
-// has.  Arithmetic is fp32 (tolerance stated in tests/test_gpu_parity.py).
+// each warp owning an 8x4 pixel block (lane = 8 * row + col).
+//
+// Entries are staged through shared memory in batches of 256, double
+// buffered: the records of batch i+1 are gathered into registers while
+// batch i is blended, so the HBM/L2 gather latency hides behind the math.
+// Each warp then ballots the batch 32 entries at a time: an entry is walked
+// only if its exact f64 pixel window (sc_splat.win, from the projection)
+// intersects the warp's ALIVE pixels (32-bit mask vs the window's 8x4
+// footprint), so saturated pixels cost nothing even while a silhouette pixel
+// of the same warp keeps the warp busy.  Pixels retire after compositing
+// once T < stop_transmittance (A8 step 7); warps stop when all 32 retired
+// and the CTA stops when every warp has.  fp32 arithmetic (tolerance stated
+// in tests/test_gpu_parity.py).
 #include <algorithm>
 
 #include "common.cuh"
 
 namespace sc {
 
-constexpr int kBatch = 256;
+constexpr int kBatch = kBlendThreads;
 
-struct __align__(16) BlendBatch {
-    float mx[kBatch], my[kBatch];
-    float ha[kBatch], b[kBatch], hc[kBatch];
-    float op[kBatch], pmin[kBatch];
-    float r[kBatch], g[kBatch], bl[kBatch];
-    short4 win[kBatch];
+struct __align__(16) BlendBuf {
+    float4 geo[kBatch];   // mx, my, 0.5 a, b
+    float4 pho[kBatch];   // 0.5 c, opacity, p_min, r
+    float2 gb[kBatch];    // g, b
+    short4 win[kBatch];   // x0, x1, y0, y1 (inclusive, absolute pixels)
     uint32_t idx[kBatch];
 };
+
+// 32-bit footprint of window w on the 8x4 block at (bx0, by0)
+__device__ __forceinline__ uint32_t block_mask(short4 w, int bx0, int by0)
+{
+    const int lo = max((int)w.x, bx0), hi = min((int)w.y, bx0 + 7);
+    const int rlo = max((int)w.z, by0), rhi = min((int)w.w, by0 + 3);
+    if (lo > hi || rlo > rhi) return 0u;
+    const uint32_t cols = (0xFFu >> (7 - (hi - bx0))) & (0xFFu << (lo - bx0));
+    const uint32_t rows = (0x01010101u << (8 * (rlo - by0))) & (0x01010101u >> (8 * (3 - (rhi - by0))));
+    return cols * rows;
+}
 
 __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
                                                          const uint32_t *__restrict__ entry_idx,
@@ -34,7 +49,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restr
                                                          int record, float *image, float *trans, float *csum,
                                                          float *cmax)
 {
-    __shared__ BlendBatch sb;
+    __shared__ BlendBuf sb[2];
     const int tile = blockIdx.x;
     const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -47,56 +62,64 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restr
     bool warp_done = __all_sync(0xffffffffu, done);
     const uint32_t start = tile_off[tile], end = tile_off[tile + 1];
 
-    for (uint32_t base = start; base < end; base += kBatch) {
-        if (__syncthreads_and(warp_done)) break;
+    // register staging of one batch (this thread's entry)
+    float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra;
+    uint32_t rs = 0;
+    bool rv = false;
+    auto fetch = [&](uint32_t base) {
         const uint32_t e = base + tid;
-        if (e < end) {
-            uint32_t s = entry_idx[e];
+        rv = e < end;
+        if (rv) {
+            uint32_t s = __ldg(entry_idx + e);
             if ((int64_t)s >= n_splats) s = 0;   // only reachable on workspace overflow
             const float4 *src = reinterpret_cast<const float4 *>(splats + s);
-            const float4 a = __ldg(src), c = __ldg(src + 1), d = __ldg(src + 2);
-            sb.mx[tid] = a.x;
-            sb.my[tid] = a.y;
-            sb.ha[tid] = a.z;
-            sb.b[tid] = a.w;
-            sb.hc[tid] = c.x;
-            sb.op[tid] = c.y;
-            sb.pmin[tid] = c.z;
-            sb.r[tid] = c.w;
-            sb.g[tid] = d.x;
-            sb.bl[tid] = d.y;
-            const uint32_t w01 = __float_as_uint(d.z), w23 = __float_as_uint(d.w);
-            sb.win[tid] = make_short4((short)(w01 & 0xFFFF), (short)(w01 >> 16), (short)(w23 & 0xFFFF),
-                                      (short)(w23 >> 16));
-            sb.idx[tid] = s;
-        } else {
-            sb.win[tid] = make_short4(1, 0, 1, 0);
+            ra = __ldg(src);
+            rb = __ldg(src + 1);
+            rc = __ldg(src + 2);
+            rs = s;
         }
-        __syncthreads();
-        const int nb = (int)std::min<uint32_t>(kBatch, end - base);
+    };
+    fetch(start);
+    int buf = 0;
+    for (uint32_t base = start; base < end; base += kBatch) {
+        BlendBuf &B = sb[buf];
+        B.geo[tid] = ra;
+        B.pho[tid] = rb;
+        B.gb[tid] = make_float2(rc.x, rc.y);
+        if (rv) {
+            const uint32_t w01 = __float_as_uint(rc.z), w23 = __float_as_uint(rc.w);
+            B.win[tid] = make_short4((short)(w01 & 0xFFFF), (short)(w01 >> 16), (short)(w23 & 0xFFFF),
+                                     (short)(w23 >> 16));
+        } else {
+            B.win[tid] = make_short4(1, 0, 1, 0);
+        }
+        B.idx[tid] = rs;
+        if (__syncthreads_and(warp_done)) break;
+        if (base + kBatch < end) fetch(base + kBatch);   // overlaps the blending below
+        const int nb = (int)min((uint32_t)kBatch, end - base);
         if (!warp_done) {
             for (int k0 = 0; k0 < nb; k0 += 32) {
+                const uint32_t alive = __ballot_sync(0xffffffffu, !done);
                 const int jj = k0 + lane;
-                bool hit = false;
-                if (jj < nb) {
-                    const short4 w = sb.win[jj];
-                    hit = w.x <= bx0 + 7 && w.y >= bx0 && w.z <= by0 + 3 && w.w >= by0;
-                }
+                const bool hit = jj < nb && (block_mask(B.win[jj], bx0, by0) & alive) != 0u;
                 uint32_t m = __ballot_sync(0xffffffffu, hit);
                 while (m) {
                     const int j = k0 + __ffs(m) - 1;
                     m &= m - 1;
-                    const short4 w = sb.win[j];
+                    const short4 w = B.win[j];
                     float contrib = 0.0f;
                     if (!done && px >= w.x && px <= w.y && py >= w.z && py <= w.w) {
-                        const float dx = fpx - sb.mx[j], dy = fpy - sb.my[j];
-                        const float power = -(sb.ha[j] * dx * dx + sb.hc[j] * dy * dy) - sb.b[j] * dx * dy;
-                        if (!(power > 0.0f || power < sb.pmin[j])) {
-                            const float alpha = fminf(0.99f, sb.op[j] * __expf(power));
+                        const float4 g = B.geo[j];
+                        const float4 p = B.pho[j];
+                        const float dx = fpx - g.x, dy = fpy - g.y;
+                        const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
+                        if (!(power > 0.0f || power < p.z)) {
+                            const float alpha = fminf(0.99f, p.y * __expf(power));
+                            const float2 c2 = B.gb[j];
                             contrib = alpha * T;
-                            cr += contrib * sb.r[j];
-                            cg += contrib * sb.g[j];
-                            cb += contrib * sb.bl[j];
+                            cr += contrib * p.w;
+                            cg += contrib * c2.x;
+                            cb += contrib * c2.y;
                             T = T * (1.0f - alpha);
                             if (T < stop_t) done = true;
                         }
@@ -106,14 +129,14 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restr
                         float mxc = contrib;
                         for (int o = 16; o > 0; o >>= 1) mxc = fmaxf(mxc, __shfl_xor_sync(0xffffffffu, mxc, o));
                         if (lane == 0 && mxc > 0.0f)
-                            atomicMax(reinterpret_cast<int *>(cmax) + sb.idx[j], __float_as_int(mxc));
+                            atomicMax(reinterpret_cast<int *>(cmax) + B.idx[j], __float_as_int(mxc));
                     }
                 }
                 warp_done = __all_sync(0xffffffffu, done);
                 if (warp_done) break;
             }
         }
-        __syncthreads();
+        buf ^= 1;
     }
     if (inside) {
         const int64_t p = (int64_t)py * width + px;

@@ -37,7 +37,8 @@ struct Counters {
     unsigned long long passed;
     unsigned long long entries;
     unsigned long long entries_eff;    // entries, or 0 when they overflow the workspace
-    unsigned long long pad[2];
+    unsigned long long dmin_inv;       // ~bits(min passed depth)  (atomicMax of ~bits; 0 = none)
+    unsigned long long dmax;           // bits(max passed depth)   (positive doubles order as u64)
 };
 
 // Workspace carve-out (all offsets 256-byte aligned), see api.cu:carve().
@@ -133,8 +134,8 @@ cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_op
 cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
                            uint32_t *keys, uint32_t *vals, double *depth64, ushort4 *rect, double *dbg_f64,
-                           int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats,
-                           unsigned long long *passed_ctr, cudaStream_t st);
+                           int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr,
+                           cudaStream_t st);
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
                        sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out, cudaStream_t st);
 cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,

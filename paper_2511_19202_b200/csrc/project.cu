@@ -31,14 +31,14 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
                                                  sc_opts opts, sc_splat *splats, uint32_t *keys, uint32_t *vals,
                                                  double *depth64, ushort4 *rect, double *dbg_f64, int32_t *dbg_rect,
                                                  uint8_t *dbg_flags, sc_frame_stats *stats,
-                                                 unsigned long long *passed_ctr)
+                                                 Counters *ctr)
 {
     const int64_t n = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
     const double lim_x = 1.3 * cam.tan_x, lim_y = 1.3 * cam.tan_y;
     const double focal = cam.focal;
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const double log_min_alpha = log(1.0 / 255.0);
-    unsigned long long n_passed = 0, n_skipped = 0;
+    unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0;
 
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
         const sc_survivor sv = surv[k];
@@ -133,6 +133,11 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
             passed = tx1 > tx0 && ty1 > ty0;
         }
         n_passed += passed;
+        if (passed) {
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(tz);
+            dmin_inv = max(dmin_inv, ~bits);
+            dmax_bits = max(dmax_bits, bits);
+        }
 
         // --- colour (sc/raster.py:198-226) and opacity (sc/asset.py:44-51) ---
         int deg = as.sh_degree;
@@ -204,9 +209,7 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
         }
         splats[k] = sp;
         if (keys) {
-            keys[k] = passed ? float_key((float)tz) : 0xFFFFFFFFu;
-            vals[k] = (uint32_t)k;
-            depth64[k] = tz;
+            depth64[k] = passed ? tz : -1.0;   // sort keys are quantised in k_depth_keys
             rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0,
                                    (unsigned short)ty1);
         }
@@ -222,11 +225,17 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
     for (int o = 16; o > 0; o >>= 1) {
         n_passed += __shfl_down_sync(0xffffffffu, n_passed, o);
         n_skipped += __shfl_down_sync(0xffffffffu, n_skipped, o);
+        dmin_inv = max(dmin_inv, __shfl_down_sync(0xffffffffu, dmin_inv, o));
+        dmax_bits = max(dmax_bits, __shfl_down_sync(0xffffffffu, dmax_bits, o));
     }
     if ((threadIdx.x & 31) == 0) {
         if (n_passed) {
             atomicAdd((unsigned long long *)&stats->passed, n_passed);
-            if (passed_ctr) atomicAdd(passed_ctr, n_passed);
+            if (ctr) {
+                atomicAdd(&ctr->passed, n_passed);
+                atomicMax(&ctr->dmin_inv, dmin_inv);
+                atomicMax(&ctr->dmax, dmax_bits);
+            }
         }
         if (n_skipped) atomicAdd((unsigned long long *)&stats->skipped, n_skipped);
     }
@@ -235,8 +244,8 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
 cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
                            uint32_t *keys, uint32_t *vals, double *depth64, ushort4 *rect, double *dbg_f64,
-                           int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats,
-                           unsigned long long *passed_ctr, cudaStream_t st)
+                           int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr,
+                           cudaStream_t st)
 {
     if (n_max <= 0) return cudaSuccess;
     int dev = 0, nsm = 148;
@@ -244,7 +253,7 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 8);
     SC_LAUNCH(k_project, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, keys, vals, depth64,
-              rect, dbg_f64, dbg_rect, dbg_flags, stats, passed_ctr);
+              rect, dbg_f64, dbg_rect, dbg_flags, stats, ctr);
     return cudaGetLastError();
 }
 

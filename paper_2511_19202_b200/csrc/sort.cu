@@ -270,7 +270,30 @@ static cudaError_t radix_sort(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// tie-fix: equal f32 keys -> order by (f64 depth, survivor index)
+// depth keys: frame-adaptive 32-bit quantisation of the f64 depth over the
+// passed splats' [dmin, dmax] (monotone non-decreasing, so key order agrees
+// with f64 order wherever keys differ; equal keys go to the tie-fix).  Much
+// finer than an f32 key over the same range, so ties are rare.
+// ---------------------------------------------------------------------------
+__global__ void k_depth_keys(const double *depth64, const unsigned long long *n_dev, int64_t n_host,
+                             const Counters *ctr, uint32_t *keys, uint32_t *vals)
+{
+    const int64_t n = dev_count(n_dev, n_host);
+    const double dmin = __longlong_as_double((long long)~ctr->dmin_inv);
+    const double dmax = __longlong_as_double((long long)ctr->dmax);
+    constexpr double kTop = 4294967040.0;   // < 0xFFFFFFFF, which marks non-passed splats
+    const double scale = (ctr->passed > 0 && dmax > dmin) ? kTop / (dmax - dmin) : 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double d = depth64[k];
+        uint32_t key = 0xFFFFFFFFu;
+        if (d >= 0.0) key = (uint32_t)fmin(floor((d - dmin) * scale), kTop);
+        keys[k] = key;
+        vals[k] = (uint32_t)k;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tie-fix: equal keys -> order by (f64 depth, survivor index)
 // ---------------------------------------------------------------------------
 __global__ void k_tiefix(const uint32_t *keys, uint32_t *vals, const double *depth64, const unsigned long long *n_dev,
                         int64_t n_host, sc_frame_stats *stats)
@@ -368,6 +391,7 @@ cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_
 {
     cudaError_t e;
     uint32_t *keys_s = nullptr, *order = nullptr;
+    SC_LAUNCH(k_depth_keys, grid_for(n_max, 256), 256, 0, st, ws.depth64, n_dev, n_max, ws.ctr, ws.key_a, ws.val_a);
     e = radix_sort(ws.key_a, ws.val_a, ws.key_b, ws.val_b, n_dev, n_max, 32, ws.hist, ws.scan_part, &keys_s, &order,
                    st);
     if (e != cudaSuccess) return e;

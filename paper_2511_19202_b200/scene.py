@@ -400,8 +400,13 @@ class Renderer:
         return self.workspaces[key]
 
     def render_device(self, cam, opts: RenderOptions | None = None, out: DeviceFrame | None = None,
-                      return_survivors: bool = False) -> DeviceFrame:
-        """Enqueue one frame on the current stream; no host synchronisation."""
+                      return_survivors: bool = False, stage_events=None) -> DeviceFrame:
+        """Enqueue one frame on the current stream; no host synchronisation.
+
+        ``stage_events``: optional 5 timing-enabled torch.cuda.Event objects,
+        recorded by the library at the stage boundaries (frame start, after
+        cull+MLP, projection, sort/binning, blend).
+        """
         import torch
 
         opts = opts or RenderOptions()
@@ -425,6 +430,15 @@ class Renderer:
         fo.contrib_sum = nat.ptr(out.contrib_sum) if opts.record_contributions else 0
         fo.contrib_max = nat.ptr(out.contrib_max) if opts.record_contributions else 0
         fo.survivors = nat.ptr(out.survivors) if return_survivors else 0
+        if stage_events is not None:
+            handles = (ctypes.c_void_p * nat.N_STAGE_EVENTS)()
+            for i, ev in enumerate(stage_events[:nat.N_STAGE_EVENTS]):
+                if not ev.cuda_event:
+                    ev.record()            # torch creates the CUDA event lazily
+                handles[i] = ev.cuda_event
+            fo.stage_events = ctypes.cast(handles, ctypes.c_void_p)
+            fo.n_stage_events = nat.N_STAGE_EVENTS
+            self._event_handles = handles  # keep alive until the call returns
         camc = nat.camera_struct(cam)
         optc = opts.struct(cam)
         nat.check(lib.sc_render_composed(ctypes.byref(self.dscene.struct), ctypes.byref(camc), ctypes.byref(optc),

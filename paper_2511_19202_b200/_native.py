@@ -16,6 +16,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsplatcull_b200.so")
+if os.environ.get("SPLATCULL_B200_DEBUG_LIB"):       # instrumented build (scripts/blend_stats.py only)
+    LIB_PATH = os.path.join(_HERE, "libsplatcull_b200_dbg.so")
 
 SC_OK = 0
 SC_FRUSTUM_MARGIN, SC_FRUSTUM_STRICT, SC_FRUSTUM_OFF = 0, 1, 2

@@ -23,6 +23,13 @@ namespace sc {
 
 constexpr int kBatch = kBlendThreads;
 
+#ifdef SC_BLEND_STATS
+// instrumented build only (libsplatcull_b200_dbg.so): per tile
+// [entries, batches walked, (entry, warp) hits, pixel evaluations, cycles, 0, 0, 0]
+constexpr int kDbgTiles = 32400;
+__device__ unsigned long long g_blend_dbg[kDbgTiles * 8];
+#endif
+
 struct __align__(16) BlendBuf {
     float4 geo[kBatch];   // mx, my, 0.5 a, b
     float4 pho[kBatch];   // 0.5 c, opacity, p_min, r
@@ -81,7 +88,14 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restr
     };
     fetch(start);
     int buf = 0;
+#ifdef SC_BLEND_STATS
+    unsigned long long d_batches = 0, d_hits = 0, d_evals = 0;
+    const long long d_t0 = clock64();
+#endif
     for (uint32_t base = start; base < end; base += kBatch) {
+#ifdef SC_BLEND_STATS
+        d_batches++;
+#endif
         BlendBuf &B = sb[buf];
         B.geo[tid] = ra;
         B.pho[tid] = rb;
@@ -108,6 +122,10 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restr
                     m &= m - 1;
                     const short4 w = B.win[j];
                     float contrib = 0.0f;
+#ifdef SC_BLEND_STATS
+                    d_hits += (lane == 0);
+                    d_evals += (!done && px >= w.x && px <= w.y && py >= w.z && py <= w.w);
+#endif
                     if (!done && px >= w.x && px <= w.y && py >= w.z && py <= w.w) {
                         const float4 g = B.geo[j];
                         const float4 p = B.pho[j];
@@ -138,6 +156,24 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restr
         }
         buf ^= 1;
     }
+#ifdef SC_BLEND_STATS
+    for (int o = 16; o > 0; o >>= 1) {
+        d_hits += __shfl_down_sync(0xffffffffu, d_hits, o);
+        d_evals += __shfl_down_sync(0xffffffffu, d_evals, o);
+    }
+    if (tile < kDbgTiles) {
+        unsigned long long *dd = g_blend_dbg + 8 * (size_t)tile;
+        if (lane == 0) {
+            atomicAdd(dd + 2, d_hits);
+            atomicAdd(dd + 3, d_evals);
+        }
+        if (tid == 0) {
+            dd[0] = end - start;
+            dd[1] = d_batches;
+            dd[4] = (unsigned long long)(clock64() - d_t0);
+        }
+    }
+#endif
     if (inside) {
         const int64_t p = (int64_t)py * width + px;
         image[3 * p + 0] = cr + T * bg_r;
@@ -183,3 +219,15 @@ cudaError_t launch_count_used(const float *cmax, const unsigned long long *n_dev
 }
 
 }  // namespace sc
+
+#ifdef SC_BLEND_STATS
+extern "C" __attribute__((visibility("default"))) int sc_debug_blend_stats(unsigned long long *host, int64_t n_tiles,
+                                                                            int reset)
+{
+    const size_t bytes = sizeof(unsigned long long) * 8 * (size_t)std::min<int64_t>(n_tiles, sc::kDbgTiles);
+    if (reset) return (int)cudaMemset(sc::g_blend_dbg, 0, sizeof(sc::g_blend_dbg)) == 0 ? 0 : 2;
+    void *p = nullptr;
+    if (cudaGetSymbolAddress(&p, sc::g_blend_dbg) != cudaSuccess) return 2;
+    return cudaMemcpy(host, p, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
+}
+#endif

@@ -1,143 +1,160 @@
 // Stage (e): per-tile front-to-back alpha blending.
 //
 // Reference: composite_tiles (sc/_kernels.py:190-275) + finish()
-// (sc/raster.py:267-282).  One CTA per 16x16 tile, one thread per pixel,
-// each warp owning an 8x4 pixel block (lane = 8 * row + col).
+// (sc/raster.py:267-282).  Semantics per pixel are the reference's: walk the
+// tile's entries in (depth, index) order, skip splats with alpha0 < 1/255,
+// composite inside the splat's exact f64 pixel window when
+// p_min <= power <= 0, alpha = min(0.99, alpha0 e^power), retire the pixel
+// after compositing once T < stop_transmittance.  fp32 arithmetic
+// (tolerance stated in tests/test_gpu_parity.py).
 //
-// Entries are staged through shared memory in batches of 256, double
-// buffered: the records of batch i+1 are gathered into registers while
-// batch i is blended, so the HBM/L2 gather latency hides behind the math.
-// Each warp then ballots the batch 32 entries at a time: an entry is walked
-// only if its exact f64 pixel window (sc_splat.win, from the projection)
-// intersects the warp's ALIVE pixels (32-bit mask vs the window's 8x4
-// footprint), so saturated pixels cost nothing even while a silhouette pixel
-// of the same warp keeps the warp busy.  Pixels retire after compositing
-// once T < stop_transmittance (A8 step 7); warps stop when all 32 retired
-// and the CTA stops when every warp has.  fp32 arithmetic (tolerance stated
-// in tests/test_gpu_parity.py).
+// B200 mapping — every warp is an independent worker with no CTA barrier:
+//   * a warp owns an 8x4 pixel block (lane = 8 row + col) of one 16x16 tile;
+//     a CTA is 4 warps = half a tile, and CTAs are dispatched heaviest tile
+//     first (LPT order by log2 entry count, k_tile_order) so the long
+//     silhouette tiles of a 100M-Gaussian frame start at once instead of
+//     forming the tail;
+//   * the warp walks its tile's entry list 128 entries at a time: entry
+//     indices (coalesced) and the 8-byte pixel windows (gather) of the NEXT
+//     128 are prefetched into registers while the current 128 are blended;
+//   * an entry is processed only when its window intersects the warp's ALIVE
+//     pixels (32-bit footprint mask vs ballot of live lanes), so saturated
+//     pixels cost nothing; the lanes that hit load their entry's 48-byte
+//     record and the warp broadcasts each hit's fields with shuffles;
+//   * a warp exits when its 32 pixels have retired.
+// The first version staged 256-entry batches in shared memory behind a CTA
+// barrier; ncu showed the barrier stall dominating (warps with silhouette
+// pixels held the other seven) and one SM busy for the whole kernel.
 #include <algorithm>
 
 #include "common.cuh"
 
 namespace sc {
 
-constexpr int kBatch = kBlendThreads;
-
 #ifdef SC_BLEND_STATS
 // instrumented build only (libsplatcull_b200_dbg.so): per tile
-// [entries, batches walked, (entry, warp) hits, pixel evaluations, cycles, 0, 0, 0]
+// [entries, entry slots walked, (entry, warp) hits, pixel evaluations, max warp cycles, 0, 0, 0]
 constexpr int kDbgTiles = 32400;
 __device__ unsigned long long g_blend_dbg[kDbgTiles * 8];
 #endif
 
-struct __align__(16) BlendBuf {
-    float4 geo[kBatch];   // mx, my, 0.5 a, b
-    float4 pho[kBatch];   // 0.5 c, opacity, p_min, r
-    float2 gb[kBatch];    // g, b
-    short4 win[kBatch];   // x0, x1, y0, y1 (inclusive, absolute pixels)
-    uint32_t idx[kBatch];
-};
+constexpr int kBlendWarps = 4;              // warps per CTA (half a tile)
+constexpr int kSlots = 4;                   // 32-entry slots per prefetch group
 
 // 32-bit footprint of window w on the 8x4 block at (bx0, by0)
-__device__ __forceinline__ uint32_t block_mask(short4 w, int bx0, int by0)
+__device__ __forceinline__ uint32_t block_mask(int x0, int x1, int y0, int y1, int bx0, int by0)
 {
-    const int lo = max((int)w.x, bx0), hi = min((int)w.y, bx0 + 7);
-    const int rlo = max((int)w.z, by0), rhi = min((int)w.w, by0 + 3);
+    const int lo = max(x0, bx0), hi = min(x1, bx0 + 7);
+    const int rlo = max(y0, by0), rhi = min(y1, by0 + 3);
     if (lo > hi || rlo > rhi) return 0u;
     const uint32_t cols = (0xFFu >> (7 - (hi - bx0))) & (0xFFu << (lo - bx0));
     const uint32_t rows = (0x01010101u << (8 * (rlo - by0))) & (0x01010101u >> (8 * (3 - (rhi - by0))));
     return cols * rows;
 }
 
-__global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
-                                                         const uint32_t *__restrict__ entry_idx,
-                                                         const uint32_t *__restrict__ tile_off, int width, int height,
-                                                         int n_tx, float stop_t, float bg_r, float bg_g, float bg_b,
-                                                         int record, float *image, float *trans, float *csum,
-                                                         float *cmax)
+__device__ __forceinline__ int lo16(uint32_t w) { return (int)(int16_t)(w & 0xFFFFu); }
+__device__ __forceinline__ int hi16(uint32_t w) { return (int)(int16_t)(w >> 16); }
+
+__global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
+                                                            const uint32_t *__restrict__ entry_idx,
+                                                            const uint32_t *__restrict__ tile_off,
+                                                            const uint32_t *__restrict__ task_order, int width,
+                                                            int height, int n_tx, float stop_t, float bg_r,
+                                                            float bg_g, float bg_b, int record, float *image,
+                                                            float *trans, float *csum, float *cmax)
 {
-    __shared__ BlendBuf sb[2];
-    const int tile = blockIdx.x;
+    const uint32_t task = task_order ? task_order[blockIdx.x] : blockIdx.x;
+    const int tile = (int)(task >> 1), half = (int)(task & 1);
     const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int bx0 = txi * kTile + (wid & 1) * 8, by0 = tyi * kTile + (wid >> 1) * 4;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int bx0 = txi * kTile + (wid & 1) * 8, by0 = tyi * kTile + half * 8 + (wid >> 1) * 4;
     const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
     const bool inside = px < width && py < height;
     const float fpx = (float)px, fpy = (float)py;
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cs = 0.0f;
     bool done = !inside;
-    bool warp_done = __all_sync(0xffffffffu, done);
     const uint32_t start = tile_off[tile], end = tile_off[tile + 1];
-
-    // register staging of one batch (this thread's entry)
-    float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra, rc = ra;
-    uint32_t rs = 0;
-    bool rv = false;
-    auto fetch = [&](uint32_t base) {
-        const uint32_t e = base + tid;
-        rv = e < end;
-        if (rv) {
-            uint32_t s = __ldg(entry_idx + e);
-            if ((int64_t)s >= n_splats) s = 0;   // only reachable on workspace overflow
-            const float4 *src = reinterpret_cast<const float4 *>(splats + s);
-            ra = __ldg(src);
-            rb = __ldg(src + 1);
-            rc = __ldg(src + 2);
-            rs = s;
-        }
-    };
-    fetch(start);
-    int buf = 0;
+    const char *rec = reinterpret_cast<const char *>(splats);
 #ifdef SC_BLEND_STATS
-    unsigned long long d_batches = 0, d_hits = 0, d_evals = 0;
+    unsigned long long d_slots = 0, d_hits = 0, d_evals = 0;
     const long long d_t0 = clock64();
 #endif
-    for (uint32_t base = start; base < end; base += kBatch) {
-#ifdef SC_BLEND_STATS
-        d_batches++;
-#endif
-        BlendBuf &B = sb[buf];
-        B.geo[tid] = ra;
-        B.pho[tid] = rb;
-        B.gb[tid] = make_float2(rc.x, rc.y);
-        if (rv) {
-            const uint32_t w01 = __float_as_uint(rc.z), w23 = __float_as_uint(rc.w);
-            B.win[tid] = make_short4((short)(w01 & 0xFFFF), (short)(w01 >> 16), (short)(w23 & 0xFFFF),
-                                     (short)(w23 >> 16));
-        } else {
-            B.win[tid] = make_short4(1, 0, 1, 0);
+
+    uint32_t idx[kSlots], wx[kSlots], wy[kSlots];   // current group (per lane: entries base + 32 k + lane)
+    uint32_t nidx[kSlots], nwx[kSlots], nwy[kSlots];
+    auto prefetch = [&](uint32_t base, uint32_t *pi, uint32_t *px_, uint32_t *py_) {
+#pragma unroll
+        for (int k = 0; k < kSlots; k++) {
+            const uint32_t e = base + 32u * k + lane;
+            uint32_t s = 0xFFFFFFFFu;
+            if (e < end) {
+                s = __ldg(entry_idx + e);
+                if ((int64_t)s >= n_splats) s = 0xFFFFFFFFu;   // only reachable on workspace overflow
+            }
+            pi[k] = s;
         }
-        B.idx[tid] = rs;
-        if (__syncthreads_and(warp_done)) break;
-        if (base + kBatch < end) fetch(base + kBatch);   // overlaps the blending below
-        const int nb = (int)min((uint32_t)kBatch, end - base);
-        if (!warp_done) {
-            for (int k0 = 0; k0 < nb; k0 += 32) {
+#pragma unroll
+        for (int k = 0; k < kSlots; k++) {
+            uint2 w = make_uint2(0x00000001u, 0x00000001u);   // empty window (x0=1 > x1=0)
+            if (pi[k] != 0xFFFFFFFFu) w = __ldg(reinterpret_cast<const uint2 *>(rec + 48 * (size_t)pi[k] + 40));
+            px_[k] = w.x;
+            py_[k] = w.y;
+        }
+    };
+
+    if (!__all_sync(0xffffffffu, done) && start < end) {
+        prefetch(start, idx, wx, wy);
+        for (uint32_t base = start; base < end; base += 32u * kSlots) {
+            const bool more = base + 32u * kSlots < end;
+            if (more) prefetch(base + 32u * kSlots, nidx, nwx, nwy);
+#pragma unroll
+            for (int k = 0; k < kSlots; k++) {
                 const uint32_t alive = __ballot_sync(0xffffffffu, !done);
-                const int jj = k0 + lane;
-                const bool hit = jj < nb && (block_mask(B.win[jj], bx0, by0) & alive) != 0u;
+                if (!alive) break;
+                const bool hit = (block_mask(lo16(wx[k]), hi16(wx[k]), lo16(wy[k]), hi16(wy[k]), bx0, by0) & alive) != 0u;
                 uint32_t m = __ballot_sync(0xffffffffu, hit);
+#ifdef SC_BLEND_STATS
+                d_slots++;
+#endif
+                if (!m) continue;
+                float4 ga = make_float4(0.f, 0.f, 0.f, 0.f), pa = ga;
+                float2 gb2 = make_float2(0.f, 0.f);
+                if (hit) {
+                    const float4 *src = reinterpret_cast<const float4 *>(rec + 48 * (size_t)idx[k]);
+                    ga = __ldg(src);
+                    pa = __ldg(src + 1);
+                    gb2 = __ldg(reinterpret_cast<const float2 *>(src + 2));
+                }
                 while (m) {
-                    const int j = k0 + __ffs(m) - 1;
+                    const int srcl = __ffs(m) - 1;
                     m &= m - 1;
-                    const short4 w = B.win[j];
+                    const uint32_t swx = __shfl_sync(0xffffffffu, wx[k], srcl);
+                    const uint32_t swy = __shfl_sync(0xffffffffu, wy[k], srcl);
+                    const float mx = __shfl_sync(0xffffffffu, ga.x, srcl);
+                    const float my = __shfl_sync(0xffffffffu, ga.y, srcl);
+                    const float ha = __shfl_sync(0xffffffffu, ga.z, srcl);
+                    const float hb = __shfl_sync(0xffffffffu, ga.w, srcl);
+                    const float hc = __shfl_sync(0xffffffffu, pa.x, srcl);
+                    const float op = __shfl_sync(0xffffffffu, pa.y, srcl);
+                    const float pmin = __shfl_sync(0xffffffffu, pa.z, srcl);
+                    const float c0 = __shfl_sync(0xffffffffu, pa.w, srcl);
+                    const float c1 = __shfl_sync(0xffffffffu, gb2.x, srcl);
+                    const float c2 = __shfl_sync(0xffffffffu, gb2.y, srcl);
                     float contrib = 0.0f;
+                    const bool in_win = px >= lo16(swx) && px <= hi16(swx) && py >= lo16(swy) && py <= hi16(swy);
 #ifdef SC_BLEND_STATS
                     d_hits += (lane == 0);
-                    d_evals += (!done && px >= w.x && px <= w.y && py >= w.z && py <= w.w);
+                    d_evals += (!done && in_win);
 #endif
-                    if (!done && px >= w.x && px <= w.y && py >= w.z && py <= w.w) {
-                        const float4 g = B.geo[j];
-                        const float4 p = B.pho[j];
-                        const float dx = fpx - g.x, dy = fpy - g.y;
-                        const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
-                        if (!(power > 0.0f || power < p.z)) {
-                            const float alpha = fminf(0.99f, p.y * __expf(power));
-                            const float2 c2 = B.gb[j];
+                    if (!done && in_win) {
+                        const float dx = fpx - mx, dy = fpy - my;
+                        const float power = -(ha * dx * dx + hc * dy * dy) - hb * dx * dy;
+                        if (!(power > 0.0f || power < pmin)) {
+                            const float alpha = fminf(0.99f, op * __expf(power));
                             contrib = alpha * T;
-                            cr += contrib * p.w;
-                            cg += contrib * c2.x;
-                            cb += contrib * c2.y;
+                            cr += contrib * c0;
+                            cg += contrib * c1;
+                            cb += contrib * c2;
                             T = T * (1.0f - alpha);
                             if (T < stop_t) done = true;
                         }
@@ -146,32 +163,29 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restr
                         cs += contrib;
                         float mxc = contrib;
                         for (int o = 16; o > 0; o >>= 1) mxc = fmaxf(mxc, __shfl_xor_sync(0xffffffffu, mxc, o));
-                        if (lane == 0 && mxc > 0.0f)
-                            atomicMax(reinterpret_cast<int *>(cmax) + B.idx[j], __float_as_int(mxc));
+                        const uint32_t sidx = __shfl_sync(0xffffffffu, idx[k], srcl);
+                        if (lane == 0 && mxc > 0.0f) atomicMax(reinterpret_cast<int *>(cmax) + sidx, __float_as_int(mxc));
                     }
                 }
-                warp_done = __all_sync(0xffffffffu, done);
-                if (warp_done) break;
+            }
+            if (__all_sync(0xffffffffu, done) || !more) break;
+#pragma unroll
+            for (int k = 0; k < kSlots; k++) {
+                idx[k] = nidx[k];
+                wx[k] = nwx[k];
+                wy[k] = nwy[k];
             }
         }
-        buf ^= 1;
     }
 #ifdef SC_BLEND_STATS
-    for (int o = 16; o > 0; o >>= 1) {
-        d_hits += __shfl_down_sync(0xffffffffu, d_hits, o);
-        d_evals += __shfl_down_sync(0xffffffffu, d_evals, o);
-    }
-    if (tile < kDbgTiles) {
+    for (int o = 16; o > 0; o >>= 1) d_evals += __shfl_down_sync(0xffffffffu, d_evals, o);
+    if (tile < kDbgTiles && lane == 0) {
         unsigned long long *dd = g_blend_dbg + 8 * (size_t)tile;
-        if (lane == 0) {
-            atomicAdd(dd + 2, d_hits);
-            atomicAdd(dd + 3, d_evals);
-        }
-        if (tid == 0) {
-            dd[0] = end - start;
-            dd[1] = d_batches;
-            dd[4] = (unsigned long long)(clock64() - d_t0);
-        }
+        dd[0] = end - start;
+        atomicAdd(dd + 1, d_slots);
+        atomicAdd(dd + 2, d_hits);
+        atomicAdd(dd + 3, d_evals);
+        atomicMax(dd + 4, (unsigned long long)(clock64() - d_t0));
     }
 #endif
     if (inside) {
@@ -181,6 +195,34 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(const sc_splat *__restr
         image[3 * p + 2] = cb + T * bg_b;
         trans[p] = T;
         if (record && csum) csum[p] = cs;
+    }
+}
+
+// LPT dispatch order: half-tile tasks of heavier tiles first (bucketed by
+// floor(log2(entries)); order inside a bucket is irrelevant to the result).
+__global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *tile_off, int64_t n_tiles, uint32_t *order)
+{
+    __shared__ uint32_t hist[33], base[33];
+    if (threadIdx.x < 33) hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint32_t c = tile_off[t + 1] - tile_off[t];
+        atomicAdd(&hist[c ? 32 - __clz(c) : 0], 2u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 32; b >= 0; b--) {
+            base[b] = run;
+            run += hist[b];
+        }
+    }
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+        const uint32_t c = tile_off[t + 1] - tile_off[t];
+        const uint32_t pos = atomicAdd(&base[c ? 32 - __clz(c) : 0], 2u);
+        order[pos] = (uint32_t)(2 * t);
+        order[pos + 1] = (uint32_t)(2 * t + 1);
     }
 }
 
@@ -197,11 +239,13 @@ __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev,
 
 cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
                          const sc_camera &cam, const sc_opts &opts, const sc_frame_out &out, int64_t n_splats,
-                         cudaStream_t st)
+                         uint32_t *task_order, cudaStream_t st)
 {
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
-    SC_LAUNCH(k_blend, n_tx * n_ty, kBlendThreads, 0, st, splats, n_splats, entry_idx, tile_off, cam.width,
-              cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
+    const int64_t n_tiles = (int64_t)n_tx * n_ty;
+    if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, tile_off, n_tiles, task_order);
+    SC_LAUNCH(k_blend, (int)(2 * n_tiles), kBlendWarps * 32, 0, st, splats, n_splats, entry_idx, tile_off, task_order,
+              cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
               (float)opts.background[1], (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image,
               out.trans, out.contrib_sum, out.contrib_max);
     return cudaGetLastError();
@@ -224,10 +268,10 @@ cudaError_t launch_count_used(const float *cmax, const unsigned long long *n_dev
 extern "C" __attribute__((visibility("default"))) int sc_debug_blend_stats(unsigned long long *host, int64_t n_tiles,
                                                                             int reset)
 {
-    const size_t bytes = sizeof(unsigned long long) * 8 * (size_t)std::min<int64_t>(n_tiles, sc::kDbgTiles);
-    if (reset) return (int)cudaMemset(sc::g_blend_dbg, 0, sizeof(sc::g_blend_dbg)) == 0 ? 0 : 2;
     void *p = nullptr;
     if (cudaGetSymbolAddress(&p, sc::g_blend_dbg) != cudaSuccess) return 2;
+    if (reset) return cudaMemset(p, 0, sizeof(sc::g_blend_dbg)) == cudaSuccess ? 0 : 2;
+    const size_t bytes = sizeof(unsigned long long) * 8 * (size_t)std::min<int64_t>(n_tiles, sc::kDbgTiles);
     return cudaMemcpy(host, p, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
 #endif

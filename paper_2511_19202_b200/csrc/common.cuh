@@ -56,6 +56,7 @@ struct Ws {
     uint32_t *ekey_a, *ekey_b;       // [capE]
     uint32_t *eval_a, *eval_b;       // [capE]
     uint32_t *tile_off;              // [n_tiles + 1]
+    uint32_t *task_order;            // [2 n_tiles] blend dispatch order (heavy tiles first)
     uint32_t *hist;                  // radix histograms [256 * nblk_max]
     uint32_t *scan_part;             // scan partials
     int64_t capS, capE, max_chunks, nblk_max, n_tiles;
@@ -140,7 +141,7 @@ cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_
                        sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out, cudaStream_t st);
 cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
                          const sc_camera &cam, const sc_opts &opts, const sc_frame_out &out,
-                         int64_t n_splats, cudaStream_t st);
+                         int64_t n_splats, uint32_t *task_order, cudaStream_t st);
 cudaError_t launch_vis_mlp(const sc_vis_weights *w, const float *x, int64_t n, float *logits,
                            cudaStream_t st);
 cudaError_t launch_encode_features(const float *params, const float *x, int64_t n, uint16_t *feat,

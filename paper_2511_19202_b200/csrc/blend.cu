@@ -52,6 +52,19 @@ __device__ __forceinline__ uint32_t block_mask(int x0, int x1, int y0, int y1, i
     return cols * rows;
 }
 
+// 32x32 bit-matrix transpose across a warp: lane r holds row r on entry and
+// column r on exit (bit c of the result = bit r of lane c's input).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane)
+{
+    constexpr uint32_t kMask[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0, j = 16; s < 5; s++, j >>= 1) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~kMask[s]) | ((y >> j) & kMask[s])) : ((x & kMask[s]) | ((y << j) & ~kMask[s]));
+    }
+    return x;
+}
+
 __device__ __forceinline__ int lo16(uint32_t w) { return (int)(int16_t)(w & 0xFFFFu); }
 __device__ __forceinline__ int hi16(uint32_t w) { return (int)(int16_t)(w >> 16); }
 
@@ -111,25 +124,32 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
             for (int k = 0; k < kSlots; k++) {
                 const uint32_t alive = __ballot_sync(0xffffffffu, !done);
                 if (!alive) break;
-                const bool hit = (block_mask(lo16(wx[k]), hi16(wx[k]), lo16(wy[k]), hi16(wy[k]), bx0, by0) & alive) != 0u;
-                uint32_t m = __ballot_sync(0xffffffffu, hit);
+                // footprint of this lane's entry on the warp's alive pixels
+                const uint32_t fp =
+                    block_mask(lo16(wx[k]), hi16(wx[k]), lo16(wy[k]), hi16(wy[k]), bx0, by0) & alive;
 #ifdef SC_BLEND_STATS
                 d_slots++;
 #endif
-                if (!m) continue;
+                if (!__any_sync(0xffffffffu, fp != 0u)) continue;
                 float4 ga = make_float4(0.f, 0.f, 0.f, 0.f), pa = ga;
                 float2 gb2 = make_float2(0.f, 0.f);
-                if (hit) {
+                if (fp) {
                     const float4 *src = reinterpret_cast<const float4 *>(rec + 48 * (size_t)idx[k]);
                     ga = __ldg(src);
                     pa = __ldg(src + 1);
                     gb2 = __ldg(reinterpret_cast<const float2 *>(src + 2));
                 }
-                while (m) {
-                    const int srcl = __ffs(m) - 1;
-                    m &= m - 1;
-                    const uint32_t swx = __shfl_sync(0xffffffffu, wx[k], srcl);
-                    const uint32_t swy = __shfl_sync(0xffffffffu, wy[k], srcl);
+#ifdef SC_BLEND_STATS
+                d_hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
+#endif
+                // 32x32 bit transpose: bit j of `mine` = entry (slot lane) j covers my pixel
+                uint32_t mine = transpose32(fp, lane);
+                // each lane walks its own entries in order; the warp iterates
+                // max-over-lanes times (fields fetched from lane j by shuffle)
+                while (__any_sync(0xffffffffu, mine != 0u)) {
+                    const bool act = mine != 0u;
+                    const int srcl = act ? __ffs(mine) - 1 : lane;
+                    mine &= mine - 1u;
                     const float mx = __shfl_sync(0xffffffffu, ga.x, srcl);
                     const float my = __shfl_sync(0xffffffffu, ga.y, srcl);
                     const float ha = __shfl_sync(0xffffffffu, ga.z, srcl);
@@ -140,31 +160,29 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                     const float c0 = __shfl_sync(0xffffffffu, pa.w, srcl);
                     const float c1 = __shfl_sync(0xffffffffu, gb2.x, srcl);
                     const float c2 = __shfl_sync(0xffffffffu, gb2.y, srcl);
-                    float contrib = 0.0f;
-                    const bool in_win = px >= lo16(swx) && px <= hi16(swx) && py >= lo16(swy) && py <= hi16(swy);
+                    const uint32_t sidx = record ? __shfl_sync(0xffffffffu, idx[k], srcl) : 0u;
 #ifdef SC_BLEND_STATS
-                    d_hits += (lane == 0);
-                    d_evals += (!done && in_win);
+                    d_evals += act;
 #endif
-                    if (!done && in_win) {
+                    if (act) {
                         const float dx = fpx - mx, dy = fpy - my;
                         const float power = -(ha * dx * dx + hc * dy * dy) - hb * dx * dy;
                         if (!(power > 0.0f || power < pmin)) {
                             const float alpha = fminf(0.99f, op * __expf(power));
-                            contrib = alpha * T;
+                            const float contrib = alpha * T;
                             cr += contrib * c0;
                             cg += contrib * c1;
                             cb += contrib * c2;
                             T = T * (1.0f - alpha);
-                            if (T < stop_t) done = true;
+                            if (record) {
+                                cs += contrib;
+                                if (contrib > 0.0f) atomicMax(reinterpret_cast<int *>(cmax) + sidx, __float_as_int(contrib));
+                            }
+                            if (T < stop_t) {
+                                done = true;
+                                mine = 0u;
+                            }
                         }
-                    }
-                    if (record) {
-                        cs += contrib;
-                        float mxc = contrib;
-                        for (int o = 16; o > 0; o >>= 1) mxc = fmaxf(mxc, __shfl_xor_sync(0xffffffffu, mxc, o));
-                        const uint32_t sidx = __shfl_sync(0xffffffffu, idx[k], srcl);
-                        if (lane == 0 && mxc > 0.0f) atomicMax(reinterpret_cast<int *>(cmax) + sidx, __float_as_int(mxc));
                     }
                 }
             }

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     const uint32_t start = tile_off[tile], end = tile_off[tile + 1];
     const char *rec = reinterpret_cast<const char *>(splats);
 #ifdef SC_BLEND_STATS
-    unsigned long long d_slots = 0, d_hits = 0, d_evals = 0;
+    unsigned long long d_slots = 0, d_hits = 0, d_evals = 0, d_iters = 0;
     const long long d_t0 = clock64();
 #endif
 
@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                     const uint32_t sidx = record ? __shfl_sync(0xffffffffu, idx[k], srcl) : 0u;
 #ifdef SC_BLEND_STATS
                     d_evals += act;
+                    d_iters += (lane == 0);
 #endif
                     if (act) {
                         const float dx = fpx - mx, dy = fpy - my;
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
         atomicAdd(dd + 2, d_hits);
         atomicAdd(dd + 3, d_evals);
         atomicMax(dd + 4, (unsigned long long)(clock64() - d_t0));
+        atomicAdd(dd + 5, d_iters);
     }
 #endif
     if (inside) {

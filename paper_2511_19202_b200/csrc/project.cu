@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
         double tx, ty, tz;
         cam_xyz(cam, m0, m1, m2, tx, ty, tz);
         bool valid = false;
-        double mx = 0.0, my = 0.0, ca = 0.0, cb = 0.0, cc = 0.0, radius = 0.0, det = 0.0;
+        double mx = 0.0, my = 0.0, ca = 0.0, cb = 0.0, cc = 0.0, radius = 0.0, det = 0.0, cov_a = 0.0, cov_c = 0.0;
         if (tz > cam.near_) {
             const double txz = tx / tz, tyz = ty / tz;
             const double ctxz = fmin(fmax(txz, -lim_x), lim_x);
@@ -107,6 +107,8 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
             const double c = v0 * j10 + v1 * j11 + v2 * j12 + opts.dilation;
             mx = focal * txz + (double)(cam.width - 1) / 2.0;
             my = focal * tyz + (double)(cam.height - 1) / 2.0;
+            cov_a = a;
+            cov_c = c;
             det = a * c - b * b;
             if (det <= 1e-12) {
                 n_skipped++;
@@ -197,10 +199,18 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
         sp.p_min = (float)(log_min_alpha - log_op);
         for (int ch = 0; ch < 3; ch++) sp.rgb[ch] = (float)clampd(col[ch] + 0.5, 0.0, 1.0);
         if (passed && !(op < 1.0 / 255.0)) {
-            sp.win[0] = clamp16(floor(mx - radius));
-            sp.win[1] = clamp16(floor(mx + radius) + 1.0);
-            sp.win[2] = clamp16(floor(my - radius));
-            sp.win[3] = clamp16(floor(my + radius) + 1.0);
+            // reference pixel window (sc/_kernels.py:224-227), intersected with the
+            // bounding box of the alpha >= 1/255 support {1/2 d^T cov^-1 d <= L},
+            // L = log(op) - log(1/255): |dx| <= sqrt(2 L cov_xx).  Pixels outside the
+            // box fail the reference's `power < p_min` test, so the image is
+            // unchanged; the box is widened by 1e-6 relative + 1e-3 px for safety.
+            const double L = log_op - log_min_alpha;
+            const double ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-6) + 1e-3;
+            const double ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-6) + 1e-3;
+            sp.win[0] = clamp16(fmax(floor(mx - radius), ceil(mx - ex)));
+            sp.win[1] = clamp16(fmin(floor(mx + radius) + 1.0, floor(mx + ex)));
+            sp.win[2] = clamp16(fmax(floor(my - radius), ceil(my - ey)));
+            sp.win[3] = clamp16(fmin(floor(my + radius) + 1.0, floor(my + ey)));
         } else {   // skipped by the blend (reference: `op < min_alpha: continue`)
             sp.win[0] = 1;
             sp.win[1] = 0;

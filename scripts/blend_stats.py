@@ -36,7 +36,9 @@ ent, bat, hits, evals, cyc = (buf[:, i].astype(np.float64) for i in range(5))
 print(st)
 print(f"tiles {n_tiles}, entries {ent.sum():.3e}, batches walked {bat.sum():.3e} "
       f"(full walk {np.ceil(ent / 256).sum():.3e})")
-print(f"warp hits {hits.sum():.3e}  pixel evals {evals.sum():.3e}  lane efficiency {evals.sum() / max(1, 32 * hits.sum()):.3f}")
+iters = buf[:, 5].astype(np.float64)
+print(f"warp hits {hits.sum():.3e}  pixel evals {evals.sum():.3e}  warp iterations {iters.sum():.3e}  "
+      f"lane efficiency {evals.sum() / max(1, 32 * iters.sum()):.3f}")
 order = np.argsort(-cyc)
 print("cycles: total %.3e  max %.3e  p99 %.3e  median(nonempty) %.3e" %
       (cyc.sum(), cyc.max(), np.percentile(cyc, 99), np.median(cyc[ent > 0])))

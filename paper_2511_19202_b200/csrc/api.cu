@@ -219,7 +219,7 @@ static int run_bin(const sc_scene *scene, const sc_survivor *surv, const unsigne
     SC_TRY(sc::launch_project(*scene, surv, n_dev, n_max, *cam, *opts, splats, w.key_a, w.val_a, w.depth64, w.rect,
                               nullptr, nullptr, nullptr, stats, w.ctr, st),
            "project");
-    SC_TRY(sc::launch_bin(w, n_dev, n_max, *cam, stats, order, entries, st), "bin/sort");
+    SC_TRY(sc::launch_bin(w, n_dev, n_max, *cam, splats, stats, order, entries, nullptr, st), "bin/sort");
     return SC_OK;
 }
 
@@ -258,7 +258,8 @@ int sc_blend(const sc_splat *splats, int64_t n_splats, const uint32_t *entry_idx
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (opts->record_contributions && n_splats > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)n_splats, st), "memset contrib_max");
-    SC_TRY(sc::launch_blend(splats, entry_idx, tile_offsets, *cam, *opts, *out, n_splats, nullptr, st), "blend");
+    SC_TRY(sc::launch_blend(splats, entry_idx, tile_offsets, nullptr, *cam, *opts, *out, n_splats, nullptr, st),
+           "blend");
     return SC_OK;
 }
 
@@ -290,11 +291,14 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
            "project");
     SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;
-    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, stats, &order, &entries, st), "bin/sort");
+    uint32_t *ewin[2] = {nullptr, nullptr};
+    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.splats, stats, &order, &entries, ewin, st),
+           "bin/sort");
     SC_TRY(mark(3), "event");
     if (opts->record_contributions && w.capS > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
-    SC_TRY(sc::launch_blend(w.splats, entries, w.tile_off, *cam, *opts, *out, w.capS, w.task_order, st), "blend");
+    SC_TRY(sc::launch_blend(w.splats, entries, w.tile_off, ewin, *cam, *opts, *out, w.capS, w.task_order, st),
+           "blend");
     SC_TRY(mark(4), "event");
     if (opts->record_contributions)
         SC_TRY(sc::launch_count_used(out->contrib_max, &w.ctr->survivors, w.capS, stats, st), "count used");

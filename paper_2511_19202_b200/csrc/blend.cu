@@ -38,7 +38,7 @@ constexpr int kDbgTiles = 32400;
 __device__ unsigned long long g_blend_dbg[kDbgTiles * 8];
 #endif
 
-constexpr int kBlendWarps = 4;              // warps per CTA (half a tile)
+constexpr int kBlendWarps = 8;              // warps per CTA (one 16x16 tile)
 constexpr int kSlots = 4;                   // 32-entry slots per prefetch group
 
 // 32-bit footprint of window w on the 8x4 block at (bx0, by0)
@@ -71,16 +71,17 @@ __device__ __forceinline__ int hi16(uint32_t w) { return (int)(int16_t)(w >> 16)
 __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
                                                             const uint32_t *__restrict__ entry_idx,
                                                             const uint32_t *__restrict__ tile_off,
+                                                            const uint32_t *__restrict__ ewx,
+                                                            const uint32_t *__restrict__ ewy,
                                                             const uint32_t *__restrict__ task_order, int width,
                                                             int height, int n_tx, float stop_t, float bg_r,
                                                             float bg_g, float bg_b, int record, float *image,
                                                             float *trans, float *csum, float *cmax)
 {
-    const uint32_t task = task_order ? task_order[blockIdx.x] : blockIdx.x;
-    const int tile = (int)(task >> 1), half = (int)(task & 1);
+    const int tile = (int)(task_order ? task_order[blockIdx.x] : blockIdx.x);
     const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int bx0 = txi * kTile + (wid & 1) * 8, by0 = tyi * kTile + half * 8 + (wid >> 1) * 4;
+    const int bx0 = txi * kTile + (wid & 1) * 8, by0 = tyi * kTile + (wid >> 1) * 4;
     const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
     const bool inside = px < width && py < height;
     const float fpx = (float)px, fpy = (float)py;
@@ -109,7 +110,14 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
 #pragma unroll
         for (int k = 0; k < kSlots; k++) {
             uint2 w = make_uint2(0x00000001u, 0x00000001u);   // empty window (x0=1 > x1=0)
-            if (pi[k] != 0xFFFFFFFFu) w = __ldg(reinterpret_cast<const uint2 *>(rec + 48 * (size_t)pi[k] + 40));
+            if (pi[k] != 0xFFFFFFFFu) {
+                if (ewx) {   // entry-aligned copy: coalesced, no dependent gather
+                    const uint32_t e = base + 32u * k + lane;
+                    w = make_uint2(__ldg(ewx + e), __ldg(ewy + e));
+                } else {
+                    w = __ldg(reinterpret_cast<const uint2 *>(rec + 48 * (size_t)pi[k] + 40));
+                }
+            }
             px_[k] = w.x;
             py_[k] = w.y;
         }
@@ -218,8 +226,8 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     }
 }
 
-// LPT dispatch order: half-tile tasks of heavier tiles first (bucketed by
-// floor(log2(entries)); order inside a bucket is irrelevant to the result).
+// LPT dispatch order: heavier tiles first (bucketed by floor(log2(entries));
+// the order inside a bucket is irrelevant to the result).
 __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *tile_off, int64_t n_tiles, uint32_t *order)
 {
     __shared__ uint32_t hist[33], base[33];
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *tile_off, i
     __syncthreads();
     for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
         const uint32_t c = tile_off[t + 1] - tile_off[t];
-        atomicAdd(&hist[c ? 32 - __clz(c) : 0], 2u);
+        atomicAdd(&hist[c ? 32 - __clz(c) : 0], 1u);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -240,9 +248,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *tile_off, i
     __syncthreads();
     for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
         const uint32_t c = tile_off[t + 1] - tile_off[t];
-        const uint32_t pos = atomicAdd(&base[c ? 32 - __clz(c) : 0], 2u);
-        order[pos] = (uint32_t)(2 * t);
-        order[pos + 1] = (uint32_t)(2 * t + 1);
+        order[atomicAdd(&base[c ? 32 - __clz(c) : 0], 1u)] = (uint32_t)t;
     }
 }
 
@@ -258,13 +264,14 @@ __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev,
 }
 
 cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
-                         const sc_camera &cam, const sc_opts &opts, const sc_frame_out &out, int64_t n_splats,
-                         uint32_t *task_order, cudaStream_t st)
+                         const uint32_t *const *ewin, const sc_camera &cam, const sc_opts &opts,
+                         const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const int64_t n_tiles = (int64_t)n_tx * n_ty;
     if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, tile_off, n_tiles, task_order);
-    SC_LAUNCH(k_blend, (int)(2 * n_tiles), kBlendWarps * 32, 0, st, splats, n_splats, entry_idx, tile_off, task_order,
+    const uint32_t *ewx = ewin ? ewin[0] : nullptr, *ewy = ewin ? ewin[1] : nullptr;
+    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, 0, st, splats, n_splats, entry_idx, tile_off, ewx, ewy, task_order,
               cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
               (float)opts.background[1], (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image,
               out.trans, out.contrib_sum, out.contrib_max);

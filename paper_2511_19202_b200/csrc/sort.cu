@@ -363,15 +363,24 @@ __global__ void k_entry_emit(const uint32_t *order, const ushort4 *rect, const u
     }
 }
 
-// tile_off[t] = first entry index with tile >= t, for t in [0, n_tiles]
-__global__ void k_tile_offsets(const uint32_t *ekey, const unsigned long long *e_dev, int64_t cap_e, int64_t n_tiles,
-                               uint32_t *tile_off)
+// tile_off[t] = first entry index with tile >= t, for t in [0, n_tiles]; and
+// the entry-aligned copy of each entry's pixel window (ewx = x0 | x1 << 16,
+// ewy = y0 | y1 << 16), gathered once here so the blend's warps stream it
+// coalesced instead of each re-gathering it from the splat records.
+__global__ void k_tile_offsets(const uint32_t *ekey, const uint32_t *eval, const sc_splat *splats,
+                               const unsigned long long *e_dev, int64_t cap_e, int64_t n_tiles, uint32_t *tile_off,
+                               uint32_t *ewx, uint32_t *ewy)
 {
     const int64_t E = std::min<int64_t>((int64_t)*e_dev, cap_e);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= E; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t prev = i > 0 ? (int64_t)ekey[i - 1] : -1;
         const int64_t cur = i < E ? (int64_t)ekey[i] : n_tiles;
         for (int64_t t = prev + 1; t <= cur; t++) tile_off[t] = (uint32_t)i;
+        if (i < E) {
+            const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + eval[i]) + 40));
+            ewx[i] = w.x;
+            ewy[i] = w.y;
+        }
     }
 }
 
@@ -387,7 +396,8 @@ static int grid_for(int64_t n, int threads)
 // from the projection.  Outputs: order (passed survivors by (depth, index)),
 // entries (survivor index per entry, tile-major), ws.tile_off, stats.entries.
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
-                       sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out, cudaStream_t st)
+                       const sc_splat *splats, sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out,
+                       uint32_t **win_out, cudaStream_t st)
 {
     cudaError_t e;
     uint32_t *keys_s = nullptr, *order = nullptr;
@@ -409,10 +419,17 @@ cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_
     e = radix_sort(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, bits, ws.hist,
                    ws.scan_part, &ek, &ev, st);
     if (e != cudaSuccess) return e;
-    SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE, ws.n_tiles,
-              ws.tile_off);
+    // the ping-pong buffers not holding the sorted entries are free: window copy
+    uint32_t *ewx = (ek == ws.ekey_a) ? ws.ekey_b : ws.ekey_a;
+    uint32_t *ewy = (ev == ws.eval_a) ? ws.eval_b : ws.eval_a;
+    SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, ev, splats, &ws.ctr->entries_eff, ws.capE,
+              ws.n_tiles, ws.tile_off, ewx, ewy);
     *order_out = order;
     *entries_out = ev;
+    if (win_out) {
+        win_out[0] = ewx;
+        win_out[1] = ewy;
+    }
     return cudaGetLastError();
 }
 

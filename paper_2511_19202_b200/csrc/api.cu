@@ -291,8 +291,8 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
            "project");
     SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;
-    uint32_t *ewin[2] = {nullptr, nullptr};
-    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.splats, stats, &order, &entries, ewin, st),
+    uint16_t *ewin = nullptr;
+    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.splats, stats, &order, &entries, &ewin, st),
            "bin/sort");
     SC_TRY(mark(3), "event");
     if (opts->record_contributions && w.capS > 0)

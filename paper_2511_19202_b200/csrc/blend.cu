@@ -71,8 +71,7 @@ __device__ __forceinline__ int hi16(uint32_t w) { return (int)(int16_t)(w >> 16)
 __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
                                                             const uint32_t *__restrict__ entry_idx,
                                                             const uint32_t *__restrict__ tile_off,
-                                                            const uint32_t *__restrict__ ewx,
-                                                            const uint32_t *__restrict__ ewy,
+                                                            const uint16_t *__restrict__ ewin,
                                                             const uint32_t *__restrict__ task_order, int width,
                                                             int height, int n_tx, float stop_t, float bg_r,
                                                             float bg_g, float bg_b, int record, float *image,
@@ -81,8 +80,9 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     const int tile = (int)(task_order ? task_order[blockIdx.x] : blockIdx.x);
     const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int bx0 = txi * kTile + (wid & 1) * 8, by0 = tyi * kTile + (wid >> 1) * 4;
-    const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
+    const int ox = txi * kTile, oy = tyi * kTile;              // tile origin
+    const int bx0 = (wid & 1) * 8, by0 = (wid >> 1) * 4;        // warp block, tile-relative
+    const int px = ox + bx0 + (lane & 7), py = oy + by0 + (lane >> 3);
     const bool inside = px < width && py < height;
     const float fpx = (float)px, fpy = (float)py;
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cs = 0.0f;
@@ -94,47 +94,49 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     const long long d_t0 = clock64();
 #endif
 
-    uint32_t idx[kSlots], wx[kSlots], wy[kSlots];   // current group (per lane: entries base + 32 k + lane)
-    uint32_t nidx[kSlots], nwx[kSlots], nwy[kSlots];
-    auto prefetch = [&](uint32_t base, uint32_t *pi, uint32_t *px_, uint32_t *py_) {
+    // per lane, slot k of the current group: entry base + 32 k + lane.
+    // code = tile-relative window x0 | x1 << 4 | y0 << 8 | y1 << 12 (x0 > x1: empty)
+    uint32_t code[kSlots], ncode[kSlots], idx[kSlots], nidx[kSlots];
+    auto prefetch = [&](uint32_t base, uint32_t *pc, uint32_t *pi) {
 #pragma unroll
         for (int k = 0; k < kSlots; k++) {
             const uint32_t e = base + 32u * k + lane;
-            uint32_t s = 0xFFFFFFFFu;
+            pc[k] = 0x000Fu;
+            pi[k] = 0xFFFFFFFFu;
             if (e < end) {
-                s = __ldg(entry_idx + e);
-                if ((int64_t)s >= n_splats) s = 0xFFFFFFFFu;   // only reachable on workspace overflow
-            }
-            pi[k] = s;
-        }
-#pragma unroll
-        for (int k = 0; k < kSlots; k++) {
-            uint2 w = make_uint2(0x00000001u, 0x00000001u);   // empty window (x0=1 > x1=0)
-            if (pi[k] != 0xFFFFFFFFu) {
-                if (ewx) {   // entry-aligned copy: coalesced, no dependent gather
-                    const uint32_t e = base + 32u * k + lane;
-                    w = make_uint2(__ldg(ewx + e), __ldg(ewy + e));
+                if (ewin) {           // entry-aligned stream: 2 bytes, coalesced; index loaded on a hit
+                    pc[k] = __ldg(ewin + e);
                 } else {
-                    w = __ldg(reinterpret_cast<const uint2 *>(rec + 48 * (size_t)pi[k] + 40));
+                    uint32_t s = __ldg(entry_idx + e);
+                    pi[k] = (int64_t)s < n_splats ? s : 0xFFFFFFFFu;
                 }
             }
-            px_[k] = w.x;
-            py_[k] = w.y;
+        }
+        if (!ewin) {
+#pragma unroll
+            for (int k = 0; k < kSlots; k++) {
+                if (pi[k] == 0xFFFFFFFFu) continue;
+                const uint2 w = __ldg(reinterpret_cast<const uint2 *>(rec + 48 * (size_t)pi[k] + 40));
+                const int x0 = max(lo16(w.x) - ox, 0), x1 = min(hi16(w.x) - ox, 15);
+                const int y0 = max(lo16(w.y) - oy, 0), y1 = min(hi16(w.y) - oy, 15);
+                if (x0 <= x1 && y0 <= y1) pc[k] = (uint32_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12));
+            }
         }
     };
 
     if (!__all_sync(0xffffffffu, done) && start < end) {
-        prefetch(start, idx, wx, wy);
+        prefetch(start, code, idx);
         for (uint32_t base = start; base < end; base += 32u * kSlots) {
             const bool more = base + 32u * kSlots < end;
-            if (more) prefetch(base + 32u * kSlots, nidx, nwx, nwy);
+            if (more) prefetch(base + 32u * kSlots, ncode, nidx);
 #pragma unroll
             for (int k = 0; k < kSlots; k++) {
                 const uint32_t alive = __ballot_sync(0xffffffffu, !done);
                 if (!alive) break;
                 // footprint of this lane's entry on the warp's alive pixels
+                const uint32_t c = code[k];
                 const uint32_t fp =
-                    block_mask(lo16(wx[k]), hi16(wx[k]), lo16(wy[k]), hi16(wy[k]), bx0, by0) & alive;
+                    block_mask(c & 15u, (c >> 4) & 15u, (c >> 8) & 15u, c >> 12, bx0, by0) & alive;
 #ifdef SC_BLEND_STATS
                 d_slots++;
 #endif
@@ -142,6 +144,10 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                 float4 ga = make_float4(0.f, 0.f, 0.f, 0.f), pa = ga;
                 float2 gb2 = make_float2(0.f, 0.f);
                 if (fp) {
+                    if (ewin) {
+                        const uint32_t s = __ldg(entry_idx + base + 32u * k + lane);
+                        idx[k] = (int64_t)s < n_splats ? s : 0u;
+                    }
                     const float4 *src = reinterpret_cast<const float4 *>(rec + 48 * (size_t)idx[k]);
                     ga = __ldg(src);
                     pa = __ldg(src + 1);
@@ -199,8 +205,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
 #pragma unroll
             for (int k = 0; k < kSlots; k++) {
                 idx[k] = nidx[k];
-                wx[k] = nwx[k];
-                wy[k] = nwy[k];
+                code[k] = ncode[k];
             }
         }
     }
@@ -264,14 +269,13 @@ __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev,
 }
 
 cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
-                         const uint32_t *const *ewin, const sc_camera &cam, const sc_opts &opts,
+                         const uint16_t *ewin, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const int64_t n_tiles = (int64_t)n_tx * n_ty;
     if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, tile_off, n_tiles, task_order);
-    const uint32_t *ewx = ewin ? ewin[0] : nullptr, *ewy = ewin ? ewin[1] : nullptr;
-    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, 0, st, splats, n_splats, entry_idx, tile_off, ewx, ewy, task_order,
+    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, 0, st, splats, n_splats, entry_idx, tile_off, ewin, task_order,
               cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
               (float)opts.background[1], (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image,
               out.trans, out.contrib_sum, out.contrib_max);

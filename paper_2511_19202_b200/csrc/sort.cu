@@ -169,75 +169,74 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t 
                                                                  int shift, const uint32_t *hist_scanned,
                                                                  int64_t nblk)
 {
+    // Stable local ranking with warp-private digit counters: warp w owns the
+    // contiguous slice [w * 512, (w + 1) * 512) of the block's keys (read 32 at
+    // a time, coalesced), ranks each round with match_any, and keeps running
+    // per-digit counts in its own smem row — no block barrier until the end,
+    // where one per-digit prefix over warps and one scan over digits give every
+    // key its block-local position.  (Index order = warp-major order, so the
+    // ranking is stable.)
+    constexpr int kWarps = kRadixThreads / 32;
+    constexpr int kPerWarp = kRadixTile / kWarps;
     __shared__ uint32_t s_keys[kRadixTile];
     __shared__ uint32_t s_vals[kRadixTile];
-    __shared__ uint32_t s_wcnt[kRadixThreads / 32][256];
+    __shared__ uint32_t s_wcnt[kWarps][256];
     __shared__ uint32_t s_dstart[256];   // block-local start of each digit
     __shared__ uint32_t s_gbase[256];    // global scatter base of each digit
-    __shared__ uint32_t s_run[256];      // running count per digit over rounds
     __shared__ uint32_t s_warp[32];
     const int64_t n = dev_count(n_dev, n_host);
     const int64_t base = (int64_t)blockIdx.x * kRadixTile;
     if (base >= n) return;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int cnt = (int)std::min<int64_t>(kRadixTile, n - base);
+#pragma unroll
+    for (int w = 0; w < kWarps; w++) s_wcnt[w][tid] = 0;
+    s_gbase[tid] = hist_scanned[(int64_t)tid * nblk + blockIdx.x];
 
-    uint32_t k[kRadixItems], v[kRadixItems];
+    uint32_t k[kRadixItems], v[kRadixItems], rk[kRadixItems];
 #pragma unroll
     for (int j = 0; j < kRadixItems; j++) {
-        const int i = j * kRadixThreads + tid;
+        const int i = wid * kPerWarp + j * 32 + lane;
         k[j] = i < cnt ? keys_in[base + i] : 0u;
         v[j] = i < cnt ? vals_in[base + i] : 0u;
     }
-    // block-local digit histogram -> digit starts
-    s_run[tid] = 0;
-    for (int w = 0; w < kRadixThreads / 32; w++) s_wcnt[w][tid] = 0;
     __syncthreads();
+    const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < kRadixItems; j++) {
-        const int i = j * kRadixThreads + tid;
-        if (i < cnt) atomicAdd(&s_run[(k[j] >> shift) & 0xFFu], 1u);
-    }
-    __syncthreads();
-    {
-        uint32_t total;
-        const uint32_t c = s_run[tid];
-        const uint32_t e = block_excl_scan<kRadixThreads>(c, s_warp, total);
-        s_dstart[tid] = e;
-        s_gbase[tid] = hist_scanned[(int64_t)tid * nblk + blockIdx.x];
-        s_run[tid] = 0;
-    }
-    __syncthreads();
-    // stable ranking, one round per 256 consecutive items
-#pragma unroll 1
-    for (int j = 0; j < kRadixItems; j++) {
-        const int i = j * kRadixThreads + tid;
-        const bool ok = i < cnt;
+        const bool ok = wid * kPerWarp + j * 32 + lane < cnt;
         const uint32_t d = ok ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane;   // unique dummy digit
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t rank = __popc(peers & lanemask_lt());
-        if (ok && rank == 0) s_wcnt[wid][d] = __popc(peers);
-        __syncthreads();
-        {   // per digit: exclusive prefix over warps, then advance the running count
-            uint32_t run = s_run[tid];
+        const uint32_t r = __popc(peers & lt);
+        const uint32_t prev = ok ? s_wcnt[wid][d] : 0u;
+        __syncwarp();
+        if (ok && r == 0) s_wcnt[wid][d] = prev + __popc(peers);
+        __syncwarp();
+        rk[j] = prev + r;
+    }
+    __syncthreads();
+    {   // per digit (thread = digit): exclusive prefix over warps, then scan over digits
+        uint32_t run = 0;
 #pragma unroll
-            for (int w = 0; w < kRadixThreads / 32; w++) {
-                const uint32_t c = s_wcnt[w][tid];
-                s_wcnt[w][tid] = run;
-                run += c;
-            }
-            s_run[tid] = run;
+        for (int w = 0; w < kWarps; w++) {
+            const uint32_t c = s_wcnt[w][tid];
+            s_wcnt[w][tid] = run;
+            run += c;
         }
-        __syncthreads();
-        if (ok) {
-            const uint32_t pos = s_dstart[d] + s_wcnt[wid][d] + rank;
+        uint32_t total;
+        s_dstart[tid] = block_excl_scan<kRadixThreads>(run, s_warp, total);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRadixItems; j++) {
+        if (wid * kPerWarp + j * 32 + lane < cnt) {
+            const uint32_t d = (k[j] >> shift) & 0xFFu;
+            const uint32_t pos = s_dstart[d] + s_wcnt[wid][d] + rk[j];
             s_keys[pos] = k[j];
             s_vals[pos] = v[j];
         }
-        __syncthreads();
-        for (int w = 0; w < kRadixThreads / 32; w++) s_wcnt[w][tid] = 0;
-        __syncthreads();
     }
+    __syncthreads();
     // coalesced write-out: consecutive positions of one digit are contiguous in the output
     for (int i = tid; i < cnt; i += kRadixThreads) {
         const uint32_t key = s_keys[i];
@@ -328,17 +327,21 @@ __global__ void k_tiefix(const uint32_t *keys, uint32_t *vals, const double *dep
 // ---------------------------------------------------------------------------
 // entries: per passed splat (depth order) count, scan, emit (tile, survivor)
 // ---------------------------------------------------------------------------
+// The rect of each splat is gathered once here (depth order) and kept
+// contiguous in (rlo, rhi) so the emission pass reads it coalesced.
 __global__ void k_entry_count(const uint32_t *order, const ushort4 *rect, const unsigned long long *n_dev,
-                              int64_t n_host, uint32_t *cnt)
+                              int64_t n_host, uint32_t *cnt, uint32_t *rlo, uint32_t *rhi)
 {
     const int64_t n = dev_count(n_dev, n_host);
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
         const ushort4 r = rect[order[k]];
         cnt[k] = (uint32_t)(r.y - r.x) * (uint32_t)(r.w - r.z);
+        rlo[k] = (uint32_t)r.x | ((uint32_t)r.y << 16);
+        rhi[k] = (uint32_t)r.z | ((uint32_t)r.w << 16);
     }
 }
 
-__global__ void k_entry_emit(const uint32_t *order, const ushort4 *rect, const uint32_t *off,
+__global__ void k_entry_emit(const uint32_t *order, const uint32_t *rlo, const uint32_t *rhi, const uint32_t *off,
                              const unsigned long long *n_dev, int64_t n_host, int n_tx, uint32_t *ekey,
                              uint32_t *eval, const unsigned long long *e_total, unsigned long long *e_eff, int64_t cap_e,
                              sc_frame_stats *stats)
@@ -352,7 +355,8 @@ __global__ void k_entry_emit(const uint32_t *order, const ushort4 *rect, const u
     if (over) return;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t sv = order[k];
-        const ushort4 r = rect[sv];
+        const uint32_t a = rlo[k], b = rhi[k];
+        const ushort4 r = make_ushort4(a & 0xFFFF, a >> 16, b & 0xFFFF, b >> 16);
         uint32_t o = off[k];
         for (int y = r.z; y < r.w; y++)
             for (int x = r.x; x < r.y; x++) {
@@ -364,12 +368,13 @@ __global__ void k_entry_emit(const uint32_t *order, const ushort4 *rect, const u
 }
 
 // tile_off[t] = first entry index with tile >= t, for t in [0, n_tiles]; and
-// the entry-aligned copy of each entry's pixel window (ewx = x0 | x1 << 16,
-// ewy = y0 | y1 << 16), gathered once here so the blend's warps stream it
-// coalesced instead of each re-gathering it from the splat records.
+// each entry's pixel window clipped to its tile, 4 bits per bound
+// (x0 | x1 << 4 | y0 << 8 | y1 << 12, tile-relative; x0 > x1 = empty),
+// gathered once here so the blend's 8 warps per tile stream 2 bytes per
+// entry instead of each re-gathering the window from the splat records.
 __global__ void k_tile_offsets(const uint32_t *ekey, const uint32_t *eval, const sc_splat *splats,
-                               const unsigned long long *e_dev, int64_t cap_e, int64_t n_tiles, uint32_t *tile_off,
-                               uint32_t *ewx, uint32_t *ewy)
+                               const unsigned long long *e_dev, int64_t cap_e, int64_t n_tiles, int n_tx,
+                               uint32_t *tile_off, uint16_t *ewin)
 {
     const int64_t E = std::min<int64_t>((int64_t)*e_dev, cap_e);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= E; i += (int64_t)gridDim.x * blockDim.x) {
@@ -378,8 +383,12 @@ __global__ void k_tile_offsets(const uint32_t *ekey, const uint32_t *eval, const
         for (int64_t t = prev + 1; t <= cur; t++) tile_off[t] = (uint32_t)i;
         if (i < E) {
             const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + eval[i]) + 40));
-            ewx[i] = w.x;
-            ewy[i] = w.y;
+            const int tile = (int)cur, ox = (tile % n_tx) * kTile, oy = (tile / n_tx) * kTile;
+            const int x0 = max((int)(int16_t)(w.x & 0xFFFF) - ox, 0), x1 = min((int)(int16_t)(w.x >> 16) - ox, 15);
+            const int y0 = max((int)(int16_t)(w.y & 0xFFFF) - oy, 0), y1 = min((int)(int16_t)(w.y >> 16) - oy, 15);
+            uint16_t code = 0x000F;   // empty
+            if (x0 <= x1 && y0 <= y1) code = (uint16_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12));
+            ewin[i] = code;
         }
     }
 }
@@ -397,7 +406,7 @@ static int grid_for(int64_t n, int threads)
 // entries (survivor index per entry, tile-major), ws.tile_off, stats.entries.
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
                        const sc_splat *splats, sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out,
-                       uint32_t **win_out, cudaStream_t st)
+                       uint16_t **win_out, cudaStream_t st)
 {
     cudaError_t e;
     uint32_t *keys_s = nullptr, *order = nullptr;
@@ -407,10 +416,12 @@ cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_
     if (e != cudaSuccess) return e;
     const unsigned long long *p_dev = &ws.ctr->passed;   // passed splats lead the sorted order
     SC_LAUNCH(k_tiefix, grid_for(n_max, 256), 256, 0, st, keys_s, order, ws.depth64, p_dev, n_max, stats);
-    SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, ws.ecount);
+    // both key buffers are free once the tie-fix is done: depth-ordered rects
+    uint32_t *rlo = ws.key_a, *rhi = ws.key_b;
+    SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, ws.ecount, rlo, rhi);
     e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, &stats->entries, st);
     if (e != cudaSuccess) return e;
-    SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, ws.rect, ws.ecount, p_dev, n_max, ws.n_tx,
+    SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max, ws.n_tx,
               ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
     int bits = 0;
     while ((1ll << bits) < ws.n_tiles) bits += 8;
@@ -419,17 +430,13 @@ cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_
     e = radix_sort(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, bits, ws.hist,
                    ws.scan_part, &ek, &ev, st);
     if (e != cudaSuccess) return e;
-    // the ping-pong buffers not holding the sorted entries are free: window copy
-    uint32_t *ewx = (ek == ws.ekey_a) ? ws.ekey_b : ws.ekey_a;
-    uint32_t *ewy = (ev == ws.eval_a) ? ws.eval_b : ws.eval_a;
+    // the ping-pong key buffer not holding the sorted keys is free: window stream
+    uint16_t *ewin = reinterpret_cast<uint16_t *>((ek == ws.ekey_a) ? ws.ekey_b : ws.ekey_a);
     SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, ev, splats, &ws.ctr->entries_eff, ws.capE,
-              ws.n_tiles, ws.tile_off, ewx, ewy);
+              ws.n_tiles, ws.n_tx, ws.tile_off, ewin);
     *order_out = order;
     *entries_out = ev;
-    if (win_out) {
-        win_out[0] = ewx;
-        win_out[1] = ewy;
-    }
+    if (win_out) *win_out = ewin;
     return cudaGetLastError();
 }
 

@@ -3,28 +3,31 @@
 // Reference: composite_tiles (sc/_kernels.py:190-275) + finish()
 // (sc/raster.py:267-282).  Semantics per pixel are the reference's: walk the
 // tile's entries in (depth, index) order, skip splats with alpha0 < 1/255,
-// composite inside the splat's exact f64 pixel window when
-// p_min <= power <= 0, alpha = min(0.99, alpha0 e^power), retire the pixel
-// after compositing once T < stop_transmittance.  fp32 arithmetic
-// (tolerance stated in tests/test_gpu_parity.py).
+// composite inside the splat's pixel window when p_min <= power <= 0,
+// alpha = min(0.99, alpha0 e^power), retire the pixel after compositing once
+// T < stop_transmittance.  fp32 arithmetic (tolerance stated in
+// tests/test_gpu_parity.py).
 //
-// B200 mapping — every warp is an independent worker with no CTA barrier:
-//   * a warp owns an 8x4 pixel block (lane = 8 row + col) of one 16x16 tile;
-//     a CTA is 4 warps = half a tile, and CTAs are dispatched heaviest tile
-//     first (LPT order by log2 entry count, k_tile_order) so the long
-//     silhouette tiles of a 100M-Gaussian frame start at once instead of
-//     forming the tail;
-//   * the warp walks its tile's entry list 128 entries at a time: entry
-//     indices (coalesced) and the 8-byte pixel windows (gather) of the NEXT
-//     128 are prefetched into registers while the current 128 are blended;
-//   * an entry is processed only when its window intersects the warp's ALIVE
-//     pixels (32-bit footprint mask vs ballot of live lanes), so saturated
-//     pixels cost nothing; the lanes that hit load their entry's 48-byte
-//     record and the warp broadcasts each hit's fields with shuffles;
+// B200 mapping — one CTA per 16x16 tile, 8 warps, no CTA barrier at all:
+//   * a warp owns an 8x4 pixel block (lane = 8 row + col) and walks the
+//     tile's entry list on its own; CTAs are dispatched heaviest tile first
+//     (LPT order by log2 entry count, k_tile_order);
+//   * the list is consumed as a 4-deep software pipeline of 64-entry groups:
+//     group g+3: entry indices + 16-bit tile-relative windows (coalesced
+//                stream written by the binning pass) in flight to registers,
+//     g+1, g+2:  48-byte splat records of the entries whose window touches
+//                an ALIVE pixel of the block in flight by cp.async into the
+//                warp's private shared-memory ring (alive only shrinks, so the
+//                mask at issue time is a superset of what is needed: exact),
+//     g:         blended from shared memory;
+//   * per 32 entries the warp transposes the 32 footprints (32x32 bit
+//     transpose over shuffles) so each lane walks only the entries covering
+//     its own pixel; the warp iterates max-over-lanes times;
 //   * a warp exits when its 32 pixels have retired.
-// The first version staged 256-entry batches in shared memory behind a CTA
-// barrier; ncu showed the barrier stall dominating (warps with silhouette
-// pixels held the other seven) and one SM busy for the whole kernel.
+// History (ncu, config-3 far view): a 256-entry CTA batch behind a barrier was
+// barrier-stall bound (42 ms); barrier-free warps with per-hit shuffles were
+// then bound by re-gathering windows (65 GB DRAM per launch) and finally by
+// the dependent-load chain per 32 entries; this pipeline removes both.
 #include <algorithm>
 
 #include "common.cuh"
@@ -33,15 +36,18 @@ namespace sc {
 
 #ifdef SC_BLEND_STATS
 // instrumented build only (libsplatcull_b200_dbg.so): per tile
-// [entries, entry slots walked, (entry, warp) hits, pixel evaluations, max warp cycles, 0, 0, 0]
+// [entries, 32-entry slots walked, (entry, warp) hits, pixel evaluations, max warp cycles, warp iterations, 0, 0]
 constexpr int kDbgTiles = 32400;
 __device__ unsigned long long g_blend_dbg[kDbgTiles * 8];
 #endif
 
-constexpr int kBlendWarps = 8;              // warps per CTA (one 16x16 tile)
-constexpr int kSlots = 4;                   // 32-entry slots per prefetch group
+constexpr int kBlendWarps = 8;           // warps per CTA (one 16x16 tile)
+constexpr int kGroup = 64;               // entries per pipeline group
+constexpr int kGS = kGroup / 32;         // 32-entry slots per group
+constexpr int kRecStages = 3;            // record ring depth (groups) per warp
+constexpr size_t kBlendSmem = sizeof(float4) * 3 * kGroup * kRecStages * kBlendWarps;
 
-// 32-bit footprint of window w on the 8x4 block at (bx0, by0)
+// 32-bit footprint of the window [x0, x1] x [y0, y1] (tile-relative) on the 8x4 block at (bx0, by0)
 __device__ __forceinline__ uint32_t block_mask(int x0, int x1, int y0, int y1, int bx0, int by0)
 {
     const int lo = max(x0, bx0), hi = min(x1, bx0 + 7);
@@ -50,6 +56,11 @@ __device__ __forceinline__ uint32_t block_mask(int x0, int x1, int y0, int y1, i
     const uint32_t cols = (0xFFu >> (7 - (hi - bx0))) & (0xFFu << (lo - bx0));
     const uint32_t rows = (0x01010101u << (8 * (rlo - by0))) & (0x01010101u >> (8 * (3 - (rhi - by0))));
     return cols * rows;
+}
+
+__device__ __forceinline__ uint32_t code_mask(uint32_t c, int bx0, int by0)
+{
+    return block_mask(c & 15u, (c >> 4) & 15u, (c >> 8) & 15u, c >> 12, bx0, by0);
 }
 
 // 32x32 bit-matrix transpose across a warp: lane r holds row r on entry and
@@ -68,6 +79,19 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane)
 __device__ __forceinline__ int lo16(uint32_t w) { return (int)(int16_t)(w & 0xFFFFu); }
 __device__ __forceinline__ int hi16(uint32_t w) { return (int)(int16_t)(w >> 16); }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr uint32_t kNoEntry = 0xFFFFFFFFu;
+constexpr uint32_t kEmptyCode = 0x000Fu;   // x0 = 15 > x1 = 0
+
 __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
                                                             const uint32_t *__restrict__ entry_idx,
                                                             const uint32_t *__restrict__ tile_off,
@@ -77,6 +101,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                                                             float bg_g, float bg_b, int record, float *image,
                                                             float *trans, float *csum, float *cmax)
 {
+    extern __shared__ float4 s_dyn[];
     const int tile = (int)(task_order ? task_order[blockIdx.x] : blockIdx.x);
     const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -88,106 +113,103 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cs = 0.0f;
     bool done = !inside;
     const uint32_t start = tile_off[tile], end = tile_off[tile + 1];
-    const char *rec = reinterpret_cast<const char *>(splats);
+    float4 *ring = s_dyn + (size_t)wid * (3 * kGroup * kRecStages);   // [stage][entry][3]
 #ifdef SC_BLEND_STATS
     unsigned long long d_slots = 0, d_hits = 0, d_evals = 0, d_iters = 0;
     const long long d_t0 = clock64();
 #endif
 
-    // per lane, slot k of the current group: entry base + 32 k + lane.
-    // code = tile-relative window x0 | x1 << 4 | y0 << 8 | y1 << 12 (x0 > x1: empty)
-    uint32_t code[kSlots], ncode[kSlots], idx[kSlots], nidx[kSlots];
-    auto prefetch = [&](uint32_t base, uint32_t *pc, uint32_t *pi) {
+    // meta of a group: per lane, slot s holds entry base + 32 s + lane
+    auto load_meta = [&](uint32_t base, uint32_t *c, uint32_t *ix) {
 #pragma unroll
-        for (int k = 0; k < kSlots; k++) {
-            const uint32_t e = base + 32u * k + lane;
-            pc[k] = 0x000Fu;
-            pi[k] = 0xFFFFFFFFu;
+        for (int s = 0; s < kGS; s++) {
+            const uint32_t e = base + 32u * s + lane;
+            c[s] = kEmptyCode;
+            ix[s] = kNoEntry;
             if (e < end) {
-                if (ewin) {           // entry-aligned stream: 2 bytes, coalesced; index loaded on a hit
-                    pc[k] = __ldg(ewin + e);
-                } else {
-                    uint32_t s = __ldg(entry_idx + e);
-                    pi[k] = (int64_t)s < n_splats ? s : 0xFFFFFFFFu;
+                const uint32_t v = __ldg(entry_idx + e);
+                if ((int64_t)v < n_splats) {
+                    ix[s] = v;
+                    c[s] = ewin ? (uint32_t)__ldg(ewin + e) : kNoEntry;   // kNoEntry: derive from the record
                 }
             }
         }
-        if (!ewin) {
+        if (!ewin) {   // stage-level API without the binning pass: clip the record's window here
 #pragma unroll
-            for (int k = 0; k < kSlots; k++) {
-                if (pi[k] == 0xFFFFFFFFu) continue;
-                const uint2 w = __ldg(reinterpret_cast<const uint2 *>(rec + 48 * (size_t)pi[k] + 40));
+            for (int s = 0; s < kGS; s++) {
+                if (ix[s] == kNoEntry) continue;
+                const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + ix[s]) + 40));
                 const int x0 = max(lo16(w.x) - ox, 0), x1 = min(hi16(w.x) - ox, 15);
                 const int y0 = max(lo16(w.y) - oy, 0), y1 = min(hi16(w.y) - oy, 15);
-                if (x0 <= x1 && y0 <= y1) pc[k] = (uint32_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12));
+                c[s] = (x0 <= x1 && y0 <= y1) ? (uint32_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12)) : kEmptyCode;
             }
         }
     };
+    // cp.async the records of entries touching alive pixels into ring stage `st`
+    auto stage = [&](int st, const uint32_t *c, const uint32_t *ix, uint32_t alive) {
+#pragma unroll
+        for (int s = 0; s < kGS; s++) {
+            if (ix[s] != kNoEntry && (code_mask(c[s], bx0, by0) & alive)) {
+                const float4 *src = reinterpret_cast<const float4 *>(splats + ix[s]);
+                float4 *dst = ring + ((size_t)st * kGroup + 32 * s + lane) * 3;
+                cp_async16(dst, src);
+                cp_async16(dst + 1, src + 1);
+                cp_async16(dst + 2, src + 2);
+            }
+        }
+        cp_async_commit();
+    };
 
     if (!__all_sync(0xffffffffu, done) && start < end) {
-        prefetch(start, code, idx);
-        for (uint32_t base = start; base < end; base += 32u * kSlots) {
-            const bool more = base + 32u * kSlots < end;
-            if (more) prefetch(base + 32u * kSlots, ncode, nidx);
+        uint32_t c0[kGS], i0[kGS], c1[kGS], i1[kGS], c2[kGS], i2[kGS], c3[kGS], i3[kGS];
+        const uint32_t alive0 = __ballot_sync(0xffffffffu, !done);
+        load_meta(start, c0, i0);
+        load_meta(start + kGroup, c1, i1);
+        load_meta(start + 2 * kGroup, c2, i2);
+        stage(0, c0, i0, alive0);
+        stage(1, c1, i1, alive0);
+        int st = 0;
+        for (uint32_t base = start; base < end; base += kGroup) {
+            const uint32_t alive_now = __ballot_sync(0xffffffffu, !done);
+            if (!alive_now) break;
+            load_meta(base + 3 * kGroup, c3, i3);                     // group g+3 meta
+            stage(st == 0 ? 2 : st - 1, c2, i2, alive_now);           // group g+2 records (ring slot (g+2) % 3)
+            cp_async_wait<2>();                                        // group g's records have landed
+            __syncwarp();
+            const float4 *grp = ring + (size_t)st * kGroup * 3;
 #pragma unroll
-            for (int k = 0; k < kSlots; k++) {
+            for (int s = 0; s < kGS; s++) {
                 const uint32_t alive = __ballot_sync(0xffffffffu, !done);
                 if (!alive) break;
-                // footprint of this lane's entry on the warp's alive pixels
-                const uint32_t c = code[k];
-                const uint32_t fp =
-                    block_mask(c & 15u, (c >> 4) & 15u, (c >> 8) & 15u, c >> 12, bx0, by0) & alive;
+                const uint32_t fp = code_mask(c0[s], bx0, by0) & alive;
 #ifdef SC_BLEND_STATS
                 d_slots++;
-#endif
-                if (!__any_sync(0xffffffffu, fp != 0u)) continue;
-                float4 ga = make_float4(0.f, 0.f, 0.f, 0.f), pa = ga;
-                float2 gb2 = make_float2(0.f, 0.f);
-                if (fp) {
-                    if (ewin) {
-                        const uint32_t s = __ldg(entry_idx + base + 32u * k + lane);
-                        idx[k] = (int64_t)s < n_splats ? s : 0u;
-                    }
-                    const float4 *src = reinterpret_cast<const float4 *>(rec + 48 * (size_t)idx[k]);
-                    ga = __ldg(src);
-                    pa = __ldg(src + 1);
-                    gb2 = __ldg(reinterpret_cast<const float2 *>(src + 2));
-                }
-#ifdef SC_BLEND_STATS
                 d_hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
 #endif
-                // 32x32 bit transpose: bit j of `mine` = entry (slot lane) j covers my pixel
-                uint32_t mine = transpose32(fp, lane);
-                // each lane walks its own entries in order; the warp iterates
-                // max-over-lanes times (fields fetched from lane j by shuffle)
+                if (!__any_sync(0xffffffffu, fp != 0u)) continue;
+                uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
                 while (__any_sync(0xffffffffu, mine != 0u)) {
                     const bool act = mine != 0u;
-                    const int srcl = act ? __ffs(mine) - 1 : lane;
+                    const int j = act ? __ffs(mine) - 1 : lane;
                     mine &= mine - 1u;
-                    const float mx = __shfl_sync(0xffffffffu, ga.x, srcl);
-                    const float my = __shfl_sync(0xffffffffu, ga.y, srcl);
-                    const float ha = __shfl_sync(0xffffffffu, ga.z, srcl);
-                    const float hb = __shfl_sync(0xffffffffu, ga.w, srcl);
-                    const float hc = __shfl_sync(0xffffffffu, pa.x, srcl);
-                    const float op = __shfl_sync(0xffffffffu, pa.y, srcl);
-                    const float pmin = __shfl_sync(0xffffffffu, pa.z, srcl);
-                    const float c0 = __shfl_sync(0xffffffffu, pa.w, srcl);
-                    const float c1 = __shfl_sync(0xffffffffu, gb2.x, srcl);
-                    const float c2 = __shfl_sync(0xffffffffu, gb2.y, srcl);
-                    const uint32_t sidx = record ? __shfl_sync(0xffffffffu, idx[k], srcl) : 0u;
+                    const uint32_t sidx = record ? __shfl_sync(0xffffffffu, i0[s], j) : 0u;
 #ifdef SC_BLEND_STATS
                     d_evals += act;
                     d_iters += (lane == 0);
 #endif
                     if (act) {
-                        const float dx = fpx - mx, dy = fpy - my;
-                        const float power = -(ha * dx * dx + hc * dy * dy) - hb * dx * dy;
-                        if (!(power > 0.0f || power < pmin)) {
-                            const float alpha = fminf(0.99f, op * __expf(power));
+                        const float4 *r = grp + (32 * s + j) * 3;
+                        const float4 g = r[0];   // mx, my, 0.5 a, b
+                        const float4 p = r[1];   // 0.5 c, opacity, p_min, red
+                        const float dx = fpx - g.x, dy = fpy - g.y;
+                        const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
+                        if (!(power > 0.0f || power < p.z)) {
+                            const float2 q = *reinterpret_cast<const float2 *>(r + 2);   // green, blue
+                            const float alpha = fminf(0.99f, p.y * __expf(power));
                             const float contrib = alpha * T;
-                            cr += contrib * c0;
-                            cg += contrib * c1;
-                            cb += contrib * c2;
+                            cr += contrib * p.w;
+                            cg += contrib * q.x;
+                            cb += contrib * q.y;
                             T = T * (1.0f - alpha);
                             if (record) {
                                 cs += contrib;
@@ -201,13 +223,16 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                     }
                 }
             }
-            if (__all_sync(0xffffffffu, done) || !more) break;
+            __syncwarp();   // ring slot st is refilled by the stage() call of the next-but-one iteration
 #pragma unroll
-            for (int k = 0; k < kSlots; k++) {
-                idx[k] = nidx[k];
-                code[k] = ncode[k];
+            for (int s = 0; s < kGS; s++) {
+                c0[s] = c1[s]; i0[s] = i1[s];
+                c1[s] = c2[s]; i1[s] = i2[s];
+                c2[s] = c3[s]; i2[s] = i3[s];
             }
+            st = (st == kRecStages - 1) ? 0 : st + 1;
         }
+        cp_async_wait<0>();
     }
 #ifdef SC_BLEND_STATS
     for (int o = 16; o > 0; o >>= 1) d_evals += __shfl_down_sync(0xffffffffu, d_evals, o);
@@ -272,11 +297,17 @@ cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, cons
                          const uint16_t *ewin, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_blend, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBlendSmem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const int64_t n_tiles = (int64_t)n_tx * n_ty;
     if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, tile_off, n_tiles, task_order);
-    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, 0, st, splats, n_splats, entry_idx, tile_off, ewin, task_order,
-              cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
+    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kBlendSmem, st, splats, n_splats, entry_idx, tile_off, ewin,
+              task_order, cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
               (float)opts.background[1], (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image,
               out.trans, out.contrib_sum, out.contrib_max);
     return cudaGetLastError();

@@ -145,11 +145,15 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
             }
         }
     };
-    // cp.async the records of entries touching alive pixels into ring stage `st`
-    auto stage = [&](int st, const uint32_t *c, const uint32_t *ix, uint32_t alive) {
+    // cp.async the records of entries touching alive pixels into ring stage
+    // `st`; the code register is replaced by that footprint (geometric & alive
+    // at issue time), which the processing step only has to AND with alive.
+    auto stage = [&](int st, uint32_t *c, const uint32_t *ix, uint32_t alive) {
 #pragma unroll
         for (int s = 0; s < kGS; s++) {
-            if (ix[s] != kNoEntry && (code_mask(c[s], bx0, by0) & alive)) {
+            const uint32_t fp = ix[s] != kNoEntry ? (code_mask(c[s], bx0, by0) & alive) : 0u;
+            c[s] = fp;
+            if (fp) {
                 const float4 *src = reinterpret_cast<const float4 *>(splats + ix[s]);
                 float4 *dst = ring + ((size_t)st * kGroup + 32 * s + lane) * 3;
                 cp_async16(dst, src);
@@ -160,77 +164,111 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
         cp_async_commit();
     };
 
-    if (!__all_sync(0xffffffffu, done) && start < end) {
-        uint32_t c0[kGS], i0[kGS], c1[kGS], i1[kGS], c2[kGS], i2[kGS], c3[kGS], i3[kGS];
-        const uint32_t alive0 = __ballot_sync(0xffffffffu, !done);
-        load_meta(start, c0, i0);
-        load_meta(start + kGroup, c1, i1);
-        load_meta(start + 2 * kGroup, c2, i2);
-        stage(0, c0, i0, alive0);
-        stage(1, c1, i1, alive0);
-        int st = 0;
-        for (uint32_t base = start; base < end; base += kGroup) {
-            const uint32_t alive_now = __ballot_sync(0xffffffffu, !done);
-            if (!alive_now) break;
-            load_meta(base + 3 * kGroup, c3, i3);                     // group g+3 meta
-            stage(st == 0 ? 2 : st - 1, c2, i2, alive_now);           // group g+2 records (ring slot (g+2) % 3)
-            cp_async_wait<2>();                                        // group g's records have landed
-            __syncwarp();
-            const float4 *grp = ring + (size_t)st * kGroup * 3;
+    // One pipeline step for group g: fA = footprints of g (records in ring
+    // slot st), cS/iS = meta of g+2 (staged now into ring slot (g+2) % 3),
+    // cL/iL = register set receiving the meta of g+4.  Five register sets
+    // rotate through the manually unrolled loop below, so no register copy
+    // ever waits on an in-flight load.
+    auto step = [&](uint32_t base, const uint32_t *fA, const uint32_t *iA, uint32_t *cS, const uint32_t *iS,
+                    uint32_t *cL, uint32_t *iL, int st) -> bool {
+        const uint32_t alive_now = __ballot_sync(0xffffffffu, !done);
+        if (!alive_now) return false;
+        load_meta(base + 4 * kGroup, cL, iL);                      // group g+4 meta
+        stage(st == 0 ? 2 : st - 1, cS, iS, alive_now);            // group g+2 records
+        cp_async_wait<2>();                                         // group g's records have landed
+        __syncwarp();
+        const float4 *grp = ring + (size_t)st * kGroup * 3;
 #pragma unroll
-            for (int s = 0; s < kGS; s++) {
-                const uint32_t alive = __ballot_sync(0xffffffffu, !done);
-                if (!alive) break;
-                const uint32_t fp = code_mask(c0[s], bx0, by0) & alive;
+        for (int s = 0; s < kGS; s++) {
+            const uint32_t alive = __ballot_sync(0xffffffffu, !done);
+            if (!alive) break;
+            const uint32_t fp = fA[s] & alive;
 #ifdef SC_BLEND_STATS
-                d_slots++;
-                d_hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
+            d_slots++;
+            d_hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
 #endif
-                if (!__any_sync(0xffffffffu, fp != 0u)) continue;
-                uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
-                while (__any_sync(0xffffffffu, mine != 0u)) {
-                    const bool act = mine != 0u;
-                    const int j = act ? __ffs(mine) - 1 : lane;
-                    mine &= mine - 1u;
-                    const uint32_t sidx = record ? __shfl_sync(0xffffffffu, i0[s], j) : 0u;
+            if (!__any_sync(0xffffffffu, fp != 0u)) continue;
+            uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
+            while (__any_sync(0xffffffffu, mine != 0u)) {
+                const bool act = mine != 0u;
+                const int j = act ? __ffs(mine) - 1 : lane;
+                mine &= mine - 1u;
+                const uint32_t sidx = record ? __shfl_sync(0xffffffffu, iA[s], j) : 0u;
 #ifdef SC_BLEND_STATS
-                    d_evals += act;
-                    d_iters += (lane == 0);
+                d_evals += act;
+                d_iters += (lane == 0);
 #endif
-                    if (act) {
-                        const float4 *r = grp + (32 * s + j) * 3;
-                        const float4 g = r[0];   // mx, my, 0.5 a, b
-                        const float4 p = r[1];   // 0.5 c, opacity, p_min, red
-                        const float dx = fpx - g.x, dy = fpy - g.y;
-                        const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
-                        if (!(power > 0.0f || power < p.z)) {
-                            const float2 q = *reinterpret_cast<const float2 *>(r + 2);   // green, blue
-                            const float alpha = fminf(0.99f, p.y * __expf(power));
-                            const float contrib = alpha * T;
-                            cr += contrib * p.w;
-                            cg += contrib * q.x;
-                            cb += contrib * q.y;
-                            T = T * (1.0f - alpha);
-                            if (record) {
-                                cs += contrib;
-                                if (contrib > 0.0f) atomicMax(reinterpret_cast<int *>(cmax) + sidx, __float_as_int(contrib));
-                            }
-                            if (T < stop_t) {
-                                done = true;
-                                mine = 0u;
-                            }
+                if (act) {
+                    const float4 *r = grp + (32 * s + j) * 3;
+                    const float4 g = r[0];   // mx, my, 0.5 a, b
+                    const float4 p = r[1];   // 0.5 c, opacity, p_min, red
+                    const float dx = fpx - g.x, dy = fpy - g.y;
+                    const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
+                    if (!(power > 0.0f || power < p.z)) {
+                        const float2 q = *reinterpret_cast<const float2 *>(r + 2);   // green, blue
+                        const float alpha = fminf(0.99f, p.y * __expf(power));
+                        const float contrib = alpha * T;
+                        cr += contrib * p.w;
+                        cg += contrib * q.x;
+                        cb += contrib * q.y;
+                        T = T * (1.0f - alpha);
+                        if (record) {
+                            cs += contrib;
+                            if (contrib > 0.0f) atomicMax(reinterpret_cast<int *>(cmax) + sidx, __float_as_int(contrib));
+                        }
+                        if (T < stop_t) {
+                            done = true;
+                            mine = 0u;
                         }
                     }
                 }
             }
-            __syncwarp();   // ring slot st is refilled by the stage() call of the next-but-one iteration
-#pragma unroll
-            for (int s = 0; s < kGS; s++) {
-                c0[s] = c1[s]; i0[s] = i1[s];
-                c1[s] = c2[s]; i1[s] = i2[s];
-                c2[s] = c3[s]; i2[s] = i3[s];
-            }
-            st = (st == kRecStages - 1) ? 0 : st + 1;
+        }
+        __syncwarp();   // ring slot st is refilled by the stage() of the next step
+        return base + kGroup < end;
+    };
+
+    if (!__all_sync(0xffffffffu, done) && start < end) {
+        uint32_t c0[kGS], i0[kGS], c1[kGS], i1[kGS], c2[kGS], i2[kGS], c3[kGS], i3[kGS], c4[kGS], i4[kGS];
+        const uint32_t alive0 = __ballot_sync(0xffffffffu, !done);
+        load_meta(start, c0, i0);
+        load_meta(start + kGroup, c1, i1);
+        load_meta(start + 2 * kGroup, c2, i2);
+        load_meta(start + 3 * kGroup, c3, i3);
+        stage(0, c0, i0, alive0);
+        stage(1, c1, i1, alive0);
+        uint32_t base = start;
+        for (;;) {
+            if (!step(base, c0, i0, c2, i2, c4, i4, 0)) break;
+            base += kGroup;
+            if (!step(base, c1, i1, c3, i3, c0, i0, 1)) break;
+            base += kGroup;
+            if (!step(base, c2, i2, c4, i4, c1, i1, 2)) break;
+            base += kGroup;
+            if (!step(base, c3, i3, c0, i0, c2, i2, 0)) break;
+            base += kGroup;
+            if (!step(base, c4, i4, c1, i1, c3, i3, 1)) break;
+            base += kGroup;
+            if (!step(base, c0, i0, c2, i2, c4, i4, 2)) break;
+            base += kGroup;
+            if (!step(base, c1, i1, c3, i3, c0, i0, 0)) break;
+            base += kGroup;
+            if (!step(base, c2, i2, c4, i4, c1, i1, 1)) break;
+            base += kGroup;
+            if (!step(base, c3, i3, c0, i0, c2, i2, 2)) break;
+            base += kGroup;
+            if (!step(base, c4, i4, c1, i1, c3, i3, 0)) break;
+            base += kGroup;
+            if (!step(base, c0, i0, c2, i2, c4, i4, 1)) break;
+            base += kGroup;
+            if (!step(base, c1, i1, c3, i3, c0, i0, 2)) break;
+            base += kGroup;
+            if (!step(base, c2, i2, c4, i4, c1, i1, 0)) break;
+            base += kGroup;
+            if (!step(base, c3, i3, c0, i0, c2, i2, 1)) break;
+            base += kGroup;
+            if (!step(base, c4, i4, c1, i1, c3, i3, 2)) break;
+            base += kGroup;
         }
         cp_async_wait<0>();
     }

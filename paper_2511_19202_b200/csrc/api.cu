@@ -291,7 +291,7 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
            "project");
     SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;
-    uint16_t *ewin = nullptr;
+    uint32_t *ewin = nullptr;
     SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.splats, stats, &order, &entries, &ewin, st),
            "bin/sort");
     SC_TRY(mark(3), "event");

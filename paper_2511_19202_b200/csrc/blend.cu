@@ -42,10 +42,12 @@ __device__ unsigned long long g_blend_dbg[kDbgTiles * 8];
 #endif
 
 constexpr int kBlendWarps = 8;           // warps per CTA (one 16x16 tile)
-constexpr int kGroup = 64;               // entries per pipeline group
-constexpr int kGS = kGroup / 32;         // 32-entry slots per group
-constexpr int kRecStages = 3;            // record ring depth (groups) per warp
-constexpr size_t kBlendSmem = sizeof(float4) * 3 * kGroup * kRecStages * kBlendWarps;
+constexpr int kG = 32;                   // entries per pipeline group
+constexpr int kMetaStages = 6;           // meta ring (index + window code) depth: issued 5 groups ahead
+constexpr int kRecStages = 4;            // record ring depth: issued 3 groups ahead
+constexpr size_t kMetaBytesW = sizeof(uint2) * kG * kMetaStages;
+constexpr size_t kRecBytesW = sizeof(float4) * 3 * kG * kRecStages;
+constexpr size_t kBlendSmem = (kMetaBytesW + kRecBytesW) * kBlendWarps;
 
 // 32-bit footprint of the window [x0, x1] x [y0, y1] (tile-relative) on the 8x4 block at (bx0, by0)
 __device__ __forceinline__ uint32_t block_mask(int x0, int x1, int y0, int y1, int bx0, int by0)
@@ -60,7 +62,7 @@ __device__ __forceinline__ uint32_t block_mask(int x0, int x1, int y0, int y1, i
 
 __device__ __forceinline__ uint32_t code_mask(uint32_t c, int bx0, int by0)
 {
-    return block_mask(c & 15u, (c >> 4) & 15u, (c >> 8) & 15u, c >> 12, bx0, by0);
+    return block_mask(c & 15u, (c >> 4) & 15u, (c >> 8) & 15u, (c >> 12) & 15u, bx0, by0);
 }
 
 // 32x32 bit-matrix transpose across a warp: lane r holds row r on entry and
@@ -79,11 +81,17 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane)
 __device__ __forceinline__ int lo16(uint32_t w) { return (int)(int16_t)(w & 0xFFFFu); }
 __device__ __forceinline__ int hi16(uint32_t w) { return (int)(int16_t)(w >> 16); }
 
+__device__ __forceinline__ uint32_t smem_u32p(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-                 "l"(gmem)
-                 : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32p(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32p(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -95,7 +103,7 @@ constexpr uint32_t kEmptyCode = 0x000Fu;   // x0 = 15 > x1 = 0
 __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
                                                             const uint32_t *__restrict__ entry_idx,
                                                             const uint32_t *__restrict__ tile_off,
-                                                            const uint16_t *__restrict__ ewin,
+                                                            const uint32_t *__restrict__ ewin,
                                                             const uint32_t *__restrict__ task_order, int width,
                                                             int height, int n_tx, float stop_t, float bg_r,
                                                             float bg_g, float bg_b, int record, float *image,
@@ -113,162 +121,133 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cs = 0.0f;
     bool done = !inside;
     const uint32_t start = tile_off[tile], end = tile_off[tile + 1];
-    float4 *ring = s_dyn + (size_t)wid * (3 * kGroup * kRecStages);   // [stage][entry][3]
+    // this warp's private rings: meta [kMetaStages][32] (index, code -> footprint), records [kRecStages][32][3]
+    uint2 *meta = reinterpret_cast<uint2 *>(reinterpret_cast<char *>(s_dyn) + wid * (kMetaBytesW + kRecBytesW));
+    float4 *recs = reinterpret_cast<float4 *>(reinterpret_cast<char *>(meta) + kMetaBytesW);
 #ifdef SC_BLEND_STATS
     unsigned long long d_slots = 0, d_hits = 0, d_evals = 0, d_iters = 0;
     const long long d_t0 = clock64();
 #endif
 
-    // meta of a group: per lane, slot s holds entry base + 32 s + lane
-    auto load_meta = [&](uint32_t base, uint32_t *c, uint32_t *ix) {
-#pragma unroll
-        for (int s = 0; s < kGS; s++) {
-            const uint32_t e = base + 32u * s + lane;
-            c[s] = kEmptyCode;
-            ix[s] = kNoEntry;
-            if (e < end) {
+    // meta of group q (entries start + 32 q + lane) -> meta slot ms, asynchronously
+    auto issue_meta = [&](uint32_t q, int ms) {
+        const uint32_t e = start + kG * q + lane;
+        uint2 *dst = meta + ms * kG + lane;
+        if (e < end) {
+            if (ewin) {
+                cp_async4(&dst->x, entry_idx + e);
+                cp_async4(&dst->y, ewin + e);
+            } else {   // stage-level API without the binning pass: clip the record's window here
                 const uint32_t v = __ldg(entry_idx + e);
+                uint32_t code = kEmptyCode;
                 if ((int64_t)v < n_splats) {
-                    ix[s] = v;
-                    c[s] = ewin ? (uint32_t)__ldg(ewin + e) : kNoEntry;   // kNoEntry: derive from the record
+                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + v) + 40));
+                    const int x0 = max(lo16(w.x) - ox, 0), x1 = min(hi16(w.x) - ox, 15);
+                    const int y0 = max(lo16(w.y) - oy, 0), y1 = min(hi16(w.y) - oy, 15);
+                    if (x0 <= x1 && y0 <= y1) code = (uint32_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12));
                 }
+                *dst = make_uint2(v, code);
             }
-        }
-        if (!ewin) {   // stage-level API without the binning pass: clip the record's window here
-#pragma unroll
-            for (int s = 0; s < kGS; s++) {
-                if (ix[s] == kNoEntry) continue;
-                const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + ix[s]) + 40));
-                const int x0 = max(lo16(w.x) - ox, 0), x1 = min(hi16(w.x) - ox, 15);
-                const int y0 = max(lo16(w.y) - oy, 0), y1 = min(hi16(w.y) - oy, 15);
-                c[s] = (x0 <= x1 && y0 <= y1) ? (uint32_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12)) : kEmptyCode;
-            }
+        } else {
+            *dst = make_uint2(kNoEntry, kEmptyCode);
         }
     };
-    // cp.async the records of entries touching alive pixels into ring stage
-    // `st`; the code register is replaced by that footprint (geometric & alive
-    // at issue time), which the processing step only has to AND with alive.
-    auto stage = [&](int st, uint32_t *c, const uint32_t *ix, uint32_t alive) {
-#pragma unroll
-        for (int s = 0; s < kGS; s++) {
-            const uint32_t fp = ix[s] != kNoEntry ? (code_mask(c[s], bx0, by0) & alive) : 0u;
-            c[s] = fp;
-            if (fp) {
-                const float4 *src = reinterpret_cast<const float4 *>(splats + ix[s]);
-                float4 *dst = ring + ((size_t)st * kGroup + 32 * s + lane) * 3;
-                cp_async16(dst, src);
-                cp_async16(dst + 1, src + 1);
-                cp_async16(dst + 2, src + 2);
-            }
+    // records of the entries in meta slot ms that touch alive pixels -> record
+    // slot rs (cp.async); the code is replaced by that footprint
+    auto issue_rec = [&](int ms, int rs, uint32_t alive) {
+        uint2 *m = meta + ms * kG + lane;
+        const uint2 v = *m;
+        const uint32_t fp = ((int64_t)v.x < n_splats) ? (code_mask(v.y, bx0, by0) & alive) : 0u;
+        m->y = fp;
+        if (fp) {
+            const float4 *src = reinterpret_cast<const float4 *>(splats + v.x);
+            float4 *dst = recs + (rs * kG + lane) * 3;
+            cp_async16(dst, src);
+            cp_async16(dst + 1, src + 1);
+            cp_async16(dst + 2, src + 2);
         }
-        cp_async_commit();
     };
 
-    // One pipeline step for group g: fA = footprints of g (records in ring
-    // slot st), cS/iS = meta of g+2 (staged now into ring slot (g+2) % 3),
-    // cL/iL = register set receiving the meta of g+4.  Five register sets
-    // rotate through the manually unrolled loop below, so no register copy
-    // ever waits on an in-flight load.
-    auto step = [&](uint32_t base, const uint32_t *fA, const uint32_t *iA, uint32_t *cS, const uint32_t *iS,
-                    uint32_t *cL, uint32_t *iL, int st) -> bool {
-        const uint32_t alive_now = __ballot_sync(0xffffffffu, !done);
-        if (!alive_now) return false;
-        load_meta(base + 4 * kGroup, cL, iL);                      // group g+4 meta
-        stage(st == 0 ? 2 : st - 1, cS, iS, alive_now);            // group g+2 records
-        cp_async_wait<2>();                                         // group g's records have landed
+    if (!__all_sync(0xffffffffu, done) && start < end) {
+        // prologue, commit order: [meta 0-2], [rec 0], [meta 3], [rec 1], [meta 4], [rec 2]
+        issue_meta(0, 0);
+        issue_meta(1, 1);
+        issue_meta(2, 2);
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncwarp();
-        const float4 *grp = ring + (size_t)st * kGroup * 3;
-#pragma unroll
-        for (int s = 0; s < kGS; s++) {
-            const uint32_t alive = __ballot_sync(0xffffffffu, !done);
-            if (!alive) break;
-            const uint32_t fp = fA[s] & alive;
+        const uint32_t alive0 = __ballot_sync(0xffffffffu, !done);
+        issue_rec(0, 0, alive0);
+        cp_async_commit();
+        issue_meta(3, 3);
+        cp_async_commit();
+        issue_rec(1, 1, alive0);
+        cp_async_commit();
+        issue_meta(4, 4);
+        cp_async_commit();
+        issue_rec(2, 2, alive0);
+        cp_async_commit();
+        int ms = 0, rs = 0;   // slots of group g
+        for (uint32_t q = 0; start + kG * q < end; q++) {
+            // pending at most: [rec g+1], [meta g+4], [rec g+2]  ->  rec g and meta g+3 have landed
+            cp_async_wait<3>();
+            __syncwarp();
+            const uint32_t alive_now = __ballot_sync(0xffffffffu, !done);
+            if (!alive_now) break;
+            const int ms5 = ms == 0 ? 5 : ms - 1, ms3 = ms >= 3 ? ms - 3 : ms + 3;
+            const int rs3 = rs == 0 ? 3 : rs - 1;
+            issue_meta(q + 5, ms5);            // group g+5 meta   (slot of g-1, consumed)
+            cp_async_commit();
+            issue_rec(ms3, rs3, alive_now);    // group g+3 records (slot of g-1, consumed)
+            cp_async_commit();
+            // ---- blend group g ----
+            const uint2 m = meta[ms * kG + lane];
+            const uint32_t fp = m.y & alive_now;
 #ifdef SC_BLEND_STATS
             d_slots++;
             d_hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
 #endif
-            if (!__any_sync(0xffffffffu, fp != 0u)) continue;
-            uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
-            while (__any_sync(0xffffffffu, mine != 0u)) {
-                const bool act = mine != 0u;
-                const int j = act ? __ffs(mine) - 1 : lane;
-                mine &= mine - 1u;
-                const uint32_t sidx = record ? __shfl_sync(0xffffffffu, iA[s], j) : 0u;
+            if (__any_sync(0xffffffffu, fp != 0u)) {
+                const float4 *grp = recs + rs * kG * 3;
+                uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
+                while (__any_sync(0xffffffffu, mine != 0u)) {
+                    const bool act = mine != 0u;
+                    const int j = act ? __ffs(mine) - 1 : lane;
+                    mine &= mine - 1u;
+                    const uint32_t sidx = record ? __shfl_sync(0xffffffffu, m.x, j) : 0u;
 #ifdef SC_BLEND_STATS
-                d_evals += act;
-                d_iters += (lane == 0);
+                    d_evals += act;
+                    d_iters += (lane == 0);
 #endif
-                if (act) {
-                    const float4 *r = grp + (32 * s + j) * 3;
-                    const float4 g = r[0];   // mx, my, 0.5 a, b
-                    const float4 p = r[1];   // 0.5 c, opacity, p_min, red
-                    const float dx = fpx - g.x, dy = fpy - g.y;
-                    const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
-                    if (!(power > 0.0f || power < p.z)) {
-                        const float2 q = *reinterpret_cast<const float2 *>(r + 2);   // green, blue
-                        const float alpha = fminf(0.99f, p.y * __expf(power));
-                        const float contrib = alpha * T;
-                        cr += contrib * p.w;
-                        cg += contrib * q.x;
-                        cb += contrib * q.y;
-                        T = T * (1.0f - alpha);
-                        if (record) {
-                            cs += contrib;
-                            if (contrib > 0.0f) atomicMax(reinterpret_cast<int *>(cmax) + sidx, __float_as_int(contrib));
-                        }
-                        if (T < stop_t) {
-                            done = true;
-                            mine = 0u;
+                    if (act) {
+                        const float4 *r = grp + j * 3;
+                        const float4 g = r[0];   // mx, my, 0.5 a, b
+                        const float4 p = r[1];   // 0.5 c, opacity, p_min, red
+                        const float dx = fpx - g.x, dy = fpy - g.y;
+                        const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
+                        if (!(power > 0.0f || power < p.z)) {
+                            const float2 c2 = *reinterpret_cast<const float2 *>(r + 2);   // green, blue
+                            const float alpha = fminf(0.99f, p.y * __expf(power));
+                            const float contrib = alpha * T;
+                            cr += contrib * p.w;
+                            cg += contrib * c2.x;
+                            cb += contrib * c2.y;
+                            T = T * (1.0f - alpha);
+                            if (record) {
+                                cs += contrib;
+                                if (contrib > 0.0f) atomicMax(reinterpret_cast<int *>(cmax) + sidx, __float_as_int(contrib));
+                            }
+                            if (T < stop_t) {
+                                done = true;
+                                mine = 0u;
+                            }
                         }
                     }
                 }
             }
-        }
-        __syncwarp();   // ring slot st is refilled by the stage() of the next step
-        return base + kGroup < end;
-    };
-
-    if (!__all_sync(0xffffffffu, done) && start < end) {
-        uint32_t c0[kGS], i0[kGS], c1[kGS], i1[kGS], c2[kGS], i2[kGS], c3[kGS], i3[kGS], c4[kGS], i4[kGS];
-        const uint32_t alive0 = __ballot_sync(0xffffffffu, !done);
-        load_meta(start, c0, i0);
-        load_meta(start + kGroup, c1, i1);
-        load_meta(start + 2 * kGroup, c2, i2);
-        load_meta(start + 3 * kGroup, c3, i3);
-        stage(0, c0, i0, alive0);
-        stage(1, c1, i1, alive0);
-        uint32_t base = start;
-        for (;;) {
-            if (!step(base, c0, i0, c2, i2, c4, i4, 0)) break;
-            base += kGroup;
-            if (!step(base, c1, i1, c3, i3, c0, i0, 1)) break;
-            base += kGroup;
-            if (!step(base, c2, i2, c4, i4, c1, i1, 2)) break;
-            base += kGroup;
-            if (!step(base, c3, i3, c0, i0, c2, i2, 0)) break;
-            base += kGroup;
-            if (!step(base, c4, i4, c1, i1, c3, i3, 1)) break;
-            base += kGroup;
-            if (!step(base, c0, i0, c2, i2, c4, i4, 2)) break;
-            base += kGroup;
-            if (!step(base, c1, i1, c3, i3, c0, i0, 0)) break;
-            base += kGroup;
-            if (!step(base, c2, i2, c4, i4, c1, i1, 1)) break;
-            base += kGroup;
-            if (!step(base, c3, i3, c0, i0, c2, i2, 2)) break;
-            base += kGroup;
-            if (!step(base, c4, i4, c1, i1, c3, i3, 0)) break;
-            base += kGroup;
-            if (!step(base, c0, i0, c2, i2, c4, i4, 1)) break;
-            base += kGroup;
-            if (!step(base, c1, i1, c3, i3, c0, i0, 2)) break;
-            base += kGroup;
-            if (!step(base, c2, i2, c4, i4, c1, i1, 0)) break;
-            base += kGroup;
-            if (!step(base, c3, i3, c0, i0, c2, i2, 1)) break;
-            base += kGroup;
-            if (!step(base, c4, i4, c1, i1, c3, i3, 2)) break;
-            base += kGroup;
+            __syncwarp();   // slots of group g are refilled two steps from now
+            ms = ms == kMetaStages - 1 ? 0 : ms + 1;
+            rs = rs == kRecStages - 1 ? 0 : rs + 1;
         }
         cp_async_wait<0>();
     }
@@ -332,7 +311,7 @@ __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev,
 }
 
 cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
-                         const uint16_t *ewin, const sc_camera &cam, const sc_opts &opts,
+                         const uint32_t *ewin, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
     static bool attr_set = false;

@@ -139,10 +139,10 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
                            cudaStream_t st);
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
                        const sc_splat *splats, sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out,
-                       uint16_t **win_out, cudaStream_t st);
+                       uint32_t **win_out, cudaStream_t st);
 // ewin: entry-aligned tile-relative windows from launch_bin, or NULL (gathered from the records)
 cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
-                         const uint16_t *ewin, const sc_camera &cam, const sc_opts &opts,
+                         const uint32_t *ewin, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st);
 cudaError_t launch_vis_mlp(const sc_vis_weights *w, const float *x, int64_t n, float *logits,
                            cudaStream_t st);

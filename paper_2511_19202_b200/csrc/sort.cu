@@ -374,7 +374,7 @@ __global__ void k_entry_emit(const uint32_t *order, const uint32_t *rlo, const u
 // entry instead of each re-gathering the window from the splat records.
 __global__ void k_tile_offsets(const uint32_t *ekey, const uint32_t *eval, const sc_splat *splats,
                                const unsigned long long *e_dev, int64_t cap_e, int64_t n_tiles, int n_tx,
-                               uint32_t *tile_off, uint16_t *ewin)
+                               uint32_t *tile_off, uint32_t *ewin)
 {
     const int64_t E = std::min<int64_t>((int64_t)*e_dev, cap_e);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= E; i += (int64_t)gridDim.x * blockDim.x) {
@@ -386,8 +386,8 @@ __global__ void k_tile_offsets(const uint32_t *ekey, const uint32_t *eval, const
             const int tile = (int)cur, ox = (tile % n_tx) * kTile, oy = (tile / n_tx) * kTile;
             const int x0 = max((int)(int16_t)(w.x & 0xFFFF) - ox, 0), x1 = min((int)(int16_t)(w.x >> 16) - ox, 15);
             const int y0 = max((int)(int16_t)(w.y & 0xFFFF) - oy, 0), y1 = min((int)(int16_t)(w.y >> 16) - oy, 15);
-            uint16_t code = 0x000F;   // empty
-            if (x0 <= x1 && y0 <= y1) code = (uint16_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12));
+            uint32_t code = 0x000F;   // empty
+            if (x0 <= x1 && y0 <= y1) code = (uint32_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12));
             ewin[i] = code;
         }
     }
@@ -406,7 +406,7 @@ static int grid_for(int64_t n, int threads)
 // entries (survivor index per entry, tile-major), ws.tile_off, stats.entries.
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
                        const sc_splat *splats, sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out,
-                       uint16_t **win_out, cudaStream_t st)
+                       uint32_t **win_out, cudaStream_t st)
 {
     cudaError_t e;
     uint32_t *keys_s = nullptr, *order = nullptr;
@@ -431,7 +431,7 @@ cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_
                    ws.scan_part, &ek, &ev, st);
     if (e != cudaSuccess) return e;
     // the ping-pong key buffer not holding the sorted keys is free: window stream
-    uint16_t *ewin = reinterpret_cast<uint16_t *>((ek == ws.ekey_a) ? ws.ekey_b : ws.ekey_a);
+    uint32_t *ewin = (ek == ws.ekey_a) ? ws.ekey_b : ws.ekey_a;
     SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, ev, splats, &ws.ctr->entries_eff, ws.capE,
               ws.n_tiles, ws.n_tx, ws.tile_off, ewin);
     *order_out = order;

@@ -354,7 +354,7 @@ def main():
         "per_view_ms": {["near", "mid", "far"][k] if ncam == 3 else str(k): float(np.mean(v))
                         for k, v in sorted(per_view.items())},
         "stage_ms": mean_stage,
-        "frame_counts": [{k: s[k] for k in ("pairs_tested", "frustum_passed", "mlp_queried", "mlp_culled",
+        "frame_counts": [{k: s[k] for k in ("pairs_tested", "frustum_passed", "mlp_queried", "mlp_culled", "block_entries",
                                             "survivors", "passed", "entries")} for s in stats if s],
         "roofline": roof, "roofline_frame": frame_roof,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),

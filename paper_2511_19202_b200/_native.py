@@ -64,11 +64,11 @@ class ScScene(ctypes.Structure):
 
 
 STATS_FIELDS = ("instances_visible", "pairs_tested", "frustum_passed", "mlp_queried", "mlp_culled",
-                "survivors", "passed", "skipped", "entries", "used", "max_tie_run", "overflow")
+                "survivors", "passed", "skipped", "entries", "used", "max_tie_run", "overflow", "block_entries")
 
 
 class ScFrameStats(ctypes.Structure):
-    _fields_ = [(n, c_i64) for n in STATS_FIELDS] + [("reserved", c_i64 * 4)]
+    _fields_ = [(n, c_i64) for n in STATS_FIELDS] + [("reserved", c_i64 * 3)]
 
 
 class ScSurvivor(ctypes.Structure):

@@ -48,7 +48,8 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
     size_t inst, chunk_state, ctr, surv, splats, key_a, key_b, val_a, val_b, depth64, rect, ecount, ekey_a, ekey_b,
-        eval_a, eval_b, tile_off, task_order, hist, scan_part, total;
+        eval_a, eval_b, tile_off, task_order, boff, lidx, lcode, hist, scan_part, total;
+    int64_t capL;
     int64_t max_chunks, nblk_max, n_tiles;
     int n_tx, n_ty;
 };
@@ -88,6 +89,10 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.eval_b = take(4 * (size_t)capE);
     L.tile_off = take(4 * (size_t)(L.n_tiles + 1));
     L.task_order = take(4 * (size_t)(2 * L.n_tiles));
+    L.capL = 2 * capE;
+    L.boff = take(4 * (size_t)(8 * L.n_tiles + 1));
+    L.lidx = take(4 * (size_t)L.capL);
+    L.lcode = take(4 * (size_t)L.capL);
     L.hist = take(4 * (size_t)(256 * L.nblk_max));
     L.scan_part = take(4 * (size_t)part);
     L.total = off;
@@ -121,6 +126,10 @@ int carve(const sc_workspace *ws, int32_t w, int32_t h, sc::Ws &out)
     out.eval_b = reinterpret_cast<uint32_t *>(b + L.eval_b);
     out.tile_off = reinterpret_cast<uint32_t *>(b + L.tile_off);
     out.task_order = reinterpret_cast<uint32_t *>(b + L.task_order);
+    out.boff = reinterpret_cast<uint32_t *>(b + L.boff);
+    out.lidx = reinterpret_cast<uint32_t *>(b + L.lidx);
+    out.lcode = reinterpret_cast<uint32_t *>(b + L.lcode);
+    out.capL = L.capL;
     out.hist = reinterpret_cast<uint32_t *>(b + L.hist);
     out.scan_part = reinterpret_cast<uint32_t *>(b + L.scan_part);
     out.capS = ws->cap_survivors;
@@ -258,7 +267,7 @@ int sc_blend(const sc_splat *splats, int64_t n_splats, const uint32_t *entry_idx
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (opts->record_contributions && n_splats > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)n_splats, st), "memset contrib_max");
-    SC_TRY(sc::launch_blend(splats, entry_idx, tile_offsets, nullptr, *cam, *opts, *out, n_splats, nullptr, st),
+    SC_TRY(sc::launch_blend(splats, entry_idx, tile_offsets, nullptr, nullptr, *cam, *opts, *out, n_splats, nullptr, st),
            "blend");
     return SC_OK;
 }
@@ -297,7 +306,8 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
     SC_TRY(mark(3), "event");
     if (opts->record_contributions && w.capS > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
-    SC_TRY(sc::launch_blend(w.splats, entries, w.tile_off, ewin, *cam, *opts, *out, w.capS, w.task_order, st),
+    const sc::BlockLists lists{w.boff, w.lidx, w.lcode, &w.ctr->lists_ok};
+    SC_TRY(sc::launch_blend(w.splats, entries, w.tile_off, ewin, &lists, *cam, *opts, *out, w.capS, w.task_order, st),
            "blend");
     SC_TRY(mark(4), "event");
     if (opts->record_contributions)

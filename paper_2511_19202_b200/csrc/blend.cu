@@ -104,6 +104,10 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                                                             const uint32_t *__restrict__ entry_idx,
                                                             const uint32_t *__restrict__ tile_off,
                                                             const uint32_t *__restrict__ ewin,
+                                                            const uint32_t *__restrict__ boff,
+                                                            const uint32_t *__restrict__ lidx,
+                                                            const uint32_t *__restrict__ lcode,
+                                                            const unsigned long long *__restrict__ lists_ok,
                                                             const uint32_t *__restrict__ task_order, int width,
                                                             int height, int n_tx, float stop_t, float bg_r,
                                                             float bg_g, float bg_b, int record, float *image,
@@ -120,7 +124,20 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     const float fpx = (float)px, fpy = (float)py;
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cs = 0.0f;
     bool done = !inside;
-    const uint32_t start = tile_off[tile], end = tile_off[tile + 1];
+    // this warp's entry stream: its (tile, block) list when the binning pass built
+    // the lists, else the whole tile list (windows clipped from the records if
+    // no code stream is given — stage-level API)
+    uint32_t start, end;
+    const uint32_t *sidx = entry_idx, *scode = ewin;
+    if (boff && *lists_ok) {
+        start = boff[8 * tile + wid];
+        end = boff[8 * tile + wid + 1];
+        sidx = lidx;
+        scode = lcode;
+    } else {
+        start = tile_off[tile];
+        end = tile_off[tile + 1];
+    }
     // this warp's private rings: meta [kMetaStages][32] (index, code -> footprint), records [kRecStages][32][3]
     uint2 *meta = reinterpret_cast<uint2 *>(reinterpret_cast<char *>(s_dyn) + wid * (kMetaBytesW + kRecBytesW));
     float4 *recs = reinterpret_cast<float4 *>(reinterpret_cast<char *>(meta) + kMetaBytesW);
@@ -134,11 +151,11 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
         const uint32_t e = start + kG * q + lane;
         uint2 *dst = meta + ms * kG + lane;
         if (e < end) {
-            if (ewin) {
-                cp_async4(&dst->x, entry_idx + e);
-                cp_async4(&dst->y, ewin + e);
+            if (scode) {
+                cp_async4(&dst->x, sidx + e);
+                cp_async4(&dst->y, scode + e);
             } else {   // stage-level API without the binning pass: clip the record's window here
-                const uint32_t v = __ldg(entry_idx + e);
+                const uint32_t v = __ldg(sidx + e);
                 uint32_t code = kEmptyCode;
                 if ((int64_t)v < n_splats) {
                     const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + v) + 40));
@@ -311,7 +328,7 @@ __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev,
 }
 
 cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
-                         const uint32_t *ewin, const sc_camera &cam, const sc_opts &opts,
+                         const uint32_t *ewin, const BlockLists *lists, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
     static bool attr_set = false;
@@ -324,7 +341,8 @@ cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, cons
     const int64_t n_tiles = (int64_t)n_tx * n_ty;
     if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, tile_off, n_tiles, task_order);
     SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kBlendSmem, st, splats, n_splats, entry_idx, tile_off, ewin,
-              task_order, cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
+              lists ? lists->boff : nullptr, lists ? lists->lidx : nullptr, lists ? lists->lcode : nullptr,
+              lists ? lists->ok : nullptr, task_order, cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
               (float)opts.background[1], (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image,
               out.trans, out.contrib_sum, out.contrib_max);
     return cudaGetLastError();

@@ -393,6 +393,113 @@ __global__ void k_tile_offsets(const uint32_t *ekey, const uint32_t *eval, const
     }
 }
 
+// ---------------------------------------------------------------------------
+// per-(tile, 8x4 pixel block) entry lists for the blend: list (t, b) is the
+// stable (depth-order) subsequence of tile t's entries whose clipped window
+// touches block b (b = 2 row + col: x in [8 col, 8 col + 7], y in [4 row, 4 row + 3]).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kEmpty = 0x000Fu;   // empty window code (x0 = 15 > x1 = 0)
+
+__device__ __forceinline__ uint32_t code_blocks(uint32_t c)
+{
+    const uint32_t x0 = c & 15u, x1 = (c >> 4) & 15u, y0 = (c >> 8) & 15u, y1 = (c >> 12) & 15u;
+    if (x0 > x1 || y0 > y1) return 0u;
+    const uint32_t cols = (x0 <= 7u ? 1u : 0u) | (x1 >= 8u ? 2u : 0u);
+    const uint32_t r0 = y0 >> 2, r1 = y1 >> 2;
+    uint32_t m = 0u;
+#pragma unroll
+    for (uint32_t r = 0; r < 4; r++)
+        if (r >= r0 && r <= r1) m |= cols << (2 * r);
+    return m;
+}
+
+__global__ void __launch_bounds__(256) k_block_count(const uint32_t *tile_off, const uint32_t *ewin, uint32_t *bcnt)
+{
+    __shared__ uint32_t s_cnt[8][8];
+    const int tile = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t s = tile_off[tile], e = tile_off[tile + 1];
+    uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t i = s + wid * 32u + lane; i - lane < e; i += 256u) {
+        const uint32_t m = i < e ? code_blocks(__ldg(ewin + i)) : 0u;
+#pragma unroll
+        for (int b = 0; b < 8; b++) cnt[b] += __popc(__ballot_sync(0xffffffffu, (m >> b) & 1u));
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int b = 0; b < 8; b++) s_cnt[wid][b] = cnt[b];
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        uint32_t t = 0;
+        for (int w = 0; w < 8; w++) t += s_cnt[w][threadIdx.x];
+        bcnt[8 * (size_t)tile + threadIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_block_fill(const uint32_t *tile_off, const uint32_t *ewin,
+                                                    const uint32_t *entry_idx, uint32_t *boff, int64_t n_tiles,
+                                                    uint32_t *lidx, uint32_t *lcode, int64_t cap_l, Counters *ctr,
+                                                    sc_frame_stats *stats)
+{
+    __shared__ uint32_t s_cnt[8][8];   // [warp][block]: members in this chunk -> exclusive prefix
+    __shared__ uint32_t s_pos[8];      // next output position of each block list
+    const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned long long total = ctr->block_entries;
+    const bool ok = total <= (unsigned long long)cap_l;
+    if (blockIdx.x == 0 && tid == 0) {
+        ctr->lists_ok = ok ? 1ull : 0ull;
+        boff[8 * n_tiles] = (uint32_t)total;
+        stats->block_entries = (int64_t)total;
+        if (!ok) atomicOr((unsigned long long *)&stats->overflow, 4ull);
+    }
+    if (!ok) return;
+    const uint32_t s = tile_off[tile], e = tile_off[tile + 1];
+    if (tid < 8) s_pos[tid] = boff[8 * (size_t)tile + tid];
+    const uint32_t lt = lanemask_lt();
+    uint32_t i = s + tid;
+    uint32_t c = kEmpty, v = 0u;
+    if (i < e) {
+        c = __ldg(ewin + i);
+        v = __ldg(entry_idx + i);
+    }
+    for (uint32_t chunk = s; chunk < e; chunk += 256u, i += 256u) {
+        // prefetch the next chunk while this one is ranked
+        uint32_t nc = kEmpty, nv = 0u;
+        if (i + 256u < e) {
+            nc = __ldg(ewin + i + 256u);
+            nv = __ldg(entry_idx + i + 256u);
+        }
+        const uint32_t m = i < e ? code_blocks(c) : 0u;
+        uint32_t bal[8];
+#pragma unroll
+        for (int b = 0; b < 8; b++) bal[b] = __ballot_sync(0xffffffffu, (m >> b) & 1u);
+        if (lane == 0)
+#pragma unroll
+            for (int b = 0; b < 8; b++) s_cnt[wid][b] = __popc(bal[b]);
+        __syncthreads();
+        if (tid < 8) {
+            uint32_t run = s_pos[tid];
+            for (int w = 0; w < 8; w++) {
+                const uint32_t k = s_cnt[w][tid];
+                s_cnt[w][tid] = run;
+                run += k;
+            }
+            s_pos[tid] = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            if ((m >> b) & 1u) {
+                const uint32_t pos = s_cnt[wid][b] + __popc(bal[b] & lt);
+                lidx[pos] = v;
+                lcode[pos] = c;
+            }
+        }
+        __syncthreads();
+        c = nc;
+        v = nv;
+    }
+}
+
 static int grid_for(int64_t n, int threads)
 {
     int dev = 0, nsm = 148;
@@ -434,6 +541,12 @@ cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_
     uint32_t *ewin = (ek == ws.ekey_a) ? ws.ekey_b : ws.ekey_a;
     SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, ev, splats, &ws.ctr->entries_eff, ws.capE,
               ws.n_tiles, ws.n_tx, ws.tile_off, ewin);
+    // the blend's per-(tile, 8x4 block) lists: count, scan, stable fill
+    SC_LAUNCH(k_block_count, (int)ws.n_tiles, 256, 0, st, ws.tile_off, ewin, ws.boff);
+    e = scan_excl(ws.boff, ws.boff, nullptr, 8 * ws.n_tiles, ws.scan_part, &ws.ctr->block_entries, nullptr, st);
+    if (e != cudaSuccess) return e;
+    SC_LAUNCH(k_block_fill, (int)ws.n_tiles, 256, 0, st, ws.tile_off, ewin, ev, ws.boff, ws.n_tiles, ws.lidx, ws.lcode,
+              ws.capL, ws.ctr, stats);
     *order_out = order;
     *entries_out = ev;
     if (win_out) *win_out = ewin;

@@ -463,7 +463,8 @@ class Renderer:
             st = nat.stats_dict(frame.stats_raw.cpu().numpy())
             if not st["overflow"]:
                 break
-            self.workspace(cam).grow(st["survivors"], st["entries"])
+            # block lists live in 2 x cap_entries, so they grow with the entry capacity
+            self.workspace(cam).grow(st["survivors"], max(st["entries"], (st["block_entries"] + 1) // 2))
         else:
             raise nat.NativeError("workspace overflow persists after regrowing")
         render_ms = float(ev0.elapsed_time(ev1))

@@ -165,7 +165,7 @@ typedef struct sc_frame_stats {
     int64_t used;                /* splats with contribution_max > 0 (record mode) */
     int64_t max_tie_run;         /* longest run of equal f32 depth keys (tie-fix work) */
     int64_t overflow;            /* bit0 survivors, bit1 entries, bit2 block lists: re-render with more capacity */
-    int64_t block_entries;       /* (entry, 8x4 pixel block) pairs in the blend's per-warp lists */
+    int64_t block_entries;       /* frame path: (splat, 8x4 pixel block) entries binned for the blend */
     int64_t reserved[3];
 } sc_frame_stats;
 

@@ -48,8 +48,7 @@ size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
     size_t inst, chunk_state, ctr, surv, splats, key_a, key_b, val_a, val_b, depth64, rect, ecount, ekey_a, ekey_b,
-        eval_a, eval_b, tile_off, task_order, boff, lidx, lcode, hist, scan_part, total;
-    int64_t capL;
+        eval_a, eval_b, tile_off, task_order, boff, hist, scan_part, total;
     int64_t max_chunks, nblk_max, n_tiles;
     int n_tx, n_ty;
 };
@@ -89,10 +88,7 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.eval_b = take(4 * (size_t)capE);
     L.tile_off = take(4 * (size_t)(L.n_tiles + 1));
     L.task_order = take(4 * (size_t)(2 * L.n_tiles));
-    L.capL = 2 * capE;
     L.boff = take(4 * (size_t)(8 * L.n_tiles + 1));
-    L.lidx = take(4 * (size_t)L.capL);
-    L.lcode = take(4 * (size_t)L.capL);
     L.hist = take(4 * (size_t)(256 * L.nblk_max));
     L.scan_part = take(4 * (size_t)part);
     L.total = off;
@@ -127,9 +123,6 @@ int carve(const sc_workspace *ws, int32_t w, int32_t h, sc::Ws &out)
     out.tile_off = reinterpret_cast<uint32_t *>(b + L.tile_off);
     out.task_order = reinterpret_cast<uint32_t *>(b + L.task_order);
     out.boff = reinterpret_cast<uint32_t *>(b + L.boff);
-    out.lidx = reinterpret_cast<uint32_t *>(b + L.lidx);
-    out.lcode = reinterpret_cast<uint32_t *>(b + L.lcode);
-    out.capL = L.capL;
     out.hist = reinterpret_cast<uint32_t *>(b + L.hist);
     out.scan_part = reinterpret_cast<uint32_t *>(b + L.scan_part);
     out.capS = ws->cap_survivors;
@@ -228,7 +221,7 @@ static int run_bin(const sc_scene *scene, const sc_survivor *surv, const unsigne
     SC_TRY(sc::launch_project(*scene, surv, n_dev, n_max, *cam, *opts, splats, w.key_a, w.val_a, w.depth64, w.rect,
                               nullptr, nullptr, nullptr, stats, w.ctr, st),
            "project");
-    SC_TRY(sc::launch_bin(w, n_dev, n_max, *cam, splats, stats, order, entries, nullptr, st), "bin/sort");
+    SC_TRY(sc::launch_bin(w, n_dev, n_max, *cam, splats, stats, false, order, entries, nullptr, st), "bin/sort");
     return SC_OK;
 }
 
@@ -267,8 +260,8 @@ int sc_blend(const sc_splat *splats, int64_t n_splats, const uint32_t *entry_idx
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (opts->record_contributions && n_splats > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)n_splats, st), "memset contrib_max");
-    SC_TRY(sc::launch_blend(splats, entry_idx, tile_offsets, nullptr, nullptr, *cam, *opts, *out, n_splats, nullptr, st),
-           "blend");
+    const sc::BlendLists lists{tile_offsets, entry_idx, nullptr, false};
+    SC_TRY(sc::launch_blend(splats, lists, *cam, *opts, *out, n_splats, nullptr, st), "blend");
     return SC_OK;
 }
 
@@ -300,15 +293,14 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
            "project");
     SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;
-    uint32_t *ewin = nullptr;
-    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.splats, stats, &order, &entries, &ewin, st),
+    uint32_t *bkeys = nullptr;
+    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.splats, stats, true, &order, &entries, &bkeys, st),
            "bin/sort");
     SC_TRY(mark(3), "event");
     if (opts->record_contributions && w.capS > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
-    const sc::BlockLists lists{w.boff, w.lidx, w.lcode, &w.ctr->lists_ok};
-    SC_TRY(sc::launch_blend(w.splats, entries, w.tile_off, ewin, &lists, *cam, *opts, *out, w.capS, w.task_order, st),
-           "blend");
+    const sc::BlendLists lists{w.boff, entries, bkeys, true};
+    SC_TRY(sc::launch_blend(w.splats, lists, *cam, *opts, *out, w.capS, w.task_order, st), "blend");
     SC_TRY(mark(4), "event");
     if (opts->record_contributions)
         SC_TRY(sc::launch_count_used(out->contrib_max, &w.ctr->survivors, w.capS, stats, st), "count used");

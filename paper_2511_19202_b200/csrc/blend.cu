@@ -49,20 +49,14 @@ constexpr size_t kMetaBytesW = sizeof(uint2) * kG * kMetaStages;
 constexpr size_t kRecBytesW = sizeof(float4) * 3 * kG * kRecStages;
 constexpr size_t kBlendSmem = (kMetaBytesW + kRecBytesW) * kBlendWarps;
 
-// 32-bit footprint of the window [x0, x1] x [y0, y1] (tile-relative) on the 8x4 block at (bx0, by0)
-__device__ __forceinline__ uint32_t block_mask(int x0, int x1, int y0, int y1, int bx0, int by0)
+// 32-bit footprint (lane = 8 row + col) of a block-relative window code
+// x0 | x1 << 3 | y0 << 6 | y1 << 8 on the 8x4 block; 0 when x0 > x1
+__device__ __forceinline__ uint32_t code_mask(uint32_t c)
 {
-    const int lo = max(x0, bx0), hi = min(x1, bx0 + 7);
-    const int rlo = max(y0, by0), rhi = min(y1, by0 + 3);
-    if (lo > hi || rlo > rhi) return 0u;
-    const uint32_t cols = (0xFFu >> (7 - (hi - bx0))) & (0xFFu << (lo - bx0));
-    const uint32_t rows = (0x01010101u << (8 * (rlo - by0))) & (0x01010101u >> (8 * (3 - (rhi - by0))));
+    const uint32_t x0 = c & 7u, x1 = (c >> 3) & 7u, y0 = (c >> 6) & 3u, y1 = (c >> 8) & 3u;
+    const uint32_t cols = (0xFFu >> (7u - x1)) & (0xFFu << x0) & 0xFFu;
+    const uint32_t rows = (0x01010101u << (8u * y0)) & (0x01010101u >> (8u * (3u - y1)));
     return cols * rows;
-}
-
-__device__ __forceinline__ uint32_t code_mask(uint32_t c, int bx0, int by0)
-{
-    return block_mask(c & 15u, (c >> 4) & 15u, (c >> 8) & 15u, (c >> 12) & 15u, bx0, by0);
 }
 
 // 32x32 bit-matrix transpose across a warp: lane r holds row r on entry and
@@ -98,16 +92,12 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr uint32_t kNoEntry = 0xFFFFFFFFu;
-constexpr uint32_t kEmptyCode = 0x000Fu;   // x0 = 15 > x1 = 0
+constexpr uint32_t kEmptyCode = 0x0007u;   // x0 = 7 > x1 = 0
 
 __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
-                                                            const uint32_t *__restrict__ entry_idx,
-                                                            const uint32_t *__restrict__ tile_off,
-                                                            const uint32_t *__restrict__ ewin,
-                                                            const uint32_t *__restrict__ boff,
-                                                            const uint32_t *__restrict__ lidx,
-                                                            const uint32_t *__restrict__ lcode,
-                                                            const unsigned long long *__restrict__ lists_ok,
+                                                            const uint32_t *__restrict__ offsets,
+                                                            const uint32_t *__restrict__ vals,
+                                                            const uint32_t *__restrict__ keys, int blocks,
                                                             const uint32_t *__restrict__ task_order, int width,
                                                             int height, int n_tx, float stop_t, float bg_r,
                                                             float bg_g, float bg_b, int record, float *image,
@@ -124,20 +114,11 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     const float fpx = (float)px, fpy = (float)py;
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cs = 0.0f;
     bool done = !inside;
-    // this warp's entry stream: its (tile, block) list when the binning pass built
-    // the lists, else the whole tile list (windows clipped from the records if
-    // no code stream is given — stage-level API)
-    uint32_t start, end;
-    const uint32_t *sidx = entry_idx, *scode = ewin;
-    if (boff && *lists_ok) {
-        start = boff[8 * tile + wid];
-        end = boff[8 * tile + wid + 1];
-        sidx = lidx;
-        scode = lcode;
-    } else {
-        start = tile_off[tile];
-        end = tile_off[tile + 1];
-    }
+    // this warp's entry stream: its (tile, block) list in the frame path, else
+    // the whole tile list (stage-level API; windows clipped from the records)
+    const uint32_t start = blocks ? offsets[8 * tile + wid] : offsets[tile];
+    const uint32_t end = blocks ? offsets[8 * tile + wid + 1] : offsets[tile + 1];
+    const int gx0 = ox + bx0, gy0 = oy + by0;                  // warp block, absolute pixels
     // this warp's private rings: meta [kMetaStages][32] (index, code -> footprint), records [kRecStages][32][3]
     uint2 *meta = reinterpret_cast<uint2 *>(reinterpret_cast<char *>(s_dyn) + wid * (kMetaBytesW + kRecBytesW));
     float4 *recs = reinterpret_cast<float4 *>(reinterpret_cast<char *>(meta) + kMetaBytesW);
@@ -151,17 +132,18 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
         const uint32_t e = start + kG * q + lane;
         uint2 *dst = meta + ms * kG + lane;
         if (e < end) {
-            if (scode) {
-                cp_async4(&dst->x, sidx + e);
-                cp_async4(&dst->y, scode + e);
-            } else {   // stage-level API without the binning pass: clip the record's window here
-                const uint32_t v = __ldg(sidx + e);
+            if (blocks) {   // key = block id << 10 | block-relative window (masked in issue_rec)
+                cp_async4(&dst->x, vals + e);
+                cp_async4(&dst->y, keys + e);
+            } else {        // tile list: clip the record's window to this warp's block here
+                const uint32_t v = __ldg(vals + e);
                 uint32_t code = kEmptyCode;
                 if ((int64_t)v < n_splats) {
                     const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + v) + 40));
-                    const int x0 = max(lo16(w.x) - ox, 0), x1 = min(hi16(w.x) - ox, 15);
-                    const int y0 = max(lo16(w.y) - oy, 0), y1 = min(hi16(w.y) - oy, 15);
-                    if (x0 <= x1 && y0 <= y1) code = (uint32_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12));
+                    const int x0 = max(lo16(w.x), gx0), x1 = min(hi16(w.x), gx0 + 7);
+                    const int y0 = max(lo16(w.y), gy0), y1 = min(hi16(w.y), gy0 + 3);
+                    if (x0 <= x1 && y0 <= y1)
+                        code = (uint32_t)((x0 - gx0) | ((x1 - gx0) << 3) | ((y0 - gy0) << 6) | ((y1 - gy0) << 8));
                 }
                 *dst = make_uint2(v, code);
             }
@@ -174,7 +156,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     auto issue_rec = [&](int ms, int rs, uint32_t alive) {
         uint2 *m = meta + ms * kG + lane;
         const uint2 v = *m;
-        const uint32_t fp = ((int64_t)v.x < n_splats) ? (code_mask(v.y, bx0, by0) & alive) : 0u;
+        const uint32_t fp = ((int64_t)v.x < n_splats) ? (code_mask(v.y & 0x3FFu) & alive) : 0u;
         m->y = fp;
         if (fp) {
             const float4 *src = reinterpret_cast<const float4 *>(splats + v.x);
@@ -290,15 +272,23 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     }
 }
 
-// LPT dispatch order: heavier tiles first (bucketed by floor(log2(entries));
-// the order inside a bucket is irrelevant to the result).
-__global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *tile_off, int64_t n_tiles, uint32_t *order)
+// LPT dispatch order: heavier tiles first, bucketed by floor(log2(weight)),
+// weight = the longest list among the tile's `stride` lists (the tile's
+// critical path); the order inside a bucket is irrelevant to the result.
+__device__ __forceinline__ uint32_t tile_weight(const uint32_t *off, int64_t t, int stride)
+{
+    uint32_t w = 0;
+    for (int b = 0; b < stride; b++) w = max(w, off[stride * t + b + 1] - off[stride * t + b]);
+    return w;
+}
+
+__global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_t n_tiles, int stride, uint32_t *order)
 {
     __shared__ uint32_t hist[33], base[33];
     if (threadIdx.x < 33) hist[threadIdx.x] = 0;
     __syncthreads();
     for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-        const uint32_t c = tile_off[t + 1] - tile_off[t];
+        const uint32_t c = tile_weight(off, t, stride);
         atomicAdd(&hist[c ? 32 - __clz(c) : 0], 1u);
     }
     __syncthreads();
@@ -311,7 +301,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *tile_off, i
     }
     __syncthreads();
     for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-        const uint32_t c = tile_off[t + 1] - tile_off[t];
+        const uint32_t c = tile_weight(off, t, stride);
         order[atomicAdd(&base[c ? 32 - __clz(c) : 0], 1u)] = (uint32_t)t;
     }
 }
@@ -327,8 +317,7 @@ __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev,
     if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)&stats->used, c);
 }
 
-cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
-                         const uint32_t *ewin, const BlockLists *lists, const sc_camera &cam, const sc_opts &opts,
+cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
     static bool attr_set = false;
@@ -339,10 +328,9 @@ cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, cons
     }
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const int64_t n_tiles = (int64_t)n_tx * n_ty;
-    if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, tile_off, n_tiles, task_order);
-    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kBlendSmem, st, splats, n_splats, entry_idx, tile_off, ewin,
-              lists ? lists->boff : nullptr, lists ? lists->lidx : nullptr, lists ? lists->lcode : nullptr,
-              lists ? lists->ok : nullptr, task_order, cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
+    if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, n_tiles, lists.blocks ? 8 : 1, task_order);
+    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kBlendSmem, st, splats, n_splats, lists.offsets, lists.vals,
+              lists.keys, lists.blocks ? 1 : 0, task_order, cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
               (float)opts.background[1], (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image,
               out.trans, out.contrib_sum, out.contrib_max);
     return cudaGetLastError();

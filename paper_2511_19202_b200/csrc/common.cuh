@@ -39,8 +39,6 @@ struct Counters {
     unsigned long long entries_eff;    // entries, or 0 when they overflow the workspace
     unsigned long long dmin_inv;       // ~bits(min passed depth)  (atomicMax of ~bits; 0 = none)
     unsigned long long dmax;           // bits(max passed depth)   (positive doubles order as u64)
-    unsigned long long block_entries;  // total length of the per-block lists
-    unsigned long long lists_ok;       // 1 if the block lists fit the workspace
 };
 
 // Workspace carve-out (all offsets 256-byte aligned), see api.cu:carve().
@@ -60,8 +58,6 @@ struct Ws {
     uint32_t *tile_off;              // [n_tiles + 1]
     uint32_t *task_order;            // [2 n_tiles] blend dispatch order (heavy tiles first)
     uint32_t *boff;                  // [8 n_tiles + 1] offsets of the per-(tile, 8x4 block) entry lists
-    uint32_t *lidx, *lcode;          // [capL] block lists: survivor index, tile-relative window code
-    int64_t capL;                    // = 2 capE
     uint32_t *hist;                  // radix histograms [256 * nblk_max]
     uint32_t *scan_part;             // scan partials
     int64_t capS, capE, max_chunks, nblk_max, n_tiles;
@@ -143,16 +139,20 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
                            int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr,
                            cudaStream_t st);
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
-                       const sc_splat *splats, sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out,
-                       uint32_t **win_out, cudaStream_t st);
-// per-(tile, 8x4 block) entry lists built by launch_bin for the blend
-struct BlockLists {
-    const uint32_t *boff, *lidx, *lcode;
-    const unsigned long long *ok;
+                       const sc_splat *splats, sc_frame_stats *stats, bool blocks, uint32_t **order_out,
+                       uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st);
+// Blend input, one of:
+//  * block lists (frame path): boff [8 n_tiles + 1], vals = survivor per entry,
+//    keys = block id << 10 | block-relative window;
+//  * tile lists (stage-level API): tile_off [n_tiles + 1], vals = entry_idx,
+//    keys = NULL (windows read from the splat records).
+struct BlendLists {
+    const uint32_t *offsets;
+    const uint32_t *vals;
+    const uint32_t *keys;
+    bool blocks;
 };
-// ewin: entry-aligned tile-relative windows from launch_bin, or NULL (gathered from the records)
-cudaError_t launch_blend(const sc_splat *splats, const uint32_t *entry_idx, const uint32_t *tile_off,
-                         const uint32_t *ewin, const BlockLists *lists, const sc_camera &cam, const sc_opts &opts,
+cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st);
 cudaError_t launch_vis_mlp(const sc_vis_weights *w, const float *x, int64_t n, float *logits,
                            cudaStream_t st);

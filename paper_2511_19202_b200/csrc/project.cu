@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
     const double focal = cam.focal;
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const double log_min_alpha = log(1.0 / 255.0);
-    unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0;
+    unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0;
 
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
         const sc_survivor sv = surv[k];
@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
         }
         n_passed += passed;
         if (passed) {
+            n_tentries += (unsigned long long)((tx1 - tx0) * (ty1 - ty0));   // reference tile entries
             const unsigned long long bits = (unsigned long long)__double_as_longlong(tz);
             dmin_inv = max(dmin_inv, ~bits);
             dmax_bits = max(dmax_bits, bits);
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
     for (int o = 16; o > 0; o >>= 1) {
         n_passed += __shfl_down_sync(0xffffffffu, n_passed, o);
         n_skipped += __shfl_down_sync(0xffffffffu, n_skipped, o);
+        n_tentries += __shfl_down_sync(0xffffffffu, n_tentries, o);
         dmin_inv = max(dmin_inv, __shfl_down_sync(0xffffffffu, dmin_inv, o));
         dmax_bits = max(dmax_bits, __shfl_down_sync(0xffffffffu, dmax_bits, o));
     }
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
             }
         }
         if (n_skipped) atomicAdd((unsigned long long *)&stats->skipped, n_skipped);
+        if (n_tentries) atomicAdd((unsigned long long *)&stats->entries, n_tentries);
     }
 }
 

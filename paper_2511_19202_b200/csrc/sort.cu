@@ -249,13 +249,14 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t 
 
 // Sorts (keys, vals) in place-ish over `bits` low bits; result ends in the
 // buffer pointed to by *keys_res / *vals_res (ping-pong).
+// Sorts on key bits [bit_lo, bit_hi) (8-bit digits; bits below bit_lo ride along unsorted).
 static cudaError_t radix_sort(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, const unsigned long long *n_dev,
-                              int64_t n_max, int bits, uint32_t *hist, uint32_t *part, uint32_t **keys_res,
-                              uint32_t **vals_res, cudaStream_t st)
+                              int64_t n_max, int bit_lo, int bit_hi, uint32_t *hist, uint32_t *part,
+                              uint32_t **keys_res, uint32_t **vals_res, cudaStream_t st)
 {
     const int64_t nblk = std::max<int64_t>(1, (n_max + kRadixTile - 1) / kRadixTile);
     uint32_t *ki = ka, *vi = va, *ko = kb, *vo = vb;
-    for (int shift = 0; shift < bits; shift += 8) {
+    for (int shift = bit_lo; shift < bit_hi; shift += 8) {
         SC_LAUNCH(k_radix_hist, (int)nblk, kRadixThreads, 0, st, ki, n_dev, n_max, shift, hist, nblk);
         cudaError_t e = scan_excl(hist, hist, nullptr, 256 * nblk, part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;
@@ -367,136 +368,93 @@ __global__ void k_entry_emit(const uint32_t *order, const uint32_t *rlo, const u
     }
 }
 
-// tile_off[t] = first entry index with tile >= t, for t in [0, n_tiles]; and
-// each entry's pixel window clipped to its tile, 4 bits per bound
-// (x0 | x1 << 4 | y0 << 8 | y1 << 12, tile-relative; x0 > x1 = empty),
-// gathered once here so the blend's 8 warps per tile stream 2 bytes per
-// entry instead of each re-gathering the window from the splat records.
-__global__ void k_tile_offsets(const uint32_t *ekey, const uint32_t *eval, const sc_splat *splats,
-                               const unsigned long long *e_dev, int64_t cap_e, int64_t n_tiles, int n_tx,
-                               uint32_t *tile_off, uint32_t *ewin)
+// tile_off[t] = first entry index with tile >= t, for t in [0, n_tiles] (the
+// reference's `counts`; stage-level API only)
+__global__ void k_tile_offsets(const uint32_t *ekey, const unsigned long long *e_dev, int64_t cap_e, int64_t n_tiles,
+                               uint32_t *tile_off)
 {
     const int64_t E = std::min<int64_t>((int64_t)*e_dev, cap_e);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= E; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t prev = i > 0 ? (int64_t)ekey[i - 1] : -1;
         const int64_t cur = i < E ? (int64_t)ekey[i] : n_tiles;
         for (int64_t t = prev + 1; t <= cur; t++) tile_off[t] = (uint32_t)i;
-        if (i < E) {
-            const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + eval[i]) + 40));
-            const int tile = (int)cur, ox = (tile % n_tx) * kTile, oy = (tile / n_tx) * kTile;
-            const int x0 = max((int)(int16_t)(w.x & 0xFFFF) - ox, 0), x1 = min((int)(int16_t)(w.x >> 16) - ox, 15);
-            const int y0 = max((int)(int16_t)(w.y & 0xFFFF) - oy, 0), y1 = min((int)(int16_t)(w.y >> 16) - oy, 15);
-            uint32_t code = 0x000F;   // empty
-            if (x0 <= x1 && y0 <= y1) code = (uint32_t)(x0 | (x1 << 4) | (y0 << 8) | (y1 << 12));
-            ewin[i] = code;
-        }
     }
 }
 
 // ---------------------------------------------------------------------------
-// per-(tile, 8x4 pixel block) entry lists for the blend: list (t, b) is the
-// stable (depth-order) subsequence of tile t's entries whose clipped window
-// touches block b (b = 2 row + col: x in [8 col, 8 col + 7], y in [4 row, 4 row + 3]).
+// Frame-path binning: 8x4 pixel blocks instead of 16x16 tiles.
+//
+// Each passed splat (in depth order) emits one entry per 8x4 block its pixel
+// window touches; block b of tile t has id 8 t + b (b = 2 row + col: x in
+// [8 col, 8 col + 7], y in [4 row, 4 row + 3]), so a tile's blocks are
+// contiguous.  The sort key is id << 10 | the window clipped to the block
+// (x0 | x1 << 3 | y0 << 6 | y1 << 8, block-relative); the radix sort only
+// sorts the id bits, so the clipped window rides along.  Being a stable sort
+// of the depth-ordered emission, block list (t, b) is exactly the depth-order
+// subsequence of the reference's tile-t entry list whose window touches
+// block b (the only entries the reference composites onto those pixels):
+// one blend warp walks one list.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kEmpty = 0x000Fu;   // empty window code (x0 = 15 > x1 = 0)
+constexpr int kCodeBits = 10;
 
-__device__ __forceinline__ uint32_t code_blocks(uint32_t c)
+__global__ void k_bentry_count(const uint32_t *order, const sc_splat *splats, const unsigned long long *n_dev,
+                               int64_t n_host, int width, int height, uint32_t *cnt, uint32_t *wlo, uint32_t *whi)
 {
-    const uint32_t x0 = c & 15u, x1 = (c >> 4) & 15u, y0 = (c >> 8) & 15u, y1 = (c >> 12) & 15u;
-    if (x0 > x1 || y0 > y1) return 0u;
-    const uint32_t cols = (x0 <= 7u ? 1u : 0u) | (x1 >= 8u ? 2u : 0u);
-    const uint32_t r0 = y0 >> 2, r1 = y1 >> 2;
-    uint32_t m = 0u;
-#pragma unroll
-    for (uint32_t r = 0; r < 4; r++)
-        if (r >= r0 && r <= r1) m |= cols << (2 * r);
-    return m;
-}
-
-__global__ void __launch_bounds__(256) k_block_count(const uint32_t *tile_off, const uint32_t *ewin, uint32_t *bcnt)
-{
-    __shared__ uint32_t s_cnt[8][8];
-    const int tile = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t s = tile_off[tile], e = tile_off[tile + 1];
-    uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (uint32_t i = s + wid * 32u + lane; i - lane < e; i += 256u) {
-        const uint32_t m = i < e ? code_blocks(__ldg(ewin + i)) : 0u;
-#pragma unroll
-        for (int b = 0; b < 8; b++) cnt[b] += __popc(__ballot_sync(0xffffffffu, (m >> b) & 1u));
-    }
-    if (lane == 0)
-#pragma unroll
-        for (int b = 0; b < 8; b++) s_cnt[wid][b] = cnt[b];
-    __syncthreads();
-    if (threadIdx.x < 8) {
-        uint32_t t = 0;
-        for (int w = 0; w < 8; w++) t += s_cnt[w][threadIdx.x];
-        bcnt[8 * (size_t)tile + threadIdx.x] = t;
+    const int64_t n = dev_count(n_dev, n_host);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + order[k]) + 40));
+        // pixels outside the image are never composited (reference th/tw clamp)
+        const int x0 = max((int)(int16_t)(w.x & 0xFFFF), 0), x1 = min((int)(int16_t)(w.x >> 16), width - 1);
+        const int y0 = max((int)(int16_t)(w.y & 0xFFFF), 0), y1 = min((int)(int16_t)(w.y >> 16), height - 1);
+        uint32_t c = 0;
+        if (x0 <= x1 && y0 <= y1) c = (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
+        cnt[k] = c;
+        wlo[k] = (uint32_t)x0 | ((uint32_t)x1 << 16);
+        whi[k] = (uint32_t)y0 | ((uint32_t)y1 << 16);
     }
 }
 
-__global__ void __launch_bounds__(256) k_block_fill(const uint32_t *tile_off, const uint32_t *ewin,
-                                                    const uint32_t *entry_idx, uint32_t *boff, int64_t n_tiles,
-                                                    uint32_t *lidx, uint32_t *lcode, int64_t cap_l, Counters *ctr,
-                                                    sc_frame_stats *stats)
+__global__ void k_bentry_emit(const uint32_t *order, const uint32_t *wlo, const uint32_t *whi, const uint32_t *off,
+                              const unsigned long long *n_dev, int64_t n_host, int n_tx, uint32_t *ekey,
+                              uint32_t *eval, const unsigned long long *e_total, unsigned long long *e_eff,
+                              int64_t cap_e, sc_frame_stats *stats)
 {
-    __shared__ uint32_t s_cnt[8][8];   // [warp][block]: members in this chunk -> exclusive prefix
-    __shared__ uint32_t s_pos[8];      // next output position of each block list
-    const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const unsigned long long total = ctr->block_entries;
-    const bool ok = total <= (unsigned long long)cap_l;
-    if (blockIdx.x == 0 && tid == 0) {
-        ctr->lists_ok = ok ? 1ull : 0ull;
-        boff[8 * n_tiles] = (uint32_t)total;
-        stats->block_entries = (int64_t)total;
-        if (!ok) atomicOr((unsigned long long *)&stats->overflow, 4ull);
+    const int64_t n = dev_count(n_dev, n_host);
+    const bool over = (int64_t)*e_total > cap_e;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *e_eff = over ? 0ull : *e_total;
+        stats->block_entries = (int64_t)*e_total;
+        if (over) atomicOr((unsigned long long *)&stats->overflow, 2ull);
     }
-    if (!ok) return;
-    const uint32_t s = tile_off[tile], e = tile_off[tile + 1];
-    if (tid < 8) s_pos[tid] = boff[8 * (size_t)tile + tid];
-    const uint32_t lt = lanemask_lt();
-    uint32_t i = s + tid;
-    uint32_t c = kEmpty, v = 0u;
-    if (i < e) {
-        c = __ldg(ewin + i);
-        v = __ldg(entry_idx + i);
-    }
-    for (uint32_t chunk = s; chunk < e; chunk += 256u, i += 256u) {
-        // prefetch the next chunk while this one is ranked
-        uint32_t nc = kEmpty, nv = 0u;
-        if (i + 256u < e) {
-            nc = __ldg(ewin + i + 256u);
-            nv = __ldg(entry_idx + i + 256u);
-        }
-        const uint32_t m = i < e ? code_blocks(c) : 0u;
-        uint32_t bal[8];
-#pragma unroll
-        for (int b = 0; b < 8; b++) bal[b] = __ballot_sync(0xffffffffu, (m >> b) & 1u);
-        if (lane == 0)
-#pragma unroll
-            for (int b = 0; b < 8; b++) s_cnt[wid][b] = __popc(bal[b]);
-        __syncthreads();
-        if (tid < 8) {
-            uint32_t run = s_pos[tid];
-            for (int w = 0; w < 8; w++) {
-                const uint32_t k = s_cnt[w][tid];
-                s_cnt[w][tid] = run;
-                run += k;
-            }
-            s_pos[tid] = run;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int b = 0; b < 8; b++) {
-            if ((m >> b) & 1u) {
-                const uint32_t pos = s_cnt[wid][b] + __popc(bal[b] & lt);
-                lidx[pos] = v;
-                lcode[pos] = c;
+    if (over) return;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = wlo[k], b = whi[k];
+        const int x0 = (int)(a & 0xFFFF), x1 = (int)(a >> 16), y0 = (int)(b & 0xFFFF), y1 = (int)(b >> 16);
+        if (x0 > x1 || y0 > y1) continue;
+        const uint32_t sv = order[k];
+        uint32_t o = off[k];
+        for (int by = y0 >> 2; by <= (y1 >> 2); by++) {
+            const int ry0 = max(y0 - 4 * by, 0), ry1 = min(y1 - 4 * by, 3);
+            for (int bx = x0 >> 3; bx <= (x1 >> 3); bx++) {
+                const int rx0 = max(x0 - 8 * bx, 0), rx1 = min(x1 - 8 * bx, 7);
+                const uint32_t id = (uint32_t)(((by >> 2) * n_tx + (bx >> 1)) * 8 + (by & 3) * 2 + (bx & 1));
+                ekey[o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
+                eval[o] = sv;
+                o++;
             }
         }
-        __syncthreads();
-        c = nc;
-        v = nv;
+    }
+}
+
+// boff[b] = first entry with block id >= b, for b in [0, n_blocks]
+__global__ void k_block_offsets(const uint32_t *ekey, const unsigned long long *e_dev, int64_t cap_e,
+                                int64_t n_blocks, uint32_t *boff)
+{
+    const int64_t E = std::min<int64_t>((int64_t)*e_dev, cap_e);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= E; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev = i > 0 ? (int64_t)(ekey[i - 1] >> kCodeBits) : -1;
+        const int64_t cur = i < E ? (int64_t)(ekey[i] >> kCodeBits) : n_blocks;
+        for (int64_t t = prev + 1; t <= cur; t++) boff[t] = (uint32_t)i;
     }
 }
 
@@ -508,48 +466,62 @@ static int grid_for(int64_t n, int threads)
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)nsm * 16));
 }
 
-// n_dev: survivor count (device).  Inputs: ws.key_a / val_a / depth64 / rect
-// from the projection.  Outputs: order (passed survivors by (depth, index)),
-// entries (survivor index per entry, tile-major), ws.tile_off, stats.entries.
+static int bits_for(int64_t n)
+{
+    int b = 0;
+    while ((1ll << b) < n) b++;
+    return b;
+}
+
+// n_dev: survivor count (device).  Inputs: ws.depth64 / rect and the splat
+// records from the projection.  Always: order = passed survivors by (depth,
+// index).  blocks = true (frame path): block lists (entries_out = survivor per
+// entry, keys_out = id << 10 | window, ws.boff).  blocks = false (stage-level
+// API, parity with the reference): tile entries and ws.tile_off, exactly
+// bin_tiles' output.
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
-                       const sc_splat *splats, sc_frame_stats *stats, uint32_t **order_out, uint32_t **entries_out,
-                       uint32_t **win_out, cudaStream_t st)
+                       const sc_splat *splats, sc_frame_stats *stats, bool blocks, uint32_t **order_out,
+                       uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st)
 {
     cudaError_t e;
     uint32_t *keys_s = nullptr, *order = nullptr;
     SC_LAUNCH(k_depth_keys, grid_for(n_max, 256), 256, 0, st, ws.depth64, n_dev, n_max, ws.ctr, ws.key_a, ws.val_a);
-    e = radix_sort(ws.key_a, ws.val_a, ws.key_b, ws.val_b, n_dev, n_max, 32, ws.hist, ws.scan_part, &keys_s, &order,
+    e = radix_sort(ws.key_a, ws.val_a, ws.key_b, ws.val_b, n_dev, n_max, 0, 32, ws.hist, ws.scan_part, &keys_s, &order,
                    st);
     if (e != cudaSuccess) return e;
     const unsigned long long *p_dev = &ws.ctr->passed;   // passed splats lead the sorted order
     SC_LAUNCH(k_tiefix, grid_for(n_max, 256), 256, 0, st, keys_s, order, ws.depth64, p_dev, n_max, stats);
-    // both key buffers are free once the tie-fix is done: depth-ordered rects
+    // both key buffers are free once the tie-fix is done: depth-ordered rects / windows
     uint32_t *rlo = ws.key_a, *rhi = ws.key_b;
-    SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, ws.ecount, rlo, rhi);
-    e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, &stats->entries, st);
-    if (e != cudaSuccess) return e;
-    SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max, ws.n_tx,
-              ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
-    int bits = 0;
-    while ((1ll << bits) < ws.n_tiles) bits += 8;
     uint32_t *ek = nullptr, *ev = nullptr;
-    if (bits == 0) bits = 8;
-    e = radix_sort(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, bits, ws.hist,
-                   ws.scan_part, &ek, &ev, st);
-    if (e != cudaSuccess) return e;
-    // the ping-pong key buffer not holding the sorted keys is free: window stream
-    uint32_t *ewin = (ek == ws.ekey_a) ? ws.ekey_b : ws.ekey_a;
-    SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, ev, splats, &ws.ctr->entries_eff, ws.capE,
-              ws.n_tiles, ws.n_tx, ws.tile_off, ewin);
-    // the blend's per-(tile, 8x4 block) lists: count, scan, stable fill
-    SC_LAUNCH(k_block_count, (int)ws.n_tiles, 256, 0, st, ws.tile_off, ewin, ws.boff);
-    e = scan_excl(ws.boff, ws.boff, nullptr, 8 * ws.n_tiles, ws.scan_part, &ws.ctr->block_entries, nullptr, st);
-    if (e != cudaSuccess) return e;
-    SC_LAUNCH(k_block_fill, (int)ws.n_tiles, 256, 0, st, ws.tile_off, ewin, ev, ws.boff, ws.n_tiles, ws.lidx, ws.lcode,
-              ws.capL, ws.ctr, stats);
+    if (blocks) {
+        SC_LAUNCH(k_bentry_count, grid_for(n_max, 256), 256, 0, st, order, splats, p_dev, n_max, cam.width, cam.height,
+                  ws.ecount, rlo, rhi);
+        e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, nullptr, st);
+        if (e != cudaSuccess) return e;
+        SC_LAUNCH(k_bentry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max, ws.n_tx,
+                  ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
+        const int64_t n_blocks = 8 * ws.n_tiles;
+        e = radix_sort(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, kCodeBits,
+                       kCodeBits + bits_for(n_blocks), ws.hist, ws.scan_part, &ek, &ev, st);
+        if (e != cudaSuccess) return e;
+        SC_LAUNCH(k_block_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE, n_blocks,
+                  ws.boff);
+    } else {
+        SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, ws.ecount, rlo, rhi);
+        e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, &stats->entries, st);
+        if (e != cudaSuccess) return e;
+        SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max, ws.n_tx,
+                  ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
+        e = radix_sort(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, 0,
+                       std::max(1, bits_for(ws.n_tiles)), ws.hist, ws.scan_part, &ek, &ev, st);
+        if (e != cudaSuccess) return e;
+        SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE,
+                  ws.n_tiles, ws.tile_off);
+    }
     *order_out = order;
     *entries_out = ev;
-    if (win_out) *win_out = ewin;
+    if (keys_out) *keys_out = ek;
     return cudaGetLastError();
 }
 

@@ -463,8 +463,8 @@ class Renderer:
             st = nat.stats_dict(frame.stats_raw.cpu().numpy())
             if not st["overflow"]:
                 break
-            # block lists live in 2 x cap_entries, so they grow with the entry capacity
-            self.workspace(cam).grow(st["survivors"], max(st["entries"], (st["block_entries"] + 1) // 2))
+            # the frame path bins (splat, 8x4 block) pairs: block_entries of them
+            self.workspace(cam).grow(st["survivors"], max(st["entries"], st["block_entries"]))
         else:
             raise nat.NativeError("workspace overflow persists after regrowing")
         render_ms = float(ev0.elapsed_time(ev1))

@@ -205,13 +205,16 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
             // L = log(op) - log(1/255): |dx| <= sqrt(2 L cov_xx).  Pixels outside the
             // box fail the reference's `power < p_min` test, so the image is
             // unchanged; the box is widened by 1e-6 relative + 1e-3 px for safety.
+            // Also clipped to the splat's tile rectangle in pixels: the reference only
+            // composites a splat inside tiles whose list holds it, and its window can
+            // reach one pixel past the rect (A8 step 3).
             const double L = log_op - log_min_alpha;
             const double ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-6) + 1e-3;
             const double ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-6) + 1e-3;
-            sp.win[0] = clamp16(fmax(floor(mx - radius), ceil(mx - ex)));
-            sp.win[1] = clamp16(fmin(floor(mx + radius) + 1.0, floor(mx + ex)));
-            sp.win[2] = clamp16(fmax(floor(my - radius), ceil(my - ey)));
-            sp.win[3] = clamp16(fmin(floor(my + radius) + 1.0, floor(my + ey)));
+            sp.win[0] = clamp16(fmax(fmax(floor(mx - radius), ceil(mx - ex)), (double)(kTile * tx0)));
+            sp.win[1] = clamp16(fmin(fmin(floor(mx + radius) + 1.0, floor(mx + ex)), (double)(kTile * tx1 - 1)));
+            sp.win[2] = clamp16(fmax(fmax(floor(my - radius), ceil(my - ey)), (double)(kTile * ty0)));
+            sp.win[3] = clamp16(fmin(fmin(floor(my + radius) + 1.0, floor(my + ey)), (double)(kTile * ty1 - 1)));
         } else {   // skipped by the blend (reference: `op < min_alpha: continue`)
             sp.win[0] = 1;
             sp.win[1] = 0;

@@ -427,20 +427,57 @@ __global__ void k_bentry_emit(const uint32_t *order, const uint32_t *wlo, const 
         if (over) atomicOr((unsigned long long *)&stats->overflow, 2ull);
     }
     if (over) return;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = wlo[k], b = whi[k];
-        const int x0 = (int)(a & 0xFFFF), x1 = (int)(a >> 16), y0 = (int)(b & 0xFFFF), y1 = (int)(b >> 16);
-        if (x0 > x1 || y0 > y1) continue;
-        const uint32_t sv = order[k];
-        uint32_t o = off[k];
-        for (int by = y0 >> 2; by <= (y1 >> 2); by++) {
-            const int ry0 = max(y0 - 4 * by, 0), ry1 = min(y1 - 4 * by, 3);
-            for (int bx = x0 >> 3; bx <= (x1 >> 3); bx++) {
-                const int rx0 = max(x0 - 8 * bx, 0), rx1 = min(x1 - 8 * bx, 7);
+    // Warp-cooperative, load-balanced: a warp owns 32 consecutive splats and
+    // emits their (contiguous) entries 32 at a time, lane l producing output
+    // o = step + l; the owning splat is found by an upper-bound search over the
+    // warp's exclusive counts (5 shuffles).  Splats covering thousands of
+    // blocks (close to the camera) no longer serialise one thread, and the
+    // stores are coalesced.
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 32; base < n; base += n_warps * 32) {
+        const int64_t k = base + lane;
+        int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
+        uint32_t sv = 0;
+        if (k < n) {
+            const uint32_t a = wlo[k], b = whi[k];
+            x0 = (int)(a & 0xFFFF);
+            x1 = (int)(a >> 16);
+            y0 = (int)(b & 0xFFFF);
+            y1 = (int)(b >> 16);
+            sv = order[k];
+        }
+        const uint32_t cnt = (x0 <= x1 && y0 <= y1) ? (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1)) : 0u;
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
+            if (lane >= s) incl += y;
+        }
+        const uint32_t excl = incl - cnt;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t obase = __shfl_sync(0xffffffffu, off[base], 0);
+        for (uint32_t o0 = 0; o0 < total; o0 += 32) {
+            const uint32_t o = o0 + lane;
+            int s = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t e = __shfl_sync(0xffffffffu, excl, s + step);
+                if (e <= o) s += step;
+            }
+            const uint32_t li = o - __shfl_sync(0xffffffffu, excl, s);
+            const int X0 = __shfl_sync(0xffffffffu, x0, s), X1 = __shfl_sync(0xffffffffu, x1, s);
+            const int Y0 = __shfl_sync(0xffffffffu, y0, s), Y1 = __shfl_sync(0xffffffffu, y1, s);
+            const uint32_t v = __shfl_sync(0xffffffffu, sv, s);
+            if (o < total) {
+                const int w = X1 / 8 - X0 / 8 + 1;
+                const int bx = X0 / 8 + (int)(li % (uint32_t)w), by = Y0 / 4 + (int)(li / (uint32_t)w);
+                const int rx0 = max(X0 - 8 * bx, 0), rx1 = min(X1 - 8 * bx, 7);
+                const int ry0 = max(Y0 - 4 * by, 0), ry1 = min(Y1 - 4 * by, 3);
                 const uint32_t id = (uint32_t)(((by >> 2) * n_tx + (bx >> 1)) * 8 + (by & 3) * 2 + (bx & 1));
-                ekey[o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
-                eval[o] = sv;
-                o++;
+                ekey[obase + o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
+                eval[obase + o] = v;
             }
         }
     }

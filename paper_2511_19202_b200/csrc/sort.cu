@@ -407,10 +407,15 @@ __global__ void k_bentry_count(const uint32_t *order, const sc_splat *splats, co
         const int x0 = max((int)(int16_t)(w.x & 0xFFFF), 0), x1 = min((int)(int16_t)(w.x >> 16), width - 1);
         const int y0 = max((int)(int16_t)(w.y & 0xFFFF), 0), y1 = min((int)(int16_t)(w.y >> 16), height - 1);
         uint32_t c = 0;
-        if (x0 <= x1 && y0 <= y1) c = (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
+        if (x0 <= x1 && y0 <= y1) {
+            c = (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
+            wlo[k] = (uint32_t)x0 | ((uint32_t)x1 << 16);
+            whi[k] = (uint32_t)y0 | ((uint32_t)y1 << 16);
+        } else {   // canonical empty window: the emission recomputes the count from these
+            wlo[k] = 1u;
+            whi[k] = 1u;
+        }
         cnt[k] = c;
-        wlo[k] = (uint32_t)x0 | ((uint32_t)x1 << 16);
-        whi[k] = (uint32_t)y0 | ((uint32_t)y1 << 16);
     }
 }
 

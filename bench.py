@@ -169,6 +169,7 @@ def algorithmic_bytes(st, n_assets_gauss, n_inst, pixels):
 
 
 def traffic_from_profiles():
+    """DRAM bytes per k_blend launch from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "blend_dram_bytes.json")
     try:
         with open(path) as f:
@@ -311,15 +312,27 @@ def main():
     n_gauss = sum(len(a.asset) for a in wl.scene.assets)
     pixels = int(cams[0].width) * int(cams[0].height)
     alg = [algorithmic_bytes(stats[ci], n_gauss, wl.scene.n_instances, pixels) for ci in range(ncam)]
-    dom = max(mean_stage, key=mean_stage.get)
-    dom_bytes = float(np.mean([a[dom][0] for a in alg]))
-    dom_flops = float(np.mean([a[dom][1] for a in alg]))
-    t_dom = mean_stage[dom] / 1e3
-    roof = {"kernel": dom, "bound": "hbm", "achieved": dom_bytes / t_dom / 1e9, "peak": hbm, "unit": "GB/s",
-            "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)" if src == "measured" else src}
-    roof["frac"] = roof["achieved"] / roof["peak"]
+    def stage_roof(name):
+        b = float(np.mean([a[name][0] for a in alg]))
+        f = float(np.mean([a[name][1] for a in alg]))
+        t = mean_stage[name] / 1e3
+        r_ = {"bound": "hbm", "achieved": b / t / 1e9, "peak": hbm, "unit": "GB/s",
+              "algorithmic_bytes": b, "ms": mean_stage[name]}
+        if f > 0:
+            r_["tensor_achieved_tflops"] = f / t / 1e12
+            r_["tensor_frac"] = r_["tensor_achieved_tflops"] / tflops
+        r_["frac"] = r_["achieved"] / r_["peak"]
+        return r_
+
+    roof_stages = {k: stage_roof(k) for k in mean_stage}
+    # dominant single kernel: k_blend (the stage-3 -> stage-4 events bracket only
+    # k_tile_order (~0.03 ms) and k_blend)
+    roof = dict(roof_stages["blend"])
+    roof["kernel"] = "k_blend"
+    roof["peak_source"] = f"{src} (MEASURED_PEAKS.json hbm_gbs)" if src == "measured" else src
+    roof["units"] = "SURVEY §8d: 4 E + 36 E + 12 P bytes per launch, E = reference tile entries, P = pixels"
     tr = traffic_from_profiles()
-    roof["traffic"] = tr.get("per_launch_bytes") if tr and tr.get("kernel") == dom else None
+    roof["traffic"] = tr.get("per_launch_bytes") if tr and tr.get("kernel") == "k_blend" else None
     t_roof = float(np.mean([sum(b for b, _ in a.values()) / (hbm * 1e9) + sum(f for _, f in a.values()) /
                             (tflops * 1e12) for a in alg]))
     frame_roof = {"t_roof_ms": 1e3 * t_roof, "t_measured_ms": total_ms / K, "frac": 1e3 * t_roof / (total_ms / K)}
@@ -356,7 +369,7 @@ def main():
         "stage_ms": mean_stage,
         "frame_counts": [{k: s[k] for k in ("pairs_tested", "frustum_passed", "mlp_queried", "mlp_culled", "block_entries",
                                             "survivors", "passed", "entries")} for s in stats if s],
-        "roofline": roof, "roofline_frame": frame_roof,
+        "roofline": roof, "roofline_stages": roof_stages, "roofline_frame": frame_roof,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
         "wall_s": wall,
     }

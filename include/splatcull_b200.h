@@ -172,15 +172,21 @@ typedef struct sc_frame_stats {
 /* Survivor = (instance index, gaussian index within its asset). */
 typedef struct sc_survivor { uint32_t inst, gid; } sc_survivor;
 
-/* Per-survivor splat record consumed by the blend (48 B). */
+/* Per-survivor splat record consumed by the blend (32 B = one sector).
+ * opacity is implied: alpha = min(0.99, exp(power - p_min) / 255), which equals
+ * opacity * exp(power) for p_min = log(1/255) - log(opacity). */
 typedef struct sc_splat {
     float mx, my;                /* pixel-space mean */
     float half_a, b, half_c;     /* 0.5 conic_a, conic_b, 0.5 conic_c */
-    float opacity;               /* sigmoid(logit) */
-    float p_min;                 /* log(1/255) - log(opacity) */
-    float rgb[3];
-    int16_t win[4];              /* pixel window x0, x1, y0, y1 (inclusive), f64-exact */
+    float p_min;                 /* log(1/255) - log(opacity); +inf = skipped (opacity < 1/255) */
+    uint16_t rgb[3];             /* fp16 colour */
+    uint16_t reserved;
 } sc_splat;
+
+/* Per-survivor pixel window [x0, x1] x [y0, y1] (inclusive, absolute pixels):
+ * the reference window (sc/_kernels.py:224-227) intersected with the
+ * alpha >= 1/255 support box and the tile rectangle, computed in f64. */
+typedef struct sc_window { int16_t x0, x1, y0, y1; } sc_window;
 
 /* Bytes of workspace for the given capacities (align 256).  Host call. */
 SC_API size_t sc_workspace_bytes(int64_t n_instances, int64_t max_pairs, int64_t cap_survivors,
@@ -227,8 +233,8 @@ SC_API int sc_cull_mlp(const sc_scene *scene, const sc_camera *cam, const sc_opt
  * (bit0 valid after clip, bit1 passed).
  */
 SC_API int sc_project(const sc_scene *scene, const sc_survivor *survivors, int64_t n,
-               const sc_camera *cam, const sc_opts *opts, sc_splat *splats, double *dbg_f64,
-               int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, void *stream);
+               const sc_camera *cam, const sc_opts *opts, sc_splat *splats, sc_window *windows,
+               double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, void *stream);
 
 /*
  * Stages (c)+(d) on an explicit survivor list: projection, (depth, index)
@@ -240,17 +246,17 @@ SC_API int sc_project(const sc_scene *scene, const sc_survivor *survivors, int64
  */
 SC_API int sc_bin_sort(const sc_scene *scene, const sc_survivor *survivors, int64_t n,
                 const sc_camera *cam, const sc_opts *opts, const sc_workspace *ws,
-                sc_splat *splats, uint32_t *entry_idx, uint32_t *tile_offsets,
+                sc_splat *splats, sc_window *windows, uint32_t *entry_idx, uint32_t *tile_offsets,
                 uint32_t *order_idx, sc_frame_stats *stats, void *stream);
 
 /*
- * Stage (e) on explicit inputs: splats [n_splats] (sc_project output),
- * entry_idx [E] and tile_offsets [n_tiles + 1] (uint32; e.g. the oracle's
- * bin_tiles output) -> image / trans (+ contrib_sum / contrib_max).
+ * Stage (e) on explicit inputs: splats / windows [n_splats] (sc_project
+ * output), entry_idx [E] and tile_offsets [n_tiles + 1] (uint32; e.g. the
+ * oracle's bin_tiles output) -> image / trans (+ contrib_sum / contrib_max).
  */
-SC_API int sc_blend(const sc_splat *splats, int64_t n_splats, const uint32_t *entry_idx,
-             const uint32_t *tile_offsets, const sc_camera *cam, const sc_opts *opts,
-             const sc_frame_out *out, void *stream);
+SC_API int sc_blend(const sc_splat *splats, const sc_window *windows, int64_t n_splats,
+             const uint32_t *entry_idx, const uint32_t *tile_offsets, const sc_camera *cam,
+             const sc_opts *opts, const sc_frame_out *out, void *stream);
 
 /* Batched visibility MLP on materialised inputs x [n][16] f32 -> logits [n]. */
 SC_API int sc_vis_mlp_forward(const sc_vis_weights *w, const float *x, int64_t n, float *logits,

@@ -77,7 +77,11 @@ class ScSurvivor(ctypes.Structure):
 
 class ScSplat(ctypes.Structure):
     _fields_ = [("mx", c_f32), ("my", c_f32), ("half_a", c_f32), ("b", c_f32), ("half_c", c_f32),
-                ("opacity", c_f32), ("p_min", c_f32), ("rgb", c_f32 * 3), ("win", ctypes.c_int16 * 4)]
+                ("p_min", c_f32), ("rgb", c_u16 * 3), ("reserved", c_u16)]
+
+
+class ScWindow(ctypes.Structure):
+    _fields_ = [("x0", ctypes.c_int16), ("x1", ctypes.c_int16), ("y0", ctypes.c_int16), ("y1", ctypes.c_int16)]
 
 
 class ScFrameOut(ctypes.Structure):
@@ -96,7 +100,8 @@ class ScWorkspace(ctypes.Structure):
 
 STATS_BYTES = ctypes.sizeof(ScFrameStats)
 SPLAT_BYTES = ctypes.sizeof(ScSplat)
-assert SPLAT_BYTES == 48, SPLAT_BYTES
+WINDOW_BYTES = ctypes.sizeof(ScWindow)
+assert SPLAT_BYTES == 32 and WINDOW_BYTES == 8, (SPLAT_BYTES, WINDOW_BYTES)
 
 # exported symbol -> (restype, argtypes); mirrors include/splatcull_b200.h
 SIGNATURES = {
@@ -106,9 +111,9 @@ SIGNATURES = {
     "sc_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32]),
     "sc_render_composed": (c_i32, [P, P, P, P, P, P]),
     "sc_cull_mlp": (c_i32, [P, P, P, P, P, c_i64, P, P]),
-    "sc_project": (c_i32, [P, P, c_i64, P, P, P, P, P, P, P, P]),
-    "sc_bin_sort": (c_i32, [P, P, c_i64, P, P, P, P, P, P, P, P, P]),
-    "sc_blend": (c_i32, [P, c_i64, P, P, P, P, P, P]),
+    "sc_project": (c_i32, [P, P, c_i64, P, P, P, P, P, P, P, P, P]),
+    "sc_bin_sort": (c_i32, [P, P, c_i64, P, P, P, P, P, P, P, P, P, P]),
+    "sc_blend": (c_i32, [P, P, c_i64, P, P, P, P, P, P]),
     "sc_vis_mlp_forward": (c_i32, [P, P, c_i64, P, P]),
     "sc_encode_features": (c_i32, [P, P, c_i64, P, P]),
 }

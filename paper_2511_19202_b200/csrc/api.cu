@@ -47,7 +47,7 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
-    size_t inst, chunk_state, ctr, surv, splats, key_a, key_b, val_a, val_b, depth64, rect, ecount, ekey_a, ekey_b,
+    size_t inst, chunk_state, ctr, surv, splats, wins, key_a, key_b, val_a, val_b, depth64, rect, ecount, ekey_a, ekey_b,
         eval_a, eval_b, tile_off, task_order, boff, hist, scan_part, total;
     int64_t max_chunks, nblk_max, n_tiles;
     int n_tx, n_ty;
@@ -75,6 +75,7 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.ctr = take(sizeof(sc::Counters));
     L.surv = take(sizeof(sc_survivor) * (size_t)capS);
     L.splats = take(sizeof(sc_splat) * (size_t)capS);
+    L.wins = take(sizeof(sc_window) * (size_t)capS);
     L.key_a = take(4 * (size_t)capS);
     L.key_b = take(4 * (size_t)capS);
     L.val_a = take(4 * (size_t)capS);
@@ -109,6 +110,7 @@ int carve(const sc_workspace *ws, int32_t w, int32_t h, sc::Ws &out)
     out.ctr = reinterpret_cast<sc::Counters *>(b + L.ctr);
     out.surv = reinterpret_cast<sc_survivor *>(b + L.surv);
     out.splats = reinterpret_cast<sc_splat *>(b + L.splats);
+    out.wins = reinterpret_cast<sc_window *>(b + L.wins);
     out.key_a = reinterpret_cast<uint32_t *>(b + L.key_a);
     out.key_b = reinterpret_cast<uint32_t *>(b + L.key_b);
     out.val_a = reinterpret_cast<uint32_t *>(b + L.val_a);
@@ -199,35 +201,26 @@ int sc_cull_mlp(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts
 }
 
 int sc_project(const sc_scene *scene, const sc_survivor *survivors, int64_t n, const sc_camera *cam,
-               const sc_opts *opts, sc_splat *splats, double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags,
-               sc_frame_stats *stats, void *stream)
+               const sc_opts *opts, sc_splat *splats, sc_window *windows, double *dbg_f64, int32_t *dbg_rect,
+               uint8_t *dbg_flags, sc_frame_stats *stats, void *stream)
 {
     int rc;
     if ((rc = check_scene(scene)) || (rc = check_camera(cam)) || (rc = check_opts(opts))) return rc;
-    if (n < 0 || (n > 0 && (!survivors || !splats))) return fail(SC_ERR_INVALID, "bad survivor / splat buffers%s");
+    if (n < 0 || (n > 0 && (!survivors || !splats || !windows)))
+        return fail(SC_ERR_INVALID, "bad survivor / splat / window buffers%s");
     if (!stats) return fail(SC_ERR_INVALID, "stats is NULL%s");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
-    SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, nullptr, nullptr, nullptr, nullptr,
-                              dbg_f64, dbg_rect, dbg_flags, stats, nullptr, st),
+    SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, windows, nullptr, nullptr, dbg_f64,
+                              dbg_rect, dbg_flags, stats, nullptr, st),
            "project");
-    return SC_OK;
-}
-
-static int run_bin(const sc_scene *scene, const sc_survivor *surv, const unsigned long long *n_dev, int64_t n_max,
-                   const sc_camera *cam, const sc_opts *opts, sc::Ws &w, sc_splat *splats, sc_frame_stats *stats,
-                   uint32_t **order, uint32_t **entries, cudaStream_t st)
-{
-    SC_TRY(sc::launch_project(*scene, surv, n_dev, n_max, *cam, *opts, splats, w.key_a, w.val_a, w.depth64, w.rect,
-                              nullptr, nullptr, nullptr, stats, w.ctr, st),
-           "project");
-    SC_TRY(sc::launch_bin(w, n_dev, n_max, *cam, splats, stats, false, order, entries, nullptr, st), "bin/sort");
     return SC_OK;
 }
 
 int sc_bin_sort(const sc_scene *scene, const sc_survivor *survivors, int64_t n, const sc_camera *cam,
-                const sc_opts *opts, const sc_workspace *ws, sc_splat *splats, uint32_t *entry_idx,
-                uint32_t *tile_offsets, uint32_t *order_idx, sc_frame_stats *stats, void *stream)
+                const sc_opts *opts, const sc_workspace *ws, sc_splat *splats, sc_window *windows,
+                uint32_t *entry_idx, uint32_t *tile_offsets, uint32_t *order_idx, sc_frame_stats *stats,
+                void *stream)
 {
     int rc;
     if ((rc = check_scene(scene)) || (rc = check_camera(cam)) || (rc = check_opts(opts))) return rc;
@@ -236,10 +229,15 @@ int sc_bin_sort(const sc_scene *scene, const sc_survivor *survivors, int64_t n, 
     if ((rc = carve(ws, cam->width, cam->height, w))) return rc;
     if (n > w.capS) return fail(SC_ERR_INVALID, "n exceeds workspace cap_survivors%s");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    sc_window *wins = windows ? windows : w.wins;
     SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
     SC_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(sc::Counters), st), "memset counters");
     uint32_t *order = nullptr, *entries = nullptr;
-    if ((rc = run_bin(scene, survivors, nullptr, n, cam, opts, w, splats, stats, &order, &entries, st))) return rc;
+    SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, wins, w.depth64, w.rect, nullptr,
+                              nullptr, nullptr, stats, w.ctr, st),
+           "project");
+    // reference tile binning (bin_tiles semantics) for parity with the oracle
+    SC_TRY(sc::launch_bin(w, nullptr, n, *cam, wins, stats, false, &order, &entries, nullptr, st), "bin/sort");
     if (order_idx && n > 0) SC_TRY(cudaMemcpyAsync(order_idx, order, 4 * (size_t)n, cudaMemcpyDeviceToDevice, st), "copy order");
     if (entry_idx && w.capE > 0)
         SC_TRY(cudaMemcpyAsync(entry_idx, entries, 4 * (size_t)w.capE, cudaMemcpyDeviceToDevice, st), "copy entries");
@@ -249,18 +247,20 @@ int sc_bin_sort(const sc_scene *scene, const sc_survivor *survivors, int64_t n, 
     return SC_OK;
 }
 
-int sc_blend(const sc_splat *splats, int64_t n_splats, const uint32_t *entry_idx, const uint32_t *tile_offsets,
-             const sc_camera *cam, const sc_opts *opts, const sc_frame_out *out, void *stream)
+int sc_blend(const sc_splat *splats, const sc_window *windows, int64_t n_splats, const uint32_t *entry_idx,
+             const uint32_t *tile_offsets, const sc_camera *cam, const sc_opts *opts, const sc_frame_out *out,
+             void *stream)
 {
     int rc;
     if ((rc = check_camera(cam)) || (rc = check_opts(opts))) return rc;
-    if (!out || !out->image || !out->trans || !tile_offsets) return fail(SC_ERR_INVALID, "output buffers are NULL%s");
+    if (!out || !out->image || !out->trans || !tile_offsets || (n_splats > 0 && (!splats || !windows)))
+        return fail(SC_ERR_INVALID, "input / output buffers are NULL%s");
     if (opts->record_contributions && (!out->contrib_max || !out->contrib_sum))
         return fail(SC_ERR_INVALID, "record_contributions needs contrib_max and contrib_sum%s");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (opts->record_contributions && n_splats > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)n_splats, st), "memset contrib_max");
-    const sc::BlendLists lists{tile_offsets, entry_idx, nullptr, false};
+    const sc::BlendLists lists{tile_offsets, entry_idx, nullptr, windows, false};
     SC_TRY(sc::launch_blend(splats, lists, *cam, *opts, *out, n_splats, nullptr, st), "blend");
     return SC_OK;
 }
@@ -288,18 +288,18 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
     SC_TRY(sc::launch_prep(*scene, *cam, *opts, w, stats, st), "prep");
     SC_TRY(sc::launch_cull(*scene, *cam, *opts, w, w.surv, w.capS, stats, st), "cull");
     SC_TRY(mark(1), "event");
-    SC_TRY(sc::launch_project(*scene, w.surv, &w.ctr->survivors, w.capS, *cam, *opts, w.splats, w.key_a, w.val_a,
-                              w.depth64, w.rect, nullptr, nullptr, nullptr, stats, w.ctr, st),
+    SC_TRY(sc::launch_project(*scene, w.surv, &w.ctr->survivors, w.capS, *cam, *opts, w.splats, w.wins, w.depth64,
+                              nullptr, nullptr, nullptr, nullptr, stats, w.ctr, st),
            "project");
     SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;
     uint32_t *bkeys = nullptr;
-    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.splats, stats, true, &order, &entries, &bkeys, st),
+    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.wins, stats, true, &order, &entries, &bkeys, st),
            "bin/sort");
     SC_TRY(mark(3), "event");
     if (opts->record_contributions && w.capS > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
-    const sc::BlendLists lists{w.boff, entries, bkeys, true};
+    const sc::BlendLists lists{w.boff, entries, bkeys, nullptr, true};
     SC_TRY(sc::launch_blend(w.splats, lists, *cam, *opts, *out, w.capS, w.task_order, st), "blend");
     SC_TRY(mark(4), "event");
     if (opts->record_contributions)

@@ -46,7 +46,7 @@ constexpr int kG = 32;                   // entries per pipeline group
 constexpr int kMetaStages = 6;           // meta ring (index + window code) depth: issued 5 groups ahead
 constexpr int kRecStages = 4;            // record ring depth: issued 3 groups ahead
 constexpr size_t kMetaBytesW = sizeof(uint2) * kG * kMetaStages;
-constexpr size_t kRecBytesW = sizeof(float4) * 3 * kG * kRecStages;
+constexpr size_t kRecBytesW = sizeof(float4) * 2 * kG * kRecStages;   // 32-byte sc_splat records
 constexpr size_t kBlendSmem = (kMetaBytesW + kRecBytesW) * kBlendWarps;
 
 // 32-bit footprint (lane = 8 row + col) of a block-relative window code
@@ -97,7 +97,8 @@ constexpr uint32_t kEmptyCode = 0x0007u;   // x0 = 7 > x1 = 0
 __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
                                                             const uint32_t *__restrict__ offsets,
                                                             const uint32_t *__restrict__ vals,
-                                                            const uint32_t *__restrict__ keys, int blocks,
+                                                            const uint32_t *__restrict__ keys,
+                                                            const sc_window *__restrict__ wins, int blocks,
                                                             const uint32_t *__restrict__ task_order, int width,
                                                             int height, int n_tx, float stop_t, float bg_r,
                                                             float bg_g, float bg_b, int record, float *image,
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                 const uint32_t v = __ldg(vals + e);
                 uint32_t code = kEmptyCode;
                 if ((int64_t)v < n_splats) {
-                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + v) + 40));
+                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(wins + v));
                     const int x0 = max(lo16(w.x), gx0), x1 = min(hi16(w.x), gx0 + 7);
                     const int y0 = max(lo16(w.y), gy0), y1 = min(hi16(w.y), gy0 + 3);
                     if (x0 <= x1 && y0 <= y1)
@@ -160,10 +161,9 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
         m->y = fp;
         if (fp) {
             const float4 *src = reinterpret_cast<const float4 *>(splats + v.x);
-            float4 *dst = recs + (rs * kG + lane) * 3;
+            float4 *dst = recs + (rs * kG + lane) * 2;
             cp_async16(dst, src);
             cp_async16(dst + 1, src + 1);
-            cp_async16(dst + 2, src + 2);
         }
     };
 
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
             d_hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
 #endif
             if (__any_sync(0xffffffffu, fp != 0u)) {
-                const float4 *grp = recs + rs * kG * 3;
+                const float4 *grp = recs + rs * kG * 2;
                 uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
                 while (__any_sync(0xffffffffu, mine != 0u)) {
                     const bool act = mine != 0u;
@@ -219,18 +219,20 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                     d_iters += (lane == 0);
 #endif
                     if (act) {
-                        const float4 *r = grp + j * 3;
+                        const float4 *r = grp + j * 2;
                         const float4 g = r[0];   // mx, my, 0.5 a, b
-                        const float4 p = r[1];   // 0.5 c, opacity, p_min, red
+                        const float4 p = r[1];   // 0.5 c, p_min, rgb (fp16 x3)
                         const float dx = fpx - g.x, dy = fpy - g.y;
                         const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
-                        if (!(power > 0.0f || power < p.z)) {
-                            const float2 c2 = *reinterpret_cast<const float2 *>(r + 2);   // green, blue
-                            const float alpha = fminf(0.99f, p.y * __expf(power));
+                        if (!(power > 0.0f || power < p.y)) {
+                            // opacity * e^power == e^(power - p_min) / 255
+                            const float alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
                             const float contrib = alpha * T;
-                            cr += contrib * p.w;
-                            cg += contrib * c2.x;
-                            cb += contrib * c2.y;
+                            const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
+                            const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
+                            cr += contrib * __low2float(rg);
+                            cg += contrib * __high2float(rg);
+                            cb += contrib * __low2float(bx);
                             T = T * (1.0f - alpha);
                             if (record) {
                                 cs += contrib;
@@ -330,7 +332,7 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
     const int64_t n_tiles = (int64_t)n_tx * n_ty;
     if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, n_tiles, lists.blocks ? 8 : 1, task_order);
     SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kBlendSmem, st, splats, n_splats, lists.offsets, lists.vals,
-              lists.keys, lists.blocks ? 1 : 0, task_order, cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
+              lists.keys, lists.wins, lists.blocks ? 1 : 0, task_order, cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
               (float)opts.background[1], (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image,
               out.trans, out.contrib_sum, out.contrib_max);
     return cudaGetLastError();

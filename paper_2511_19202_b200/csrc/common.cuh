@@ -48,6 +48,7 @@ struct Ws {
     Counters *ctr;
     sc_survivor *surv;               // [capS]
     sc_splat *splats;                // [capS]
+    sc_window *wins;                 // [capS]
     uint32_t *key_a, *key_b;         // [capS]
     uint32_t *val_a, *val_b;         // [capS]
     double *depth64;                 // [capS]
@@ -135,11 +136,11 @@ cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_op
                         sc_survivor *out, int64_t cap, sc_frame_stats *stats, cudaStream_t st);
 cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
-                           uint32_t *keys, uint32_t *vals, double *depth64, ushort4 *rect, double *dbg_f64,
+                           sc_window *wins, double *depth64, ushort4 *rect, double *dbg_f64,
                            int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr,
                            cudaStream_t st);
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
-                       const sc_splat *splats, sc_frame_stats *stats, bool blocks, uint32_t **order_out,
+                       const sc_window *wins, sc_frame_stats *stats, bool blocks, uint32_t **order_out,
                        uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st);
 // Blend input, one of:
 //  * block lists (frame path): boff [8 n_tiles + 1], vals = survivor per entry,
@@ -150,6 +151,7 @@ struct BlendLists {
     const uint32_t *offsets;
     const uint32_t *vals;
     const uint32_t *keys;
+    const sc_window *wins;   // tile lists only: windows to clip per warp block
     bool blocks;
 };
 cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,

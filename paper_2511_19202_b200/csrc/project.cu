@@ -28,7 +28,7 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) { retur
 
 __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_survivor *surv,
                                                  const unsigned long long *n_dev, int64_t n_host, sc_camera cam,
-                                                 sc_opts opts, sc_splat *splats, uint32_t *keys, uint32_t *vals,
+                                                 sc_opts opts, sc_splat *splats, sc_window *wins,
                                                  double *depth64, ushort4 *rect, double *dbg_f64, int32_t *dbg_rect,
                                                  uint8_t *dbg_flags, sc_frame_stats *stats,
                                                  Counters *ctr)
@@ -180,15 +180,18 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
                 }
             }
         }
-        const double xl = (double)mo.w;
-        double op;
-        if (xl >= 0.0) {
-            op = 1.0 / (1.0 + exp(-xl));
+        // opacity = sigmoid(logit) (sc/asset.py:44-51) in fp32: it only feeds the
+        // fp32 blend (alpha, p_min) and the widened support box below
+        const float xl = mo.w;
+        float op;
+        if (xl >= 0.0f) {
+            op = 1.0f / (1.0f + expf(-xl));
         } else {
-            const double e = exp(xl);
-            op = e / (1.0 + e);
+            const float e = expf(xl);
+            op = e / (1.0f + e);
         }
-        const double log_op = log(op > 1e-300 ? op : 1e-300);
+        const bool skip = !(op >= 1.0f / 255.0f);   // reference: `op < min_alpha: continue`
+        const float p_min = skip ? __int_as_float(0x7f800000) : (float)log_min_alpha - logf(op);
 
         sc_splat sp;
         sp.mx = (float)mx;
@@ -196,10 +199,12 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
         sp.half_a = (float)(0.5 * ca);
         sp.b = (float)cb;
         sp.half_c = (float)(0.5 * cc);
-        sp.opacity = (float)op;
-        sp.p_min = (float)(log_min_alpha - log_op);
-        for (int ch = 0; ch < 3; ch++) sp.rgb[ch] = (float)clampd(col[ch] + 0.5, 0.0, 1.0);
-        if (passed && !(op < 1.0 / 255.0)) {
+        sp.p_min = p_min;
+        for (int ch = 0; ch < 3; ch++)
+            sp.rgb[ch] = __half_as_ushort(__float2half_rn((float)clampd(col[ch] + 0.5, 0.0, 1.0)));
+        sp.reserved = 0;
+        sc_window win;
+        if (passed && !skip) {
             // reference pixel window (sc/_kernels.py:224-227), intersected with the
             // bounding box of the alpha >= 1/255 support {1/2 d^T cov^-1 d <= L},
             // L = log(op) - log(1/255): |dx| <= sqrt(2 L cov_xx).  Pixels outside the
@@ -208,25 +213,24 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
             // Also clipped to the splat's tile rectangle in pixels: the reference only
             // composites a splat inside tiles whose list holds it, and its window can
             // reach one pixel past the rect (A8 step 3).
-            const double L = log_op - log_min_alpha;
-            const double ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-6) + 1e-3;
-            const double ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-6) + 1e-3;
-            sp.win[0] = clamp16(fmax(fmax(floor(mx - radius), ceil(mx - ex)), (double)(kTile * tx0)));
-            sp.win[1] = clamp16(fmin(fmin(floor(mx + radius) + 1.0, floor(mx + ex)), (double)(kTile * tx1 - 1)));
-            sp.win[2] = clamp16(fmax(fmax(floor(my - radius), ceil(my - ey)), (double)(kTile * ty0)));
-            sp.win[3] = clamp16(fmin(fmin(floor(my + radius) + 1.0, floor(my + ey)), (double)(kTile * ty1 - 1)));
-        } else {   // skipped by the blend (reference: `op < min_alpha: continue`)
-            sp.win[0] = 1;
-            sp.win[1] = 0;
-            sp.win[2] = 1;
-            sp.win[3] = 0;
+            // L = -p_min; the fp32 opacity's error is far inside the widening
+            const double L = -(double)p_min;
+            const double ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-5) + 1e-3;
+            const double ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-5) + 1e-3;
+            win.x0 = clamp16(fmax(fmax(floor(mx - radius), ceil(mx - ex)), (double)(kTile * tx0)));
+            win.x1 = clamp16(fmin(fmin(floor(mx + radius) + 1.0, floor(mx + ex)), (double)(kTile * tx1 - 1)));
+            win.y0 = clamp16(fmax(fmax(floor(my - radius), ceil(my - ey)), (double)(kTile * ty0)));
+            win.y1 = clamp16(fmin(fmin(floor(my + radius) + 1.0, floor(my + ey)), (double)(kTile * ty1 - 1)));
+        } else {   // never composited
+            win.x0 = 1;
+            win.x1 = 0;
+            win.y0 = 1;
+            win.y1 = 0;
         }
         splats[k] = sp;
-        if (keys) {
-            depth64[k] = passed ? tz : -1.0;   // sort keys are quantised in k_depth_keys
-            rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0,
-                                   (unsigned short)ty1);
-        }
+        wins[k] = win;
+        if (depth64) depth64[k] = passed ? tz : -1.0;   // sort keys are quantised in k_depth_keys
+        if (rect) rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0, (unsigned short)ty1);
         if (dbg_f64) {
             double *d = dbg_f64 + 8 * k;
             d[0] = mx; d[1] = my; d[2] = ca; d[3] = cb; d[4] = cc; d[5] = tz; d[6] = radius; d[7] = det;
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
 
 cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
-                           uint32_t *keys, uint32_t *vals, double *depth64, ushort4 *rect, double *dbg_f64,
+                           sc_window *wins, double *depth64, ushort4 *rect, double *dbg_f64,
                            int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr,
                            cudaStream_t st)
 {
@@ -268,7 +272,7 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 8);
-    SC_LAUNCH(k_project, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, keys, vals, depth64,
+    SC_LAUNCH(k_project, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins, depth64,
               rect, dbg_f64, dbg_rect, dbg_flags, stats, ctr);
     return cudaGetLastError();
 }

@@ -397,12 +397,12 @@ __global__ void k_tile_offsets(const uint32_t *ekey, const unsigned long long *e
 // ---------------------------------------------------------------------------
 constexpr int kCodeBits = 10;
 
-__global__ void k_bentry_count(const uint32_t *order, const sc_splat *splats, const unsigned long long *n_dev,
+__global__ void k_bentry_count(const uint32_t *order, const sc_window *wins, const unsigned long long *n_dev,
                                int64_t n_host, int width, int height, uint32_t *cnt, uint32_t *wlo, uint32_t *whi)
 {
     const int64_t n = dev_count(n_dev, n_host);
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(reinterpret_cast<const char *>(splats + order[k]) + 40));
+        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(wins + order[k]));
         // pixels outside the image are never composited (reference th/tw clamp)
         const int x0 = max((int)(int16_t)(w.x & 0xFFFF), 0), x1 = min((int)(int16_t)(w.x >> 16), width - 1);
         const int y0 = max((int)(int16_t)(w.y & 0xFFFF), 0), y1 = min((int)(int16_t)(w.y >> 16), height - 1);
@@ -522,7 +522,7 @@ static int bits_for(int64_t n)
 // API, parity with the reference): tile entries and ws.tile_off, exactly
 // bin_tiles' output.
 cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
-                       const sc_splat *splats, sc_frame_stats *stats, bool blocks, uint32_t **order_out,
+                       const sc_window *wins, sc_frame_stats *stats, bool blocks, uint32_t **order_out,
                        uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st)
 {
     cudaError_t e;
@@ -537,7 +537,7 @@ cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_
     uint32_t *rlo = ws.key_a, *rhi = ws.key_b;
     uint32_t *ek = nullptr, *ev = nullptr;
     if (blocks) {
-        SC_LAUNCH(k_bentry_count, grid_for(n_max, 256), 256, 0, st, order, splats, p_dev, n_max, cam.width, cam.height,
+        SC_LAUNCH(k_bentry_count, grid_for(n_max, 256), 256, 0, st, order, wins, p_dev, n_max, cam.width, cam.height,
                   ws.ecount, rlo, rhi);
         e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, nullptr, st);
         if (e != cudaSuccess) return e;

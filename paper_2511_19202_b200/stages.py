@@ -49,18 +49,20 @@ def project(dscene: DeviceScene, surv_inst, surv_gid, cam, opts: RenderOptions):
     sv = _survivor_tensor(surv_inst, surv_gid, dev)
     n = int(sv.shape[0])
     splats = torch.empty((max(n, 1), nat.SPLAT_BYTES), dtype=torch.uint8, device=dev)
+    wins = torch.empty((max(n, 1), nat.WINDOW_BYTES), dtype=torch.uint8, device=dev)
     dbg = torch.empty((max(n, 1), 8), dtype=torch.float64, device=dev)
     rect = torch.empty((max(n, 1), 4), dtype=torch.int32, device=dev)
     flags = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
     stats = torch.empty(nat.STATS_BYTES, dtype=torch.uint8, device=dev)
     camc, optc = nat.camera_struct(cam), opts.struct(cam)
     nat.check(lib.sc_project(ctypes.byref(dscene.struct), nat.ptr(sv), n, ctypes.byref(camc), ctypes.byref(optc),
-                             nat.ptr(splats), nat.ptr(dbg), nat.ptr(rect), nat.ptr(flags), nat.ptr(stats),
+                             nat.ptr(splats), nat.ptr(wins), nat.ptr(dbg), nat.ptr(rect), nat.ptr(flags),
+                             nat.ptr(stats),
                              nat.stream_handle()), "sc_project")
     d = dbg[:n].cpu().numpy()
     return {"mean2d": d[:, 0:2], "conic": d[:, 2:5], "depth": d[:, 5], "radius": d[:, 6], "det": d[:, 7],
             "rect": rect[:n].cpu().numpy(), "valid": (flags[:n].cpu().numpy() & 1) > 0,
-            "passed": (flags[:n].cpu().numpy() & 2) > 0, "splats": splats[:n],
+            "passed": (flags[:n].cpu().numpy() & 2) > 0, "splats": splats[:n], "windows": wins[:n],
             "stats": nat.stats_dict(stats.cpu().numpy())}
 
 
@@ -76,23 +78,25 @@ def bin_sort(dscene: DeviceScene, surv_inst, surv_gid, cam, opts: RenderOptions,
     ws = Workspace(dscene, cam.width, cam.height, cap_s=max(n, 1), cap_e=cap_e)
     n_tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
     splats = torch.empty((max(n, 1), nat.SPLAT_BYTES), dtype=torch.uint8, device=dev)
+    wins = torch.empty((max(n, 1), nat.WINDOW_BYTES), dtype=torch.uint8, device=dev)
     entries = torch.empty(max(cap_e, 1), dtype=torch.int32, device=dev)
     offs = torch.empty(n_tiles + 1, dtype=torch.int32, device=dev)
     order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     stats = torch.empty(nat.STATS_BYTES, dtype=torch.uint8, device=dev)
     camc, optc = nat.camera_struct(cam), opts.struct(cam)
     nat.check(lib.sc_bin_sort(ctypes.byref(dscene.struct), nat.ptr(sv), n, ctypes.byref(camc), ctypes.byref(optc),
-                              ctypes.byref(ws.struct), nat.ptr(splats), nat.ptr(entries), nat.ptr(offs),
+                              ctypes.byref(ws.struct), nat.ptr(splats), nat.ptr(wins), nat.ptr(entries), nat.ptr(offs),
                               nat.ptr(order), nat.ptr(stats), nat.stream_handle()), "sc_bin_sort")
     st = nat.stats_dict(stats.cpu().numpy())
     if st["overflow"]:
         raise nat.NativeError(f"entry capacity {cap_e} too small for {st['entries']} entries")
     return {"order_idx": order[:st["passed"]].cpu().numpy().view(np.uint32).astype(np.int64),
             "entry_idx": entries[:st["entries"]].cpu().numpy().view(np.uint32).astype(np.int64),
-            "counts": offs.cpu().numpy().view(np.uint32).astype(np.int64), "splats": splats[:n], "stats": st}
+            "counts": offs.cpu().numpy().view(np.uint32).astype(np.int64), "splats": splats[:n],
+            "windows": wins[:n], "stats": st}
 
 
-def blend(splats, entry_idx, counts, cam, opts: RenderOptions, n_splats: int | None = None):
+def blend(splats, windows, entry_idx, counts, cam, opts: RenderOptions, n_splats: int | None = None):
     """Stage (e) on explicit entries: -> (image, trans[, contrib_sum, contrib_max]) numpy."""
     import torch
 
@@ -111,7 +115,7 @@ def blend(splats, entry_idx, counts, cam, opts: RenderOptions, n_splats: int | N
     fo.image, fo.trans = nat.ptr(image), nat.ptr(trans)
     fo.contrib_sum, fo.contrib_max = nat.ptr(csum), nat.ptr(cmax)
     camc, optc = nat.camera_struct(cam), opts.struct(cam)
-    nat.check(lib.sc_blend(nat.ptr(splats), n, nat.ptr(ent) if ent.numel() else 0, nat.ptr(off),
+    nat.check(lib.sc_blend(nat.ptr(splats), nat.ptr(windows), n, nat.ptr(ent) if ent.numel() else 0, nat.ptr(off),
                            ctypes.byref(camc), ctypes.byref(optc), ctypes.byref(fo), nat.stream_handle()),
               "sc_blend")
     res = {"image": image.cpu().numpy(), "trans": trans.cpu().numpy()}

@@ -14,7 +14,7 @@ for ci in range(3):
     out, st = r.render(cam, return_survivors=True)
     s = out.survivors
     b = stages.bin_sort(r.dscene, s[:, 0], s[:, 1], cam, RenderOptions())
-    res = stages.blend(b["splats"], b["entry_idx"], b["counts"], cam, RenderOptions(), n_splats=len(s))
+    res = stages.blend(b["splats"], b["windows"], b["entry_idx"], b["counts"], cam, RenderOptions(), n_splats=len(s))
     d = np.abs(out.image - res["image"])
     print(ci, "maxdiff frame-path vs tile-path", d.max(), "bad px", (d.max(axis=2) > 1e-3).sum(), "blocks", st.max_tie_run, st.entries, st.passed)
     ys, xs = np.nonzero(d.max(axis=2) > 1e-3)

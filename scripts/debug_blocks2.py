@@ -23,15 +23,15 @@ print("caps", ws.cap_s, ws.cap_e)
 out, _ = r.render(cam, return_survivors=True)
 s = out.survivors
 b = stages.bin_sort(r.dscene, s[:, 0], s[:, 1], cam, RenderOptions())
-res = stages.blend(b["splats"], b["entry_idx"], b["counts"], cam, RenderOptions(), n_splats=len(s))
+res = stages.blend(b["splats"], b["windows"], b["entry_idx"], b["counts"], cam, RenderOptions(), n_splats=len(s))
 d = np.abs(out.image - res["image"]).max(axis=2)
 ys, xs = np.nonzero(d > 1e-3)
 print("bad", len(ys))
 for y, x in list(zip(ys, xs))[:5]:
     print((y, x), "frame", out.image[y, x], out.final_transmittance[y, x], "tile", res["image"][y, x], res["trans"][y, x])
-sp = b["splats"].cpu().numpy().view(np.uint8).reshape(-1, 48)
-win = sp[:, 40:48].copy().view(np.int16).reshape(-1, 4)
-f = sp[:, :40].copy().view(np.float32).reshape(-1, 10)
+sp = b["splats"].cpu().numpy().view(np.uint8).reshape(-1, nat.SPLAT_BYTES)
+win = b["windows"].cpu().numpy().view(np.int16).reshape(-1, 4)
+f = sp[:, :24].copy().view(np.float32).reshape(-1, 6)
 w = (win[:, 1] - win[:, 0]).astype(int)
 print("splats", len(win), "width>100", (w > 100).sum(), "max width", w.max(), "neg x0", (win[:, 0] < 0).sum())
 big = w > 100

@@ -96,7 +96,7 @@ def test_blend_with_reference_entries(golden):
     n = len(asset)
     o = _opts(**opts)
     p = stages.project(ds, np.zeros(n, np.int64), np.arange(n), cam, o)
-    res = stages.blend(p["splats"], z["entry_idx"], z["counts"], cam, o, n_splats=n)
+    res = stages.blend(p["splats"], p["windows"], z["entry_idx"], z["counts"], cam, o, n_splats=n)
     _image_close(res["image"], z["image"])
     _image_close(res["trans"], z["final_transmittance"])
     if opts.get("record_contributions"):
@@ -234,7 +234,7 @@ def test_composed_pipeline_vs_oracle(cam_i):
     np.testing.assert_array_equal(b["order_idx"], ref.stages.order_idx)
     np.testing.assert_array_equal(b["entry_idx"], ref.stages.entry_idx)
     np.testing.assert_array_equal(b["counts"], ref.stages.counts)
-    res = stages.blend(b["splats"], b["entry_idx"], b["counts"], cam, RenderOptions(),
+    res = stages.blend(b["splats"], b["windows"], b["entry_idx"], b["counts"], cam, RenderOptions(),
                        n_splats=len(ref.cull.surv_inst))
     _image_close(res["image"], ref.out.image)
 

@@ -42,7 +42,7 @@ def test_workspace_bytes_is_host_computable():
 
 
 STRUCTS = ["sc_camera", "sc_opts", "sc_asset_rec", "sc_instance_rec", "sc_vis_weights", "sc_scene",
-           "sc_frame_stats", "sc_survivor", "sc_splat", "sc_frame_out", "sc_workspace"]
+           "sc_frame_stats", "sc_survivor", "sc_splat", "sc_window", "sc_frame_out", "sc_workspace"]
 
 
 @pytest.mark.parametrize("name", STRUCTS)
@@ -51,7 +51,7 @@ def test_struct_layout_matches_c(name, tmp_path):
 
     py = {"sc_camera": nat.ScCamera, "sc_opts": nat.ScOpts, "sc_asset_rec": nat.ScAssetRec,
           "sc_instance_rec": nat.ScInstanceRec, "sc_vis_weights": nat.ScVisWeights, "sc_scene": nat.ScScene,
-          "sc_frame_stats": nat.ScFrameStats, "sc_survivor": nat.ScSurvivor, "sc_splat": nat.ScSplat,
+          "sc_frame_stats": nat.ScFrameStats, "sc_survivor": nat.ScSurvivor, "sc_splat": nat.ScSplat, "sc_window": nat.ScWindow,
           "sc_frame_out": nat.ScFrameOut, "sc_workspace": nat.ScWorkspace}[name]
     lines = [f'printf("%zu\\n", sizeof({name}));']
     for fname, _t in py._fields_:

@@ -47,8 +47,8 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
-    size_t inst, chunk_state, ctr, surv, splats, wins, key_a, key_b, val_a, val_b, depth64, rect, ecount, ekey_a, ekey_b,
-        eval_a, eval_b, tile_off, task_order, boff, hist, scan_part, total;
+    size_t inst, chunk_state, ctr, surv, splats, wins, key_a, key_b, pv_a, pv_b, depth64, rect, ecount, ekey_a, ekey_b,
+        eval_a, eval_b, tile_off, task_order, boff, rs_counts, scan_part, total;
     int64_t max_chunks, nblk_max, n_tiles;
     int n_tx, n_ty;
 };
@@ -62,8 +62,7 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.max_chunks = max_pairs / sc::kChunk + n_inst + 1;
     const int64_t big = std::max<int64_t>(std::max<int64_t>(capS, capE), 1);
     L.nblk_max = (big + sc::kRadixTile - 1) / sc::kRadixTile;
-    const int64_t part = std::max<int64_t>((256 * L.nblk_max + sc::kScanTile - 1) / sc::kScanTile,
-                                           (big + sc::kScanTile - 1) / sc::kScanTile) + 1;
+    const int64_t part = (std::max<int64_t>(256 * L.nblk_max, big) + sc::kScanTile - 1) / sc::kScanTile + 1;
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
@@ -76,21 +75,22 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.surv = take(sizeof(sc_survivor) * (size_t)capS);
     L.splats = take(sizeof(sc_splat) * (size_t)capS);
     L.wins = take(sizeof(sc_window) * (size_t)capS);
-    L.key_a = take(4 * (size_t)capS);
-    L.key_b = take(4 * (size_t)capS);
-    L.val_a = take(4 * (size_t)capS);
-    L.val_b = take(4 * (size_t)capS);
+    // +16 bytes: onesweep bulk copies round the last tile up to 16 bytes
+    L.key_a = take(4 * (size_t)capS + 16);
+    L.key_b = take(4 * (size_t)capS + 16);
+    L.pv_a = take(8 * (size_t)capS + 16);
+    L.pv_b = take(8 * (size_t)capS + 16);
     L.depth64 = take(8 * (size_t)capS);
     L.rect = take(8 * (size_t)capS);
     L.ecount = take(4 * (size_t)capS);
-    L.ekey_a = take(4 * (size_t)capE);
-    L.ekey_b = take(4 * (size_t)capE);
-    L.eval_a = take(4 * (size_t)capE);
-    L.eval_b = take(4 * (size_t)capE);
+    L.ekey_a = take(4 * (size_t)capE + 16);
+    L.ekey_b = take(4 * (size_t)capE + 16);
+    L.eval_a = take(4 * (size_t)capE + 16);
+    L.eval_b = take(4 * (size_t)capE + 16);
     L.tile_off = take(4 * (size_t)(L.n_tiles + 1));
     L.task_order = take(4 * (size_t)(2 * L.n_tiles));
     L.boff = take(4 * (size_t)(8 * L.n_tiles + 1));
-    L.hist = take(4 * (size_t)(256 * L.nblk_max));
+    L.rs_counts = take(4 * (size_t)(256 * L.nblk_max));
     L.scan_part = take(4 * (size_t)part);
     L.total = off;
     return L;
@@ -113,8 +113,8 @@ int carve(const sc_workspace *ws, int32_t w, int32_t h, sc::Ws &out)
     out.wins = reinterpret_cast<sc_window *>(b + L.wins);
     out.key_a = reinterpret_cast<uint32_t *>(b + L.key_a);
     out.key_b = reinterpret_cast<uint32_t *>(b + L.key_b);
-    out.val_a = reinterpret_cast<uint32_t *>(b + L.val_a);
-    out.val_b = reinterpret_cast<uint32_t *>(b + L.val_b);
+    out.pv_a = reinterpret_cast<uint2 *>(b + L.pv_a);
+    out.pv_b = reinterpret_cast<uint2 *>(b + L.pv_b);
     out.depth64 = reinterpret_cast<double *>(b + L.depth64);
     out.rect = reinterpret_cast<ushort4 *>(b + L.rect);
     out.ecount = reinterpret_cast<uint32_t *>(b + L.ecount);
@@ -125,7 +125,7 @@ int carve(const sc_workspace *ws, int32_t w, int32_t h, sc::Ws &out)
     out.tile_off = reinterpret_cast<uint32_t *>(b + L.tile_off);
     out.task_order = reinterpret_cast<uint32_t *>(b + L.task_order);
     out.boff = reinterpret_cast<uint32_t *>(b + L.boff);
-    out.hist = reinterpret_cast<uint32_t *>(b + L.hist);
+    out.rs_counts = reinterpret_cast<uint32_t *>(b + L.rs_counts);
     out.scan_part = reinterpret_cast<uint32_t *>(b + L.scan_part);
     out.capS = ws->cap_survivors;
     out.capE = ws->cap_entries;
@@ -211,8 +211,8 @@ int sc_project(const sc_scene *scene, const sc_survivor *survivors, int64_t n, c
     if (!stats) return fail(SC_ERR_INVALID, "stats is NULL%s");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
-    SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, windows, nullptr, nullptr, dbg_f64,
-                              dbg_rect, dbg_flags, stats, nullptr, st),
+    SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, windows, nullptr, nullptr, nullptr,
+                              nullptr, dbg_f64, dbg_rect, dbg_flags, stats, nullptr, st),
            "project");
     return SC_OK;
 }
@@ -234,10 +234,11 @@ int sc_bin_sort(const sc_scene *scene, const sc_survivor *survivors, int64_t n, 
     SC_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(sc::Counters), st), "memset counters");
     uint32_t *order = nullptr, *entries = nullptr;
     SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, wins, w.depth64, w.rect, nullptr,
-                              nullptr, nullptr, stats, w.ctr, st),
+                              nullptr, nullptr, nullptr, nullptr, stats, w.ctr, st),
            "project");
     // reference tile binning (bin_tiles semantics) for parity with the oracle
-    SC_TRY(sc::launch_bin(w, nullptr, n, *cam, wins, stats, false, &order, &entries, nullptr, st), "bin/sort");
+    SC_TRY(sc::launch_bin(w, *scene, survivors, nullptr, n, *cam, wins, stats, false, &order, &entries, nullptr, st),
+           "bin/sort");
     if (order_idx && n > 0) SC_TRY(cudaMemcpyAsync(order_idx, order, 4 * (size_t)n, cudaMemcpyDeviceToDevice, st), "copy order");
     if (entry_idx && w.capE > 0)
         SC_TRY(cudaMemcpyAsync(entry_idx, entries, 4 * (size_t)w.capE, cudaMemcpyDeviceToDevice, st), "copy entries");
@@ -288,13 +289,14 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
     SC_TRY(sc::launch_prep(*scene, *cam, *opts, w, stats, st), "prep");
     SC_TRY(sc::launch_cull(*scene, *cam, *opts, w, w.surv, w.capS, stats, st), "cull");
     SC_TRY(mark(1), "event");
-    SC_TRY(sc::launch_project(*scene, w.surv, &w.ctr->survivors, w.capS, *cam, *opts, w.splats, w.wins, w.depth64,
-                              nullptr, nullptr, nullptr, nullptr, stats, w.ctr, st),
+    SC_TRY(sc::launch_project(*scene, w.surv, &w.ctr->survivors, w.capS, *cam, *opts, w.splats, w.wins, nullptr,
+                              nullptr, w.key_a, w.pv_a, nullptr, nullptr, nullptr, stats, w.ctr, st),
            "project");
     SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;
     uint32_t *bkeys = nullptr;
-    SC_TRY(sc::launch_bin(w, &w.ctr->survivors, w.capS, *cam, w.wins, stats, true, &order, &entries, &bkeys, st),
+    SC_TRY(sc::launch_bin(w, *scene, w.surv, &w.ctr->survivors, w.capS, *cam, w.wins, stats, true, &order, &entries,
+                          &bkeys, st),
            "bin/sort");
     SC_TRY(mark(3), "event");
     if (opts->record_contributions && w.capS > 0)

@@ -14,7 +14,7 @@ constexpr int kCullTilesPerChunk = 8;  // chunk = 1024 (instance, gaussian) pair
 constexpr int kChunk = kCullThreads * kCullTilesPerChunk;
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
-constexpr int kRadixTile = kRadixThreads * kRadixItems;   // 4096 keys per block
+constexpr int kRadixTile = 4096;                          // radix sort tile (count matrix sizing)
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
@@ -39,6 +39,8 @@ struct Counters {
     unsigned long long entries_eff;    // entries, or 0 when they overflow the workspace
     unsigned long long dmin_inv;       // ~bits(min passed depth)  (atomicMax of ~bits; 0 = none)
     unsigned long long dmax;           // bits(max passed depth)   (positive doubles order as u64)
+    unsigned long long tie_runs;       // runs of equal depth keys found by the tie-fix
+    double key_dmin, key_scale;        // frame path: depth-key quantisation from the instance spheres (k_prep)
 };
 
 // Workspace carve-out (all offsets 256-byte aligned), see api.cu:carve().
@@ -49,9 +51,9 @@ struct Ws {
     sc_survivor *surv;               // [capS]
     sc_splat *splats;                // [capS]
     sc_window *wins;                 // [capS]
-    uint32_t *key_a, *key_b;         // [capS]
-    uint32_t *val_a, *val_b;         // [capS]
-    double *depth64;                 // [capS]
+    uint32_t *key_a, *key_b;         // [capS]  depth keys (ping-pong)
+    uint2 *pv_a, *pv_b;              // [capS]  (survivor index, packed pixel window) riding the depth sort
+    double *depth64;                 // [capS]  stage-level API only
     ushort4 *rect;                   // [capS]  tx0, tx1, ty0, ty1
     uint32_t *ecount;                // [capS]  tile count -> exclusive offsets
     uint32_t *ekey_a, *ekey_b;       // [capE]
@@ -59,7 +61,7 @@ struct Ws {
     uint32_t *tile_off;              // [n_tiles + 1]
     uint32_t *task_order;            // [2 n_tiles] blend dispatch order (heavy tiles first)
     uint32_t *boff;                  // [8 n_tiles + 1] offsets of the per-(tile, 8x4 block) entry lists
-    uint32_t *hist;                  // radix histograms [256 * nblk_max]
+    uint32_t *rs_counts;             // radix pass digit counts -> bases, digit-major [256][nblk_max]
     uint32_t *scan_part;             // scan partials
     int64_t capS, capE, max_chunks, nblk_max, n_tiles;
     int n_tx, n_ty;
@@ -104,6 +106,44 @@ __device__ __forceinline__ void cam_xyz(const sc_camera &c, double m0, double m1
     tz = R[6] * (m0 - c.pos[0]) + R[7] * (m1 - c.pos[1]) + R[8] * (m2 - c.pos[2]);
 }
 
+// Packed pixel window (frame path sort payload): the window clamped to the
+// image, x0 | y0 << 12 | (x1 - x0) << 24 | (y1 - y0) << 28 when it is at most
+// 16 x 16 pixels and y0 < 4095; else kWinEscape (read sc_window from the
+// array) or kWinEmpty.  Both sentinels have y0 = 4095, never a compact value.
+constexpr uint32_t kWinEmpty = 0xFFFFFFFFu;
+constexpr uint32_t kWinEscape = 0xFFFFFFFEu;
+
+__host__ __device__ __forceinline__ uint32_t pack_window(int x0, int x1, int y0, int y1, int width, int height)
+{
+    x0 = x0 > 0 ? x0 : 0;
+    y0 = y0 > 0 ? y0 : 0;
+    x1 = x1 < width - 1 ? x1 : width - 1;
+    y1 = y1 < height - 1 ? y1 : height - 1;
+    if (x0 > x1 || y0 > y1) return kWinEmpty;
+    if (x1 - x0 > 15 || y1 - y0 > 15 || x0 > 4095 || y0 >= 4095) return kWinEscape;
+    return (uint32_t)x0 | ((uint32_t)y0 << 12) | ((uint32_t)(x1 - x0) << 24) | ((uint32_t)(y1 - y0) << 28);
+}
+
+// -> false for an empty window
+__device__ __forceinline__ bool unpack_window(uint32_t p, uint32_t idx, const sc_window *wins, int width, int height,
+                                              int &x0, int &x1, int &y0, int &y1)
+{
+    if (p == kWinEmpty) return false;
+    if (p == kWinEscape) {
+        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(wins + idx));
+        x0 = max((int)(int16_t)(w.x & 0xFFFF), 0);
+        x1 = min((int)(int16_t)(w.x >> 16), width - 1);
+        y0 = max((int)(int16_t)(w.y & 0xFFFF), 0);
+        y1 = min((int)(int16_t)(w.y >> 16), height - 1);
+        return x0 <= x1 && y0 <= y1;
+    }
+    x0 = (int)(p & 0xFFFu);
+    y0 = (int)((p >> 12) & 0xFFFu);
+    x1 = x0 + (int)((p >> 24) & 0xFu);
+    y1 = y0 + (int)(p >> 28);
+    return true;
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt()
 {
     uint32_t m;
@@ -136,12 +176,17 @@ cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_op
                         sc_survivor *out, int64_t cap, sc_frame_stats *stats, cudaStream_t st);
 cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
-                           sc_window *wins, double *depth64, ushort4 *rect, double *dbg_f64,
-                           int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr,
-                           cudaStream_t st);
-cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
-                       const sc_window *wins, sc_frame_stats *stats, bool blocks, uint32_t **order_out,
-                       uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st);
+                           sc_window *wins, double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
+                           double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats,
+                           Counters *ctr, cudaStream_t st);
+// equal depth keys -> (f64 depth, survivor index) order; depth from depth64 or
+// recomputed from the survivor (project.cu, -fmad=false)
+cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const sc_camera &cam, const uint32_t *keys,
+                          uint2 *pv, const double *depth64, const unsigned long long *n_dev, int64_t n_max,
+                          uint32_t *run_list, Counters *ctr, sc_frame_stats *stats, cudaStream_t st);
+cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
+                       int64_t n_max, const sc_camera &cam, const sc_window *wins, sc_frame_stats *stats, bool blocks,
+                       uint32_t **order_out, uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st);
 // Blend input, one of:
 //  * block lists (frame path): boff [8 n_tiles + 1], vals = survivor per entry,
 //    keys = block id << 10 | block-relative window;

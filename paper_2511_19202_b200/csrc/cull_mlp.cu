@@ -22,12 +22,16 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
 {
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_running;
-    __shared__ unsigned long long s_pairs, s_vis;
+    __shared__ unsigned long long s_pairs, s_vis, s_dlo, s_dhi;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // passed splats have depth > near; non-negative doubles order as their bits
+    const double d_floor = fmax(cam.near_, 0.0);
     if (tid == 0) {
         s_running = 0;
         s_pairs = 0;
         s_vis = 0;
+        s_dlo = (unsigned long long)__double_as_longlong(INFINITY);
+        s_dhi = 0ull;
     }
     __syncthreads();
     const double f = cam.focal;
@@ -45,13 +49,13 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
             for (int k = 0; k < 3; k++)
                 fr.fwd_local[k] = (float)(in.R[k] * cam.rot[6] + in.R[3 + k] * cam.rot[7] + in.R[6 + k] * cam.rot[8]);
             int vis = a.count > 0;
+            // sphere around the instance covering every instanced mean, with slack
+            // for the f32 rounding of instanced means
+            const double tmax = fmax(fabs(in.t[0]), fmax(fabs(in.t[1]), fabs(in.t[2])));
+            const double rho = in.s * a.bound_local * (1.0 + 1e-6) + 1e-6 * (2.0 * tmax + in.s * a.bound_local) + 1e-9;
+            double cx, cy, cz;
+            cam_xyz(cam, in.t[0], in.t[1], in.t[2], cx, cy, cz);
             if (opts.frustum_mode != SC_FRUSTUM_OFF && vis) {
-                // sphere around the instance covering every instanced mean, with slack
-                // for the f32 rounding of instanced means
-                double tmax = fmax(fabs(in.t[0]), fmax(fabs(in.t[1]), fabs(in.t[2])));
-                double rho = in.s * a.bound_local * (1.0 + 1e-6) + 1e-6 * (2.0 * tmax + in.s * a.bound_local) + 1e-9;
-                double cx, cy, cz;
-                cam_xyz(cam, in.t[0], in.t[1], in.t[2], cx, cy, cz);
                 if (cz + rho <= cam.near_) vis = 0;
                 double mg = 0.0, pad = 0.0, xlo = 0.0, xhi = (double)(cam.width - 1), ylo = 0.0,
                        yhi = (double)(cam.height - 1);
@@ -70,6 +74,12 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
                 if (f * cy + kl * cz + mg + rho * sqrt(f * f + kl * kl) < 0.0) vis = 0;
                 kh = cyp - pad - yhi;
                 if (f * cy + kh * cz - mg - rho * sqrt(f * f + kh * kh) > 0.0) vis = 0;
+            }
+            if (vis) {   // depth range of every instanced mean of a visible instance (frame-path sort keys)
+                const double lo = fmax(cz - rho * (1.0 + 1e-9), d_floor);
+                const double hi = fmax(cz + rho * (1.0 + 1e-9), lo);
+                atomicMin(&s_dlo, (unsigned long long)__double_as_longlong(lo));
+                atomicMax(&s_dhi, (unsigned long long)__double_as_longlong(hi));
             }
             fr.visible = vis;
             nch = vis ? (uint32_t)((a.count + kChunk - 1) / kChunk) : 0u;
@@ -110,6 +120,10 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
         ws.ctr->total_chunks = s_running;
         ws.ctr->chunk_ticket = 0;
         stats->instances_visible = (int64_t)s_vis;
+        // frame-path depth keys: floor((tz - dmin) * scale) over [dmin, dmax] (k_project)
+        const double dlo = __longlong_as_double((long long)s_dlo), dhi = __longlong_as_double((long long)s_dhi);
+        ws.ctr->key_dmin = s_vis ? dlo : 0.0;
+        ws.ctr->key_scale = (s_vis && dhi > dlo) ? 4294967040.0 / (dhi - dlo) : 0.0;
         stats->pairs_tested = (int64_t)s_pairs;
     }
 }

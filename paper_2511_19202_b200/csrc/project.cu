@@ -26,13 +26,15 @@ __device__ __forceinline__ int16_t clamp16(double v)
 
 __device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-__global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_survivor *surv,
+__global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_survivor *surv,
                                                  const unsigned long long *n_dev, int64_t n_host, sc_camera cam,
                                                  sc_opts opts, sc_splat *splats, sc_window *wins,
-                                                 double *depth64, ushort4 *rect, double *dbg_f64, int32_t *dbg_rect,
-                                                 uint8_t *dbg_flags, sc_frame_stats *stats,
-                                                 Counters *ctr)
+                                                 double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
+                                                 double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags,
+                                                 sc_frame_stats *stats, Counters *ctr)
 {
+    // frame path: depth keys quantised over the instance spheres' depth range (k_prep)
+    const double key_dmin = keys ? ctr->key_dmin : 0.0, key_scale = keys ? ctr->key_scale : 0.0;
     const int64_t n = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
     const double lim_x = 1.3 * cam.tan_x, lim_y = 1.3 * cam.tan_y;
     const double focal = cam.focal;
@@ -229,7 +231,16 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
         }
         splats[k] = sp;
         wins[k] = win;
-        if (depth64) depth64[k] = passed ? tz : -1.0;   // sort keys are quantised in k_depth_keys
+        if (depth64) depth64[k] = passed ? tz : -1.0;   // stage API: sort keys are quantised in k_depth_keys
+        if (keys) {
+            // monotone non-decreasing in tz (clamped subtraction, positive scale, floor): equal keys are
+            // re-ordered by (tz, index) in the tie-fix; non-passed splats sink to the end
+            constexpr double kTop = 4294967040.0;
+            keys[k] = passed ? (uint32_t)fmin(floor(fmax(tz - key_dmin, 0.0) * key_scale), kTop) : 0xFFFFFFFFu;
+            pv[k] = make_uint2((uint32_t)k, passed ? pack_window(win.x0, win.x1, win.y0, win.y1, cam.width,
+                                                                 cam.height)
+                                                   : kWinEmpty);
+        }
         if (rect) rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0, (unsigned short)ty1);
         if (dbg_f64) {
             double *d = dbg_f64 + 8 * k;
@@ -263,9 +274,9 @@ __global__ void __launch_bounds__(256) k_project(sc_scene scene, const sc_surviv
 
 cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
-                           sc_window *wins, double *depth64, ushort4 *rect, double *dbg_f64,
-                           int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr,
-                           cudaStream_t st)
+                           sc_window *wins, double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
+                           double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats,
+                           Counters *ctr, cudaStream_t st)
 {
     if (n_max <= 0) return cudaSuccess;
     int dev = 0, nsm = 148;
@@ -273,7 +284,163 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 8);
     SC_LAUNCH(k_project, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins, depth64,
-              rect, dbg_f64, dbg_rect, dbg_flags, stats, ctr);
+              rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// tie-fix: runs of equal depth keys -> (f64 depth, survivor index) order, the
+// reference's argsort(kind="stable") order (sc/raster.py:319).  The depth is
+// read from depth64 (stage API) or recomputed from the survivor exactly as the
+// projection computes it (frame path; this TU is -fmad=false).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double tie_depth(const sc_scene &scene, const sc_survivor *surv, const sc_camera &cam,
+                                            const double *depth64, uint32_t idx)
+{
+    if (depth64) return depth64[idx];
+    const sc_survivor sv = surv[idx];
+    const sc_instance_rec &in = scene.instances[sv.inst];
+    const int64_t g = scene.assets[in.asset].offset + sv.gid;
+    const float4 mo = __ldg(reinterpret_cast<const float4 *>(scene.mean_opa) + g);
+    const float3 mw = inst_mean(in, mo.x, mo.y, mo.z);
+    double tx, ty, tz;
+    cam_xyz(cam, mw.x, mw.y, mw.z, tx, ty, tz);
+    return tz;
+}
+
+// pass 1: heads of runs of >= 2 equal keys -> run_list (order irrelevant).
+// A thread scans 8 consecutive keys; one global atomic per 2048-key CTA chunk.
+__global__ void __launch_bounds__(256) k_tie_heads(const uint32_t *keys, const unsigned long long *n_dev,
+                                                   int64_t n_host, uint32_t *run_list, Counters *ctr)
+{
+    __shared__ uint32_t s_warp[8], s_base;
+    const int64_t n = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t cbase = blockIdx.x * 2048ll; cbase < n; cbase += (int64_t)gridDim.x * 2048) {
+        const int64_t i0 = cbase + 8 * threadIdx.x;
+        uint32_t kv[10];   // keys i0 - 1 .. i0 + 8
+        uint32_t heads = 0;
+        if (i0 < n) {
+            if (i0 + 8 <= n && (i0 & 3) == 0) {
+                const uint4 a = __ldg(reinterpret_cast<const uint4 *>(keys + i0));
+                const uint4 b = __ldg(reinterpret_cast<const uint4 *>(keys + i0) + 1);
+                kv[1] = a.x; kv[2] = a.y; kv[3] = a.z; kv[4] = a.w; kv[5] = b.x; kv[6] = b.y; kv[7] = b.z; kv[8] = b.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; j++) kv[j + 1] = i0 + j < n ? keys[i0 + j] : 0u;
+            }
+            kv[0] = i0 > 0 ? keys[i0 - 1] : ~kv[1];
+            kv[9] = i0 + 8 < n ? keys[i0 + 8] : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int64_t i = i0 + j;
+                const bool h = i + 1 < n && kv[j] != kv[j + 1] && kv[j + 1] == kv[j + 2];
+                heads |= (uint32_t)h << j;
+            }
+        }
+        uint32_t c = __popc(heads), x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[wid] = x;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < 8; w++) {
+                const uint32_t ww = s_warp[w];
+                s_warp[w] = t;
+                t += ww;
+            }
+            s_base = t ? (uint32_t)atomicAdd(&ctr->tie_runs, (unsigned long long)t) : 0u;
+        }
+        __syncthreads();
+        uint32_t slot = s_base + s_warp[wid] + x - c;
+        while (heads) {
+            const int j = __ffs(heads) - 1;
+            heads &= heads - 1;
+            run_list[slot++] = (uint32_t)(i0 + j);
+        }
+        __syncthreads();
+    }
+}
+
+// pass 2: one thread per run, insertion sort on (depth, index); runs of up to
+// kTieRegs elements have their depths computed independently (ILP)
+constexpr int kTieRegs = 8;
+__global__ void k_tie_runs(sc_scene scene, const sc_survivor *surv, sc_camera cam, const uint32_t *keys, uint2 *pv,
+                           const double *depth64, const unsigned long long *n_dev, int64_t n_host,
+                           const uint32_t *run_list, const Counters *ctr, sc_frame_stats *stats)
+{
+    const int64_t n = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
+    const int64_t runs = (int64_t)ctr->tie_runs;
+    unsigned long long longest = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < runs; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = run_list[r];
+        const uint32_t key = keys[i];
+        int64_t e = i + 1;
+        while (e < n && keys[e] == key) e++;
+        const int len = (int)(e - i);
+        longest = max(longest, (unsigned long long)len);
+        if (len <= kTieRegs) {
+            uint2 v[kTieRegs];
+            double d[kTieRegs];
+#pragma unroll
+            for (int q = 0; q < kTieRegs; q++)
+                if (q < len) v[q] = pv[i + q];
+#pragma unroll
+            for (int q = 0; q < kTieRegs; q++)
+                if (q < len) d[q] = tie_depth(scene, surv, cam, depth64, v[q].x);
+#pragma unroll
+            for (int a = 1; a < kTieRegs; a++) {
+                if (a < len) {
+#pragma unroll
+                    for (int b = a; b > 0; b--) {   // bubble element a down (stable)
+                        const bool sw = d[b] < d[b - 1] || (d[b] == d[b - 1] && v[b].x < v[b - 1].x);
+                        if (sw) {
+                            const double td = d[b]; d[b] = d[b - 1]; d[b - 1] = td;
+                            const uint2 tv = v[b]; v[b] = v[b - 1]; v[b - 1] = tv;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kTieRegs; q++)
+                if (q < len) pv[i + q] = v[q];
+        } else {
+            for (int64_t a = i + 1; a < e; a++) {
+                const uint2 va = pv[a];
+                const double da = tie_depth(scene, surv, cam, depth64, va.x);
+                int64_t b = a - 1;
+                while (b >= i) {
+                    const uint2 vb = pv[b];
+                    const double db = tie_depth(scene, surv, cam, depth64, vb.x);
+                    if (db < da || (db == da && vb.x < va.x)) break;
+                    pv[b + 1] = vb;
+                    b--;
+                }
+                pv[b + 1] = va;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) longest = max(longest, __shfl_down_sync(0xffffffffu, longest, o));
+    if ((threadIdx.x & 31) == 0 && longest) atomicMax((unsigned long long *)&stats->max_tie_run, longest);
+}
+
+cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const sc_camera &cam, const uint32_t *keys,
+                          uint2 *pv, const double *depth64, const unsigned long long *n_dev, int64_t n_max,
+                          uint32_t *run_list, Counters *ctr, sc_frame_stats *stats, cudaStream_t st)
+{
+    if (n_max <= 0) return cudaSuccess;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 16);
+    const int64_t hblocks = std::min<int64_t>((n_max + 2047) / 2048, (int64_t)nsm * 8);
+    SC_LAUNCH(k_tie_heads, (int)std::max<int64_t>(1, hblocks), 256, 0, st, keys, n_dev, n_max, run_list, ctr);
+    SC_LAUNCH(k_tie_runs, (int)std::max<int64_t>(1, blocks / 8), 256, 0, st, scene, surv, cam, keys, pv, depth64, n_dev,
+              n_max, run_list, ctr, stats);
     return cudaGetLastError();
 }
 

@@ -108,23 +108,40 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t *in, 
     const int64_t n = dev_count(n_dev, n_host);
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     if (base >= n) return;
-    // blocked arrangement: thread t owns items [base + t*16, base + t*16 + 16)
+    // blocked arrangement: thread t owns items [base + t*16, base + t*16 + 16), moved as 4 x uint4
+    static_assert(kScanItems == 16, "vector path assumes 16 items per thread");
     uint32_t v[kScanItems];
     uint32_t sum = 0;
     const int64_t my = base + (int64_t)threadIdx.x * kScanItems;
+    const bool full = my + kScanItems <= n;
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        const int64_t i = my + j;
-        v[j] = i < n ? in[i] : 0u;
-        sum += v[j];
+        for (int q = 0; q < 4; q++) {
+            const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(in + my) + q);
+            v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++) v[j] = my + j < n ? in[my + j] : 0u;
     }
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) sum += v[j];
     uint32_t total;
     uint32_t run = block_excl_scan<kScanThreads>(sum, s_warp, total) + part[blockIdx.x];
 #pragma unroll
     for (int j = 0; j < kScanItems; j++) {
-        const int64_t i = my + j;
-        if (i < n) out[i] = run;
-        run += v[j];
+        const uint32_t x = v[j];
+        v[j] = run;
+        run += x;
+    }
+    if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            reinterpret_cast<uint4 *>(out + my)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++)
+            if (my + j < n) out[my + j] = v[j];
     }
 }
 
@@ -139,128 +156,282 @@ static cudaError_t scan_excl(const uint32_t *in, uint32_t *out, const unsigned l
 }
 
 // ---------------------------------------------------------------------------
-// LSD radix sort pass (8-bit digit), reduce-then-scan, stable.
-// hist layout: digit-major [256][nblk] so one exclusive scan yields every
-// (digit, block) scatter base.
+// LSD radix sort (8-bit digits), stable, reduce-then-scan per pass:
+//   upsweep:   per 4096-key tile, digit counts -> counts[digit][tile]
+//   scan:      one exclusive scan over the digit-major matrix = every
+//              (digit, tile) global scatter base (no inter-tile chains)
+//   downsweep: persistent CTAs; a tile's keys/values arrive by TMA bulk copy
+//              into one of two shared buffers while the previous tile is
+//              ranked and scattered; stable warp-private ranking (match.any),
+//              staging in shared memory, digit-run coalesced write-out.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t *keys, const unsigned long long *n_dev,
-                                                              int64_t n_host, int shift, uint32_t *hist,
-                                                              int64_t nblk)
+constexpr int kOsThreads = 512;
+constexpr int kOsItems = 8;
+constexpr int kOsTile = kOsThreads * kOsItems;
+constexpr int kOsWarps = kOsThreads / 32;
+static_assert(kOsTile == kRadixTile, "matrix sizing in api.cu assumes kRadixTile keys per tile");
+
+// lanes of the warp holding the same 8-bit digit: 8 ballots, constant cost
+// (match.any's cost grows with the number of distinct values in the warp)
+__device__ __forceinline__ uint32_t match_digit8(uint32_t d)
 {
-    __shared__ uint32_t h[256];
-    const int64_t n = dev_count(n_dev, n_host);
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kRadixTile;
-    if (base < n) {
-#pragma unroll 4
-        for (int j = 0; j < kRadixItems; j++) {
-            const int64_t i = base + (int64_t)j * kRadixThreads + threadIdx.x;
-            if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xFFu], 1u);
-        }
+    uint32_t m = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const uint32_t bit = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        m &= bit ? bal : ~bal;
     }
-    __syncthreads();
-    hist[(int64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
+    return m;
 }
 
-__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t *keys_in, const uint32_t *vals_in,
-                                                                 uint32_t *keys_out, uint32_t *vals_out,
-                                                                 const unsigned long long *n_dev, int64_t n_host,
-                                                                 int shift, const uint32_t *hist_scanned,
-                                                                 int64_t nblk)
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void os_mbar_init(uint64_t *bar)
 {
-    // Stable local ranking with warp-private digit counters: warp w owns the
-    // contiguous slice [w * 512, (w + 1) * 512) of the block's keys (read 32 at
-    // a time, coalesced), ranks each round with match_any, and keeps running
-    // per-digit counts in its own smem row — no block barrier until the end,
-    // where one per-digit prefix over warps and one scan over digits give every
-    // key its block-local position.  (Index order = warp-major order, so the
-    // ranking is stable.)
-    constexpr int kWarps = kRadixThreads / 32;
-    constexpr int kPerWarp = kRadixTile / kWarps;
-    __shared__ uint32_t s_keys[kRadixTile];
-    __shared__ uint32_t s_vals[kRadixTile];
-    __shared__ uint32_t s_wcnt[kWarps][256];
-    __shared__ uint32_t s_dstart[256];   // block-local start of each digit
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void os_mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "OS_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra OS_DONE;\n\t"
+        "bra OS_WAIT;\n\t"
+        "OS_DONE:\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// one thread: expect the bytes on bar, then bulk-copy the two pieces
+__device__ __forceinline__ void os_bulk_load(uint64_t *bar, void *dk, const void *sk, uint32_t bk, void *dv,
+                                             const void *sv, uint32_t bv)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bk + bv)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dk)),
+                 "l"(sk), "r"(bk), "r"(smem_addr(bar))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dv)),
+                 "l"(sv), "r"(bv), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+// Upsweep: warp-private shared histograms (plain shared atomics, no ranking),
+// keys loaded 4 per thread per load (uint4, streaming).
+__global__ void __launch_bounds__(kOsThreads) k_radix_up(const uint32_t *__restrict__ keys,
+                                                         const unsigned long long *n_dev, int64_t n_host, int shift,
+                                                         uint32_t *counts, int64_t ntiles_max)
+{
+    __shared__ uint32_t h[kOsWarps][256];
+    const int tid = threadIdx.x, wid = tid >> 5;
+    const int64_t n = dev_count(n_dev, n_host);
+    for (int64_t t = blockIdx.x; t < ntiles_max; t += gridDim.x) {
+        for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&h[0][0])[i] = 0;
+        __syncthreads();
+        const int64_t base = t * kOsTile;
+        if (base < n) {
+            const int cnt = (int)std::min<int64_t>(kOsTile, n - base);
+            uint32_t *hw = h[wid];
+#pragma unroll
+            for (int q = 0; q < kOsItems / 4; q++) {
+                const int i = 4 * (q * kOsThreads + tid);   // 4 consecutive keys
+                if (i + 4 <= cnt) {
+                    const uint4 k = __ldcs(reinterpret_cast<const uint4 *>(keys + base + i));
+                    atomicAdd(&hw[(k.x >> shift) & 0xFFu], 1u);
+                    atomicAdd(&hw[(k.y >> shift) & 0xFFu], 1u);
+                    atomicAdd(&hw[(k.z >> shift) & 0xFFu], 1u);
+                    atomicAdd(&hw[(k.w >> shift) & 0xFFu], 1u);
+                } else {
+                    for (int e = i; e < cnt && e < i + 4; e++) atomicAdd(&hw[(keys[base + e] >> shift) & 0xFFu], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        // digit-major: the matrix's exclusive scan is every (digit, tile) base; empty tiles write zeros
+        if (tid < 256) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int w = 0; w < kOsWarps; w++) c += h[w][tid];
+            counts[(int64_t)tid * ntiles_max + t] = c;
+        }
+        __syncthreads();
+    }
+}
+
+// (the ranked tile is staged back into its own input buffer for the write-out)
+template <typename V>
+struct OsSmem {
+    uint32_t in_k[2][kOsTile];
+    V in_v[2][kOsTile];
+    uint16_t wcnt[kOsWarps][256];
+};
+
+template <typename V>
+__global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__restrict__ keys_in,
+                                                              const V *__restrict__ vals_in,
+                                                              uint32_t *__restrict__ keys_out,
+                                                              V *__restrict__ vals_out,
+                                                              const unsigned long long *n_dev, int64_t n_host,
+                                                              int shift, const uint32_t *__restrict__ bases,
+                                                              int64_t ntiles_max)
+{
+    constexpr int kPerWarp = kOsTile / kOsWarps;
+    extern __shared__ __align__(128) uint4 s_dyn4[];
+    OsSmem<V> &sm = *reinterpret_cast<OsSmem<V> *>(s_dyn4);
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ uint32_t s_dstart[256];   // tile-local start of each digit
     __shared__ uint32_t s_gbase[256];    // global scatter base of each digit
     __shared__ uint32_t s_warp[32];
-    const int64_t n = dev_count(n_dev, n_host);
-    const int64_t base = (int64_t)blockIdx.x * kRadixTile;
-    if (base >= n) return;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int cnt = (int)std::min<int64_t>(kRadixTile, n - base);
-#pragma unroll
-    for (int w = 0; w < kWarps; w++) s_wcnt[w][tid] = 0;
-    s_gbase[tid] = hist_scanned[(int64_t)tid * nblk + blockIdx.x];
 
-    uint32_t k[kRadixItems], v[kRadixItems], rk[kRadixItems];
-#pragma unroll
-    for (int j = 0; j < kRadixItems; j++) {
-        const int i = wid * kPerWarp + j * 32 + lane;
-        k[j] = i < cnt ? keys_in[base + i] : 0u;
-        v[j] = i < cnt ? vals_in[base + i] : 0u;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t n = dev_count(n_dev, n_host);
+    const int64_t ntiles = (n + kOsTile - 1) / kOsTile;
+    auto issue = [&](int64_t t, int b) {
+        const int64_t base = t * kOsTile;
+        const uint32_t c = (uint32_t)std::min<int64_t>(kOsTile, n - base);
+        // sizes rounded up to 16 B (the key / value buffers carry 16 bytes of slack)
+        os_bulk_load(&s_bar[b], sm.in_k[b], keys_in + base, (c * 4u + 15u) & ~15u, sm.in_v[b], vals_in + base,
+                     (c * (uint32_t)sizeof(V) + 15u) & ~15u);
+    };
+    int64_t tile = blockIdx.x;
+    if (tile >= ntiles) return;
+    if (tid == 0) {
+        os_mbar_init(&s_bar[0]);
+        os_mbar_init(&s_bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue(tile, 0);
     }
-    __syncthreads();
+    uint32_t phase0 = 0, phase1 = 0;
+    int b = 0;
     const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int j = 0; j < kRadixItems; j++) {
-        const bool ok = wid * kPerWarp + j * 32 + lane < cnt;
-        const uint32_t d = ok ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane;   // unique dummy digit
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t r = __popc(peers & lt);
-        const uint32_t prev = ok ? s_wcnt[wid][d] : 0u;
-        __syncwarp();
-        if (ok && r == 0) s_wcnt[wid][d] = prev + __popc(peers);
-        __syncwarp();
-        rk[j] = prev + r;
-    }
-    __syncthreads();
-    {   // per digit (thread = digit): exclusive prefix over warps, then scan over digits
-        uint32_t run = 0;
-#pragma unroll
-        for (int w = 0; w < kWarps; w++) {
-            const uint32_t c = s_wcnt[w][tid];
-            s_wcnt[w][tid] = run;
-            run += c;
+    for (; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();   // buffer b^1 (previous tile) fully written out
+        if (tid == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, b ^ 1);
+        for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&sm.wcnt[0][0])[i] = 0;
+        uint32_t gb = 0;
+        if (tid < 256) gb = bases[(int64_t)tid * ntiles_max + tile];
+        const int64_t base = tile * kOsTile;
+        const int cnt = (int)std::min<int64_t>(kOsTile, n - base);
+        if (b == 0) {
+            os_mbar_wait(&s_bar[0], phase0);
+            phase0 ^= 1u;
+        } else {
+            os_mbar_wait(&s_bar[1], phase1);
+            phase1 ^= 1u;
         }
-        uint32_t total;
-        s_dstart[tid] = block_excl_scan<kRadixThreads>(run, s_warp, total);
-    }
-    __syncthreads();
+        __syncthreads();
+
+        // stable warp-private ranking: warp w owns the contiguous slice
+        // [w * 256, (w + 1) * 256) and keeps running per-digit counts
+        uint32_t k[kOsItems], rk[kOsItems], peers[kOsItems];
+        V v[kOsItems];
 #pragma unroll
-    for (int j = 0; j < kRadixItems; j++) {
-        if (wid * kPerWarp + j * 32 + lane < cnt) {
+        for (int j = 0; j < kOsItems; j++) {
+            const int i = wid * kPerWarp + j * 32 + lane;
+            k[j] = sm.in_k[b][i];
+            v[j] = sm.in_v[b][i];
+            peers[j] = match_digit8((k[j] >> shift) & 0xFFu) & __ballot_sync(0xffffffffu, i < cnt);
+        }
+#pragma unroll
+        for (int j = 0; j < kOsItems; j++) {
+            const bool ok = wid * kPerWarp + j * 32 + lane < cnt;
             const uint32_t d = (k[j] >> shift) & 0xFFu;
-            const uint32_t pos = s_dstart[d] + s_wcnt[wid][d] + rk[j];
-            s_keys[pos] = k[j];
-            s_vals[pos] = v[j];
+            const uint32_t r = __popc(peers[j] & lt);
+            const uint32_t prev = ok ? sm.wcnt[wid][d] : 0u;
+            __syncwarp();
+            if (ok && r == 0) sm.wcnt[wid][d] = (uint16_t)(prev + __popc(peers[j]));
+            __syncwarp();
+            rk[j] = prev + r;
         }
-    }
-    __syncthreads();
-    // coalesced write-out: consecutive positions of one digit are contiguous in the output
-    for (int i = tid; i < cnt; i += kRadixThreads) {
-        const uint32_t key = s_keys[i];
-        const uint32_t d = (key >> shift) & 0xFFu;
-        const uint32_t dst = s_gbase[d] + (uint32_t)i - s_dstart[d];
-        keys_out[dst] = key;
-        vals_out[dst] = s_vals[i];
+        __syncthreads();
+        uint32_t tot = 0;
+        if (tid < 256) {   // thread = digit: exclusive prefix over warps
+#pragma unroll
+            for (int w = 0; w < kOsWarps; w++) {
+                const uint32_t c = sm.wcnt[w][tid];
+                sm.wcnt[w][tid] = (uint16_t)tot;
+                tot += c;
+            }
+            s_gbase[tid] = gb;
+        }
+        {
+            uint32_t total;
+            const uint32_t ds = block_excl_scan<kOsThreads>(tid < 256 ? tot : 0u, s_warp, total);
+            if (tid < 256) s_dstart[tid] = ds;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kOsItems; j++) {
+            if (wid * kPerWarp + j * 32 + lane < cnt) {
+                const uint32_t d = (k[j] >> shift) & 0xFFu;
+                const uint32_t pos = s_dstart[d] + sm.wcnt[wid][d] + rk[j];
+                sm.in_k[b][pos] = k[j];
+                sm.in_v[b][pos] = v[j];
+            }
+        }
+        __syncthreads();
+        // coalesced write-out: consecutive positions of one digit are contiguous in the output
+#pragma unroll 4
+        for (int i = tid; i < cnt; i += kOsThreads) {
+            const uint32_t key = sm.in_k[b][i];
+            const uint32_t d = (key >> shift) & 0xFFu;
+            const uint32_t dst = s_gbase[d] + (uint32_t)i - s_dstart[d];
+            keys_out[dst] = key;
+            vals_out[dst] = sm.in_v[b][i];
+        }
+        // generic-proxy writes to buffer b above; its next refill is a TMA (async-proxy) write
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        b ^= 1;
     }
 }
 
-// Sorts (keys, vals) in place-ish over `bits` low bits; result ends in the
-// buffer pointed to by *keys_res / *vals_res (ping-pong).
-// Sorts on key bits [bit_lo, bit_hi) (8-bit digits; bits below bit_lo ride along unsorted).
-static cudaError_t radix_sort(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t *vb, const unsigned long long *n_dev,
-                              int64_t n_max, int bit_lo, int bit_hi, uint32_t *hist, uint32_t *part,
-                              uint32_t **keys_res, uint32_t **vals_res, cudaStream_t st)
+template <typename V>
+static cudaError_t radix_down_attr()
 {
-    const int64_t nblk = std::max<int64_t>(1, (n_max + kRadixTile - 1) / kRadixTile);
-    uint32_t *ki = ka, *vi = va, *ko = kb, *vo = vb;
-    for (int shift = bit_lo; shift < bit_hi; shift += 8) {
-        SC_LAUNCH(k_radix_hist, (int)nblk, kRadixThreads, 0, st, ki, n_dev, n_max, shift, hist, nblk);
-        cudaError_t e = scan_excl(hist, hist, nullptr, 256 * nblk, part, nullptr, nullptr, st);
+    static bool done = false;
+    if (done) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_radix_down<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(OsSmem<V>));
+    if (e == cudaSuccess) done = true;
+    return e;
+}
+
+static int sm_count_sort()
+{
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// Sorts (keys, vals) on key bits [bit_lo, bit_hi) (bits below bit_lo ride
+// along); the result ends in the buffers returned through keys_res / vals_res
+// (ping-pong between a and b).
+template <typename V>
+static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const unsigned long long *n_dev, int64_t n_max,
+                              int bit_lo, int bit_hi, const Ws &ws, uint32_t **keys_res, V **vals_res, cudaStream_t st)
+{
+    cudaError_t e = radix_down_attr<V>();
+    if (e != cudaSuccess) return e;
+    const int npass = std::max(1, (bit_hi - bit_lo + 7) / 8);
+    const int64_t ntiles = std::max<int64_t>(1, (n_max + kOsTile - 1) / kOsTile);
+    const int nsm = sm_count_sort();
+    uint32_t *ki = ka, *ko = kb;
+    V *vi = va, *vo = vb;
+    for (int p = 0; p < npass; p++) {
+        const int shift = bit_lo + 8 * p;
+        SC_LAUNCH(k_radix_up, (int)std::min<int64_t>(ntiles, (int64_t)nsm * 4), kOsThreads, 0, st, ki, n_dev, n_max,
+                  shift, ws.rs_counts, ntiles);
+        e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_radix_scatter, (int)nblk, kRadixThreads, 0, st, ki, vi, ko, vo, n_dev, n_max, shift, hist, nblk);
+        SC_LAUNCH(k_radix_down<V>, (int)std::min<int64_t>(ntiles, (int64_t)nsm * 2), kOsThreads, sizeof(OsSmem<V>),
+                  st, ki, vi, ko, vo, n_dev, n_max, shift, ws.rs_counts, ntiles);
         std::swap(ki, ko);
         std::swap(vi, vo);
     }
@@ -270,13 +441,14 @@ static cudaError_t radix_sort(uint32_t *ka, uint32_t *va, uint32_t *kb, uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// depth keys: frame-adaptive 32-bit quantisation of the f64 depth over the
-// passed splats' [dmin, dmax] (monotone non-decreasing, so key order agrees
-// with f64 order wherever keys differ; equal keys go to the tie-fix).  Much
-// finer than an f32 key over the same range, so ties are rare.
+// stage-level API depth keys: frame-adaptive 32-bit quantisation of the f64
+// depth over the passed splats' exact [dmin, dmax] (monotone non-decreasing,
+// so key order agrees with f64 order wherever keys differ; equal keys go to
+// the tie-fix).  The frame path quantises over the instance spheres' depth
+// range inside the projection kernel instead (no depth64 round trip).
 // ---------------------------------------------------------------------------
 __global__ void k_depth_keys(const double *depth64, const unsigned long long *n_dev, int64_t n_host,
-                             const Counters *ctr, uint32_t *keys, uint32_t *vals)
+                             const Counters *ctr, uint32_t *keys, uint2 *pv)
 {
     const int64_t n = dev_count(n_dev, n_host);
     const double dmin = __longlong_as_double((long long)~ctr->dmin_inv);
@@ -288,41 +460,15 @@ __global__ void k_depth_keys(const double *depth64, const unsigned long long *n_
         uint32_t key = 0xFFFFFFFFu;
         if (d >= 0.0) key = (uint32_t)fmin(floor((d - dmin) * scale), kTop);
         keys[k] = key;
-        vals[k] = (uint32_t)k;
+        pv[k] = make_uint2((uint32_t)k, 0u);
     }
 }
 
-// ---------------------------------------------------------------------------
-// tie-fix: equal keys -> order by (f64 depth, survivor index)
-// ---------------------------------------------------------------------------
-__global__ void k_tiefix(const uint32_t *keys, uint32_t *vals, const double *depth64, const unsigned long long *n_dev,
-                        int64_t n_host, sc_frame_stats *stats)
+__global__ void k_extract_order(const uint2 *pv, const unsigned long long *n_dev, int64_t n_host, uint32_t *order)
 {
     const int64_t n = dev_count(n_dev, n_host);
-    unsigned long long longest = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t key = keys[i];
-        if (i > 0 && keys[i - 1] == key) continue;          // not a run head
-        if (i + 1 >= n || keys[i + 1] != key) continue;     // run of length 1
-        int64_t e = i + 1;
-        while (e < n && keys[e] == key) e++;
-        longest = std::max<unsigned long long>(longest, (unsigned long long)(e - i));
-        // insertion sort on (depth64[v], v); linear when already ordered
-        for (int64_t a = i + 1; a < e; a++) {
-            const uint32_t va = vals[a];
-            const double da = depth64[va];
-            int64_t b = a - 1;
-            while (b >= i) {
-                const uint32_t vb = vals[b];
-                const double db = depth64[vb];
-                if (db < da || (db == da && vb < va)) break;
-                vals[b + 1] = vb;
-                b--;
-            }
-            vals[b + 1] = va;
-        }
-    }
-    if (longest) atomicMax((unsigned long long *)&stats->max_tie_run, longest);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        order[k] = pv[k].x;
 }
 
 // ---------------------------------------------------------------------------
@@ -397,32 +543,27 @@ __global__ void k_tile_offsets(const uint32_t *ekey, const unsigned long long *e
 // ---------------------------------------------------------------------------
 constexpr int kCodeBits = 10;
 
-__global__ void k_bentry_count(const uint32_t *order, const sc_window *wins, const unsigned long long *n_dev,
-                               int64_t n_host, int width, int height, uint32_t *cnt, uint32_t *wlo, uint32_t *whi)
+// block entries of one passed splat (depth order), window from the sort payload
+__device__ __forceinline__ uint32_t block_count(int x0, int x1, int y0, int y1)
+{
+    return (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
+}
+
+__global__ void k_bentry_count(const uint2 *pv, const sc_window *wins, const unsigned long long *n_dev,
+                               int64_t n_host, int width, int height, uint32_t *cnt)
 {
     const int64_t n = dev_count(n_dev, n_host);
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(wins + order[k]));
-        // pixels outside the image are never composited (reference th/tw clamp)
-        const int x0 = max((int)(int16_t)(w.x & 0xFFFF), 0), x1 = min((int)(int16_t)(w.x >> 16), width - 1);
-        const int y0 = max((int)(int16_t)(w.y & 0xFFFF), 0), y1 = min((int)(int16_t)(w.y >> 16), height - 1);
-        uint32_t c = 0;
-        if (x0 <= x1 && y0 <= y1) {
-            c = (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
-            wlo[k] = (uint32_t)x0 | ((uint32_t)x1 << 16);
-            whi[k] = (uint32_t)y0 | ((uint32_t)y1 << 16);
-        } else {   // canonical empty window: the emission recomputes the count from these
-            wlo[k] = 1u;
-            whi[k] = 1u;
-        }
-        cnt[k] = c;
+        const uint2 v = pv[k];
+        int x0, x1, y0, y1;
+        cnt[k] = unpack_window(v.y, v.x, wins, width, height, x0, x1, y0, y1) ? block_count(x0, x1, y0, y1) : 0u;
     }
 }
 
-__global__ void k_bentry_emit(const uint32_t *order, const uint32_t *wlo, const uint32_t *whi, const uint32_t *off,
-                              const unsigned long long *n_dev, int64_t n_host, int n_tx, uint32_t *ekey,
-                              uint32_t *eval, const unsigned long long *e_total, unsigned long long *e_eff,
-                              int64_t cap_e, sc_frame_stats *stats)
+__global__ void k_bentry_emit(const uint2 *pv, const sc_window *wins, const uint32_t *off,
+                              const unsigned long long *n_dev, int64_t n_host, int width, int height, int n_tx,
+                              uint32_t *ekey, uint32_t *eval, const unsigned long long *e_total,
+                              unsigned long long *e_eff, int64_t cap_e, sc_frame_stats *stats)
 {
     const int64_t n = dev_count(n_dev, n_host);
     const bool over = (int64_t)*e_total > cap_e;
@@ -441,19 +582,29 @@ __global__ void k_bentry_emit(const uint32_t *order, const uint32_t *wlo, const 
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = warp * 32; base < n; base += n_warps * 32) {
+    // one iteration ahead: the next 32 payloads and their output base are in flight
+    int64_t base = warp * 32;
+    uint2 nv = make_uint2(0u, kWinEmpty);
+    uint32_t noff = 0;
+    if (base < n) {
+        if (base + lane < n) nv = pv[base + lane];
+        noff = off[base];
+    }
+    for (; base < n; base += n_warps * 32) {
         const int64_t k = base + lane;
-        int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
-        uint32_t sv = 0;
-        if (k < n) {
-            const uint32_t a = wlo[k], b = whi[k];
-            x0 = (int)(a & 0xFFFF);
-            x1 = (int)(a >> 16);
-            y0 = (int)(b & 0xFFFF);
-            y1 = (int)(b >> 16);
-            sv = order[k];
+        const uint2 cv = nv;
+        const uint32_t obase = noff;
+        const int64_t nb = base + n_warps * 32;
+        if (nb < n) {
+            nv = nb + lane < n ? pv[nb + lane] : make_uint2(0u, kWinEmpty);
+            noff = off[nb];
         }
-        const uint32_t cnt = (x0 <= x1 && y0 <= y1) ? (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1)) : 0u;
+        int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
+        uint32_t sv = 0, cnt = 0;
+        if (k < n) {
+            sv = cv.x;
+            if (unpack_window(cv.y, cv.x, wins, width, height, x0, x1, y0, y1)) cnt = block_count(x0, x1, y0, y1);
+        }
         uint32_t incl = cnt;
 #pragma unroll
         for (int s = 1; s < 32; s <<= 1) {
@@ -462,7 +613,6 @@ __global__ void k_bentry_emit(const uint32_t *order, const uint32_t *wlo, const 
         }
         const uint32_t excl = incl - cnt;
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t obase = __shfl_sync(0xffffffffu, off[base], 0);
         for (uint32_t o0 = 0; o0 < total; o0 += 32) {
             const uint32_t o = o0 + lane;
             int s = 0;
@@ -477,7 +627,11 @@ __global__ void k_bentry_emit(const uint32_t *order, const uint32_t *wlo, const 
             const uint32_t v = __shfl_sync(0xffffffffu, sv, s);
             if (o < total) {
                 const int w = X1 / 8 - X0 / 8 + 1;
-                const int bx = X0 / 8 + (int)(li % (uint32_t)w), by = Y0 / 4 + (int)(li / (uint32_t)w);
+                // li / w without an integer division (li < 2^24: one correction step is exact)
+                int qy = (int)((float)li * __frcp_rn((float)w));
+                int rx = (int)li - qy * w;
+                if (rx < 0) { qy--; rx += w; } else if (rx >= w) { qy++; rx -= w; }
+                const int bx = X0 / 8 + rx, by = Y0 / 4 + qy;
                 const int rx0 = max(X0 - 8 * bx, 0), rx1 = min(X1 - 8 * bx, 7);
                 const int ry0 = max(Y0 - 4 * by, 0), ry1 = min(Y1 - 4 * by, 3);
                 const uint32_t id = (uint32_t)(((by >> 2) * n_tx + (bx >> 1)) * 8 + (by & 3) * 2 + (bx & 1));
@@ -488,24 +642,38 @@ __global__ void k_bentry_emit(const uint32_t *order, const uint32_t *wlo, const 
     }
 }
 
-// boff[b] = first entry with block id >= b, for b in [0, n_blocks]
+// boff[b] = first entry with block id >= b, for b in [0, n_blocks]; thread
+// handles 4 consecutive entries (one uint4 load)
 __global__ void k_block_offsets(const uint32_t *ekey, const unsigned long long *e_dev, int64_t cap_e,
                                 int64_t n_blocks, uint32_t *boff)
 {
     const int64_t E = std::min<int64_t>((int64_t)*e_dev, cap_e);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= E; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t prev = i > 0 ? (int64_t)(ekey[i - 1] >> kCodeBits) : -1;
-        const int64_t cur = i < E ? (int64_t)(ekey[i] >> kCodeBits) : n_blocks;
-        for (int64_t t = prev + 1; t <= cur; t++) boff[t] = (uint32_t)i;
+    const int64_t nq = E / 4 + 1;   // quads covering [0, E]
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = 4 * q;
+        uint32_t kv[4];
+        if (i0 + 4 <= E) {
+            const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(ekey) + q);
+            kv[0] = x.x; kv[1] = x.y; kv[2] = x.z; kv[3] = x.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) kv[j] = i0 + j < E ? ekey[i0 + j] : 0u;
+        }
+        int64_t prev = i0 > 0 ? (int64_t)(ekey[i0 - 1] >> kCodeBits) : -1;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int64_t i = i0 + j;
+            if (i > E) break;
+            const int64_t cur = i < E ? (int64_t)(kv[j] >> kCodeBits) : n_blocks;
+            for (int64_t t = prev + 1; t <= cur; t++) boff[t] = (uint32_t)i;
+            prev = cur;
+        }
     }
 }
 
 static int grid_for(int64_t n, int threads)
 {
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)nsm * 16));
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, (int64_t)sm_count_sort() * 16));
 }
 
 static int bits_for(int64_t n)
@@ -515,53 +683,61 @@ static int bits_for(int64_t n)
     return b;
 }
 
-// n_dev: survivor count (device).  Inputs: ws.depth64 / rect and the splat
-// records from the projection.  Always: order = passed survivors by (depth,
-// index).  blocks = true (frame path): block lists (entries_out = survivor per
-// entry, keys_out = id << 10 | window, ws.boff).  blocks = false (stage-level
-// API, parity with the reference): tile entries and ws.tile_off, exactly
-// bin_tiles' output.
-cudaError_t launch_bin(const Ws &ws, const unsigned long long *n_dev, int64_t n_max, const sc_camera &cam,
-                       const sc_window *wins, sc_frame_stats *stats, bool blocks, uint32_t **order_out,
-                       uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st)
+// n_dev: survivor count (device).  Input: ws.key_a (depth keys) + ws.pv_a
+// ((survivor index, packed window) or (index, 0)) in survivor order.
+// Always: depth sort + tie-fix (order = passed survivors by (depth, index)).
+// blocks = true (frame path): block lists (entries_out = survivor per entry,
+// keys_out = id << 10 | window, ws.boff).  blocks = false (stage-level API,
+// parity with the reference): *order_out, tile entries and ws.tile_off,
+// exactly bin_tiles' output.
+cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
+                       int64_t n_max, const sc_camera &cam, const sc_window *wins, sc_frame_stats *stats, bool blocks,
+                       uint32_t **order_out, uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st)
 {
     cudaError_t e;
-    uint32_t *keys_s = nullptr, *order = nullptr;
-    SC_LAUNCH(k_depth_keys, grid_for(n_max, 256), 256, 0, st, ws.depth64, n_dev, n_max, ws.ctr, ws.key_a, ws.val_a);
-    e = radix_sort(ws.key_a, ws.val_a, ws.key_b, ws.val_b, n_dev, n_max, 0, 32, ws.hist, ws.scan_part, &keys_s, &order,
-                   st);
+    uint32_t *keys_s = nullptr;
+    uint2 *pv_s = nullptr;
+    if (!blocks)   // stage-level API: keys from the exact depth range (the frame path's come from the projection)
+        SC_LAUNCH(k_depth_keys, grid_for(n_max, 256), 256, 0, st, ws.depth64, n_dev, n_max, ws.ctr, ws.key_a, ws.pv_a);
+    e = radix_sort<uint2>(ws.key_a, ws.pv_a, ws.key_b, ws.pv_b, n_dev, n_max, 0, 32, ws, &keys_s, &pv_s, st);
     if (e != cudaSuccess) return e;
     const unsigned long long *p_dev = &ws.ctr->passed;   // passed splats lead the sorted order
-    SC_LAUNCH(k_tiefix, grid_for(n_max, 256), 256, 0, st, keys_s, order, ws.depth64, p_dev, n_max, stats);
-    // both key buffers are free once the tie-fix is done: depth-ordered rects / windows
-    uint32_t *rlo = ws.key_a, *rhi = ws.key_b;
+    // ws.ecount is free until the entry counts: it holds the tie-run list
+    e = launch_tiefix(scene, surv, cam, keys_s, pv_s, blocks ? nullptr : ws.depth64, p_dev, n_max, ws.ecount, ws.ctr,
+                      stats, st);
+    if (e != cudaSuccess) return e;
     uint32_t *ek = nullptr, *ev = nullptr;
     if (blocks) {
-        SC_LAUNCH(k_bentry_count, grid_for(n_max, 256), 256, 0, st, order, wins, p_dev, n_max, cam.width, cam.height,
-                  ws.ecount, rlo, rhi);
+        SC_LAUNCH(k_bentry_count, grid_for(n_max, 256), 256, 0, st, pv_s, wins, p_dev, n_max, cam.width, cam.height,
+                  ws.ecount);
         e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, nullptr, st);
         if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_bentry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max, ws.n_tx,
-                  ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
+        SC_LAUNCH(k_bentry_emit, grid_for(n_max, 256), 256, 0, st, pv_s, wins, ws.ecount, p_dev, n_max, cam.width,
+                  cam.height, ws.n_tx, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
         const int64_t n_blocks = 8 * ws.n_tiles;
-        e = radix_sort(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, kCodeBits,
-                       kCodeBits + bits_for(n_blocks), ws.hist, ws.scan_part, &ek, &ev, st);
+        e = radix_sort<uint32_t>(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, kCodeBits,
+                                 kCodeBits + bits_for(n_blocks), ws, &ek, &ev, st);
         if (e != cudaSuccess) return e;
         SC_LAUNCH(k_block_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE, n_blocks,
                   ws.boff);
+        if (order_out) *order_out = nullptr;
     } else {
+        // free after the tie-fix: both key buffers and the other payload buffer
+        uint32_t *order = reinterpret_cast<uint32_t *>(pv_s == ws.pv_a ? ws.pv_b : ws.pv_a);
+        uint32_t *rlo = ws.key_a, *rhi = ws.key_b;
+        SC_LAUNCH(k_extract_order, grid_for(n_max, 256), 256, 0, st, pv_s, p_dev, n_max, order);
         SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, ws.ecount, rlo, rhi);
         e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, &stats->entries, st);
         if (e != cudaSuccess) return e;
         SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max, ws.n_tx,
                   ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
-        e = radix_sort(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, 0,
-                       std::max(1, bits_for(ws.n_tiles)), ws.hist, ws.scan_part, &ek, &ev, st);
+        e = radix_sort<uint32_t>(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, 0,
+                                 std::max(1, bits_for(ws.n_tiles)), ws, &ek, &ev, st);
         if (e != cudaSuccess) return e;
         SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE,
                   ws.n_tiles, ws.tile_off);
+        if (order_out) *order_out = order;
     }
-    *order_out = order;
     *entries_out = ev;
     if (keys_out) *keys_out = ek;
     return cudaGetLastError();

@@ -86,7 +86,8 @@ typedef struct sc_opts {
     int32_t record_contributions; /* per-splat max contribution + per-pixel sum */
     int32_t use_mlp;              /* 0: no MLP gate ("Ours w/o MLP") */
     int32_t frustum_mode;         /* SC_FRUSTUM_* */
-    int32_t reserved0;
+    int32_t exact_projection;     /* 1: all-f64 projection; 0: f32 covariance with exact f64
+                                     fallback whenever the radius / clip decision is ambiguous */
     double radius_clip;           /* <= 0: off */
     double stop_transmittance;    /* 1/255 */
     double background[3];         /* (1, 1, 1) */
@@ -166,7 +167,8 @@ typedef struct sc_frame_stats {
     int64_t max_tie_run;         /* longest run of equal f32 depth keys (tie-fix work) */
     int64_t overflow;            /* bit0 survivors, bit1 entries, bit2 block lists: re-render with more capacity */
     int64_t block_entries;       /* frame path: (splat, 8x4 pixel block) entries binned for the blend */
-    int64_t reserved[3];
+    int64_t exact_fallbacks;     /* projections that fell back to the all-f64 path (exact_projection = 0) */
+    int64_t reserved[2];
 } sc_frame_stats;
 
 /* Survivor = (instance index, gaussian index within its asset). */

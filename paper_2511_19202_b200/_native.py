@@ -34,7 +34,7 @@ class ScCamera(ctypes.Structure):
 
 class ScOpts(ctypes.Structure):
     _fields_ = [("tile_size", c_i32), ("sh_degree_eval", c_i32), ("record_contributions", c_i32),
-                ("use_mlp", c_i32), ("frustum_mode", c_i32), ("reserved0", c_i32),
+                ("use_mlp", c_i32), ("frustum_mode", c_i32), ("exact_projection", c_i32),
                 ("radius_clip", c_f64), ("stop_transmittance", c_f64), ("background", c_f64 * 3),
                 ("dilation", c_f64), ("frustum_G", c_f64)]
 
@@ -64,11 +64,12 @@ class ScScene(ctypes.Structure):
 
 
 STATS_FIELDS = ("instances_visible", "pairs_tested", "frustum_passed", "mlp_queried", "mlp_culled",
-                "survivors", "passed", "skipped", "entries", "used", "max_tie_run", "overflow", "block_entries")
+                "survivors", "passed", "skipped", "entries", "used", "max_tie_run", "overflow", "block_entries",
+                "exact_fallbacks")
 
 
 class ScFrameStats(ctypes.Structure):
-    _fields_ = [(n, c_i64) for n in STATS_FIELDS] + [("reserved", c_i64 * 3)]
+    _fields_ = [(n, c_i64) for n in STATS_FIELDS] + [("reserved", c_i64 * 2)]
 
 
 class ScSurvivor(ctypes.Structure):

@@ -27,6 +27,12 @@ struct InstFrame {
     int32_t visible;      // survived the bounding-sphere cull
     uint32_t chunk_begin; // exclusive prefix of chunk counts
     uint32_t n_chunks;
+    // MLP inputs in the instance frame (f32): R^T (m' - c) = s m + cam_local
+    float cam_local[3];   // R^T (t - c)
+    float s;              // uniform instance scale
+    float dn_a, dn_b;     // normalised distance = clamp(d_r dn_a + dn_b, -1, 1)
+    int32_t inside;       // sphere strictly inside the frustum: every pair passes the per-pair test
+    int32_t gate;         // 1: every pair is queried (d_t >= d_near), 0: none, -1: per-pair f64 test
 };
 
 // Internal counters block (device), zeroed per frame together with the stats.

@@ -48,6 +48,14 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
             fr.corr = (a.model >= 0) ? (a.f_train / cam.focal) / in.s : 0.0;
             for (int k = 0; k < 3; k++)
                 fr.fwd_local[k] = (float)(in.R[k] * cam.rot[6] + in.R[3 + k] * cam.rot[7] + in.R[6 + k] * cam.rot[8]);
+            {
+                const double d0 = in.t[0] - cam.pos[0], d1 = in.t[1] - cam.pos[1], d2 = in.t[2] - cam.pos[2];
+                for (int k = 0; k < 3; k++) fr.cam_local[k] = (float)(in.R[k] * d0 + in.R[3 + k] * d1 + in.R[6 + k] * d2);
+                fr.s = (float)in.s;
+                const double span = a.d_far - a.d_near;
+                fr.dn_a = (float)(2.0 * fr.corr / span);
+                fr.dn_b = (float)(-2.0 * a.d_near / span - 1.0);
+            }
             int vis = a.count > 0;
             // sphere around the instance covering every instanced mean, with slack
             // for the f32 rounding of instanced means
@@ -75,6 +83,43 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
                 kh = cyp - pad - yhi;
                 if (f * cy + kh * cz - mg - rho * sqrt(f * f + kh * kh) > 0.0) vis = 0;
             }
+            // Uniform instances (every pair decided the same way) skip the per-pair f64
+            // tests in k_cull.  inside: the sphere lies strictly inside z > near and the
+            // image-plane region the per-pair test accepts unconditionally
+            // ([0, TW) x [0, TH) in margin mode, where rb >= 3 px more is tolerated;
+            // [1e-3, W-1-1e-3]^2 in strict mode) -- the per-pair f64 rounding (~1e-12 px)
+            // cannot flip such a pair.
+            int inside = 0, gate = -1;
+            if (vis) {
+                if (opts.frustum_mode == SC_FRUSTUM_OFF) {
+                    inside = 1;
+                } else {
+                    const double lo = opts.frustum_mode == SC_FRUSTUM_STRICT ? 1e-3 : 0.0;
+                    const double hx = opts.frustum_mode == SC_FRUSTUM_STRICT ? (double)(cam.width - 1) - 1e-3 : TW;
+                    const double hy = opts.frustum_mode == SC_FRUSTUM_STRICT ? (double)(cam.height - 1) - 1e-3 : TH;
+                    const double rr = rho * (1.0 + 1e-6) + 1e-9;
+                    // plane  f x + (c - b) z >= 0  (mx >= b)  and  -(f x + (c - b) z) >= 0  (mx <= b)
+                    auto dist_ge = [&](double px, double pz, double k, double sign) {
+                        const double v = sign * (f * px + k * pz);
+                        return v > rr * sqrt(f * f + k * k) * (1.0 + 1e-9);
+                    };
+                    inside = (cz - rr > cam.near_ * (1.0 + 1e-9) + 1e-12) && dist_ge(cx, cz, cxp - lo, 1.0) &&
+                             dist_ge(cx, cz, cxp - hx, -1.0) && dist_ge(cy, cz, cyp - lo, 1.0) &&
+                             dist_ge(cy, cz, cyp - hy, -1.0);
+                }
+                if (a.model >= 0 && opts.use_mlp) {
+                    const double dc = sqrt((in.t[0] - cam.pos[0]) * (in.t[0] - cam.pos[0]) +
+                                           (in.t[1] - cam.pos[1]) * (in.t[1] - cam.pos[1]) +
+                                           (in.t[2] - cam.pos[2]) * (in.t[2] - cam.pos[2]));
+                    const double rr = rho * (1.0 + 1e-6) + 1e-9;
+                    if ((dc - rr) * fr.corr > a.d_near * (1.0 + 1e-9)) gate = 1;
+                    else if ((dc + rr) * fr.corr < a.d_near * (1.0 - 1e-9)) gate = 0;
+                } else {
+                    gate = 0;
+                }
+            }
+            fr.inside = inside;
+            fr.gate = gate;
             if (vis) {   // depth range of every instanced mean of a visible instance (frame-path sort keys)
                 const double lo = fmax(cz - rho * (1.0 + 1e-9), d_floor);
                 const double hi = fmax(cz + rho * (1.0 + 1e-9), lo);
@@ -205,14 +250,16 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
             if (active) {
                 const int64_t g = s_as.offset + j;
                 const float4 mo = __ldg(reinterpret_cast<const float4 *>(scene.mean_opa) + g);
-                const float smax = __ldg(scene.scale_smax + 4 * g + 3);
-                const float3 mw = inst_mean(s_in, mo.x, mo.y, mo.z);
-                const double m0 = mw.x, m1 = mw.y, m2 = mw.z;
-                if (opts.frustum_mode == SC_FRUSTUM_OFF) {
-                    pass = true;
+                // the f32 instanced mean (B2), only needed by the exact per-pair tests
+                const bool need_mean = !s_fr.inside || (model >= 0 && s_fr.gate < 0);
+                const float3 mw = need_mean ? inst_mean(s_in, mo.x, mo.y, mo.z) : make_float3(0.f, 0.f, 0.f);
+                if (s_fr.inside) {
+                    pass = true;   // k_prep: the whole instance sphere passes
                 } else {
+                    // exact per-pair test on the f32 instanced mean (B3), f64 as the oracle
+                    const float smax = __ldg(scene.scale_smax + 4 * g + 3);
                     double tx, ty, tz;
-                    cam_xyz(cam, m0, m1, m2, tx, ty, tz);
+                    cam_xyz(cam, mw.x, mw.y, mw.z, tx, ty, tz);
                     if (tz > cam.near_) {
                         const double mx = cam.focal * (tx / tz) + cxp;
                         const double my = cam.focal * (ty / tz) + cyp;
@@ -227,21 +274,26 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
                     }
                 }
                 if (pass && model >= 0) {
-                    const double dx = m0 - cam.pos[0], dy = m1 - cam.pos[1], dz = m2 - cam.pos[2];
-                    const double d_r = sqrt(dx * dx + dy * dy + dz * dz);
-                    const double d_t = d_r * s_fr.corr;
-                    if (d_t >= s_as.d_near) {
-                        queried = true;
-                        const double inv = 1.0 / d_r;
-                        const double *R = s_in.R;
-                        const float dl0 = (float)((R[0] * dx + R[3] * dy + R[6] * dz) * inv);
-                        const float dl1 = (float)((R[1] * dx + R[4] * dy + R[7] * dz) * inv);
-                        const float dl2 = (float)((R[2] * dx + R[5] * dy + R[8] * dz) * inv);
-                        double dn = 2.0 * (d_t - s_as.d_near) / (s_as.d_far - s_as.d_near) - 1.0;
-                        dn = dn < -1.0 ? -1.0 : (dn > 1.0 ? 1.0 : dn);
+                    if (s_fr.gate >= 0) {
+                        queried = s_fr.gate == 1;   // k_prep: uniform over the instance sphere
+                    } else {                        // exact Eq. 2 gate on the f32 instanced mean
+                        const double dx = (double)mw.x - cam.pos[0], dy = (double)mw.y - cam.pos[1],
+                                     dz = (double)mw.z - cam.pos[2];
+                        queried = sqrt(dx * dx + dy * dy + dz * dz) * s_fr.corr >= s_as.d_near;
+                    }
+                    if (queried) {
+                        // MLP inputs in the instance frame, f32 (they are rounded to fp16):
+                        // R^T (m' - c) = s m + R^T (t - c)
+                        const float px = fmaf(s_fr.s, mo.x, s_fr.cam_local[0]);
+                        const float py = fmaf(s_fr.s, mo.y, s_fr.cam_local[1]);
+                        const float pz = fmaf(s_fr.s, mo.z, s_fr.cam_local[2]);
+                        const float d2 = fmaf(px, px, fmaf(py, py, pz * pz));
+                        const float rinv = rsqrtf(d2);
+                        const float d_r = d2 * rinv;
+                        const float dn = fminf(fmaxf(fmaf(d_r, s_fr.dn_a, s_fr.dn_b), -1.0f), 1.0f);
                         const float ims = (float)s_as.inv_mean_scale;
-                        lo = make_uint4(pack_h2(mo.x * ims, mo.y * ims), pack_h2(mo.z * ims, dl0),
-                                        pack_h2(dl1, dl2), pack_h2((float)dn, s_fr.fwd_local[0]));
+                        lo = make_uint4(pack_h2(mo.x * ims, mo.y * ims), pack_h2(mo.z * ims, px * rinv),
+                                        pack_h2(py * rinv, pz * rinv), pack_h2(dn, s_fr.fwd_local[0]));
                         const uint4 feat = __ldg(reinterpret_cast<const uint4 *>(scene.features) + g);
                         hi = make_uint4(pack_h2(s_fr.fwd_local[1], s_fr.fwd_local[2]), feat.x, feat.y, feat.z);
                     }

@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
     const double focal = cam.focal;
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const double log_min_alpha = log(1.0 / 255.0);
-    unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0;
+    unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0, n_exact = 0;
+    const bool fast = opts.exact_projection == 0;
 
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
         const sc_survivor sv = surv[k];
@@ -54,6 +55,8 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
         // --- instancing (B2), exactly as the oracle's orc_instantiate ---
         const float3 mw = inst_mean(in, mo.x, mo.y, mo.z);
         const float4 qw = inst_quat(in, q4);
+        // fast path: f32 instance quaternion product (<= 1 ulp from the f64-rounded qw; inside the error bound)
+        const float4 qf = qw;
         const float ls0 = __double2float_rn((double)ls4.x + in.ln_s);
         const float ls1 = __double2float_rn((double)ls4.y + in.ln_s);
         const float ls2 = __double2float_rn((double)ls4.z + in.ln_s);
@@ -64,66 +67,138 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
         cam_xyz(cam, m0, m1, m2, tx, ty, tz);
         bool valid = false;
         double mx = 0.0, my = 0.0, ca = 0.0, cb = 0.0, cc = 0.0, radius = 0.0, det = 0.0, cov_a = 0.0, cov_c = 0.0;
+        float ex_f = 0.0f, ey_f = 0.0f;   // fast path: conservative support half-widths (before the L factor)
+        bool fast_done = false;
         if (tz > cam.near_) {
             const double txz = tx / tz, tyz = ty / tz;
             const double ctxz = fmin(fmax(txz, -lim_x), lim_x);
             const double ctyz = fmin(fmax(tyz, -lim_y), lim_y);
-            const double *R = cam.rot;
-            const double fz = focal / tz;
-            const double j00 = fz * R[0] - fz * ctxz * R[6];
-            const double j01 = fz * R[1] - fz * ctxz * R[7];
-            const double j02 = fz * R[2] - fz * ctxz * R[8];
-            const double j10 = fz * R[3] - fz * ctyz * R[6];
-            const double j11 = fz * R[4] - fz * ctyz * R[7];
-            const double j12 = fz * R[5] - fz * ctyz * R[8];
-
-            const double q0 = qw.x, q1 = qw.y, q2 = qw.z, q3 = qw.w;
-            const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-            const double w = q0 / qn, x = q1 / qn, y = q2 / qn, z = q3 / qn;
-            const double r00 = 1.0 - 2.0 * (y * y + z * z);
-            const double r01 = 2.0 * (x * y - w * z);
-            const double r02 = 2.0 * (x * z + w * y);
-            const double r10 = 2.0 * (x * y + w * z);
-            const double r11 = 1.0 - 2.0 * (x * x + z * z);
-            const double r12 = 2.0 * (y * z - w * x);
-            const double r20 = 2.0 * (x * z - w * y);
-            const double r21 = 2.0 * (y * z + w * x);
-            const double r22 = 1.0 - 2.0 * (x * x + y * y);
-            const double s0 = exp(2.0 * (double)ls0);
-            const double s1 = exp(2.0 * (double)ls1);
-            const double s2 = exp(2.0 * (double)ls2);
-            const double g00 = r00 * r00 * s0 + r01 * r01 * s1 + r02 * r02 * s2;
-            const double g01 = r00 * r10 * s0 + r01 * r11 * s1 + r02 * r12 * s2;
-            const double g02 = r00 * r20 * s0 + r01 * r21 * s1 + r02 * r22 * s2;
-            const double g11 = r10 * r10 * s0 + r11 * r11 * s1 + r12 * r12 * s2;
-            const double g12 = r10 * r20 * s0 + r11 * r21 * s1 + r12 * r22 * s2;
-            const double g22 = r20 * r20 * s0 + r21 * r21 * s1 + r22 * r22 * s2;
-            const double u0 = j00 * g00 + j01 * g01 + j02 * g02;
-            const double u1 = j00 * g01 + j01 * g11 + j02 * g12;
-            const double u2 = j00 * g02 + j01 * g12 + j02 * g22;
-            const double v0 = j10 * g00 + j11 * g01 + j12 * g02;
-            const double v1 = j10 * g01 + j11 * g11 + j12 * g12;
-            const double v2 = j10 * g02 + j11 * g12 + j12 * g22;
-            const double a = u0 * j00 + u1 * j01 + u2 * j02 + opts.dilation;
-            const double b = u0 * j10 + u1 * j11 + u2 * j12;
-            const double c = v0 * j10 + v1 * j11 + v2 * j12 + opts.dilation;
             mx = focal * txz + (double)(cam.width - 1) / 2.0;
             my = focal * tyz + (double)(cam.height - 1) / 2.0;
-            cov_a = a;
-            cov_c = c;
-            det = a * c - b * b;
-            if (det <= 1e-12) {
-                n_skipped++;
-            } else {
-                ca = c / det;
-                cb = -b / det;
-                cc = a / det;
-                const double mid = 0.5 * (a + c);
-                const double disc = mid * mid - det;
-                const double lam = mid + sqrt(disc > 0.0 ? disc : 0.0);
-                radius = ceil(3.0 * sqrt(lam));
-                valid = radius > 0.0;
-                if (valid && opts.radius_clip > 0.0 && det < opts.radius_clip) valid = false;
+            const double *R = cam.rot;
+            if (fast) {
+                // ---- f32 covariance / conic / eigenvalue with an error bound ----
+                // Every product below is bounded in magnitude by the "absolute"
+                // quadratic forms Ma = (sum |j0i| sqrt(g_ii))^2 (same for c, b), so the
+                // accumulated f32 error of a, b, c is <= K eps (Ma + Mc + 2 Mb) (K
+                // generous: ~40 dependent roundings, f32 exp, f32 quaternion product).
+                // The radius is taken from f32 only when the whole interval of lambda
+                // gives the same ceil(3 sqrt(lambda)); else the f64 path below runs.
+                const float fz = (float)focal / (float)tz;
+                const float cx = (float)ctxz, cy = (float)ctyz;
+                const float r0 = (float)R[0], r1 = (float)R[1], r2 = (float)R[2], r3 = (float)R[3], r4 = (float)R[4],
+                            r5 = (float)R[5], r6 = (float)R[6], r7 = (float)R[7], r8 = (float)R[8];
+                const float j00 = fz * (r0 - cx * r6), j01 = fz * (r1 - cx * r7), j02 = fz * (r2 - cx * r8);
+                const float j10 = fz * (r3 - cy * r6), j11 = fz * (r4 - cy * r7), j12 = fz * (r5 - cy * r8);
+                const float qn = rsqrtf(qf.x * qf.x + qf.y * qf.y + qf.z * qf.z + qf.w * qf.w);
+                const float w = qf.x * qn, x = qf.y * qn, y = qf.z * qn, z = qf.w * qn;
+                const float q00 = 1.0f - 2.0f * (y * y + z * z), q01 = 2.0f * (x * y - w * z), q02 = 2.0f * (x * z + w * y);
+                const float q10 = 2.0f * (x * y + w * z), q11 = 1.0f - 2.0f * (x * x + z * z), q12 = 2.0f * (y * z - w * x);
+                const float q20 = 2.0f * (x * z - w * y), q21 = 2.0f * (y * z + w * x), q22 = 1.0f - 2.0f * (x * x + y * y);
+                const float s0 = expf(2.0f * ls0), s1 = expf(2.0f * ls1), s2 = expf(2.0f * ls2);
+                const float g00 = q00 * q00 * s0 + q01 * q01 * s1 + q02 * q02 * s2;
+                const float g01 = q00 * q10 * s0 + q01 * q11 * s1 + q02 * q12 * s2;
+                const float g02 = q00 * q20 * s0 + q01 * q21 * s1 + q02 * q22 * s2;
+                const float g11 = q10 * q10 * s0 + q11 * q11 * s1 + q12 * q12 * s2;
+                const float g12 = q10 * q20 * s0 + q11 * q21 * s1 + q12 * q22 * s2;
+                const float g22 = q20 * q20 * s0 + q21 * q21 * s1 + q22 * q22 * s2;
+                const float u0 = j00 * g00 + j01 * g01 + j02 * g02;
+                const float u1 = j00 * g01 + j01 * g11 + j02 * g12;
+                const float u2 = j00 * g02 + j01 * g12 + j02 * g22;
+                const float v0 = j10 * g00 + j11 * g01 + j12 * g02;
+                const float v1 = j10 * g01 + j11 * g11 + j12 * g12;
+                const float v2 = j10 * g02 + j11 * g12 + j12 * g22;
+                const float dil = (float)opts.dilation;
+                const float fa = u0 * j00 + u1 * j01 + u2 * j02 + dil;
+                const float fb = u0 * j10 + u1 * j11 + u2 * j12;
+                const float fc = v0 * j10 + v1 * j11 + v2 * j12 + dil;
+                const float sg0 = sqrtf(g00), sg1 = sqrtf(g11), sg2 = sqrtf(g22);
+                const float na = fabsf(j00) * sg0 + fabsf(j01) * sg1 + fabsf(j02) * sg2;
+                const float nc = fabsf(j10) * sg0 + fabsf(j11) * sg1 + fabsf(j12) * sg2;
+                constexpr float kEps = 5.9604645e-08f, K = 64.0f;
+                const float err = K * kEps * (na + nc) * (na + nc) + 4.0f * kEps * fabsf(dil);
+                const float hd = 0.5f * (fa - fc);
+                const float lam = 0.5f * (fa + fc) + sqrtf(hd * hd + fb * fb);
+                const float lo = fmaxf(lam * (1.0f - 16.0f * kEps) - 2.0f * err, 0.0f);
+                const float hi = lam * (1.0f + 16.0f * kEps) + 2.0f * err;
+                const float rlo = ceilf(3.0f * sqrtf(lo) * (1.0f - 4.0f * kEps));
+                const float rhi = ceilf(3.0f * sqrtf(hi) * (1.0f + 4.0f * kEps));
+                const double fdet = (double)fa * (double)fc - (double)fb * (double)fb;
+                const double det_err = 4.0 * (double)err * ((double)fa + (double)fc + 2.0 * (double)err) + 1e-30;
+                const bool clip_ok = !(opts.radius_clip > 0.0) || fabs(fdet - opts.radius_clip) > det_err;
+                if (rlo == rhi && fdet - det_err > 1e-12 && clip_ok) {
+                    fast_done = true;
+                    radius = (double)rlo;
+                    det = fdet;
+                    const float inv = (float)(1.0 / fdet);
+                    ca = (double)(fc * inv);
+                    cb = (double)(-fb * inv);
+                    cc = (double)(fa * inv);
+                    valid = radius > 0.0;
+                    if (valid && opts.radius_clip > 0.0 && det < opts.radius_clip) valid = false;
+                    // support half-widths from conservative a, c (times sqrt(2 L) later)
+                    ex_f = sqrtf(fa + err);
+                    ey_f = sqrtf(fc + err);
+                    cov_a = (double)fa;
+                    cov_c = (double)fc;
+                }
+            }
+            if (!fast_done) {
+                n_exact++;
+                const double fz = focal / tz;
+                const double j00 = fz * R[0] - fz * ctxz * R[6];
+                const double j01 = fz * R[1] - fz * ctxz * R[7];
+                const double j02 = fz * R[2] - fz * ctxz * R[8];
+                const double j10 = fz * R[3] - fz * ctyz * R[6];
+                const double j11 = fz * R[4] - fz * ctyz * R[7];
+                const double j12 = fz * R[5] - fz * ctyz * R[8];
+
+                const double q0 = qw.x, q1 = qw.y, q2 = qw.z, q3 = qw.w;
+                const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+                const double w = q0 / qn, x = q1 / qn, y = q2 / qn, z = q3 / qn;
+                const double r00 = 1.0 - 2.0 * (y * y + z * z);
+                const double r01 = 2.0 * (x * y - w * z);
+                const double r02 = 2.0 * (x * z + w * y);
+                const double r10 = 2.0 * (x * y + w * z);
+                const double r11 = 1.0 - 2.0 * (x * x + z * z);
+                const double r12 = 2.0 * (y * z - w * x);
+                const double r20 = 2.0 * (x * z - w * y);
+                const double r21 = 2.0 * (y * z + w * x);
+                const double r22 = 1.0 - 2.0 * (x * x + y * y);
+                const double s0 = exp(2.0 * (double)ls0);
+                const double s1 = exp(2.0 * (double)ls1);
+                const double s2 = exp(2.0 * (double)ls2);
+                const double g00 = r00 * r00 * s0 + r01 * r01 * s1 + r02 * r02 * s2;
+                const double g01 = r00 * r10 * s0 + r01 * r11 * s1 + r02 * r12 * s2;
+                const double g02 = r00 * r20 * s0 + r01 * r21 * s1 + r02 * r22 * s2;
+                const double g11 = r10 * r10 * s0 + r11 * r11 * s1 + r12 * r12 * s2;
+                const double g12 = r10 * r20 * s0 + r11 * r21 * s1 + r12 * r22 * s2;
+                const double g22 = r20 * r20 * s0 + r21 * r21 * s1 + r22 * r22 * s2;
+                const double u0 = j00 * g00 + j01 * g01 + j02 * g02;
+                const double u1 = j00 * g01 + j01 * g11 + j02 * g12;
+                const double u2 = j00 * g02 + j01 * g12 + j02 * g22;
+                const double v0 = j10 * g00 + j11 * g01 + j12 * g02;
+                const double v1 = j10 * g01 + j11 * g11 + j12 * g12;
+                const double v2 = j10 * g02 + j11 * g12 + j12 * g22;
+                const double a = u0 * j00 + u1 * j01 + u2 * j02 + opts.dilation;
+                const double b = u0 * j10 + u1 * j11 + u2 * j12;
+                const double c = v0 * j10 + v1 * j11 + v2 * j12 + opts.dilation;
+                cov_a = a;
+                cov_c = c;
+                det = a * c - b * b;
+                if (det <= 1e-12) {
+                    n_skipped++;
+                } else {
+                    ca = c / det;
+                    cb = -b / det;
+                    cc = a / det;
+                    const double mid = 0.5 * (a + c);
+                    const double disc = mid * mid - det;
+                    const double lam = mid + sqrt(disc > 0.0 ? disc : 0.0);
+                    radius = ceil(3.0 * sqrt(lam));
+                    valid = radius > 0.0;
+                    if (valid && opts.radius_clip > 0.0 && det < opts.radius_clip) valid = false;
+                }
             }
         }
         // --- tile rectangle (sc/raster.py:307-314) ---
@@ -217,8 +292,15 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
             // reach one pixel past the rect (A8 step 3).
             // L = -p_min; the fp32 opacity's error is far inside the widening
             const double L = -(double)p_min;
-            const double ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-5) + 1e-3;
-            const double ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-5) + 1e-3;
+            double ex, ey;
+            if (fast_done) {   // f32: a, c widened by their error bound, then 1e-4 relative + 1e-2 px
+                const float sl = sqrtf(2.0f * (float)L);
+                ex = (double)(sl * ex_f) * (1.0 + 1e-4) + 1e-2;
+                ey = (double)(sl * ey_f) * (1.0 + 1e-4) + 1e-2;
+            } else {
+                ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-5) + 1e-3;
+                ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-5) + 1e-3;
+            }
             win.x0 = clamp16(fmax(fmax(floor(mx - radius), ceil(mx - ex)), (double)(kTile * tx0)));
             win.x1 = clamp16(fmin(fmin(floor(mx + radius) + 1.0, floor(mx + ex)), (double)(kTile * tx1 - 1)));
             win.y0 = clamp16(fmax(fmax(floor(my - radius), ceil(my - ey)), (double)(kTile * ty0)));
@@ -230,16 +312,15 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
             win.y1 = 0;
         }
         splats[k] = sp;
-        wins[k] = win;
+        const uint32_t packed = passed ? pack_window(win.x0, win.x1, win.y0, win.y1, cam.width, cam.height) : kWinEmpty;
+        if (!keys || packed == kWinEscape) wins[k] = win;   // frame path: only escapes are read back
         if (depth64) depth64[k] = passed ? tz : -1.0;   // stage API: sort keys are quantised in k_depth_keys
         if (keys) {
             // monotone non-decreasing in tz (clamped subtraction, positive scale, floor): equal keys are
             // re-ordered by (tz, index) in the tie-fix; non-passed splats sink to the end
             constexpr double kTop = 4294967040.0;
             keys[k] = passed ? (uint32_t)fmin(floor(fmax(tz - key_dmin, 0.0) * key_scale), kTop) : 0xFFFFFFFFu;
-            pv[k] = make_uint2((uint32_t)k, passed ? pack_window(win.x0, win.x1, win.y0, win.y1, cam.width,
-                                                                 cam.height)
-                                                   : kWinEmpty);
+            pv[k] = make_uint2((uint32_t)k, packed);
         }
         if (rect) rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0, (unsigned short)ty1);
         if (dbg_f64) {
@@ -255,6 +336,7 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
         n_passed += __shfl_down_sync(0xffffffffu, n_passed, o);
         n_skipped += __shfl_down_sync(0xffffffffu, n_skipped, o);
         n_tentries += __shfl_down_sync(0xffffffffu, n_tentries, o);
+        n_exact += __shfl_down_sync(0xffffffffu, n_exact, o);
         dmin_inv = max(dmin_inv, __shfl_down_sync(0xffffffffu, dmin_inv, o));
         dmax_bits = max(dmax_bits, __shfl_down_sync(0xffffffffu, dmax_bits, o));
     }
@@ -269,6 +351,7 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
         }
         if (n_skipped) atomicAdd((unsigned long long *)&stats->skipped, n_skipped);
         if (n_tentries) atomicAdd((unsigned long long *)&stats->entries, n_tentries);
+        if (fast && n_exact) atomicAdd((unsigned long long *)&stats->exact_fallbacks, n_exact);
     }
 }
 

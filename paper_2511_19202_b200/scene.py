@@ -169,6 +169,7 @@ class RenderOptions:
     dilation: float = 0.3
     use_mlp: bool = True
     frustum: str = "margin"
+    exact_projection: bool = False   # True: all-f64 projection (False: f32 covariance, exact f64 fallback)
 
     def struct(self, cam) -> nat.ScOpts:
         if self.tile_size != 16:
@@ -181,6 +182,7 @@ class RenderOptions:
         o.record_contributions = 1 if self.record_contributions else 0
         o.use_mlp = 1 if self.use_mlp else 0
         o.frustum_mode = FRUSTUM_MODES[self.frustum]
+        o.exact_projection = 1 if self.exact_projection else 0
         o.radius_clip = float(self.radius_clip) if self.radius_clip is not None else 0.0
         o.stop_transmittance = float(self.stop_transmittance)
         o.background[:] = [float(v) for v in self.background]

@@ -212,7 +212,7 @@ int sc_project(const sc_scene *scene, const sc_survivor *survivors, int64_t n, c
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     SC_TRY(cudaMemsetAsync(stats, 0, sizeof(sc_frame_stats), st), "memset stats");
     SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, windows, nullptr, nullptr, nullptr,
-                              nullptr, dbg_f64, dbg_rect, dbg_flags, stats, nullptr, st),
+                              nullptr, dbg_f64, dbg_rect, dbg_flags, stats, nullptr, nullptr, st),
            "project");
     return SC_OK;
 }
@@ -234,7 +234,7 @@ int sc_bin_sort(const sc_scene *scene, const sc_survivor *survivors, int64_t n, 
     SC_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(sc::Counters), st), "memset counters");
     uint32_t *order = nullptr, *entries = nullptr;
     SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, wins, w.depth64, w.rect, nullptr,
-                              nullptr, nullptr, nullptr, nullptr, stats, w.ctr, st),
+                              nullptr, nullptr, nullptr, nullptr, stats, w.ctr, w.ecount, st),
            "project");
     // reference tile binning (bin_tiles semantics) for parity with the oracle
     SC_TRY(sc::launch_bin(w, *scene, survivors, nullptr, n, *cam, wins, stats, false, &order, &entries, nullptr, st),
@@ -290,7 +290,7 @@ int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opt
     SC_TRY(sc::launch_cull(*scene, *cam, *opts, w, w.surv, w.capS, stats, st), "cull");
     SC_TRY(mark(1), "event");
     SC_TRY(sc::launch_project(*scene, w.surv, &w.ctr->survivors, w.capS, *cam, *opts, w.splats, w.wins, nullptr,
-                              nullptr, w.key_a, w.pv_a, nullptr, nullptr, nullptr, stats, w.ctr, st),
+                              nullptr, w.key_a, w.pv_a, nullptr, nullptr, nullptr, stats, w.ctr, w.ecount, st),
            "project");
     SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;

@@ -46,6 +46,7 @@ struct Counters {
     unsigned long long dmin_inv;       // ~bits(min passed depth)  (atomicMax of ~bits; 0 = none)
     unsigned long long dmax;           // bits(max passed depth)   (positive doubles order as u64)
     unsigned long long tie_runs;       // runs of equal depth keys found by the tie-fix
+    unsigned long long proj_deferred;  // splats the f32 projection left to the exact kernel
     double key_dmin, key_scale;        // frame path: depth-key quantisation from the instance spheres (k_prep)
 };
 
@@ -184,7 +185,7 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
                            sc_window *wins, double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
                            double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats,
-                           Counters *ctr, cudaStream_t st);
+                           Counters *ctr, uint32_t *defer_list, cudaStream_t st);
 // equal depth keys -> (f64 depth, survivor index) order; depth from depth64 or
 // recomputed from the survivor (project.cu, -fmad=false)
 cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const sc_camera &cam, const uint32_t *keys,

@@ -26,24 +26,39 @@ __device__ __forceinline__ int16_t clamp16(double v)
 
 __device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-__global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_survivor *surv,
-                                                 const unsigned long long *n_dev, int64_t n_host, sc_camera cam,
-                                                 sc_opts opts, sc_splat *splats, sc_window *wins,
-                                                 double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
-                                                 double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags,
-                                                 sc_frame_stats *stats, Counters *ctr)
+// f32 dot product with explicit FMA (this TU is -fmad=false for the f64 paths)
+__device__ __forceinline__ float fdot3(float a0, float a1, float a2, float b0, float b1, float b2)
+{
+    return fmaf(a0, b0, fmaf(a1, b1, a2 * b2));
+}
+
+// MODE kProjMixed: f32 covariance, exact f64 fallback inline (stage API);
+// kProjFast: f32 only, ambiguous splats are appended to `list` (+ ctr->proj_deferred)
+//            and projected afterwards by the exact kernel (frame path: keeps this
+//            kernel small enough for 4 CTAs per SM);
+// kProjExact: all-f64 reference path, over `list` when it is given.
+enum { kProjMixed = 0, kProjFast = 1, kProjExact = 2 };
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) k_project(
+    sc_scene scene, const sc_survivor *surv, const unsigned long long *n_dev, int64_t n_host, sc_camera cam,
+    sc_opts opts, sc_splat *splats, sc_window *wins, double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
+    double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr, uint32_t *list)
 {
     // frame path: depth keys quantised over the instance spheres' depth range (k_prep)
     const double key_dmin = keys ? ctr->key_dmin : 0.0, key_scale = keys ? ctr->key_scale : 0.0;
-    const int64_t n = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
+    const int64_t n_surv = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
+    const bool from_list = MODE == kProjExact && list != nullptr;
+    const int64_t n = from_list ? (int64_t)ctr->proj_deferred : n_surv;
     const double lim_x = 1.3 * cam.tan_x, lim_y = 1.3 * cam.tan_y;
     const double focal = cam.focal;
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const double log_min_alpha = log(1.0 / 255.0);
     unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0, n_exact = 0;
-    const bool fast = opts.exact_projection == 0;
+    const bool fast = MODE == kProjFast || (MODE == kProjMixed && opts.exact_projection == 0);
 
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n; it += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = from_list ? (int64_t)list[it] : it;
         const sc_survivor sv = surv[k];
         const sc_instance_rec &in = scene.instances[sv.inst];
         const sc_asset_rec &as = scene.assets[in.asset];
@@ -88,33 +103,33 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
                 const float cx = (float)ctxz, cy = (float)ctyz;
                 const float r0 = (float)R[0], r1 = (float)R[1], r2 = (float)R[2], r3 = (float)R[3], r4 = (float)R[4],
                             r5 = (float)R[5], r6 = (float)R[6], r7 = (float)R[7], r8 = (float)R[8];
-                const float j00 = fz * (r0 - cx * r6), j01 = fz * (r1 - cx * r7), j02 = fz * (r2 - cx * r8);
-                const float j10 = fz * (r3 - cy * r6), j11 = fz * (r4 - cy * r7), j12 = fz * (r5 - cy * r8);
-                const float qn = rsqrtf(qf.x * qf.x + qf.y * qf.y + qf.z * qf.z + qf.w * qf.w);
+                const float j00 = fz * fmaf(-cx, r6, r0), j01 = fz * fmaf(-cx, r7, r1), j02 = fz * fmaf(-cx, r8, r2);
+                const float j10 = fz * fmaf(-cy, r6, r3), j11 = fz * fmaf(-cy, r7, r4), j12 = fz * fmaf(-cy, r8, r5);
+                const float qn = rsqrtf(fmaf(qf.x, qf.x, fdot3(qf.y, qf.z, qf.w, qf.y, qf.z, qf.w)));
                 const float w = qf.x * qn, x = qf.y * qn, y = qf.z * qn, z = qf.w * qn;
                 const float q00 = 1.0f - 2.0f * (y * y + z * z), q01 = 2.0f * (x * y - w * z), q02 = 2.0f * (x * z + w * y);
                 const float q10 = 2.0f * (x * y + w * z), q11 = 1.0f - 2.0f * (x * x + z * z), q12 = 2.0f * (y * z - w * x);
                 const float q20 = 2.0f * (x * z - w * y), q21 = 2.0f * (y * z + w * x), q22 = 1.0f - 2.0f * (x * x + y * y);
                 const float s0 = expf(2.0f * ls0), s1 = expf(2.0f * ls1), s2 = expf(2.0f * ls2);
-                const float g00 = q00 * q00 * s0 + q01 * q01 * s1 + q02 * q02 * s2;
-                const float g01 = q00 * q10 * s0 + q01 * q11 * s1 + q02 * q12 * s2;
-                const float g02 = q00 * q20 * s0 + q01 * q21 * s1 + q02 * q22 * s2;
-                const float g11 = q10 * q10 * s0 + q11 * q11 * s1 + q12 * q12 * s2;
-                const float g12 = q10 * q20 * s0 + q11 * q21 * s1 + q12 * q22 * s2;
-                const float g22 = q20 * q20 * s0 + q21 * q21 * s1 + q22 * q22 * s2;
-                const float u0 = j00 * g00 + j01 * g01 + j02 * g02;
-                const float u1 = j00 * g01 + j01 * g11 + j02 * g12;
-                const float u2 = j00 * g02 + j01 * g12 + j02 * g22;
-                const float v0 = j10 * g00 + j11 * g01 + j12 * g02;
-                const float v1 = j10 * g01 + j11 * g11 + j12 * g12;
-                const float v2 = j10 * g02 + j11 * g12 + j12 * g22;
+                const float g00 = fdot3(q00 * q00, q01 * q01, q02 * q02, s0, s1, s2);
+                const float g01 = fdot3(q00 * q10, q01 * q11, q02 * q12, s0, s1, s2);
+                const float g02 = fdot3(q00 * q20, q01 * q21, q02 * q22, s0, s1, s2);
+                const float g11 = fdot3(q10 * q10, q11 * q11, q12 * q12, s0, s1, s2);
+                const float g12 = fdot3(q10 * q20, q11 * q21, q12 * q22, s0, s1, s2);
+                const float g22 = fdot3(q20 * q20, q21 * q21, q22 * q22, s0, s1, s2);
+                const float u0 = fdot3(j00, j01, j02, g00, g01, g02);
+                const float u1 = fdot3(j00, j01, j02, g01, g11, g12);
+                const float u2 = fdot3(j00, j01, j02, g02, g12, g22);
+                const float v0 = fdot3(j10, j11, j12, g00, g01, g02);
+                const float v1 = fdot3(j10, j11, j12, g01, g11, g12);
+                const float v2 = fdot3(j10, j11, j12, g02, g12, g22);
                 const float dil = (float)opts.dilation;
-                const float fa = u0 * j00 + u1 * j01 + u2 * j02 + dil;
-                const float fb = u0 * j10 + u1 * j11 + u2 * j12;
-                const float fc = v0 * j10 + v1 * j11 + v2 * j12 + dil;
+                const float fa = fdot3(u0, u1, u2, j00, j01, j02) + dil;
+                const float fb = fdot3(u0, u1, u2, j10, j11, j12);
+                const float fc = fdot3(v0, v1, v2, j10, j11, j12) + dil;
                 const float sg0 = sqrtf(g00), sg1 = sqrtf(g11), sg2 = sqrtf(g22);
-                const float na = fabsf(j00) * sg0 + fabsf(j01) * sg1 + fabsf(j02) * sg2;
-                const float nc = fabsf(j10) * sg0 + fabsf(j11) * sg1 + fabsf(j12) * sg2;
+                const float na = fdot3(fabsf(j00), fabsf(j01), fabsf(j02), sg0, sg1, sg2);
+                const float nc = fdot3(fabsf(j10), fabsf(j11), fabsf(j12), sg0, sg1, sg2);
                 constexpr float kEps = 5.9604645e-08f, K = 64.0f;
                 const float err = K * kEps * (na + nc) * (na + nc) + 4.0f * kEps * fabsf(dil);
                 const float hd = 0.5f * (fa - fc);
@@ -130,7 +145,7 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
                     fast_done = true;
                     radius = (double)rlo;
                     det = fdet;
-                    const float inv = (float)(1.0 / fdet);
+                    const float inv = 1.0f / (float)fdet;
                     ca = (double)(fc * inv);
                     cb = (double)(-fb * inv);
                     cc = (double)(fa * inv);
@@ -143,8 +158,15 @@ __global__ void __launch_bounds__(256, 2) k_project(sc_scene scene, const sc_sur
                     cov_c = (double)fc;
                 }
             }
-            if (!fast_done) {
-                n_exact++;
+            if constexpr (MODE == kProjFast) {
+                if (!fast_done) {   // ambiguous: the exact kernel projects this splat afterwards
+                    list[atomicAdd(&ctr->proj_deferred, 1ull)] = (uint32_t)k;
+                    n_exact++;
+                    continue;
+                }
+            }
+            if (MODE != kProjFast && !fast_done) {
+                if (fast) n_exact++;
                 const double fz = focal / tz;
                 const double j00 = fz * R[0] - fz * ctxz * R[6];
                 const double j01 = fz * R[1] - fz * ctxz * R[7];
@@ -359,15 +381,25 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
                            sc_window *wins, double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
                            double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats,
-                           Counters *ctr, cudaStream_t st)
+                           Counters *ctr, uint32_t *defer_list, cudaStream_t st)
 {
     if (n_max <= 0) return cudaSuccess;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 8);
-    SC_LAUNCH(k_project, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins, depth64,
-              rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr);
+    if (opts.exact_projection) {
+        SC_LAUNCH(k_project<kProjExact>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
+                  depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, nullptr);
+    } else if (defer_list && ctr) {   // lean f32 kernel, then the exact kernel over the deferred splats
+        SC_LAUNCH(k_project<kProjFast>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
+                  depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
+        SC_LAUNCH(k_project<kProjExact>, nsm, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins, depth64,
+                  rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
+    } else {
+        SC_LAUNCH(k_project<kProjMixed>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
+                  depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, nullptr);
+    }
     return cudaGetLastError();
 }
 

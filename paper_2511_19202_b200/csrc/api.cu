@@ -88,7 +88,7 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.eval_a = take(4 * (size_t)capE + 16);
     L.eval_b = take(4 * (size_t)capE + 16);
     L.tile_off = take(4 * (size_t)(L.n_tiles + 1));
-    L.task_order = take(4 * (size_t)(2 * L.n_tiles));
+    L.task_order = take(4 * (size_t)L.n_tiles);   // blend dispatch order over tiles
     L.boff = take(4 * (size_t)(8 * L.n_tiles + 1));
     L.rs_counts = take(4 * (size_t)(256 * L.nblk_max));
     L.scan_part = take(4 * (size_t)part);

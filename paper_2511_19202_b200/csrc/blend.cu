@@ -47,7 +47,7 @@ constexpr int kMetaStages = 6;           // meta ring (index + window code) dept
 constexpr int kRecStages = 4;            // record ring depth: issued 3 groups ahead
 constexpr size_t kMetaBytesW = sizeof(uint2) * kG * kMetaStages;
 constexpr size_t kRecBytesW = sizeof(float4) * 2 * kG * kRecStages;   // 32-byte sc_splat records
-constexpr size_t kBlendSmem = (kMetaBytesW + kRecBytesW) * kBlendWarps;
+constexpr size_t kWarpSmem = kMetaBytesW + kRecBytesW;   // one warp's rings
 
 // 32-bit footprint (lane = 8 row + col) of a block-relative window code
 // x0 | x1 << 3 | y0 << 6 | y1 << 8 on the 8x4 block; 0 when x0 > x1
@@ -94,57 +94,62 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr uint32_t kNoEntry = 0xFFFFFFFFu;
 constexpr uint32_t kEmptyCode = 0x0007u;   // x0 = 7 > x1 = 0
 
-__global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
-                                                            const uint32_t *__restrict__ offsets,
-                                                            const uint32_t *__restrict__ vals,
-                                                            const uint32_t *__restrict__ keys,
-                                                            const sc_window *__restrict__ wins, int blocks,
-                                                            const uint32_t *__restrict__ task_order, int width,
-                                                            int height, int n_tx, float stop_t, float bg_r,
-                                                            float bg_g, float bg_b, int record, float *image,
-                                                            float *trans, float *csum, float *cmax)
-{
-    extern __shared__ float4 s_dyn[];
-    const int tile = (int)(task_order ? task_order[blockIdx.x] : blockIdx.x);
-    const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ox = txi * kTile, oy = tyi * kTile;              // tile origin
-    const int bx0 = (wid & 1) * 8, by0 = (wid >> 1) * 4;        // warp block, tile-relative
-    const int px = ox + bx0 + (lane & 7), py = oy + by0 + (lane >> 3);
-    const bool inside = px < width && py < height;
-    const float fpx = (float)px, fpy = (float)py;
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, cs = 0.0f;
-    bool done = !inside;
-    // this warp's entry stream: its (tile, block) list in the frame path, else
-    // the whole tile list (stage-level API; windows clipped from the records)
-    const uint32_t start = blocks ? offsets[8 * tile + wid] : offsets[tile];
-    const uint32_t end = blocks ? offsets[8 * tile + wid + 1] : offsets[tile + 1];
-    const int gx0 = ox + bx0, gy0 = oy + by0;                  // warp block, absolute pixels
-    // this warp's private rings: meta [kMetaStages][32] (index, code -> footprint), records [kRecStages][32][3]
-    uint2 *meta = reinterpret_cast<uint2 *>(reinterpret_cast<char *>(s_dyn) + wid * (kMetaBytesW + kRecBytesW));
-    float4 *recs = reinterpret_cast<float4 *>(reinterpret_cast<char *>(meta) + kMetaBytesW);
+// Per-warp constants of one list walk.
+struct WalkCtx {
+    const sc_splat *__restrict__ splats;
+    int64_t n_splats;
+    const uint32_t *__restrict__ vals;
+    const uint32_t *__restrict__ keys;
+    const sc_window *__restrict__ wins;
+    int blocks;
+    int gx0, gy0;       // warp block origin, absolute pixels
+    float fpx, fpy;     // this lane's pixel
+    float stop_t;
+    int record;
+    float *cmax;
+    uint2 *meta;        // warp-private rings
+    float4 *recs;
+    int lane;
+};
+
+// Per-pixel compositing state (one pixel per lane).
+struct PixAcc {
+    float T, cr, cg, cb, cs;
+    bool done;
+};
+
 #ifdef SC_BLEND_STATS
-    unsigned long long d_slots = 0, d_hits = 0, d_evals = 0, d_iters = 0;
-    const long long d_t0 = clock64();
+struct WalkStats { unsigned long long slots, hits, evals, iters; };
+#define SC_WS_PARAM , WalkStats &d
+#define SC_WS_ARG , d
+#else
+#define SC_WS_PARAM
+#define SC_WS_ARG
 #endif
 
+// Front-to-back compositing of entries [start, end) of the warp's stream onto
+// the lanes that are not done (reference semantics, sc/_kernels.py:190-275):
+// the asynchronous meta/record pipeline described at the top of this file.
+__device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint32_t end, PixAcc &a SC_WS_PARAM)
+{
+    const int lane = c.lane;
     // meta of group q (entries start + 32 q + lane) -> meta slot ms, asynchronously
     auto issue_meta = [&](uint32_t q, int ms) {
         const uint32_t e = start + kG * q + lane;
-        uint2 *dst = meta + ms * kG + lane;
+        uint2 *dst = c.meta + ms * kG + lane;
         if (e < end) {
-            if (blocks) {   // key = block id << 10 | block-relative window (masked in issue_rec)
-                cp_async4(&dst->x, vals + e);
-                cp_async4(&dst->y, keys + e);
-            } else {        // tile list: clip the record's window to this warp's block here
-                const uint32_t v = __ldg(vals + e);
+            if (c.blocks) {   // key = block id << 10 | block-relative window (masked in issue_rec)
+                cp_async4(&dst->x, c.vals + e);
+                cp_async4(&dst->y, c.keys + e);
+            } else {          // tile list: clip the record's window to this warp's block here
+                const uint32_t v = __ldg(c.vals + e);
                 uint32_t code = kEmptyCode;
-                if ((int64_t)v < n_splats) {
-                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(wins + v));
-                    const int x0 = max(lo16(w.x), gx0), x1 = min(hi16(w.x), gx0 + 7);
-                    const int y0 = max(lo16(w.y), gy0), y1 = min(hi16(w.y), gy0 + 3);
+                if ((int64_t)v < c.n_splats) {
+                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(c.wins + v));
+                    const int x0 = max(lo16(w.x), c.gx0), x1 = min(hi16(w.x), c.gx0 + 7);
+                    const int y0 = max(lo16(w.y), c.gy0), y1 = min(hi16(w.y), c.gy0 + 3);
                     if (x0 <= x1 && y0 <= y1)
-                        code = (uint32_t)((x0 - gx0) | ((x1 - gx0) << 3) | ((y0 - gy0) << 6) | ((y1 - gy0) << 8));
+                        code = (uint32_t)((x0 - c.gx0) | ((x1 - c.gx0) << 3) | ((y0 - c.gy0) << 6) | ((y1 - c.gy0) << 8));
                 }
                 *dst = make_uint2(v, code);
             }
@@ -155,122 +160,173 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     // records of the entries in meta slot ms that touch alive pixels -> record
     // slot rs (cp.async); the code is replaced by that footprint
     auto issue_rec = [&](int ms, int rs, uint32_t alive) {
-        uint2 *m = meta + ms * kG + lane;
+        uint2 *m = c.meta + ms * kG + lane;
         const uint2 v = *m;
-        const uint32_t fp = ((int64_t)v.x < n_splats) ? (code_mask(v.y & 0x3FFu) & alive) : 0u;
+        const uint32_t fp = ((int64_t)v.x < c.n_splats) ? (code_mask(v.y & 0x3FFu) & alive) : 0u;
         m->y = fp;
         if (fp) {
-            const float4 *src = reinterpret_cast<const float4 *>(splats + v.x);
-            float4 *dst = recs + (rs * kG + lane) * 2;
+            const float4 *src = reinterpret_cast<const float4 *>(c.splats + v.x);
+            float4 *dst = c.recs + (rs * kG + lane) * 2;
             cp_async16(dst, src);
             cp_async16(dst + 1, src + 1);
         }
     };
 
-    if (!__all_sync(0xffffffffu, done) && start < end) {
-        // prologue, commit order: [meta 0-2], [rec 0], [meta 3], [rec 1], [meta 4], [rec 2]
-        issue_meta(0, 0);
-        issue_meta(1, 1);
-        issue_meta(2, 2);
-        cp_async_commit();
-        cp_async_wait<0>();
+    if (__all_sync(0xffffffffu, a.done) || start >= end) return;
+    // prologue, commit order: [meta 0-2], [rec 0], [meta 3], [rec 1], [meta 4], [rec 2]
+    issue_meta(0, 0);
+    issue_meta(1, 1);
+    issue_meta(2, 2);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    const uint32_t alive0 = __ballot_sync(0xffffffffu, !a.done);
+    issue_rec(0, 0, alive0);
+    cp_async_commit();
+    issue_meta(3, 3);
+    cp_async_commit();
+    issue_rec(1, 1, alive0);
+    cp_async_commit();
+    issue_meta(4, 4);
+    cp_async_commit();
+    issue_rec(2, 2, alive0);
+    cp_async_commit();
+    int ms = 0, rs = 0;   // slots of group g
+    for (uint32_t q = 0; start + kG * q < end; q++) {
+        // pending at most: [rec g+1], [meta g+4], [rec g+2]  ->  rec g and meta g+3 have landed
+        cp_async_wait<3>();
         __syncwarp();
-        const uint32_t alive0 = __ballot_sync(0xffffffffu, !done);
-        issue_rec(0, 0, alive0);
+        const uint32_t alive_now = __ballot_sync(0xffffffffu, !a.done);
+        if (!alive_now) break;
+        const int ms5 = ms == 0 ? 5 : ms - 1, ms3 = ms >= 3 ? ms - 3 : ms + 3;
+        const int rs3 = rs == 0 ? 3 : rs - 1;
+        issue_meta(q + 5, ms5);            // group g+5 meta   (slot of g-1, consumed)
         cp_async_commit();
-        issue_meta(3, 3);
+        issue_rec(ms3, rs3, alive_now);    // group g+3 records (slot of g-1, consumed)
         cp_async_commit();
-        issue_rec(1, 1, alive0);
-        cp_async_commit();
-        issue_meta(4, 4);
-        cp_async_commit();
-        issue_rec(2, 2, alive0);
-        cp_async_commit();
-        int ms = 0, rs = 0;   // slots of group g
-        for (uint32_t q = 0; start + kG * q < end; q++) {
-            // pending at most: [rec g+1], [meta g+4], [rec g+2]  ->  rec g and meta g+3 have landed
-            cp_async_wait<3>();
-            __syncwarp();
-            const uint32_t alive_now = __ballot_sync(0xffffffffu, !done);
-            if (!alive_now) break;
-            const int ms5 = ms == 0 ? 5 : ms - 1, ms3 = ms >= 3 ? ms - 3 : ms + 3;
-            const int rs3 = rs == 0 ? 3 : rs - 1;
-            issue_meta(q + 5, ms5);            // group g+5 meta   (slot of g-1, consumed)
-            cp_async_commit();
-            issue_rec(ms3, rs3, alive_now);    // group g+3 records (slot of g-1, consumed)
-            cp_async_commit();
-            // ---- blend group g ----
-            const uint2 m = meta[ms * kG + lane];
-            const uint32_t fp = m.y & alive_now;
+        // ---- blend group g ----
+        const uint2 m = c.meta[ms * kG + lane];
+        const uint32_t fp = m.y & alive_now;
 #ifdef SC_BLEND_STATS
-            d_slots++;
-            d_hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
+        d.slots++;
+        d.hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
 #endif
-            if (__any_sync(0xffffffffu, fp != 0u)) {
-                const float4 *grp = recs + rs * kG * 2;
-                uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
-                while (__any_sync(0xffffffffu, mine != 0u)) {
-                    const bool act = mine != 0u;
-                    const int j = act ? __ffs(mine) - 1 : lane;
-                    mine &= mine - 1u;
-                    const uint32_t sidx = record ? __shfl_sync(0xffffffffu, m.x, j) : 0u;
+        if (__any_sync(0xffffffffu, fp != 0u)) {
+            const float4 *grp = c.recs + rs * kG * 2;
+            uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
+            while (__any_sync(0xffffffffu, mine != 0u)) {
+                const bool act = mine != 0u;
+                const int j = act ? __ffs(mine) - 1 : lane;
+                mine &= mine - 1u;
+                const uint32_t sidx = c.record ? __shfl_sync(0xffffffffu, m.x, j) : 0u;
 #ifdef SC_BLEND_STATS
-                    d_evals += act;
-                    d_iters += (lane == 0);
+                d.evals += act;
+                d.iters += (lane == 0);
 #endif
-                    if (act) {
-                        const float4 *r = grp + j * 2;
-                        const float4 g = r[0];   // mx, my, 0.5 a, b
-                        const float4 p = r[1];   // 0.5 c, p_min, rgb (fp16 x3)
-                        const float dx = fpx - g.x, dy = fpy - g.y;
-                        const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
-                        if (!(power > 0.0f || power < p.y)) {
-                            // opacity * e^power == e^(power - p_min) / 255
-                            const float alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
-                            const float contrib = alpha * T;
-                            const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
-                            const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
-                            cr += contrib * __low2float(rg);
-                            cg += contrib * __high2float(rg);
-                            cb += contrib * __low2float(bx);
-                            T = T * (1.0f - alpha);
-                            if (record) {
-                                cs += contrib;
-                                if (contrib > 0.0f) atomicMax(reinterpret_cast<int *>(cmax) + sidx, __float_as_int(contrib));
-                            }
-                            if (T < stop_t) {
-                                done = true;
-                                mine = 0u;
-                            }
+                if (act) {
+                    const float4 *r = grp + j * 2;
+                    const float4 g = r[0];   // mx, my, 0.5 a, b
+                    const float4 p = r[1];   // 0.5 c, p_min, rgb (fp16 x3)
+                    const float dx = c.fpx - g.x, dy = c.fpy - g.y;
+                    const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
+                    if (!(power > 0.0f || power < p.y)) {
+                        // opacity * e^power == e^(power - p_min) / 255
+                        const float alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
+                        const float contrib = alpha * a.T;
+                        const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
+                        const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
+                        a.cr += contrib * __low2float(rg);
+                        a.cg += contrib * __high2float(rg);
+                        a.cb += contrib * __low2float(bx);
+                        a.T = a.T * (1.0f - alpha);
+                        if (c.record) {
+                            a.cs += contrib;
+                            if (contrib > 0.0f)
+                                atomicMax(reinterpret_cast<int *>(c.cmax) + sidx, __float_as_int(contrib));
+                        }
+                        if (a.T < c.stop_t) {
+                            a.done = true;
+                            mine = 0u;
                         }
                     }
                 }
             }
-            __syncwarp();   // slots of group g are refilled two steps from now
-            ms = ms == kMetaStages - 1 ? 0 : ms + 1;
-            rs = rs == kRecStages - 1 ? 0 : rs + 1;
         }
-        cp_async_wait<0>();
+        __syncwarp();   // slots of group g are refilled two steps from now
+        ms = ms == kMetaStages - 1 ? 0 : ms + 1;
+        rs = rs == kRecStages - 1 ? 0 : rs + 1;
     }
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
+// One CTA per 16x16 tile, warp w = 8x4 block w.  Frame path: the warp walks its
+// own (tile, block) list; stage-level API (tile lists): every warp walks the
+// whole tile list, clipping each record's window to its block.
+__global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
+                                                      const uint32_t *__restrict__ offsets,
+                                                      const uint32_t *__restrict__ vals,
+                                                      const uint32_t *__restrict__ keys,
+                                                      const sc_window *__restrict__ wins, int blocks,
+                                                      const uint32_t *__restrict__ task_order, int width, int height,
+                                                      int n_tx, float stop_t, float bg_r, float bg_g, float bg_b,
+                                                      int record, float *image, float *trans, float *csum,
+                                                      float *cmax)
+{
+    extern __shared__ float4 s_dyn[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WalkCtx c;
+    c.splats = splats;
+    c.n_splats = n_splats;
+    c.vals = vals;
+    c.keys = keys;
+    c.wins = wins;
+    c.blocks = blocks;
+    c.stop_t = stop_t;
+    c.record = record;
+    c.cmax = cmax;
+    c.lane = lane;
+    // this warp's private rings: meta [kMetaStages][32] (index, code -> footprint), records [kRecStages][32][2]
+    c.meta = reinterpret_cast<uint2 *>(reinterpret_cast<char *>(s_dyn) + wid * (kMetaBytesW + kRecBytesW));
+    c.recs = reinterpret_cast<float4 *>(reinterpret_cast<char *>(c.meta) + kMetaBytesW);
 #ifdef SC_BLEND_STATS
-    for (int o = 16; o > 0; o >>= 1) d_evals += __shfl_down_sync(0xffffffffu, d_evals, o);
+    WalkStats d{0, 0, 0, 0};
+    const long long d_t0 = clock64();
+#endif
+    const int tile = (int)(task_order ? task_order[blockIdx.x] : blockIdx.x);
+    const int b = wid;   // block within the tile
+    const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
+    c.gx0 = txi * kTile + (b & 1) * 8;
+    c.gy0 = tyi * kTile + (b >> 1) * 4;
+    const int px = c.gx0 + (lane & 7), py = c.gy0 + (lane >> 3);
+    const bool inside = px < width && py < height;
+    c.fpx = (float)px;
+    c.fpy = (float)py;
+    PixAcc a{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, !inside};
+    // this warp's entry stream: its (tile, block) list in the frame path, else
+    // the whole tile list (stage-level API; windows clipped from the records)
+    const uint32_t start = blocks ? offsets[8 * tile + b] : offsets[tile];
+    const uint32_t end = blocks ? offsets[8 * tile + b + 1] : offsets[tile + 1];
+    walk_list(c, start, end, a SC_WS_ARG);
+#ifdef SC_BLEND_STATS
+    for (int o = 16; o > 0; o >>= 1) d.evals += __shfl_down_sync(0xffffffffu, d.evals, o);
     if (tile < kDbgTiles && lane == 0) {
         unsigned long long *dd = g_blend_dbg + 8 * (size_t)tile;
-        dd[0] = end - start;
-        atomicAdd(dd + 1, d_slots);
-        atomicAdd(dd + 2, d_hits);
-        atomicAdd(dd + 3, d_evals);
+        atomicAdd(dd, (unsigned long long)(end - start));
+        atomicAdd(dd + 1, d.slots);
+        atomicAdd(dd + 2, d.hits);
+        atomicAdd(dd + 3, d.evals);
         atomicMax(dd + 4, (unsigned long long)(clock64() - d_t0));
-        atomicAdd(dd + 5, d_iters);
+        atomicAdd(dd + 5, d.iters);
     }
 #endif
     if (inside) {
         const int64_t p = (int64_t)py * width + px;
-        image[3 * p + 0] = cr + T * bg_r;
-        image[3 * p + 1] = cg + T * bg_g;
-        image[3 * p + 2] = cb + T * bg_b;
-        trans[p] = T;
-        if (record && csum) csum[p] = cs;
+        image[3 * p + 0] = a.cr + a.T * bg_r;
+        image[3 * p + 1] = a.cg + a.T * bg_g;
+        image[3 * p + 2] = a.cb + a.T * bg_b;
+        trans[p] = a.T;
+        if (record && csum) csum[p] = a.cs;
     }
 }
 
@@ -322,19 +378,21 @@ __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev,
 cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
+    constexpr int kSmem = (int)(kBlendWarps * kWarpSmem);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_blend, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBlendSmem);
+        cudaError_t e = cudaFuncSetAttribute(k_blend, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
     const int64_t n_tiles = (int64_t)n_tx * n_ty;
     if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, n_tiles, lists.blocks ? 8 : 1, task_order);
-    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kBlendSmem, st, splats, n_splats, lists.offsets, lists.vals,
-              lists.keys, lists.wins, lists.blocks ? 1 : 0, task_order, cam.width, cam.height, n_tx, (float)opts.stop_transmittance, (float)opts.background[0],
-              (float)opts.background[1], (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image,
-              out.trans, out.contrib_sum, out.contrib_max);
+    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
+              lists.keys, lists.wins, lists.blocks ? 1 : 0, task_order, cam.width, cam.height, n_tx,
+              (float)opts.stop_transmittance, (float)opts.background[0], (float)opts.background[1],
+              (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image, out.trans, out.contrib_sum,
+              out.contrib_max);
     return cudaGetLastError();
 }
 

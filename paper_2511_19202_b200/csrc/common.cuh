@@ -66,7 +66,7 @@ struct Ws {
     uint32_t *ekey_a, *ekey_b;       // [capE]
     uint32_t *eval_a, *eval_b;       // [capE]
     uint32_t *tile_off;              // [n_tiles + 1]
-    uint32_t *task_order;            // [2 n_tiles] blend dispatch order (heavy tiles first)
+    uint32_t *task_order;            // [n_tiles] blend dispatch order (heavy tiles first)
     uint32_t *boff;                  // [8 n_tiles + 1] offsets of the per-(tile, 8x4 block) entry lists
     uint32_t *rs_counts;             // radix pass digit counts -> bases, digit-major [256][nblk_max]
     uint32_t *scan_part;             // scan partials

@@ -613,6 +613,25 @@ __global__ void k_bentry_emit(const uint2 *pv, const sc_window *wins, const uint
         }
         const uint32_t excl = incl - cnt;
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (__reduce_max_sync(0xffffffffu, cnt) <= 16u) {
+            // small splats (the common case): each lane writes its own entries, row by row;
+            // the warp's outputs are one contiguous range, so the stores stay within a few lines
+            uint32_t o = obase + excl;
+            if (cnt) {
+                for (int by = y0 / 4; by <= y1 / 4; by++) {
+                    const int ry0 = max(y0 - 4 * by, 0), ry1 = min(y1 - 4 * by, 3);
+                    const uint32_t row = (uint32_t)(((by >> 2) * n_tx) * 8 + (by & 3) * 2);
+                    for (int bx = x0 / 8; bx <= x1 / 8; bx++) {
+                        const int rx0 = max(x0 - 8 * bx, 0), rx1 = min(x1 - 8 * bx, 7);
+                        const uint32_t id = row + (uint32_t)((bx >> 1) * 8 + (bx & 1));
+                        ekey[o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
+                        eval[o] = sv;
+                        o++;
+                    }
+                }
+            }
+            continue;
+        }
         for (uint32_t o0 = 0; o0 < total; o0 += 32) {
             const uint32_t o = o0 + lane;
             int s = 0;

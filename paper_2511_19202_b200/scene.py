@@ -154,6 +154,8 @@ class FrameStats:
     skipped: int = 0
     entries: int = 0
     max_tie_run: int = 0
+    block_entries: int = 0
+    exact_fallbacks: int = 0
 
 
 @dataclass
@@ -478,7 +480,8 @@ class Renderer:
                            preprocess_ms=float("nan"), mlp_queried=st["mlp_queried"],
                            instances_visible=st["instances_visible"], pairs_tested=st["pairs_tested"],
                            passed=st["passed"], skipped=st["skipped"], entries=st["entries"],
-                           max_tie_run=st["max_tie_run"])
+                           max_tie_run=st["max_tie_run"], block_entries=st["block_entries"],
+                           exact_fallbacks=st["exact_fallbacks"])
         if not to_host:
             return frame, stats
         out = RenderOutput(

@@ -377,3 +377,26 @@ def test_cull_counts_config3_views(view):
     if bad.size:
         assert np.all(c.flags[bad] & 2), "non-MLP decision differs"
         assert np.abs(c.logit[bad]).max() < LOGIT_MARGIN
+
+
+def test_deep_block_lists_vs_oracle():
+    """A dense asset on a small image: block lists of thousands of entries,
+    pixels that retire at different depths.  Frame path (per-block warp CTAs,
+    heaviest first) against the f64 oracle rendering the same survivors."""
+    from paper_2511_19202_b200 import synth
+    from paper_2511_19202_b200.asset import prepare
+    from paper_2511_19202_b200.camera import Camera
+    from paper_2511_19202_b200.scene import ComposedScene, InstanceTransform, RenderOptions, Renderer
+
+    sc = ComposedScene()
+    sc.add_asset(prepare(synth.make_random_cloud(400_000, seed=3)))
+    sc.add_instance(0, InstanceTransform())
+    cam = Camera.look_at((0.0, -3.2, 1.0), (0.0, 0.0, 0.0), math.radians(50.0), 96, 80)
+    r = Renderer(sc)
+    out, st = r.render(cam, RenderOptions(use_mlp=False), return_survivors=True)
+    assert st.block_entries > 500 * 8 * 6 * 5   # > 500 entries per block on average
+    s = out.survivors
+    m, ls, q, op, sh, deg = sr.instantiate(sr.SceneTables(sc), cam, s[:, 0], s[:, 1])
+    own = rr.render_arrays(m, ls, q, op, sh, deg, cam)
+    _image_close(out.image, own.image)
+    assert out.passed_count == own.passed_count

@@ -400,3 +400,26 @@ def test_deep_block_lists_vs_oracle():
     own = rr.render_arrays(m, ls, q, op, sh, deg, cam)
     _image_close(out.image, own.image)
     assert out.passed_count == own.passed_count
+
+
+def test_mlp_sweep_config4_16m():
+    """Config 4 at 16M materialised queries (uniform [-1, 1]^16, seed 0, made on
+    the device): decisions on the first 1M rows agree with the f64 MLP except
+    within the logit margin; every row gets a finite logit."""
+    import torch
+
+    from paper_2511_19202_b200 import nn, synth
+    from paper_2511_19202_b200.asset import prepare
+    from paper_2511_19202_b200.workloads import calibrated_model
+
+    m = calibrated_model(prepare(synth.make_shell(500, seed=3)), seed=3)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.rand((16 << 20, 16), generator=g, device="cuda", dtype=torch.float32) * 2.0 - 1.0
+    out = nn.forward(m, x)
+    assert bool(torch.isfinite(out).all())
+    n = 1 << 20
+    ref = m.vis_mlp.forward_host(x[:n].cpu().numpy())[:, 0]
+    got = out[:n, 0].cpu().numpy()
+    flips = (got >= 0) != (ref >= 0)
+    assert np.all(np.abs(ref[flips]) < LOGIT_MARGIN)
+    assert np.abs(got - ref).max() < 0.05

@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define SC_ABI_VERSION 1
+#define SC_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define SC_API __attribute__((visibility("default")))
@@ -93,6 +93,11 @@ typedef struct sc_opts {
     double background[3];         /* (1, 1, 1) */
     double dilation;              /* 0.3 */
     double frustum_G;             /* Jacobian bound factor */
+    /* screen band [band_y0, band_y1) in pixel rows, multiples of the tile size
+     * (band_y1 may be the image height); band_y1 <= 0: the whole image.  Only
+     * the band's pixels are written; they are identical to the whole-image
+     * render (the band's sub-frustum is a conservative superset). */
+    int32_t band_y0, band_y1;
 } sc_opts;
 
 /*

@@ -20,6 +20,7 @@ if os.environ.get("SPLATCULL_B200_DEBUG_LIB"):       # instrumented build (scrip
     LIB_PATH = os.path.join(_HERE, "libsplatcull_b200_dbg.so")
 
 SC_OK = 0
+ABI_VERSION = 2   # include/splatcull_b200.h SC_ABI_VERSION
 SC_FRUSTUM_MARGIN, SC_FRUSTUM_STRICT, SC_FRUSTUM_OFF = 0, 1, 2
 
 c_f64, c_i32, c_i64, c_f32, c_u32, c_u16 = (ctypes.c_double, ctypes.c_int32, ctypes.c_int64,
@@ -36,7 +37,7 @@ class ScOpts(ctypes.Structure):
     _fields_ = [("tile_size", c_i32), ("sh_degree_eval", c_i32), ("record_contributions", c_i32),
                 ("use_mlp", c_i32), ("frustum_mode", c_i32), ("exact_projection", c_i32),
                 ("radius_clip", c_f64), ("stop_transmittance", c_f64), ("background", c_f64 * 3),
-                ("dilation", c_f64), ("frustum_G", c_f64)]
+                ("dilation", c_f64), ("frustum_G", c_f64), ("band_y0", c_i32), ("band_y1", c_i32)]
 
 
 class ScAssetRec(ctypes.Structure):
@@ -142,7 +143,7 @@ def load(require_gpu: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.sc_abi_version() != 1:
+        if lib.sc_abi_version() != ABI_VERSION:
             raise NativeError("libsplatcull_b200.so ABI version mismatch")
         _lib = lib
     return _lib

@@ -152,6 +152,8 @@ int check_opts(const sc_opts *o)
     if (o->tile_size != sc::kTile) return fail(SC_ERR_UNSUPPORTED, "tile_size must be 16%s");
     if (o->frustum_mode < SC_FRUSTUM_MARGIN || o->frustum_mode > SC_FRUSTUM_OFF)
         return fail(SC_ERR_INVALID, "unknown frustum_mode%s");
+    if (o->band_y1 > 0 && (o->band_y0 < 0 || o->band_y0 % sc::kTile != 0 || o->band_y1 <= o->band_y0))
+        return fail(SC_ERR_INVALID, "band must be [y0, y1) with y0 a multiple of the tile size and y1 > y0%s");
     return SC_OK;
 }
 

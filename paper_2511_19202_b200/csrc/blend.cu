@@ -268,7 +268,8 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                                                       const uint32_t *__restrict__ vals,
                                                       const uint32_t *__restrict__ keys,
                                                       const sc_window *__restrict__ wins, int blocks,
-                                                      const uint32_t *__restrict__ task_order, int width, int height,
+                                                      const uint32_t *__restrict__ task_order, int tile_base,
+                                                      int width, int height,
                                                       int n_tx, float stop_t, float bg_r, float bg_g, float bg_b,
                                                       int record, float *image, float *trans, float *csum,
                                                       float *cmax)
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     WalkStats d{0, 0, 0, 0};
     const long long d_t0 = clock64();
 #endif
-    const int tile = (int)(task_order ? task_order[blockIdx.x] : blockIdx.x);
+    const int tile = (int)(task_order ? task_order[blockIdx.x] : tile_base + (int)blockIdx.x);
     const int b = wid;   // block within the tile
     const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
     c.gx0 = txi * kTile + (b & 1) * 8;
@@ -340,13 +341,14 @@ __device__ __forceinline__ uint32_t tile_weight(const uint32_t *off, int64_t t, 
     return w;
 }
 
-__global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_t n_tiles, int stride, uint32_t *order)
+__global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_t tile_base, int64_t n_tiles,
+                                                     int stride, uint32_t *order)
 {
     __shared__ uint32_t hist[33], base[33];
     if (threadIdx.x < 33) hist[threadIdx.x] = 0;
     __syncthreads();
     for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-        const uint32_t c = tile_weight(off, t, stride);
+        const uint32_t c = tile_weight(off, tile_base + t, stride);
         atomicAdd(&hist[c ? 32 - __clz(c) : 0], 1u);
     }
     __syncthreads();
@@ -359,8 +361,8 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_
     }
     __syncthreads();
     for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-        const uint32_t c = tile_weight(off, t, stride);
-        order[atomicAdd(&base[c ? 32 - __clz(c) : 0], 1u)] = (uint32_t)t;
+        const uint32_t c = tile_weight(off, tile_base + t, stride);
+        order[atomicAdd(&base[c ? 32 - __clz(c) : 0], 1u)] = (uint32_t)(tile_base + t);
     }
 }
 
@@ -385,11 +387,14 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
-    const int64_t n_tiles = (int64_t)n_tx * n_ty;
-    if (task_order) SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, n_tiles, lists.blocks ? 8 : 1, task_order);
+    const int n_tx = (cam.width + kTile - 1) / kTile;
+    const Band band = band_of(opts, cam.height);   // only the band's tiles are blended (and written)
+    const int64_t tile_base = (int64_t)band.t0 * n_tx, n_tiles = (int64_t)(band.t1 - band.t0) * n_tx;
+    if (n_tiles <= 0) return cudaSuccess;
+    if (task_order)
+        SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, tile_base, n_tiles, lists.blocks ? 8 : 1, task_order);
     SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
-              lists.keys, lists.wins, lists.blocks ? 1 : 0, task_order, cam.width, cam.height, n_tx,
+              lists.keys, lists.wins, lists.blocks ? 1 : 0, task_order, (int)tile_base, cam.width, cam.height, n_tx,
               (float)opts.stop_transmittance, (float)opts.background[0], (float)opts.background[1],
               (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image, out.trans, out.contrib_sum,
               out.contrib_max);

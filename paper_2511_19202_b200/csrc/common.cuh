@@ -35,6 +35,25 @@ struct InstFrame {
     int32_t gate;         // 1: every pair is queried (d_t >= d_near), 0: none, -1: per-pair f64 test
 };
 
+// Screen band of a render in pixel rows [y0, y1) and tile rows [t0, t1)
+// (sc_opts.band_*; the whole image when band_y1 <= 0).
+struct Band {
+    int y0, y1, t0, t1;
+};
+__host__ __device__ __forceinline__ Band band_of(const sc_opts &o, int height)
+{
+    const int n_ty = (height + kTile - 1) / kTile;
+    Band b{0, n_ty * kTile, 0, n_ty};
+    if (o.band_y1 > 0) {
+        b.t0 = o.band_y0 / kTile;
+        b.t1 = (o.band_y1 + kTile - 1) / kTile;
+        b.t1 = b.t1 < n_ty ? b.t1 : n_ty;
+        b.y0 = b.t0 * kTile;
+        b.y1 = b.t1 * kTile;
+    }
+    return b;
+}
+
 // Internal counters block (device), zeroed per frame together with the stats.
 struct Counters {
     unsigned long long chunk_ticket;   // dynamic chunk assignment for the cull kernel

@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
     const double f = cam.focal;
     const double cxp = (double)(cam.width - 1) / 2.0, cyp = (double)(cam.height - 1) / 2.0;
     const double TW = (double)(kTile * ((cam.width + kTile - 1) / kTile));
-    const double TH = (double)(kTile * ((cam.height + kTile - 1) / kTile));
+    const Band band = band_of(opts, cam.height);
+    const bool banded = opts.band_y1 > 0;
     for (int64_t base = 0; base < scene.n_instances; base += 1024) {
         const int64_t i = base + tid;
         uint32_t nch = 0;
@@ -71,7 +72,8 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
                     mg = 3.0 * f * opts.frustum_G * in.s * a.sigma_max * (1.0 + 1e-6);
                     pad = 3.0;
                     xhi = TW;
-                    yhi = TH;
+                    ylo = (double)band.y0;
+                    yhi = (double)band.y1;
                 }
                 // low side:  f t + (c + pad - lo) z + mg >= 0 must be reachable
                 double kl = cxp + pad - xlo;
@@ -83,6 +85,14 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
                 kh = cyp - pad - yhi;
                 if (f * cy + kh * cz - mg - rho * sqrt(f * f + kh * kh) > 0.0) vis = 0;
             }
+            if (banded && opts.frustum_mode != SC_FRUSTUM_MARGIN && vis) {   // band rows, margin style
+                const double mgb = 3.0 * f * opts.frustum_G * in.s * a.sigma_max * (1.0 + 1e-6);
+                if (cz + rho <= cam.near_) vis = 0;
+                double kl = cyp + 3.0 - (double)band.y0;
+                if (f * cy + kl * cz + mgb + rho * sqrt(f * f + kl * kl) < 0.0) vis = 0;
+                double kh = cyp - 3.0 - (double)band.y1;
+                if (f * cy + kh * cz - mgb - rho * sqrt(f * f + kh * kh) > 0.0) vis = 0;
+            }
             // Uniform instances (every pair decided the same way) skip the per-pair f64
             // tests in k_cull.  inside: the sphere lies strictly inside z > near and the
             // image-plane region the per-pair test accepts unconditionally
@@ -91,22 +101,28 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
             // cannot flip such a pair.
             int inside = 0, gate = -1;
             if (vis) {
+                const double rr = rho * (1.0 + 1e-6) + 1e-9;
+                // plane  f x + (c - b) z >= 0  (mx >= b)  and  -(f x + (c - b) z) >= 0  (mx <= b)
+                auto dist_ge = [&](double px, double pz, double k, double sign) {
+                    const double v = sign * (f * px + k * pz);
+                    return v > rr * sqrt(f * f + k * k) * (1.0 + 1e-9);
+                };
+                const bool front = cz - rr > cam.near_ * (1.0 + 1e-9) + 1e-12;
                 if (opts.frustum_mode == SC_FRUSTUM_OFF) {
                     inside = 1;
                 } else {
-                    const double lo = opts.frustum_mode == SC_FRUSTUM_STRICT ? 1e-3 : 0.0;
-                    const double hx = opts.frustum_mode == SC_FRUSTUM_STRICT ? (double)(cam.width - 1) - 1e-3 : TW;
-                    const double hy = opts.frustum_mode == SC_FRUSTUM_STRICT ? (double)(cam.height - 1) - 1e-3 : TH;
-                    const double rr = rho * (1.0 + 1e-6) + 1e-9;
-                    // plane  f x + (c - b) z >= 0  (mx >= b)  and  -(f x + (c - b) z) >= 0  (mx <= b)
-                    auto dist_ge = [&](double px, double pz, double k, double sign) {
-                        const double v = sign * (f * px + k * pz);
-                        return v > rr * sqrt(f * f + k * k) * (1.0 + 1e-9);
-                    };
-                    inside = (cz - rr > cam.near_ * (1.0 + 1e-9) + 1e-12) && dist_ge(cx, cz, cxp - lo, 1.0) &&
-                             dist_ge(cx, cz, cxp - hx, -1.0) && dist_ge(cy, cz, cyp - lo, 1.0) &&
-                             dist_ge(cy, cz, cyp - hy, -1.0);
+                    const bool strict = opts.frustum_mode == SC_FRUSTUM_STRICT;
+                    const double lo = strict ? 1e-3 : 0.0;
+                    const double hx = strict ? (double)(cam.width - 1) - 1e-3 : TW;
+                    const double ly = strict ? 1e-3 : (double)band.y0;
+                    const double hy = strict ? (double)(cam.height - 1) - 1e-3 : (double)band.y1;
+                    inside = front && dist_ge(cx, cz, cxp - lo, 1.0) && dist_ge(cx, cz, cxp - hx, -1.0) &&
+                             dist_ge(cy, cz, cyp - ly, 1.0) && dist_ge(cy, cz, cyp - hy, -1.0);
                 }
+                // the band rows (margin style, rb >= 3 px of slack) in the other modes
+                if (banded && opts.frustum_mode != SC_FRUSTUM_MARGIN)
+                    inside = inside && front && dist_ge(cy, cz, cyp - (double)band.y0, 1.0) &&
+                             dist_ge(cy, cz, cyp - (double)band.y1, -1.0);
                 if (a.model >= 0 && opts.use_mlp) {
                     const double dc = sqrt((in.t[0] - cam.pos[0]) * (in.t[0] - cam.pos[0]) +
                                            (in.t[1] - cam.pos[1]) * (in.t[1] - cam.pos[1]) +
@@ -209,7 +225,9 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
     const unsigned long long total = ws.ctr->total_chunks;
     const double cxp = (double)(cam.width - 1) / 2.0, cyp = (double)(cam.height - 1) / 2.0;
     const double TW = (double)(kTile * ((cam.width + kTile - 1) / kTile));
-    const double TH = (double)(kTile * ((cam.height + kTile - 1) / kTile));
+    const Band band = band_of(opts, cam.height);
+    const bool banded = opts.band_y1 > 0;
+    const double BY0 = (double)band.y0, BY1 = (double)band.y1;   // whole image: [0, TH)
 
     for (;;) {
         if (tid == 0) s_chunk = (uint32_t)atomicAdd(&ws.ctr->chunk_ticket, 1ull);
@@ -260,7 +278,9 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
                     const float smax = __ldg(scene.scale_smax + 4 * g + 3);
                     double tx, ty, tz;
                     cam_xyz(cam, mw.x, mw.y, mw.z, tx, ty, tz);
-                    if (tz > cam.near_) {
+                    if (opts.frustum_mode == SC_FRUSTUM_OFF) {
+                        pass = true;   // only the band filter below
+                    } else if (tz > cam.near_) {
                         const double mx = cam.focal * (tx / tz) + cxp;
                         const double my = cam.focal * (ty / tz) + cyp;
                         if (opts.frustum_mode == SC_FRUSTUM_STRICT) {
@@ -269,7 +289,16 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
                         } else {
                             const double sigma_w = s_in.s * (double)smax;
                             const double rb = 3.0 * (cam.focal / tz) * sigma_w * opts.frustum_G + 3.0;
-                            pass = (mx + rb >= 0.0) && (mx - rb < TW) && (my + rb >= 0.0) && (my - rb < TH);
+                            pass = (mx + rb >= 0.0) && (mx - rb < TW) && (my + rb >= BY0) && (my - rb < BY1);
+                        }
+                    }
+                    if (pass && banded && opts.frustum_mode != SC_FRUSTUM_MARGIN) {
+                        // screen band: the same conservative margin test on the band rows
+                        pass = false;
+                        if (tz > cam.near_) {
+                            const double my = cam.focal * (ty / tz) + cyp;
+                            const double rb = 3.0 * (cam.focal / tz) * (s_in.s * (double)smax) * opts.frustum_G + 3.0;
+                            pass = (my + rb >= BY0) && (my - rb < BY1);
                         }
                     }
                 }

@@ -52,7 +52,8 @@ __global__ void __launch_bounds__(256, 2) k_project(
     const int64_t n = from_list ? (int64_t)ctr->proj_deferred : n_surv;
     const double lim_x = 1.3 * cam.tan_x, lim_y = 1.3 * cam.tan_y;
     const double focal = cam.focal;
-    const int n_tx = (cam.width + kTile - 1) / kTile, n_ty = (cam.height + kTile - 1) / kTile;
+    const int n_tx = (cam.width + kTile - 1) / kTile;
+    const Band band = band_of(opts, cam.height);
     const double log_min_alpha = log(1.0 / 255.0);
     unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0, n_exact = 0;
     const bool fast = MODE == kProjFast || (MODE == kProjMixed && opts.exact_projection == 0);
@@ -229,8 +230,9 @@ __global__ void __launch_bounds__(256, 2) k_project(
         if (valid) {
             tx0 = (int)clampd(floor((mx - radius) / (double)kTile), 0.0, (double)n_tx);
             tx1 = (int)clampd(floor((mx + radius) / (double)kTile) + 1.0, 0.0, (double)n_tx);
-            ty0 = (int)clampd(floor((my - radius) / (double)kTile), 0.0, (double)n_ty);
-            ty1 = (int)clampd(floor((my + radius) / (double)kTile) + 1.0, 0.0, (double)n_ty);
+            // tile rows clamp to the band (the whole image: [0, n_ty))
+            ty0 = (int)clampd(floor((my - radius) / (double)kTile), (double)band.t0, (double)band.t1);
+            ty1 = (int)clampd(floor((my + radius) / (double)kTile) + 1.0, (double)band.t0, (double)band.t1);
             passed = tx1 > tx0 && ty1 > ty0;
         }
         n_passed += passed;

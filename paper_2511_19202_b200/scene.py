@@ -172,6 +172,7 @@ class RenderOptions:
     use_mlp: bool = True
     frustum: str = "margin"
     exact_projection: bool = False   # True: all-f64 projection (False: f32 covariance, exact f64 fallback)
+    band: tuple | None = None        # (y0, y1) pixel rows, y0 a multiple of 16: render only this screen band
 
     def struct(self, cam) -> nat.ScOpts:
         if self.tile_size != 16:
@@ -185,6 +186,11 @@ class RenderOptions:
         o.use_mlp = 1 if self.use_mlp else 0
         o.frustum_mode = FRUSTUM_MODES[self.frustum]
         o.exact_projection = 1 if self.exact_projection else 0
+        if self.band is not None:
+            y0, y1 = int(self.band[0]), int(self.band[1])
+            if y0 < 0 or y0 % 16 or y1 <= y0 or y0 >= int(cam.height):
+                raise ValueError(f"band must be (y0, y1) with 0 <= y0 < height, y0 % 16 == 0, y1 > y0; got {self.band}")
+            o.band_y0, o.band_y1 = y0, min(y1, int(cam.height))
         o.radius_clip = float(self.radius_clip) if self.radius_clip is not None else 0.0
         o.stop_transmittance = float(self.stop_transmittance)
         o.background[:] = [float(v) for v in self.background]

@@ -150,3 +150,13 @@ def camera_path(wl: Workload, frames: int, width: int, height: int) -> list[Came
         out.append(Camera.look_at([rad * math.cos(ang), rad * math.sin(ang), z], [0, 0, 0], mid.fov_y, width,
                                   height))
     return out
+
+
+def config5(frames: int = 120, width: int = 3840, height: int = 2160, **kw) -> Workload:
+    """Config 5: the config-3 scene (~100M instantiated) on a 4K orbit camera path
+    (sharded by frames or screen bands across GPUs)."""
+    wl = config3(width=width, height=height, **kw)
+    cams = camera_path(wl, frames, width, height)
+    meta = dict(wl.meta)
+    meta.update({"views": f"{frames}-frame orbit at the mid view's distance", "resolution": f"{width}x{height}"})
+    return Workload("cfg5", wl.scene, cams, meta)

@@ -423,3 +423,29 @@ def test_mlp_sweep_config4_16m():
     flips = (got >= 0) != (ref >= 0)
     assert np.all(np.abs(ref[flips]) < LOGIT_MARGIN)
     assert np.abs(got - ref).max() < 0.05
+
+
+@pytest.mark.parametrize("view", [0, 2], ids=["near", "far"])
+def test_screen_bands_equal_whole_frame(view):
+    """Band sharding: each band rendered with its sub-frustum is
+    bit-identical to the same rows of the whole-image render (same entries in
+    the same (depth, index) order per tile), for uneven bands too."""
+    import torch
+
+    from paper_2511_19202_b200 import sharding
+    from paper_2511_19202_b200.scene import RenderOptions, Renderer
+    from paper_2511_19202_b200.workloads import config3
+
+    wl = config3(n_per=8_000, n_instances=200, width=480, height=270)
+    cam = wl.cameras[view]
+    r = Renderer(wl.scene)
+    full, st = r.render(cam, RenderOptions(), to_host=False)
+    img, tr = full.image.clone(), full.trans.clone()
+    n_rows = sharding.tile_rows(cam.height)
+    for bounds in (sharding.split_rows(n_rows, 3), [0, 2, 5, 16, n_rows]):
+        for b in range(len(bounds) - 1):
+            y0, y1 = sharding.band_pixels(bounds, b, cam.height)
+            band, bst = r.render(cam, RenderOptions(band=(y0, y1)), to_host=False)
+            assert torch.equal(band.image[y0:y1], img[y0:y1]), (bounds, b)
+            assert torch.equal(band.trans[y0:y1], tr[y0:y1])
+            assert bst.instantiated <= st.instantiated

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
         assert name in _native.SIGNATURES, f"{name} has no ctypes signature"
-    assert lib.sc_abi_version() == 1
+    assert lib.sc_abi_version() == _native.ABI_VERSION == 2
 
 
 def test_workspace_bytes_is_host_computable():

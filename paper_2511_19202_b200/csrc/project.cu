@@ -19,12 +19,20 @@ __constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539
 __constant__ double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
                                 -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
 
-__device__ __forceinline__ int16_t clamp16(double v)
+__device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// sqrt.approx (rel. error < 2^-22): only where the result is widened by a margin far larger
+__device__ __forceinline__ float sqrt_approx(float x)
 {
-    return (int16_t)(v < -1.0 ? -1.0 : (v > 32767.0 ? 32767.0 : v));
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
-__device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
+// floor / ceil of an f64 value as int32, saturating (cvt.rmi / cvt.rpi clamp to the int range)
+__device__ __forceinline__ int ifloor(double v) { return __double2int_rd(v); }
+__device__ __forceinline__ int iceil(double v) { return __double2int_ru(v); }
+__device__ __forceinline__ int iclamp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // f32 dot product with explicit FMA (this TU is -fmad=false for the f64 paths)
 __device__ __forceinline__ float fdot3(float a0, float a1, float a2, float b0, float b1, float b2)
@@ -111,7 +119,7 @@ __global__ void __launch_bounds__(256, 2) k_project(
                 const float q00 = 1.0f - 2.0f * (y * y + z * z), q01 = 2.0f * (x * y - w * z), q02 = 2.0f * (x * z + w * y);
                 const float q10 = 2.0f * (x * y + w * z), q11 = 1.0f - 2.0f * (x * x + z * z), q12 = 2.0f * (y * z - w * x);
                 const float q20 = 2.0f * (x * z - w * y), q21 = 2.0f * (y * z + w * x), q22 = 1.0f - 2.0f * (x * x + y * y);
-                const float s0 = expf(2.0f * ls0), s1 = expf(2.0f * ls1), s2 = expf(2.0f * ls2);
+                const float s0 = __expf(2.0f * ls0), s1 = __expf(2.0f * ls1), s2 = __expf(2.0f * ls2);   // 2 ulp: inside K
                 const float g00 = fdot3(q00 * q00, q01 * q01, q02 * q02, s0, s1, s2);
                 const float g01 = fdot3(q00 * q10, q01 * q11, q02 * q12, s0, s1, s2);
                 const float g02 = fdot3(q00 * q20, q01 * q21, q02 * q22, s0, s1, s2);
@@ -128,7 +136,7 @@ __global__ void __launch_bounds__(256, 2) k_project(
                 const float fa = fdot3(u0, u1, u2, j00, j01, j02) + dil;
                 const float fb = fdot3(u0, u1, u2, j10, j11, j12);
                 const float fc = fdot3(v0, v1, v2, j10, j11, j12) + dil;
-                const float sg0 = sqrtf(g00), sg1 = sqrtf(g11), sg2 = sqrtf(g22);
+                const float sg0 = sqrt_approx(g00), sg1 = sqrt_approx(g11), sg2 = sqrt_approx(g22);   // bound only
                 const float na = fdot3(fabsf(j00), fabsf(j01), fabsf(j02), sg0, sg1, sg2);
                 const float nc = fdot3(fabsf(j10), fabsf(j11), fabsf(j12), sg0, sg1, sg2);
                 constexpr float kEps = 5.9604645e-08f, K = 64.0f;
@@ -153,8 +161,8 @@ __global__ void __launch_bounds__(256, 2) k_project(
                     valid = radius > 0.0;
                     if (valid && opts.radius_clip > 0.0 && det < opts.radius_clip) valid = false;
                     // support half-widths from conservative a, c (times sqrt(2 L) later)
-                    ex_f = sqrtf(fa + err);
-                    ey_f = sqrtf(fc + err);
+                    ex_f = sqrt_approx(fa + err);
+                    ey_f = sqrt_approx(fc + err);
                     cov_a = (double)fa;
                     cov_c = (double)fc;
                 }
@@ -225,14 +233,22 @@ __global__ void __launch_bounds__(256, 2) k_project(
             }
         }
         // --- tile rectangle (sc/raster.py:307-314) ---
+        // floor((m -+ r) / 16) == floor(m -+ r) >> 4: the f64 difference is rounded once
+        // either way, /16 is exact, and floor(floor(x) / 16) == floor(x / 16); the int
+        // conversions saturate, which the clamps below absorb
         int tx0 = 0, tx1 = 0, ty0 = 0, ty1 = 0;
+        int fx0 = 0, fx1 = 0, fy0 = 0, fy1 = 0;   // floor(m - r), floor(m + r)
         bool passed = false;
         if (valid) {
-            tx0 = (int)clampd(floor((mx - radius) / (double)kTile), 0.0, (double)n_tx);
-            tx1 = (int)clampd(floor((mx + radius) / (double)kTile) + 1.0, 0.0, (double)n_tx);
+            fx0 = ifloor(mx - radius);
+            fx1 = ifloor(mx + radius);
+            fy0 = ifloor(my - radius);
+            fy1 = ifloor(my + radius);
+            tx0 = iclamp(fx0 >> 4, 0, n_tx);
+            tx1 = iclamp((fx1 >> 4) + 1, 0, n_tx);
             // tile rows clamp to the band (the whole image: [0, n_ty))
-            ty0 = (int)clampd(floor((my - radius) / (double)kTile), (double)band.t0, (double)band.t1);
-            ty1 = (int)clampd(floor((my + radius) / (double)kTile) + 1.0, (double)band.t0, (double)band.t1);
+            ty0 = iclamp(fy0 >> 4, band.t0, band.t1);
+            ty1 = iclamp((fy1 >> 4) + 1, band.t0, band.t1);
             passed = tx1 > tx0 && ty1 > ty0;
         }
         n_passed += passed;
@@ -286,13 +302,13 @@ __global__ void __launch_bounds__(256, 2) k_project(
         const float xl = mo.w;
         float op;
         if (xl >= 0.0f) {
-            op = 1.0f / (1.0f + expf(-xl));
+            op = __fdividef(1.0f, 1.0f + __expf(-xl));
         } else {
-            const float e = expf(xl);
-            op = e / (1.0f + e);
+            const float e = __expf(xl);
+            op = __fdividef(e, 1.0f + e);
         }
         const bool skip = !(op >= 1.0f / 255.0f);   // reference: `op < min_alpha: continue`
-        const float p_min = skip ? __int_as_float(0x7f800000) : (float)log_min_alpha - logf(op);
+        const float p_min = skip ? __int_as_float(0x7f800000) : (float)log_min_alpha - __logf(op);
 
         sc_splat sp;
         sp.mx = (float)mx;
@@ -318,17 +334,19 @@ __global__ void __launch_bounds__(256, 2) k_project(
             const double L = -(double)p_min;
             double ex, ey;
             if (fast_done) {   // f32: a, c widened by their error bound, then 1e-4 relative + 1e-2 px
-                const float sl = sqrtf(2.0f * (float)L);
+                const float sl = sqrt_approx(2.0f * (float)L);
                 ex = (double)(sl * ex_f) * (1.0 + 1e-4) + 1e-2;
                 ey = (double)(sl * ey_f) * (1.0 + 1e-4) + 1e-2;
             } else {
                 ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-5) + 1e-3;
                 ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-5) + 1e-3;
             }
-            win.x0 = clamp16(fmax(fmax(floor(mx - radius), ceil(mx - ex)), (double)(kTile * tx0)));
-            win.x1 = clamp16(fmin(fmin(floor(mx + radius) + 1.0, floor(mx + ex)), (double)(kTile * tx1 - 1)));
-            win.y0 = clamp16(fmax(fmax(floor(my - radius), ceil(my - ey)), (double)(kTile * ty0)));
-            win.y1 = clamp16(fmin(fmin(floor(my + radius) + 1.0, floor(my + ey)), (double)(kTile * ty1 - 1)));
+            // integer form of max(floor(m - r), ceil(m - e), 16 t0) / min(floor(m + r) + 1,
+            // floor(m + e), 16 t1 - 1), clamped to the int16 window range [-1, 32767]
+            win.x0 = (int16_t)iclamp(max(max(fx0, iceil(mx - ex)), kTile * tx0), -1, 32767);
+            win.x1 = (int16_t)iclamp(min(min(min(fx1, 0x7FFFFFFE) + 1, ifloor(mx + ex)), kTile * tx1 - 1), -1, 32767);
+            win.y0 = (int16_t)iclamp(max(max(fy0, iceil(my - ey)), kTile * ty0), -1, 32767);
+            win.y1 = (int16_t)iclamp(min(min(min(fy1, 0x7FFFFFFE) + 1, ifloor(my + ey)), kTile * ty1 - 1), -1, 32767);
         } else {   // never composited
             win.x0 = 1;
             win.x1 = 0;

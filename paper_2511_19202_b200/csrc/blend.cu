@@ -9,25 +9,28 @@
 // tests/test_gpu_parity.py).
 //
 // B200 mapping — one CTA per 16x16 tile, 8 warps, no CTA barrier at all:
-//   * a warp owns an 8x4 pixel block (lane = 8 row + col) and walks the
-//     tile's entry list on its own; CTAs are dispatched heaviest tile first
+//   * a warp owns an 8x4 pixel block (lane = 8 row + col) and walks its own
+//     depth-ordered (tile, block) list; CTAs are dispatched heaviest tile first
 //     (LPT order by log2 entry count, k_tile_order);
-//   * the list is consumed as a 4-deep software pipeline of 64-entry groups:
-//     group g+3: entry indices + 16-bit tile-relative windows (coalesced
-//                stream written by the binning pass) in flight to registers,
-//     g+1, g+2:  48-byte splat records of the entries whose window touches
-//                an ALIVE pixel of the block in flight by cp.async into the
-//                warp's private shared-memory ring (alive only shrinks, so the
-//                mask at issue time is a superset of what is needed: exact),
-//     g:         blended from shared memory;
-//   * per 32 entries the warp transposes the 32 footprints (32x32 bit
-//     transpose over shuffles) so each lane walks only the entries covering
-//     its own pixel; the warp iterates max-over-lanes times;
+//   * meta stream: the list's (index, window code) pairs are read 128 entries per
+//     step (4 per lane, one step prefetched in registers); entries whose
+//     footprint misses every still-alive pixel are dropped on the spot, the
+//     others are compacted, in order, into a per-warp hit queue in shared memory
+//     (alive only shrinks, so the mask at queue time is a superset: exact);
+//   * record pipeline: 32 queued hits at a time become a stage whose 32-byte
+//     splat records are cp.async'd into one of 4 shared slots; up to 3 stages
+//     are in flight while the oldest is blended;
+//   * blending a stage: the warp transposes the 32 footprints (32x32 bit
+//     transpose over shuffles) so each lane walks only the entries covering its
+//     own pixel; the warp iterates max-over-lanes times;
 //   * a warp exits when its 32 pixels have retired.
 // History (ncu, config-3 far view): a 256-entry CTA batch behind a barrier was
 // barrier-stall bound (42 ms); barrier-free warps with per-hit shuffles were
-// then bound by re-gathering windows (65 GB DRAM per launch) and finally by
-// the dependent-load chain per 32 entries; this pipeline removes both.
+// then bound by re-gathering windows (65 GB DRAM per launch), by the
+// dependent-load chain per 32 entries (-> cp.async pipeline), by tile lists
+// (-> per-block lists) and by streaming entries that touch only retired pixels
+// (-> hit compaction: in the heaviest tiles ~80 % of entries miss every alive
+// pixel because a few pixels never saturate).
 #include <algorithm>
 
 #include "common.cuh"
@@ -42,12 +45,15 @@ __device__ unsigned long long g_blend_dbg[kDbgTiles * 8];
 #endif
 
 constexpr int kBlendWarps = 8;           // warps per CTA (one 16x16 tile)
-constexpr int kG = 32;                   // entries per pipeline group
-constexpr int kMetaStages = 6;           // meta ring (index + window code) depth: issued 5 groups ahead
-constexpr int kRecStages = 4;            // record ring depth: issued 3 groups ahead
-constexpr size_t kMetaBytesW = sizeof(uint2) * kG * kMetaStages;
+constexpr int kG = 32;                   // hits per record stage
+constexpr int kStep = 128;               // meta entries per stream step (4 per lane)
+constexpr int kHQ = 256;                 // hit queue capacity (>= kG + kStep)
+constexpr int kRecStages = 4;            // record stages: up to 3 in flight while the oldest is blended
+constexpr int kHeavyHits = 12;           // a pixel covered by >= this many entries of a stage: entry-parallel
+constexpr size_t kHQBytesW = sizeof(uint2) * kHQ;
+constexpr size_t kStageMetaBytesW = sizeof(uint2) * kG * kRecStages;
 constexpr size_t kRecBytesW = sizeof(float4) * 2 * kG * kRecStages;   // 32-byte sc_splat records
-constexpr size_t kWarpSmem = kMetaBytesW + kRecBytesW;   // one warp's rings
+constexpr size_t kWarpSmem = kHQBytesW + kStageMetaBytesW + kRecBytesW;   // one warp's queues
 
 // 32-bit footprint (lane = 8 row + col) of a block-relative window code
 // x0 | x1 << 3 | y0 << 6 | y1 << 8 on the 8x4 block; 0 when x0 > x1
@@ -91,6 +97,17 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// wait until at most n (0..3) cp.async groups are pending
+__device__ __forceinline__ void cp_async_wait_dyn(uint32_t n)
+{
+    switch (n) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    default: cp_async_wait<3>(); break;
+    }
+}
+
 constexpr uint32_t kNoEntry = 0xFFFFFFFFu;
 constexpr uint32_t kEmptyCode = 0x0007u;   // x0 = 7 > x1 = 0
 
@@ -107,8 +124,9 @@ struct WalkCtx {
     float stop_t;
     int record;
     float *cmax;
-    uint2 *meta;        // warp-private rings
-    float4 *recs;
+    uint2 *hq;          // warp-private hit queue [kHQ] (index, footprint)
+    uint2 *stage;       // [kRecStages][32] (index, footprint) of each record stage
+    float4 *recs;       // [kRecStages][32][2]
     int lane;
 };
 
@@ -128,92 +146,113 @@ struct WalkStats { unsigned long long slots, hits, evals, iters; };
 #endif
 
 // Front-to-back compositing of entries [start, end) of the warp's stream onto
-// the lanes that are not done (reference semantics, sc/_kernels.py:190-275):
-// the asynchronous meta/record pipeline described at the top of this file.
+// the lanes that are not done (reference semantics, sc/_kernels.py:190-275).
 __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint32_t end, PixAcc &a SC_WS_PARAM)
 {
     const int lane = c.lane;
-    // meta of group q (entries start + 32 q + lane) -> meta slot ms, asynchronously
-    auto issue_meta = [&](uint32_t q, int ms) {
-        const uint32_t e = start + kG * q + lane;
-        uint2 *dst = c.meta + ms * kG + lane;
-        if (e < end) {
-            if (c.blocks) {   // key = block id << 10 | block-relative window (masked in issue_rec)
-                cp_async4(&dst->x, c.vals + e);
-                cp_async4(&dst->y, c.keys + e);
-            } else {          // tile list: clip the record's window to this warp's block here
-                const uint32_t v = __ldg(c.vals + e);
-                uint32_t code = kEmptyCode;
-                if ((int64_t)v < c.n_splats) {
-                    const uint2 w = __ldg(reinterpret_cast<const uint2 *>(c.wins + v));
-                    const int x0 = max(lo16(w.x), c.gx0), x1 = min(hi16(w.x), c.gx0 + 7);
-                    const int y0 = max(lo16(w.y), c.gy0), y1 = min(hi16(w.y), c.gy0 + 3);
-                    if (x0 <= x1 && y0 <= y1)
-                        code = (uint32_t)((x0 - c.gx0) | ((x1 - c.gx0) << 3) | ((y0 - c.gy0) << 6) | ((y1 - c.gy0) << 8));
-                }
-                *dst = make_uint2(v, code);
+    if (__all_sync(0xffffffffu, a.done) || start >= end) return;
+    const uint32_t lt = lanemask_lt();
+    // meta of stream step [base, base + 128): entry base + 32 j + lane in (v[j], k[j])
+    uint32_t va[4], ka[4], vb[4], kb[4];
+    auto load_step = [&](uint32_t base, uint32_t *v, uint32_t *k) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t e = base + 32 * j + lane;
+            v[j] = kNoEntry;
+            k[j] = kEmptyCode;
+            if (e < end) {
+                v[j] = __ldg(c.vals + e);
+                if (c.blocks) k[j] = __ldg(c.keys + e);   // block id << 10 | block-relative window
             }
-        } else {
-            *dst = make_uint2(kNoEntry, kEmptyCode);
         }
     };
-    // records of the entries in meta slot ms that touch alive pixels -> record
-    // slot rs (cp.async); the code is replaced by that footprint
-    auto issue_rec = [&](int ms, int rs, uint32_t alive) {
-        uint2 *m = c.meta + ms * kG + lane;
-        const uint2 v = *m;
-        const uint32_t fp = ((int64_t)v.x < c.n_splats) ? (code_mask(v.y & 0x3FFu) & alive) : 0u;
-        m->y = fp;
-        if (fp) {
-            const float4 *src = reinterpret_cast<const float4 *>(c.splats + v.x);
-            float4 *dst = c.recs + (rs * kG + lane) * 2;
-            cp_async16(dst, src);
-            cp_async16(dst + 1, src + 1);
-        }
+    // footprint of an entry on this warp's block (tile lists: clip the record's window here)
+    auto footprint = [&](uint32_t v, uint32_t k) -> uint32_t {
+        if ((int64_t)v >= c.n_splats) return 0u;
+        if (c.blocks) return code_mask(k & 0x3FFu);
+        const uint2 w = __ldg(reinterpret_cast<const uint2 *>(c.wins + v));
+        const int x0 = max(lo16(w.x), c.gx0), x1 = min(hi16(w.x), c.gx0 + 7);
+        const int y0 = max(lo16(w.y), c.gy0), y1 = min(hi16(w.y), c.gy0 + 3);
+        if (x0 > x1 || y0 > y1) return 0u;
+        return code_mask((uint32_t)((x0 - c.gx0) | ((x1 - c.gx0) << 3) | ((y0 - c.gy0) << 6) | ((y1 - c.gy0) << 8)));
     };
 
-    if (__all_sync(0xffffffffu, a.done) || start >= end) return;
-    // prologue, commit order: [meta 0-2], [rec 0], [meta 3], [rec 1], [meta 4], [rec 2]
-    issue_meta(0, 0);
-    issue_meta(1, 1);
-    issue_meta(2, 2);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-    const uint32_t alive0 = __ballot_sync(0xffffffffu, !a.done);
-    issue_rec(0, 0, alive0);
-    cp_async_commit();
-    issue_meta(3, 3);
-    cp_async_commit();
-    issue_rec(1, 1, alive0);
-    cp_async_commit();
-    issue_meta(4, 4);
-    cp_async_commit();
-    issue_rec(2, 2, alive0);
-    cp_async_commit();
-    int ms = 0, rs = 0;   // slots of group g
-    for (uint32_t q = 0; start + kG * q < end; q++) {
-        // pending at most: [rec g+1], [meta g+4], [rec g+2]  ->  rec g and meta g+3 have landed
-        cp_async_wait<3>();
+    uint32_t mbase = start;
+    load_step(mbase, va, ka);
+    if (mbase + kStep < end) load_step(mbase + kStep, vb, kb);
+    bool meta_done = false;
+    uint32_t hq_head = 0, hq_tail = 0;   // running counters (slot = counter % kHQ)
+    uint32_t issued = 0, blended = 0;    // record stages
+    for (;;) {
+        const uint32_t alive = __ballot_sync(0xffffffffu, !a.done);
+        if (!alive) break;
+        // 1. stream meta until a full stage of hits is queued (or the list ends)
+        while (!meta_done && hq_tail - hq_head < (uint32_t)kG) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const uint32_t fp = footprint(va[j], ka[j]) & alive;
+                const uint32_t bal = __ballot_sync(0xffffffffu, fp != 0u);
+                if (fp) c.hq[(hq_tail + __popc(bal & lt)) & (kHQ - 1)] = make_uint2(va[j], fp);
+                hq_tail += __popc(bal);
+            }
+            mbase += kStep;
+            if (mbase >= end) {
+                meta_done = true;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    va[j] = vb[j];
+                    ka[j] = kb[j];
+                }
+                if (mbase + kStep < end) load_step(mbase + kStep, vb, kb);
+            }
+        }
         __syncwarp();
+        // 2. turn up to 32 queued hits into a record stage (cp.async of their records)
+        const uint32_t queued = hq_tail - hq_head;
+        const bool room = issued - blended < (uint32_t)kRecStages;
+        if (room && (queued >= (uint32_t)kG || (meta_done && queued > 0))) {
+            const uint32_t n = queued < (uint32_t)kG ? queued : (uint32_t)kG;
+            const int slot = (int)(issued % kRecStages);
+            uint2 h = make_uint2(kNoEntry, 0u);
+            if ((uint32_t)lane < n) {
+                h = c.hq[(hq_head + lane) & (kHQ - 1)];
+                h.y &= alive;
+            }
+            c.stage[slot * kG + lane] = h;
+            if (h.y) {
+                const float4 *src = reinterpret_cast<const float4 *>(c.splats + h.x);
+                float4 *dst = c.recs + (slot * kG + lane) * 2;
+                cp_async16(dst, src);
+                cp_async16(dst + 1, src + 1);
+            }
+            cp_async_commit();
+            hq_head += n;
+            issued++;
+            // keep up to three stages in flight before blending the oldest
+            if (issued - blended < (uint32_t)kRecStages && !(meta_done && hq_tail == hq_head)) continue;
+        }
+        if (issued == blended) {
+            if (meta_done && hq_tail == hq_head) break;
+            continue;
+        }
+        // 3. blend the oldest stage once its records have landed
+        cp_async_wait_dyn(issued - blended - 1);
+        __syncwarp();
+        const int slot = (int)(blended % kRecStages);
+        const uint2 m = c.stage[slot * kG + lane];
         const uint32_t alive_now = __ballot_sync(0xffffffffu, !a.done);
-        if (!alive_now) break;
-        const int ms5 = ms == 0 ? 5 : ms - 1, ms3 = ms >= 3 ? ms - 3 : ms + 3;
-        const int rs3 = rs == 0 ? 3 : rs - 1;
-        issue_meta(q + 5, ms5);            // group g+5 meta   (slot of g-1, consumed)
-        cp_async_commit();
-        issue_rec(ms3, rs3, alive_now);    // group g+3 records (slot of g-1, consumed)
-        cp_async_commit();
-        // ---- blend group g ----
-        const uint2 m = c.meta[ms * kG + lane];
         const uint32_t fp = m.y & alive_now;
 #ifdef SC_BLEND_STATS
         d.slots++;
         d.hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
 #endif
         if (__any_sync(0xffffffffu, fp != 0u)) {
-            const float4 *grp = c.recs + rs * kG * 2;
-            uint32_t mine = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
+            const float4 *grp = c.recs + slot * kG * 2;
+            const uint32_t covers = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
+            // pixels covered by many of this stage's entries are composited entry-parallel below
+            const uint32_t heavy = __ballot_sync(0xffffffffu, __popc(covers) >= kHeavyHits);
+            uint32_t mine = ((heavy >> lane) & 1u) ? 0u : covers;
             while (__any_sync(0xffffffffu, mine != 0u)) {
                 const bool act = mine != 0u;
                 const int j = act ? __ffs(mine) - 1 : lane;
@@ -251,10 +290,75 @@ __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint
                     }
                 }
             }
+            // Entry-parallel compositing of one heavy pixel at a time: lane j evaluates
+            // entry j's alpha at the pixel (alphas do not depend on T), an in-order warp
+            // prefix product of (1 - alpha) gives T before every entry, the reference's
+            // retirement cut (first T < stop after a composite) is a ballot, and the
+            // colour a warp sum.  Same terms as the serial walk, products in tree order
+            // (fp32 rounding only).
+            uint32_t hv = heavy;
+            while (hv) {
+                const int pl = __ffs(hv) - 1;
+                hv &= hv - 1u;
+                const uint32_t cov = __shfl_sync(0xffffffffu, covers, pl);
+                const float T_in = __shfl_sync(0xffffffffu, a.T, pl);
+                const float qx = __shfl_sync(0xffffffffu, c.fpx, pl), qy = __shfl_sync(0xffffffffu, c.fpy, pl);
+                float alpha = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+                if ((cov >> lane) & 1u) {
+                    const float4 *r = grp + lane * 2;
+                    const float4 g = r[0];
+                    const float4 p = r[1];
+                    const float dx = qx - g.x, dy = qy - g.y;
+                    const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
+                    if (!(power > 0.0f || power < p.y)) {
+                        alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
+                        const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
+                        const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
+                        cr = __low2float(rg);
+                        cg = __high2float(rg);
+                        cb = __low2float(bx);
+                    }
+                }
+                // inclusive prefix product of (1 - alpha) over lanes 0..j
+                float incl = 1.0f - alpha;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl *= y;
+                }
+                float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+                if (lane == 0) excl = 1.0f;
+                const float t_before = T_in * excl, t_after = T_in * incl;
+                // composited: a valid entry reached before the pixel retired
+                const bool comp = alpha > 0.0f && t_before >= c.stop_t;
+                const float contrib = comp ? alpha * t_before : 0.0f;
+                if (c.record && contrib > 0.0f) atomicMax(reinterpret_cast<int *>(c.cmax) + m.x, __float_as_int(contrib));
+                float sr = contrib * cr, sg = contrib * cg, sb = contrib * cb, sc = contrib;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+                    sg += __shfl_xor_sync(0xffffffffu, sg, o);
+                    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+                    sc += __shfl_xor_sync(0xffffffffu, sc, o);
+                }
+                const uint32_t compm = __ballot_sync(0xffffffffu, comp);
+                const float T_out = compm ? __shfl_sync(0xffffffffu, t_after, 31 - __clz(compm)) : T_in;
+                if (lane == pl) {
+                    a.cr += sr;
+                    a.cg += sg;
+                    a.cb += sb;
+                    a.cs += sc;
+                    a.T = T_out;
+                    if (T_out < c.stop_t) a.done = true;
+                }
+#ifdef SC_BLEND_STATS
+                d.evals += __popc(cov) * (lane == pl);
+                d.iters += (lane == 0);
+#endif
+            }
         }
-        __syncwarp();   // slots of group g are refilled two steps from now
-        ms = ms == kMetaStages - 1 ? 0 : ms + 1;
-        rs = rs == kRecStages - 1 ? 0 : rs + 1;
+        __syncwarp();   // the slot is refilled by a later stage
+        blended++;
     }
     cp_async_wait<0>();
     __syncwarp();
@@ -287,9 +391,11 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     c.record = record;
     c.cmax = cmax;
     c.lane = lane;
-    // this warp's private rings: meta [kMetaStages][32] (index, code -> footprint), records [kRecStages][32][2]
-    c.meta = reinterpret_cast<uint2 *>(reinterpret_cast<char *>(s_dyn) + wid * (kMetaBytesW + kRecBytesW));
-    c.recs = reinterpret_cast<float4 *>(reinterpret_cast<char *>(c.meta) + kMetaBytesW);
+    // this warp's private queues: hits [kHQ], stage metas [kRecStages][32], records [kRecStages][32][2]
+    char *wbase = reinterpret_cast<char *>(s_dyn) + wid * kWarpSmem;
+    c.hq = reinterpret_cast<uint2 *>(wbase);
+    c.stage = reinterpret_cast<uint2 *>(wbase + kHQBytesW);
+    c.recs = reinterpret_cast<float4 *>(wbase + kHQBytesW + kStageMetaBytesW);
 #ifdef SC_BLEND_STATS
     WalkStats d{0, 0, 0, 0};
     const long long d_t0 = clock64();

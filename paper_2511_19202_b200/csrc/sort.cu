@@ -268,7 +268,10 @@ struct OsSmem {
     uint16_t wcnt[kOsWarps][256];
 };
 
-template <typename V>
+// MATCH_ANY: rank with match.any (fast when a warp holds few distinct digits,
+// e.g. the block sort's high byte: screen rows follow depth order) instead of
+// the constant-cost 8-ballot match.
+template <typename V, bool MATCH_ANY>
 __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__restrict__ keys_in,
                                                               const V *__restrict__ vals_in,
                                                               uint32_t *__restrict__ keys_out,
@@ -332,7 +335,10 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
             const int i = wid * kPerWarp + j * 32 + lane;
             k[j] = sm.in_k[b][i];
             v[j] = sm.in_v[b][i];
-            peers[j] = match_digit8((k[j] >> shift) & 0xFFu) & __ballot_sync(0xffffffffu, i < cnt);
+            if constexpr (MATCH_ANY)
+                peers[j] = __match_any_sync(0xffffffffu, i < cnt ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane);
+            else
+                peers[j] = match_digit8((k[j] >> shift) & 0xFFu) & __ballot_sync(0xffffffffu, i < cnt);
         }
 #pragma unroll
         for (int j = 0; j < kOsItems; j++) {
@@ -392,8 +398,11 @@ static cudaError_t radix_down_attr()
 {
     static bool done = false;
     if (done) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_radix_down<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_radix_down<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(OsSmem<V>));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_radix_down<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(OsSmem<V>));
     if (e == cudaSuccess) done = true;
     return e;
 }
@@ -415,7 +424,8 @@ static int sm_count_sort()
 // (ping-pong between a and b).
 template <typename V>
 static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const unsigned long long *n_dev, int64_t n_max,
-                              int bit_lo, int bit_hi, const Ws &ws, uint32_t **keys_res, V **vals_res, cudaStream_t st)
+                              int bit_lo, int bit_hi, const Ws &ws, uint32_t **keys_res, V **vals_res, cudaStream_t st,
+                              bool last_match_any = false)
 {
     cudaError_t e = radix_down_attr<V>();
     if (e != cudaSuccess) return e;
@@ -430,8 +440,13 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
                   shift, ws.rs_counts, ntiles);
         e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_radix_down<V>, (int)std::min<int64_t>(ntiles, (int64_t)nsm * 2), kOsThreads, sizeof(OsSmem<V>),
-                  st, ki, vi, ko, vo, n_dev, n_max, shift, ws.rs_counts, ntiles);
+        const int grid = (int)std::min<int64_t>(ntiles, (int64_t)nsm * 2);
+        if (last_match_any && p == npass - 1)
+            SC_LAUNCH((k_radix_down<V, true>), grid, kOsThreads, sizeof(OsSmem<V>), st, ki, vi, ko, vo, n_dev, n_max,
+                      shift, ws.rs_counts, ntiles);
+        else
+            SC_LAUNCH((k_radix_down<V, false>), grid, kOsThreads, sizeof(OsSmem<V>), st, ki, vi, ko, vo, n_dev, n_max,
+                      shift, ws.rs_counts, ntiles);
         std::swap(ki, ko);
         std::swap(vi, vo);
     }
@@ -734,8 +749,10 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
         SC_LAUNCH(k_bentry_emit, grid_for(n_max, 256), 256, 0, st, pv_s, wins, ws.ecount, p_dev, n_max, cam.width,
                   cam.height, ws.n_tx, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
         const int64_t n_blocks = 8 * ws.n_tiles;
+        // last pass (block-id high byte ~ screen rows, which follow depth order): few distinct
+        // digits per warp, match.any ranks them faster than the ballot match
         e = radix_sort<uint32_t>(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, kCodeBits,
-                                 kCodeBits + bits_for(n_blocks), ws, &ek, &ev, st);
+                                 kCodeBits + bits_for(n_blocks), ws, &ek, &ev, st, true);
         if (e != cudaSuccess) return e;
         SC_LAUNCH(k_block_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE, n_blocks,
                   ws.boff);

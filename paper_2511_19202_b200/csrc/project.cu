@@ -65,6 +65,10 @@ __global__ void __launch_bounds__(256, 2) k_project(
     const double log_min_alpha = log(1.0 / 255.0);
     unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0, n_exact = 0;
     const bool fast = MODE == kProjFast || (MODE == kProjMixed && opts.exact_projection == 0);
+    // camera rotation in f32 for the f32 covariance path (loop invariant)
+    const float r0 = (float)cam.rot[0], r1 = (float)cam.rot[1], r2 = (float)cam.rot[2], r3 = (float)cam.rot[3],
+                r4 = (float)cam.rot[4], r5 = (float)cam.rot[5], r6 = (float)cam.rot[6], r7 = (float)cam.rot[7],
+                r8 = (float)cam.rot[8];
 
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n; it += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = from_list ? (int64_t)list[it] : it;
@@ -78,8 +82,9 @@ __global__ void __launch_bounds__(256, 2) k_project(
 
         // --- instancing (B2), exactly as the oracle's orc_instantiate ---
         const float3 mw = inst_mean(in, mo.x, mo.y, mo.z);
+        // q' = q_i (x) q in f64 -> f32 (B2) for both paths: the instanced render must equal the
+        // flattened one bit for bit, so q' is the same f32 value in either
         const float4 qw = inst_quat(in, q4);
-        // fast path: f32 instance quaternion product (<= 1 ulp from the f64-rounded qw; inside the error bound)
         const float4 qf = qw;
         const float ls0 = __double2float_rn((double)ls4.x + in.ln_s);
         const float ls1 = __double2float_rn((double)ls4.y + in.ln_s);
@@ -110,8 +115,6 @@ __global__ void __launch_bounds__(256, 2) k_project(
                 // gives the same ceil(3 sqrt(lambda)); else the f64 path below runs.
                 const float fz = (float)focal / (float)tz;
                 const float cx = (float)ctxz, cy = (float)ctyz;
-                const float r0 = (float)R[0], r1 = (float)R[1], r2 = (float)R[2], r3 = (float)R[3], r4 = (float)R[4],
-                            r5 = (float)R[5], r6 = (float)R[6], r7 = (float)R[7], r8 = (float)R[8];
                 const float j00 = fz * fmaf(-cx, r6, r0), j01 = fz * fmaf(-cx, r7, r1), j02 = fz * fmaf(-cx, r8, r2);
                 const float j10 = fz * fmaf(-cy, r6, r3), j11 = fz * fmaf(-cy, r7, r4), j12 = fz * fmaf(-cy, r8, r5);
                 const float qn = rsqrtf(fmaf(qf.x, qf.x, fdot3(qf.y, qf.z, qf.w, qf.y, qf.z, qf.w)));

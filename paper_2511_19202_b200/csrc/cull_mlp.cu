@@ -214,8 +214,11 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
     __shared__ sc_asset_rec s_as;
     __shared__ InstFrame s_fr;
     __shared__ sc_survivor s_surv[kChunk];
-    __shared__ uint32_t s_wcnt[kCullThreads / 32];
-    __shared__ uint32_t s_chunk, s_inst, s_prefix;
+    constexpr int kCullWarps = kCullThreads / 32;
+    static_assert(kCullTilesPerChunk * kCullWarps == 32, "one warp scans the chunk's segment counts");
+    __shared__ uint32_t s_wcnt[kCullTilesPerChunk * kCullWarps];   // survivors per (tile, warp) segment
+    __shared__ uint32_t s_segoff[kCullTilesPerChunk * kCullWarps];
+    __shared__ uint32_t s_chunk, s_inst, s_prefix, s_nc;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     mlp_setup(sm, tid);
@@ -234,6 +237,7 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
         __syncthreads();
         const uint32_t chunk = s_chunk;
         if (chunk >= total) break;
+        if (tid < kCullTilesPerChunk * kCullWarps) s_wcnt[tid] = 0;   // tiles past the chunk end stay empty
         if (tid == 0) {
             // last instance with chunk_begin <= chunk
             int64_t lo = 0, hi = scene.n_instances;
@@ -256,7 +260,6 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
         const int64_t j0 = (int64_t)(chunk - s_fr.chunk_begin) * kChunk;
         const int64_t j1 = min(j0 + (int64_t)kChunk, s_as.count);
         const uint32_t inst_id = s_inst;
-        uint32_t n_c = 0;   // survivors of this chunk so far (uniform)
 
         for (int t = 0; t < kCullTilesPerChunk; t++) {
             const int64_t jt = j0 + (int64_t)t * kCullThreads;
@@ -331,31 +334,38 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
             bool keep = pass;
             if (model >= 0) {
                 mlp_store_row(sm, tid, lo, hi);
-                if (__syncthreads_or(queried)) {
-                    const float logit = mlp_tile(sm, tid, phase);
-                    if (queried && !(logit >= s_as.logit_threshold)) keep = false;
-                }
+                float logit;
+                if (mlp_tile(sm, tid, phase, queried, &logit) && queried && !(logit >= s_as.logit_threshold))
+                    keep = false;
             }
             n_pass += pass;
             n_query += queried;
             n_cull += (pass && !keep);
-            // ordered compaction into s_surv
+            // warp-local ordered compaction: segment (t, w) of the chunk, no CTA barrier
             const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            if (lane == 0) s_wcnt[wid] = __popc(bal);
-            __syncthreads();
-            uint32_t off = n_c;
-            for (int w = 0; w < wid; w++) off += s_wcnt[w];
             if (keep) {
                 sc_survivor sv;
                 sv.inst = inst_id;
                 sv.gid = (uint32_t)j;
-                s_surv[off + __popc(bal & lanemask_lt())] = sv;
+                s_surv[t * kCullThreads + wid * 32 + __popc(bal & lanemask_lt())] = sv;
             }
-            uint32_t tot = 0;
-            for (int w = 0; w < kCullThreads / 32; w++) tot += s_wcnt[w];
-            n_c += tot;
-            __syncthreads();
+            if (lane == 0) s_wcnt[t * kCullWarps + wid] = __popc(bal);
         }
+        // chunk order = (tile, warp)-major: scan the 32 segment counts (one warp)
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t c = s_wcnt[lane];
+            uint32_t x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            s_segoff[lane] = x - c;
+            if (lane == 31) s_nc = x;
+        }
+        __syncthreads();
+        const uint32_t n_c = s_nc;
 
         // decoupled look-back over chunk aggregates
         if (tid == 0) {
@@ -385,9 +395,12 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
         }
         __syncthreads();
         const uint32_t prefix = s_prefix;
-        for (uint32_t k = tid; k < n_c; k += kCullThreads) {
-            const long long pos = (long long)prefix + k;
-            if (pos < cap) out[pos] = s_surv[k];
+        for (int t = 0; t < kCullTilesPerChunk; t++) {   // warp w copies its segments
+            const int seg = t * kCullWarps + wid;
+            if ((uint32_t)lane < s_wcnt[seg]) {
+                const long long pos = (long long)prefix + s_segoff[seg] + lane;
+                if (pos < cap) out[pos] = s_surv[t * kCullThreads + wid * 32 + lane];
+            }
         }
     }
     // stats
@@ -427,7 +440,8 @@ __global__ void __launch_bounds__(128) k_vis_forward(const sc_vis_weights *w, co
             hi = make_uint4(pack_h2(c.x, c.y), pack_h2(c.z, c.w), pack_h2(d.x, d.y), pack_h2(d.z, d.w));
         }
         mlp_store_row(sm, tid, lo, hi);
-        const float lg = mlp_tile(sm, tid, phase);
+        float lg = 0.0f;
+        mlp_tile(sm, tid, phase, true, &lg);
         if (r < n) logits[r] = lg;
     }
     mlp_teardown(sm, tid);

@@ -171,14 +171,16 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b)
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
-// Runs the three layers for the tile whose inputs are in sm.a1; returns the
-// logit of this thread's row.  Must be called by all 128 threads.
-__device__ __forceinline__ float mlp_tile(MlpSmem &sm, int tid, uint32_t &phase)
+// Runs the three layers for the tile whose inputs are in sm.a1 if any thread
+// passes `pred` (the first barrier doubles as that vote); returns whether it
+// ran, the logit of this thread's row in *logit.  Must be called by all 128
+// threads.
+__device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, bool pred, float *logit_out)
 {
     constexpr uint32_t kIdesc = idesc_f16<128, 32>();
     fence_async_smem();
     tc_fence_before();
-    __syncthreads();
+    if (!__syncthreads_or(pred)) return false;
     if (tid == 0) {
         tc_fence_after();
         mma_f16_ss(sm.tmem_base, smem_desc(smem_u32(sm.a1), 128, 256), smem_desc(smem_u32(sm.w1), 128, 256),
@@ -220,7 +222,8 @@ __device__ __forceinline__ float mlp_tile(MlpSmem &sm, int tid, uint32_t &phase)
 #pragma unroll
     for (int n = 0; n < 32; n++) logit += fmaxf(v[n] + sm.b2[n], 0.0f) * sm.w3[n];
     tc_fence_before();
-    return logit;
+    *logit_out = logit;
+    return true;
 }
 
 // CTA prologue / epilogue for kernels that use mlp_tile (blockDim = 128).

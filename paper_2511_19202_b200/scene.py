@@ -395,6 +395,15 @@ class DeviceFrame:
     survivors: "torch.Tensor | None" = None
 
 
+def _to_pinned(t):
+    """Asynchronous device->host copy into a pinned tensor (caller synchronises)."""
+    import torch
+
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    return h
+
+
 class Renderer:
     """Renders frames of one ComposedScene on one GPU."""
 
@@ -470,7 +479,14 @@ class Renderer:
             ev0.record()
             frame = self.render_device(cam, opts, return_survivors=return_survivors)
             ev1.record()
-            st = nat.stats_dict(frame.stats_raw.cpu().numpy())
+            # one batch of asynchronous copies into pinned host memory (torch's caching host
+            # allocator), then a single synchronisation
+            host = {"stats": _to_pinned(frame.stats_raw)}
+            if to_host:
+                host["image"] = _to_pinned(frame.image)
+                host["trans"] = _to_pinned(frame.trans)
+            torch.cuda.current_stream().synchronize()
+            st = nat.stats_dict(host["stats"].numpy())
             if not st["overflow"]:
                 break
             # the frame path bins (splat, 8x4 block) pairs: block_entries of them
@@ -491,8 +507,8 @@ class Renderer:
         if not to_host:
             return frame, stats
         out = RenderOutput(
-            image=frame.image.cpu().numpy(),
-            final_transmittance=frame.trans.cpu().numpy(),
+            image=host["image"].numpy(),
+            final_transmittance=host["trans"].numpy(),
             contribution_max=frame.contrib_max[:n_s].cpu().numpy() if opts.record_contributions else None,
             contribution_sum=frame.contrib_sum.cpu().numpy() if opts.record_contributions else None,
             used_count=st["used"] if opts.record_contributions else None,

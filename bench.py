@@ -224,11 +224,19 @@ def main():
     import numpy as np
     import torch
 
+    # SC_BENCH_SINGLE_DEVICE=1 (testing only): every rank on cuda:0, gloo control plane, so the
+    # multi-process paths can be exercised on a one-GPU box (NCCL needs one GPU per rank)
+    single = os.environ.get("SC_BENCH_SINGLE_DEVICE") == "1"
+    if single:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if single:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2511_19202_b200 as pkg
     from paper_2511_19202_b200 import _native as nat

@@ -49,6 +49,7 @@ constexpr int kG = 32;                   // hits per record stage
 constexpr int kStep = 128;               // meta entries per stream step (4 per lane)
 constexpr int kHQ = 256;                 // hit queue capacity (>= kG + kStep)
 constexpr int kRecStages = 4;            // record stages: up to 3 in flight while the oldest is blended
+constexpr int kMaxHeavyPixels = 8;       // ... and at most this many such pixels in the stage
 constexpr int kHeavyHits = 12;           // a pixel covered by >= this many entries of a stage: entry-parallel
 constexpr size_t kHQBytesW = sizeof(uint2) * kHQ;
 constexpr size_t kStageMetaBytesW = sizeof(uint2) * kG * kRecStages;
@@ -251,7 +252,9 @@ __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint
             const float4 *grp = c.recs + slot * kG * 2;
             const uint32_t covers = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
             // pixels covered by many of this stage's entries are composited entry-parallel below
-            const uint32_t heavy = __ballot_sync(0xffffffffu, __popc(covers) >= kHeavyHits);
+            uint32_t heavy = __ballot_sync(0xffffffffu, __popc(covers) >= kHeavyHits);
+            // when many pixels are heavy the lane-per-pixel loop is already busy on every lane
+            if (__popc(heavy) > kMaxHeavyPixels) heavy = 0u;
             uint32_t mine = ((heavy >> lane) & 1u) ? 0u : covers;
             while (__any_sync(0xffffffffu, mine != 0u)) {
                 const bool act = mine != 0u;

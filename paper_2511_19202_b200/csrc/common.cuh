@@ -65,6 +65,7 @@ struct Counters {
     unsigned long long dmin_inv;       // ~bits(min passed depth)  (atomicMax of ~bits; 0 = none)
     unsigned long long dmax;           // bits(max passed depth)   (positive doubles order as u64)
     unsigned long long tie_runs;       // runs of equal depth keys found by the tie-fix
+    unsigned long long tie_long;       // ... of which longer than 8 (one CTA each)
     unsigned long long proj_deferred;  // splats the f32 projection left to the exact kernel
     double key_dmin, key_scale;        // frame path: depth-key quantisation from the instance spheres (k_prep)
 };

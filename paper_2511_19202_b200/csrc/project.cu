@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256) k_tie_heads(const uint32_t *keys, const u
 constexpr int kTieRegs = 8;
 __global__ void k_tie_runs(sc_scene scene, const sc_survivor *surv, sc_camera cam, const uint32_t *keys, uint2 *pv,
                            const double *depth64, const unsigned long long *n_dev, int64_t n_host,
-                           const uint32_t *run_list, const Counters *ctr, sc_frame_stats *stats)
+                           const uint32_t *run_list, uint32_t *long_list, Counters *ctr, sc_frame_stats *stats)
 {
     const int64_t n = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
     const int64_t runs = (int64_t)ctr->tie_runs;
@@ -517,11 +517,15 @@ __global__ void k_tie_runs(sc_scene scene, const sc_survivor *surv, sc_camera ca
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < runs; r += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = run_list[r];
         const uint32_t key = keys[i];
+        if (i + kTieRegs < n && keys[i + kTieRegs] == key) {   // longer than kTieRegs: one CTA per run
+            long_list[atomicAdd(&ctr->tie_long, 1ull)] = (uint32_t)i;
+            continue;
+        }
         int64_t e = i + 1;
         while (e < n && keys[e] == key) e++;
         const int len = (int)(e - i);
         longest = max(longest, (unsigned long long)len);
-        if (len <= kTieRegs) {
+        {
             uint2 v[kTieRegs];
             double d[kTieRegs];
 #pragma unroll
@@ -546,7 +550,89 @@ __global__ void k_tie_runs(sc_scene scene, const sc_survivor *surv, sc_camera ca
 #pragma unroll
             for (int q = 0; q < kTieRegs; q++)
                 if (q < len) pv[i + q] = v[q];
-        } else {
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) longest = max(longest, __shfl_down_sync(0xffffffffu, longest, o));
+    if ((threadIdx.x & 31) == 0 && longest) atomicMax((unsigned long long *)&stats->max_tie_run, longest);
+}
+
+// pass 3: runs longer than kTieRegs, one CTA each: depths computed in parallel;
+// runs already in (depth, index) order (e.g. a planar asset facing the camera:
+// all depths equal) are left alone, others up to kTieSmem elements are
+// bitonic-sorted in shared memory, longer unsorted ones insertion-sorted by one
+// thread (never seen in practice).
+constexpr int kTieSmem = 2048;
+__global__ void __launch_bounds__(256) k_tie_long(sc_scene scene, const sc_survivor *surv, sc_camera cam,
+                                                  const uint32_t *keys, uint2 *pv, const double *depth64,
+                                                  const unsigned long long *n_dev, int64_t n_host,
+                                                  const uint32_t *long_list, const Counters *ctr, sc_frame_stats *stats)
+{
+    __shared__ double s_d[kTieSmem];
+    __shared__ uint2 s_v[kTieSmem];
+    __shared__ long long s_end;
+    __shared__ int s_unsorted;
+    const int64_t n = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
+    const int64_t runs = (int64_t)ctr->tie_long;
+    const int tid = threadIdx.x;
+    for (int64_t r = blockIdx.x; r < runs; r += gridDim.x) {
+        const int64_t i = long_list[r];
+        const uint32_t key = keys[i];
+        // run end: probe 256 positions per round
+        if (tid == 0) {
+            s_end = n;
+            s_unsorted = 0;
+        }
+        __syncthreads();
+        for (int64_t base = i + 1;; base += 256) {
+            const int64_t q = base + tid;
+            const bool stop = q >= n || keys[q] != key;
+            if (stop) atomicMin(&s_end, (long long)q);
+            if (__syncthreads_or(stop)) break;
+        }
+        const int64_t e = s_end;
+        const int64_t len = e - i;
+        // already ordered? (the run is in index order: ordered iff depths are non-decreasing)
+        for (int64_t a = i + 1 + tid; a < e; a += 256) {
+            const double d0 = tie_depth(scene, surv, cam, depth64, pv[a - 1].x);
+            const double d1 = tie_depth(scene, surv, cam, depth64, pv[a].x);
+            if (d1 < d0) s_unsorted = 1;
+        }
+        __syncthreads();
+        if (tid == 0) atomicMax((unsigned long long *)&stats->max_tie_run, (unsigned long long)len);
+        if (!s_unsorted) {
+            __syncthreads();
+            continue;
+        }
+        if (len <= kTieSmem) {
+            int p2 = 1;
+            while (p2 < len) p2 <<= 1;
+            for (int a = tid; a < p2; a += 256) {
+                if (a < len) {
+                    s_v[a] = pv[i + a];
+                    s_d[a] = tie_depth(scene, surv, cam, depth64, s_v[a].x);
+                } else {
+                    s_v[a] = make_uint2(0xFFFFFFFFu, 0u);
+                    s_d[a] = INFINITY;
+                }
+            }
+            __syncthreads();
+            for (int k = 2; k <= p2; k <<= 1)
+                for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                    for (int a = tid; a < p2; a += 256) {
+                        const int b = a ^ jj;
+                        if (b > a) {
+                            const bool up = (a & k) == 0;
+                            const bool gt = s_d[a] > s_d[b] || (s_d[a] == s_d[b] && s_v[a].x > s_v[b].x);
+                            if (gt == up) {
+                                const double td = s_d[a]; s_d[a] = s_d[b]; s_d[b] = td;
+                                const uint2 tv = s_v[a]; s_v[a] = s_v[b]; s_v[b] = tv;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (int a = tid; a < len; a += 256) pv[i + a] = s_v[a];
+        } else if (tid == 0) {
             for (int64_t a = i + 1; a < e; a++) {
                 const uint2 va = pv[a];
                 const double da = tie_depth(scene, surv, cam, depth64, va.x);
@@ -561,9 +647,8 @@ __global__ void k_tie_runs(sc_scene scene, const sc_survivor *surv, sc_camera ca
                 pv[b + 1] = va;
             }
         }
+        __syncthreads();
     }
-    for (int o = 16; o > 0; o >>= 1) longest = max(longest, __shfl_down_sync(0xffffffffu, longest, o));
-    if ((threadIdx.x & 31) == 0 && longest) atomicMax((unsigned long long *)&stats->max_tie_run, longest);
 }
 
 cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const sc_camera &cam, const uint32_t *keys,
@@ -577,8 +662,11 @@ cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const 
     const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 16);
     const int64_t hblocks = std::min<int64_t>((n_max + 2047) / 2048, (int64_t)nsm * 8);
     SC_LAUNCH(k_tie_heads, (int)std::max<int64_t>(1, hblocks), 256, 0, st, keys, n_dev, n_max, run_list, ctr);
+    // long runs go to the second half of the run-list buffer (runs <= n / 2 <= its half)
+    uint32_t *long_list = run_list + (n_max + 1) / 2;
     SC_LAUNCH(k_tie_runs, (int)std::max<int64_t>(1, blocks / 8), 256, 0, st, scene, surv, cam, keys, pv, depth64, n_dev,
-              n_max, run_list, ctr, stats);
+              n_max, run_list, long_list, ctr, stats);
+    SC_LAUNCH(k_tie_long, nsm * 2, 256, 0, st, scene, surv, cam, keys, pv, depth64, n_dev, n_max, long_list, ctr, stats);
     return cudaGetLastError();
 }
 

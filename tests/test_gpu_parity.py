@@ -449,3 +449,60 @@ def test_screen_bands_equal_whole_frame(view):
             assert torch.equal(band.image[y0:y1], img[y0:y1]), (bounds, b)
             assert torch.equal(band.trans[y0:y1], tr[y0:y1])
             assert bst.instantiated <= st.instantiated
+
+
+def _plane_asset(n, seed):
+    from paper_2511_19202_b200.asset import Asset
+
+    rng = np.random.default_rng(seed)
+    means = np.zeros((n, 3), np.float32)
+    means[:, :2] = rng.uniform(-1.0, 1.0, (n, 2))
+    q = np.zeros((n, 4), np.float32)
+    q[:, 0] = 1.0
+    return Asset(means=means, log_scales=np.full((n, 3), np.log(0.02), np.float32), rotations=q,
+                 opacity_logits=rng.normal(0.0, 1.5, n).astype(np.float32),
+                 sh_coeffs=rng.uniform(-1, 1, (n, 1, 3)).astype(np.float32), sh_degree=0)
+
+
+@pytest.mark.parametrize("tilt, n", [(2e-12, 1_500), (0.0, 60_000)], ids=["tilted-unsorted-run", "head-on-equal-run"])
+def test_long_depth_tie_runs(tilt, n):
+    """A plane facing the camera: every splat's depth key is equal (the frame
+    path quantises over the instance sphere), so the whole asset is one tie run.
+    Tilted by ~1e-12 the f64 depths differ and the run must be re-ordered
+    (CTA bitonic sort); head-on they are equal and the run stays in index order.
+    Image against the f64 oracle rendering the same splats."""
+    import paper_2511_19202_b200 as pkg
+    from paper_2511_19202_b200.camera import Camera
+    from paper_2511_19202_b200.scene import ComposedScene, InstanceTransform
+
+    asset = _plane_asset(n, seed=5)
+    sc = ComposedScene()
+    sc.add_asset(asset)
+    sc.add_instance(0, InstanceTransform())
+    cam = Camera.look_at((0.0, 0.0, 3.0), (tilt, 0.0, 0.0), math.radians(50.0), 96, 96, up=(0.0, 1.0, 0.0))
+    out, st = pkg.render_composed(sc, cam, use_mlp=False)
+    assert st.max_tie_run >= n // 2, st
+    ref = rr.render_arrays(asset.means, asset.log_scales, asset.rotations, asset.opacity_logits, asset.sh_coeffs,
+                           asset.sh_degree, cam)
+    _image_close(out.image, ref.image)
+
+
+def test_workspace_regrows_on_overflow():
+    """Capacities far below the frame's survivors / entries: the frame reports
+    overflow, the renderer grows the workspace and re-renders; the result equals
+    a render with ample capacity."""
+    import torch
+
+    from paper_2511_19202_b200.scene import RenderOptions, Renderer, Workspace
+    from paper_2511_19202_b200.workloads import config3
+
+    wl = config3(n_per=5_000, n_instances=100, width=320, height=180)
+    cam = wl.cameras[2]
+    big = Renderer(wl.scene)
+    ref, rst = big.render(cam, RenderOptions(), to_host=False)
+    small = Renderer(wl.scene)
+    small.workspaces[(cam.width, cam.height)] = Workspace(small.dscene, cam.width, cam.height, cap_s=1024, cap_e=4096)
+    got, gst = small.render(cam, RenderOptions(), to_host=False)
+    assert small.workspaces[(cam.width, cam.height)].cap_s >= gst.instantiated > 1024
+    assert gst.instantiated == rst.instantiated and gst.passed == rst.passed
+    assert torch.equal(got.image, ref.image)

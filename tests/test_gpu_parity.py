@@ -506,3 +506,24 @@ def test_workspace_regrows_on_overflow():
     assert small.workspaces[(cam.width, cam.height)].cap_s >= gst.instantiated > 1024
     assert gst.instantiated == rst.instantiated and gst.passed == rst.passed
     assert torch.equal(got.image, ref.image)
+
+
+@pytest.mark.parametrize("cam_i", [0, 2])
+def test_record_contributions_composed(cam_i):
+    """§8f rank 1 on a composed scene: per-splat max contribution, per-pixel
+    contribution sum and the used count (sc/_kernels.py:258-271,
+    sc/raster.py:264-273) against the oracle rendering the same survivors."""
+    import paper_2511_19202_b200 as pkg
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    cam = look_at(*CAMS[cam_i])
+    out, st = pkg.render_composed(sc, cam, record_contributions=True, return_survivors=True)
+    s = out.survivors
+    m, ls, q, op, sh, deg = sr.instantiate(sr.SceneTables(sc), cam, s[:, 0], s[:, 1])
+    ref = rr.render_arrays(m, ls, q, op, sh, deg, cam, record_contributions=True)
+    _image_close(out.image, ref.image)
+    np.testing.assert_allclose(out.contribution_max, ref.contribution_max, atol=IMG_MAX_ABS)
+    np.testing.assert_allclose(out.contribution_sum, ref.contribution_sum, atol=IMG_MAX_ABS)
+    assert abs(out.used_count - ref.used_count) <= max(2, int(0.002 * len(s)))
+    assert st.used == out.used_count

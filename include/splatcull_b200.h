@@ -21,6 +21,7 @@
  *   sc_blend            <- composite_tiles + finish()       sc/_kernels.py:168-275, sc/raster.py:267-282
  *   sc_vis_mlp_forward  <- nn.forward (16->32->32->1)
  *   sc_encode_features  <- nn.encode_features (14->32->32->6) SPEC.md:286-294
+ *   sc_visibility_labels_or <- sampling.visible_labels      sc/sampling.py:206-213
  *
  * Conventions
  *   - every pointer in the sc_* structs is DEVICE memory unless noted;
@@ -268,6 +269,14 @@ SC_API int sc_blend(const sc_splat *splats, const sc_window *windows, int64_t n_
 /* Batched visibility MLP on materialised inputs x [n][16] f32 -> logits [n]. */
 SC_API int sc_vis_mlp_forward(const sc_vis_weights *w, const float *x, int64_t n, float *logits,
                        void *stream);
+
+/* Visibility labels of one render (sc/sampling.py:206-213, visible_labels):
+ * label_bits[i / 32] |= (contrib_max[i] > 0) << (i % 32) for i < n, i.e. the
+ * OR over a view's main and auxiliary renders accumulates in place; the words
+ * read as bytes are numpy.packbits(labels, bitorder="little").  contrib_max is
+ * sc_frame_out.contrib_max of a record-mode render (survivor order = gaussian
+ * order for the single identity instance without culling). */
+SC_API int sc_visibility_labels_or(const float *contrib_max, int64_t n, uint32_t *label_bits, void *stream);
 
 /* Feature MLP 14->32->32->6: params f32 (W1,b1,W2,b2,W3,b3 row-major [out][in]),
  * inputs x [n][14] f32 -> features [n][8] fp16 (6 used, 2 zero). */

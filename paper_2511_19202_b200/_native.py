@@ -118,6 +118,7 @@ SIGNATURES = {
     "sc_blend": (c_i32, [P, P, c_i64, P, P, P, P, P, P]),
     "sc_vis_mlp_forward": (c_i32, [P, P, c_i64, P, P]),
     "sc_encode_features": (c_i32, [P, P, c_i64, P, P]),
+    "sc_visibility_labels_or": (c_i32, [P, c_i64, P, P]),
 }
 
 _lib = None

@@ -11,6 +11,7 @@
 namespace sc {
 cudaError_t launch_count_used(const float *cmax, const unsigned long long *n_dev, int64_t n_max,
                               sc_frame_stats *stats, cudaStream_t st);
+cudaError_t launch_labels_or(const float *cmax, int64_t n, uint32_t *bits, cudaStream_t st);
 }
 
 static thread_local std::string g_last_error;
@@ -319,6 +320,13 @@ int sc_vis_mlp_forward(const sc_vis_weights *w, const float *x, int64_t n, float
 {
     if (n < 0 || (n > 0 && (!w || !x || !logits))) return fail(SC_ERR_INVALID, "bad MLP forward arguments%s");
     SC_TRY(sc::launch_vis_mlp(w, x, n, logits, static_cast<cudaStream_t>(stream)), "vis mlp");
+    return SC_OK;
+}
+
+int sc_visibility_labels_or(const float *contrib_max, int64_t n, uint32_t *label_bits, void *stream)
+{
+    if (n < 0 || (n > 0 && (!contrib_max || !label_bits))) return fail(SC_ERR_INVALID, "bad label arguments%s");
+    SC_TRY(sc::launch_labels_or(contrib_max, n, label_bits, static_cast<cudaStream_t>(stream)), "labels");
     return SC_OK;
 }
 

@@ -510,6 +510,30 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
     return cudaGetLastError();
 }
 
+// Visibility labels (sc/sampling.py:206-213): bit i of the little-endian word
+// array |= (contribution_max[i] > 0); a warp packs 32 splats with one ballot.
+__global__ void k_labels_or(const float *cmax, int64_t n, uint32_t *bits)
+{
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < n;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + lane;
+        const uint32_t w = __ballot_sync(0xffffffffu, i < n && cmax[i] > 0.0f);
+        if (lane == 0 && w) bits[base >> 5] |= w;
+    }
+}
+
+cudaError_t launch_labels_or(const float *cmax, int64_t n, uint32_t *bits, cudaStream_t st)
+{
+    if (n <= 0) return cudaSuccess;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)nsm * 8));
+    SC_LAUNCH(k_labels_or, grid, 256, 0, st, cmax, n, bits);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_count_used(const float *cmax, const unsigned long long *n_dev, int64_t n_max,
                               sc_frame_stats *stats, cudaStream_t st)
 {

@@ -14,6 +14,8 @@ import tempfile
 
 import numpy as np
 
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")   # never write into /root/reference
+sys.dont_write_bytecode = True
 sys.path.insert(0, "/root/reference/pkg/src")
 import splatcull  # noqa: E402
 from splatcull import sampling, synth  # noqa: E402

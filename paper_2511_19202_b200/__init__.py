@@ -11,12 +11,13 @@ from .asset import (Asset, Gaussian, asset_hash, compute_sampling_distances, log
                     sigmoid, validate_asset)
 from .camera import Camera, diag_to_fov_y, fov_y_to_diag, train_focal
 from .nn import Mlp, VisibilityModel, encode_features, forward, init_mlp, make_model
+from .ply import load_ply, save_ply
 from .raster import RenderOutput, compute_metrics_pair, psnr, render, ssim
 from .scene import (ComposedScene, FrameStats, InstanceTransform, Renderer, RenderOptions, local_inputs,
                     render_composed)
 
 __all__ = [
-    "Asset", "Gaussian", "Camera", "RenderOutput", "asset_hash", "compute_metrics_pair",
+    "Asset", "Gaussian", "Camera", "RenderOutput", "asset_hash", "compute_metrics_pair", "load_ply", "save_ply",
     "compute_sampling_distances", "prepare", "prune", "recenter", "render", "sigmoid", "logit",
     "validate_asset", "diag_to_fov_y", "fov_y_to_diag", "train_focal", "psnr", "ssim",
     "Mlp", "VisibilityModel", "init_mlp", "make_model", "forward", "encode_features",

@@ -10,11 +10,12 @@ Importing the package needs no GPU; rendering does, and raises without one.
 from .asset import (Asset, Gaussian, asset_hash, compute_sampling_distances, logit, prepare, prune, recenter,
                     sigmoid, validate_asset)
 from .camera import Camera, diag_to_fov_y, fov_y_to_diag, train_focal
-from .nn import Mlp, VisibilityModel, encode_features, forward, init_mlp, make_model
+from .nn import Mlp, VisibilityModel, encode_features, forward, init_mlp, load_model, make_model, save_model
 from .ply import load_ply, save_ply
 from .raster import RenderOutput, compute_metrics_pair, psnr, render, ssim
 from .scene import (ComposedScene, FrameStats, InstanceTransform, Renderer, RenderOptions, local_inputs,
                     render_composed)
+from .training import TrainConfig, evaluate, grad_check, lr_at, train
 
 __all__ = [
     "Asset", "Gaussian", "Camera", "RenderOutput", "asset_hash", "compute_metrics_pair", "load_ply", "save_ply",
@@ -22,7 +23,7 @@ __all__ = [
     "validate_asset", "diag_to_fov_y", "fov_y_to_diag", "train_focal", "psnr", "ssim",
     "Mlp", "VisibilityModel", "init_mlp", "make_model", "forward", "encode_features",
     "ComposedScene", "InstanceTransform", "FrameStats", "RenderOptions", "Renderer", "render_composed",
-    "local_inputs",
+    "local_inputs", "save_model", "load_model", "TrainConfig", "train", "evaluate", "grad_check", "lr_at",
 ]
 
 __version__ = "0.1.0"

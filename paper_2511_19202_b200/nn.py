@@ -5,7 +5,8 @@ SPEC.md:240-323 (architecture, He-uniform init, 16-input layout, threshold)
 and PAPER.md:171-179 (16 inputs so the MLP maps onto tensor cores).  Weights
 live on the host as float32 (the SPEC checkpoint dtype); the device copies
 them to fp16 in shared memory (``sc_vis_mlp_forward`` / the fused cull
-kernel).  Training is offline and out of scope.
+kernel).  Training lives in train.py; checkpoints are
+``save_model`` / ``load_model`` below.
 
 Pinned decisions: hidden activations ReLU, feature
 output linear, visibility output a logit, keep iff logit >= logit(threshold).
@@ -13,7 +14,9 @@ output linear, visibility output a logit, keep iff logit >= logit(threshold).
 
 from __future__ import annotations
 
+import json
 import math
+import struct
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -162,3 +165,75 @@ def encode_features(model: VisibilityModel, asset: Asset) -> np.ndarray:
     from .scene import encode_features_device
 
     return encode_features_device(model, asset, "cuda")[:, :6].float().cpu().numpy()
+
+
+# Checkpoint: header, layer widths, float32 weights/biases (row-major (out, in)),
+# then the JSON meta.  SPEC.md nn.save_model: magic + version + normalisation
+# constants + layer dims + f32 weights, under 32 kB for the paper's sizes.
+MODEL_MAGIC = b"SCVM"
+MODEL_VERSION = 1
+_MODEL_HEADER = "<4sIQ?5dII"   # magic, version, asset hash, has hash, r, d_near, d_far, f_train, threshold, #feat, #vis
+
+
+def save_model(model: VisibilityModel, path) -> None:
+    fw, vw = model.feature_mlp.widths, model.vis_mlp.widths
+    meta = json.dumps(model.meta, sort_keys=True, default=float).encode()
+    with open(path, "wb") as fh:
+        fh.write(struct.pack(_MODEL_HEADER, MODEL_MAGIC, MODEL_VERSION, model.asset_hash or 0,
+                             model.asset_hash is not None, model.mean_scale, model.d_near, model.d_far,
+                             model.f_train, model.threshold, len(fw), len(vw)))
+        fh.write(struct.pack(f"<{len(fw) + len(vw)}I", *fw, *vw))
+        for mlp in (model.feature_mlp, model.vis_mlp):
+            for w, b in zip(mlp.weights, mlp.biases):
+                fh.write(np.ascontiguousarray(w, dtype="<f4").tobytes())
+                fh.write(np.ascontiguousarray(b, dtype="<f4").tobytes())
+        fh.write(struct.pack("<I", len(meta)))
+        fh.write(meta)
+
+
+def load_model(path) -> VisibilityModel:
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    hsize = struct.calcsize(_MODEL_HEADER)
+    if len(raw) < hsize:
+        raise ValueError(f"{path}: truncated model header")
+    magic, version, ahash, has_hash, r, dn, df, ft, thr, nf, nv = struct.unpack_from(_MODEL_HEADER, raw)
+    if magic != MODEL_MAGIC:
+        raise ValueError(f"{path}: bad magic {magic!r}")
+    if version != MODEL_VERSION:
+        raise ValueError(f"{path}: unsupported model version {version}")
+    if not (2 <= nf <= 16 and 2 <= nv <= 16):
+        raise ValueError(f"{path}: implausible layer counts {nf}, {nv}")
+    off = hsize
+    need = 4 * (nf + nv)
+    if len(raw) < off + need:
+        raise ValueError(f"{path}: truncated layer widths")
+    widths = struct.unpack_from(f"<{nf + nv}I", raw, off)
+    off += need
+
+    def read_mlp(ws):
+        nonlocal off
+        weights, biases = [], []
+        for fan_in, fan_out in zip(ws[:-1], ws[1:]):
+            for shape in ((fan_out, fan_in), (fan_out,)):
+                cnt = int(np.prod(shape))
+                if len(raw) < off + 4 * cnt:
+                    raise ValueError(f"{path}: truncated weights")
+                arr = np.frombuffer(raw, dtype="<f4", count=cnt, offset=off).reshape(shape).astype(np.float32)
+                (weights if len(shape) == 2 else biases).append(arr)
+                off += 4 * cnt
+        return Mlp(weights, biases)
+
+    feat, vis = read_mlp(widths[:nf]), read_mlp(widths[nf:])
+    if len(raw) < off + 4:
+        raise ValueError(f"{path}: truncated meta")
+    (mlen,) = struct.unpack_from("<I", raw, off)
+    off += 4
+    if len(raw) < off + mlen:
+        raise ValueError(f"{path}: truncated meta")
+    meta = json.loads(raw[off:off + mlen].decode()) if mlen else {}
+    for mlp in (feat, vis):
+        if not all(np.isfinite(a).all() for a in mlp.weights + mlp.biases):
+            raise ValueError(f"{path}: non-finite weights")
+    return VisibilityModel(feat, vis, r, dn, df, ft, threshold=thr, asset_hash=int(ahash) if has_hash else None,
+                           meta=meta)

@@ -1,0 +1,138 @@
+"""Scene-layout files and orbit_eval (SPEC.md scene module)."""
+
+import json
+import math
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+from paper_2511_19202_b200 import layout, nn, synth
+from paper_2511_19202_b200.asset import asset_hash, prepare
+from paper_2511_19202_b200.ply import save_ply
+from paper_2511_19202_b200.scene import ComposedScene, InstanceTransform
+
+CAM = {"position": [6.0, -4.0, 3.0], "target": [0.0, 0.0, 0.0], "fov_y_deg": 45.0, "width": 320, "height": 200}
+
+
+def _scene():
+    a0 = prepare(synth.make_shell(600, seed=1))
+    a1 = prepare(synth.make_slab_pair(300, 200, seed=2))
+    sc = ComposedScene()
+    sc.add_asset(a0, nn.make_model(a0, seed=3, output_bias=-2.0))
+    sc.add_asset(a1)
+    sc.add_instance(0, InstanceTransform([1.0, 2.0, 3.0], [0.5, 0.5, 0.5, 0.5], 1.5))
+    sc.add_instance(1, InstanceTransform())
+    sc.add_instance(0, InstanceTransform([-4.0, 0.0, 0.25], [1.0, 0.0, 0.0, 0.0], 0.5))
+    return sc
+
+
+def test_layout_roundtrip():
+    sc = _scene()
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "scene.json")
+        layout.save_scene(sc, path, camera=CAM)
+        back, cam = layout.load_scene(path)
+    assert len(back.assets) == 2 and back.n_instances == 3
+    for s0, s1 in zip(sc.assets, back.assets):
+        assert asset_hash(s0.asset) == asset_hash(s1.asset)
+        assert (s0.asset.d_near, s0.asset.d_far) == (s1.asset.d_near, s1.asset.d_far)
+        assert (s0.model is None) == (s1.model is None)
+        if s0.model is not None:
+            assert s1.model.asset_hash == asset_hash(s1.asset)
+            for x, y in zip(s0.model.vis_mlp.weights, s1.model.vis_mlp.weights):
+                np.testing.assert_array_equal(x, y)
+    for l0, l1 in zip(sc.instances, back.instances):
+        for t0, t1 in zip(l0, l1):
+            np.testing.assert_array_equal(t0.translation, t1.translation)
+            np.testing.assert_array_equal(t0.rotation, t1.rotation)
+            assert t0.scale == t1.scale
+    assert cam.width == 320 and cam.height == 200 and cam.fov_y == pytest.approx(math.radians(45.0))
+    np.testing.assert_array_equal(cam.position, CAM["position"])
+
+
+def test_layout_prepares_raw_ply():
+    raw = synth.make_shell(500, seed=5)
+    raw.means[:] += np.float32(3.0)
+    with tempfile.TemporaryDirectory() as d:
+        save_ply(raw, os.path.join(d, "a.ply"))
+        with open(os.path.join(d, "s.json"), "w") as fh:
+            json.dump({"assets": [{"id": "shell", "ply": "a.ply"}],
+                       "instances": [{"asset_id": "shell", "translation": [1, 2, 3]}]}, fh)
+        sc, cam = layout.load_scene(os.path.join(d, "s.json"))
+    ref = prepare(raw)
+    assert cam is None and sc.n_instances == 1
+    assert asset_hash(sc.assets[0].asset) == asset_hash(ref)
+    assert sc.assets[0].asset.d_near == ref.d_near
+
+
+@pytest.mark.parametrize("doc,match", [
+    ({"assets": []}, "non-empty"),
+    ({"assets": [{"id": 0}]}, "'id' and 'ply'"),
+    ({"assets": [{"id": 0, "ply": "a.ply"}, {"id": 0, "ply": "a.ply"}]}, "duplicate"),
+    ({"assets": [{"id": 0, "ply": "a.ply"}], "instances": [{"asset_id": 7}]}, "unknown asset"),
+    ({"assets": [{"id": 0, "ply": "a.ply"}], "instances": [{"asset_id": 0, "translation": [1, 2]}]}, "translation"),
+    ({"assets": [{"id": 0, "ply": "a.ply"}], "instances": [{"asset_id": 0, "scale": -1}]}, "scale"),
+])
+def test_layout_errors(doc, match):
+    with tempfile.TemporaryDirectory() as d:
+        save_ply(synth.make_shell(50, seed=0), os.path.join(d, "a.ply"))
+        p = os.path.join(d, "s.json")
+        with open(p, "w") as fh:
+            json.dump(doc, fh)
+        with pytest.raises(ValueError, match=match):
+            layout.load_scene(p)
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "s.json")
+        with open(p, "w") as fh:
+            fh.write("{not json")
+        with pytest.raises(ValueError, match="invalid JSON"):
+            layout.load_scene(p)
+
+
+def test_orbit_cameras_look_at_origin():
+    a = prepare(synth.make_shell(200, seed=0))
+    cams = layout.orbit_cameras(a, 8, 5.0, height_frac=0.5)
+    for c in cams:
+        np.testing.assert_allclose(np.linalg.norm(c.position[:2]), 5.0)
+        np.testing.assert_allclose(c.forward, -c.position / np.linalg.norm(c.position), atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_layout_roundtrip_renders_identically():
+    from paper_2511_19202_b200.camera import Camera
+    from paper_2511_19202_b200.scene import render_composed
+
+    sc = _scene()
+    cam = layout.camera_from_dict(CAM)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "scene.json")
+        layout.save_scene(sc, path)
+        back, _ = layout.load_scene(path)
+    assert isinstance(cam, Camera)
+    o0, s0 = render_composed(sc, cam)
+    o1, s1 = render_composed(back, cam)
+    np.testing.assert_array_equal(o0.image, o1.image)
+    assert s0.mlp_culled == s1.mlp_culled > 0
+
+
+@pytest.mark.gpu
+def test_orbit_eval_slab_trained_model():
+    """SPEC orbit_eval examples: all-visible model -> delta 0; slab asset with a
+    trained model, orbit above the front sheet -> delta_passed <= -40 % with the
+    used count kept (recall floor 0.98)."""
+    from paper_2511_19202_b200 import sampling, training
+
+    a = prepare(synth.make_slab_pair(20000, 20000, seed=3))
+    dist = 2.0 * a.d_near
+    allvis = nn.make_model(a, seed=0, output_bias=1e4)
+    ev = layout.orbit_eval(a, allvis, n_views=4, distance=dist, height_frac=0.8)
+    assert ev["delta_passed_pct"] == 0.0 and ev["used_ours"] == ev["used_gt"]
+
+    ds = sampling.extract_dataset(a, sampling.SamplingConfig(n_directions=256, n_distances=4, n_aux_views=2,
+                                                             image_size=256, seed=1))
+    model = training.train(ds, a, training.TrainConfig(iterations=3000, batch_size=1 << 15, seed=1))
+    ev = layout.orbit_eval(a, model, n_views=8, distance=dist, height_frac=0.8)
+    assert ev["delta_passed_pct"] <= -40.0, ev
+    assert ev["used_ours"] >= 0.98 * ev["used_gt"], ev

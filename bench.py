@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--frames-in-flight", type=int, default=2,
+                   help="frames rendered concurrently on separate streams (own workspaces); 1 = serial")
     return p.parse_args()
 
 
@@ -76,7 +78,9 @@ def describe(wl, args, n):
             "width": int(cam.width), "height": int(cam.height), "instances": wl.scene.n_instances,
             "instantiated_gaussians": wl.scene.n_instantiated, "views": len(wl.cameras),
             "mlp": "random-init 16->32->32->1 per asset, output bias calibrated to keep ~65% of uniform queries",
-            "l2": "flushed (256 MiB write) before every timed frame; flush excluded from the event timing",
+            "l2": "flushed (256 MiB write) before every timed frame (on the frame's stream; inside the timed "
+                  "region when frames are in flight, excluded from the serial pass's per-frame events)",
+            "frames_in_flight": 1 if args.shard == "bands" and n > 1 else args.frames_in_flight,
             "parallelism": (f"screen bands x{n} (P2P gather to rank 0)" if args.shard == "bands" else f"frames x{n}")
             if n > 1 else "single GPU"}
 
@@ -272,9 +276,43 @@ def main():
             r.render(cams[i], opts, to_host=False)
         torch.cuda.synchronize()
         dist.barrier()
+    F = max(1, args.frames_in_flight)
+    streams = [torch.cuda.Stream() for _ in range(F)]
+    pframes = [[None] * ncam for _ in range(F)]
+    if F > 1:   # size the extra slots' workspaces
+        for j in range(1, F):
+            for ci in range(ncam):
+                pframes[j][ci] = r.render_device(cams[ci], opts, slot=j)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def pipelined_pass():
+        """K frames, frame i on stream i % F with workspace slot i % F; one pair of events
+        around the whole pass on the main stream (device time, max over ranks later)."""
+        main_s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for st in streams:
+            st.wait_stream(main_s)
+        for i in range(K):
+            ci = (i + rank) % ncam
+            j = i % F
+            with torch.cuda.stream(streams[j]):
+                flush.fill_(i & 0xFF)
+                pframes[j][ci] = r.render_device(cams[ci], opts, out=pframes[j][ci], slot=j)
+        for st in streams:
+            main_s.wait_stream(st)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
     launches0 = lib.sc_kernel_launches()
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
+        pipe_ms = pipelined_pass() if (F > 1 and not bands) else None
+        pipe_launches = lib.sc_kernel_launches() - launches0
+        # serial pass (one frame in flight): per-frame and per-stage events bracket the kernels alone
         for i in range(K):
             ci = i % ncam if bands else (i + rank) % ncam
             flush.fill_(i & 0xFF)
@@ -298,7 +336,7 @@ def main():
                 ev_e[i].record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-    launches = lib.sc_kernel_launches() - launches0
+    launches = (pipe_launches if pipe_ms is not None else lib.sc_kernel_launches() - launches0)
     if dist:
         dist.barrier()
     dev_ms = [ev_s[i].elapsed_time(ev_e[i]) for i in range(K)]
@@ -308,15 +346,16 @@ def main():
         dev_ms = [float(x) for x in t]
     stage_ms = {name: [stage_ev[i][j].elapsed_time(stage_ev[i][j + 1]) for i in range(K)]
                 for j, name in enumerate(nat.STAGE_NAMES)}
-    total_ms = float(sum(dev_ms))
+    total_ms = float(sum(dev_ms))   # serial pass
     peak_gb = torch.cuda.max_memory_allocated() / 1e9
     stats = [nat.stats_dict(f.stats_raw.cpu().numpy()) if f is not None else None for f in frames]
     if any(s and s["overflow"] for s in stats):
         raise RuntimeError("workspace overflow inside the timed region")
     if dist:
-        t = torch.tensor([total_ms, peak_gb], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_ms, peak_gb, pipe_ms or 0.0], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, peak_gb = float(t[0]), float(t[1])
+        pipe_ms = float(t[2]) if pipe_ms is not None else None
     frames_done = K if bands else world * K   # bands: all ranks render each of the K frames together
 
     # ---------------- e2e through the public API ----------------
@@ -328,9 +367,14 @@ def main():
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
+        seq = [cams[(i + rank) % ncam] for i in range(ke)]
         t0 = time.perf_counter()
-        for i in range(ke):
-            out, fst = pkg.render_composed(wl.scene, cams[(i + rank) % ncam])
+        if F > 1:
+            for out, fst in pkg.render_path(wl.scene, seq, frames_in_flight=F):
+                pass
+        else:
+            for cam in seq:
+                out, fst = pkg.render_composed(wl.scene, cam)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         if dist:
@@ -341,7 +385,9 @@ def main():
         e2e = {"value": world * ke / e2e_s, "unit": "FPS",
                "h2d_bytes_per_step": 136 + 80,
                "d2h_bytes_per_step": h * w * 3 * 4 + h * w * 4 + nat.STATS_BYTES,
-               "api": "paper_2511_19202_b200.render_composed -> RenderOutput (numpy image + transmittance)"}
+               "api": (f"paper_2511_19202_b200.render_path(scene, cams, frames_in_flight={F}) -> RenderOutput per "
+                       "frame (numpy image + transmittance)") if F > 1 else
+                      "paper_2511_19202_b200.render_composed -> RenderOutput (numpy image + transmittance)"}
 
     if rank != 0:
         if dist:
@@ -380,7 +426,8 @@ def main():
     roof["traffic"] = tr.get("per_launch_bytes") if tr and tr.get("kernel") == "k_blend" else None
     t_roof = float(np.mean([sum(b for b, _ in a.values()) / (hbm * 1e9) + sum(f for _, f in a.values()) /
                             (tflops * 1e12) for a in alg]))
-    frame_roof = {"t_roof_ms": 1e3 * t_roof, "t_measured_ms": total_ms / K, "frac": 1e3 * t_roof / (total_ms / K)}
+    head_ms = pipe_ms if pipe_ms is not None else total_ms
+    frame_roof = {"t_roof_ms": 1e3 * t_roof, "t_measured_ms": head_ms / K, "frac": 1e3 * t_roof / (head_ms / K)}
 
     # ---------------- CPU oracle beside it: baseline + PSNR ----------------
     cpu = None
@@ -400,10 +447,12 @@ def main():
                    "frame": "far view of the CPU sample scene, each side with its own cull/MLP survivors",
                    "survivors_gpu": gst.instantiated, "survivors_cpu": ref.stats["instantiated"]}
 
-    value = frames_done / (total_ms / 1e3)
+    value = frames_done / (head_ms / 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": "FPS", "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "strong" if bands else "weak",
+        "ms_per_step": head_ms / K,
+        "serial": {"value": frames_done / (total_ms / 1e3), "ms_per_step": total_ms / K,
+                   "note": "one frame in flight; per_view_ms, stage_ms and the rooflines come from this pass"}, "higher_is_better": True, "scaling": "strong" if bands else "weak",
         "vs_baseline": None,
         "dtype": "f64 (cull, projection, keys) + fp16/f32 tensor-core MLP + fp32 blend",
         "data": "synthetic (seeded reference generators, random-init visibility MLPs)",

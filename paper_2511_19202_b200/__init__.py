@@ -15,7 +15,7 @@ from .layout import load_scene, orbit_eval, save_scene
 from .ply import load_ply, save_ply
 from .raster import RenderOutput, compute_metrics_pair, psnr, render, ssim
 from .scene import (ComposedScene, FrameStats, InstanceTransform, Renderer, RenderOptions, local_inputs,
-                    render_composed)
+                    render_composed, render_path)
 from .training import TrainConfig, evaluate, grad_check, lr_at, train
 
 __all__ = [
@@ -24,7 +24,7 @@ __all__ = [
     "validate_asset", "diag_to_fov_y", "fov_y_to_diag", "train_focal", "psnr", "ssim",
     "Mlp", "VisibilityModel", "init_mlp", "make_model", "forward", "encode_features",
     "ComposedScene", "InstanceTransform", "FrameStats", "RenderOptions", "Renderer", "render_composed",
-    "local_inputs", "save_model", "load_model", "TrainConfig", "train", "load_scene", "save_scene", "orbit_eval", "evaluate", "grad_check", "lr_at",
+    "local_inputs", "render_path", "save_model", "load_model", "TrainConfig", "train", "load_scene", "save_scene", "orbit_eval", "evaluate", "grad_check", "lr_at",
 ]
 
 __version__ = "0.1.0"

@@ -18,6 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsplatcull_b200.so")
 if os.environ.get("SPLATCULL_B200_DEBUG_LIB"):       # instrumented build (scripts/blend_stats.py only)
     LIB_PATH = os.path.join(_HERE, "libsplatcull_b200_dbg.so")
+if os.environ.get("SPLATCULL_B200_VARIANT"):         # A/B builds of kernel variants (scripts/ab_variants.py only)
+    LIB_PATH = os.path.abspath(os.environ["SPLATCULL_B200_VARIANT"])
 
 SC_OK = 0
 ABI_VERSION = 2   # include/splatcull_b200.h SC_ABI_VERSION

@@ -412,25 +412,30 @@ class Renderer:
         self.dscene = DeviceScene(scene, device)
         self.workspaces: dict[tuple[int, int], Workspace] = {}
 
-    def workspace(self, cam) -> Workspace:
-        key = (int(cam.width), int(cam.height))
+    def workspace(self, cam, slot: int = 0) -> Workspace:
+        """The workspace of this resolution (``slot`` > 0: one more per frame in flight)."""
+        key = (int(cam.width), int(cam.height)) + ((int(slot),) if slot else ())
         if key not in self.workspaces:
-            self.workspaces[key] = Workspace(self.dscene, *key)
+            base = self.workspaces.get(key[:2]) if slot else None   # extra slots start at slot 0's capacities
+            self.workspaces[key] = Workspace(self.dscene, int(cam.width), int(cam.height),
+                                             cap_s=base.cap_s if base else None, cap_e=base.cap_e if base else None)
         return self.workspaces[key]
 
     def render_device(self, cam, opts: RenderOptions | None = None, out: DeviceFrame | None = None,
-                      return_survivors: bool = False, stage_events=None) -> DeviceFrame:
+                      return_survivors: bool = False, stage_events=None, slot: int = 0) -> DeviceFrame:
         """Enqueue one frame on the current stream; no host synchronisation.
 
         ``stage_events``: optional 5 timing-enabled torch.cuda.Event objects,
         recorded by the library at the stage boundaries (frame start, after
-        cull+MLP, projection, sort/binning, blend).
+        cull+MLP, projection, sort/binning, blend).  ``slot``: which of the
+        per-frame-in-flight workspaces to use (frames rendered concurrently on
+        different streams need different slots).
         """
         import torch
 
         opts = opts or RenderOptions()
         lib = nat.load()
-        ws = self.workspace(cam)
+        ws = self.workspace(cam, slot)
         dev = self.dscene.device
         h, w = int(cam.height), int(cam.width)
         if out is None or out.image.shape != (h, w, 3):
@@ -517,6 +522,99 @@ class Renderer:
             out.survivors = frame.survivors[:n_s].cpu().numpy().astype(np.int64)
         return out, stats
 
+    def render_path(self, cams, opts: RenderOptions | None = None, frames_in_flight: int = 2,
+                    to_host: bool = True):
+        """Render a camera path; yields (RenderOutput, FrameStats) per camera, in order.
+
+        Frame i is rendered on stream i % F with its own workspace and output
+        buffers (F = ``frames_in_flight``), so the kernels of consecutive
+        frames overlap on the GPU and the device->host copies of frame i run
+        while frame i + 1 renders.  Each frame is bit-identical to
+        ``render(cam, opts)``.  ``to_host=False`` yields (DeviceFrame,
+        FrameStats); a DeviceFrame stays valid until F further frames have
+        been yielded.
+        """
+        import torch
+
+        from .raster import RenderOutput
+
+        opts = opts or RenderOptions()
+        F = max(1, int(frames_in_flight))
+        cams = list(cams)
+        main = torch.cuda.current_stream()
+        streams = [torch.cuda.Stream(device=self.dscene.device) for _ in range(F)]
+        frames: list[DeviceFrame | None] = [None] * F
+        pending: list[dict | None] = [None] * F
+
+        def launch(i):
+            slot = i % F
+            st = streams[slot]
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
+                frames[slot] = self.render_device(cams[i], opts, out=frames[slot], slot=slot)
+                ev1.record()
+                f = frames[slot]
+                host = {"stats": _to_pinned(f.stats_raw)}
+                if to_host:
+                    host["image"] = _to_pinned(f.image)
+                    host["trans"] = _to_pinned(f.trans)
+                    if opts.record_contributions:
+                        host["contrib_sum"] = _to_pinned(f.contrib_sum)
+                        host["contrib_max"] = _to_pinned(f.contrib_max)
+                done = torch.cuda.Event()
+                done.record()
+            pending[slot] = {"i": i, "ev0": ev0, "ev1": ev1, "host": host, "done": done}
+
+        def collect(i):
+            slot = i % F
+            p = pending[slot]
+            p["done"].synchronize()
+            st = nat.stats_dict(p["host"]["stats"].numpy())
+            if st["overflow"]:
+                # regrow this slot's workspace and re-render the frame on its stream
+                torch.cuda.synchronize()
+                self.workspace(cams[i], slot).grow(st["survivors"], max(st["entries"], st["block_entries"]))
+                launch(i)
+                return collect(i)
+            n_s = st["survivors"]
+            stats = FrameStats(frustum_passed=st["frustum_passed"], mlp_culled=st["mlp_culled"], instantiated=n_s,
+                               used=st["used"] if opts.record_contributions else None,
+                               mem_bytes_instantiated=self._payload_bytes_per_survivor(n_s, frames[slot], False),
+                               render_ms=float(p["ev0"].elapsed_time(p["ev1"])), mlp_ms=float("nan"),
+                               preprocess_ms=float("nan"), mlp_queried=st["mlp_queried"],
+                               instances_visible=st["instances_visible"], pairs_tested=st["pairs_tested"],
+                               passed=st["passed"], skipped=st["skipped"], entries=st["entries"],
+                               max_tie_run=st["max_tie_run"], block_entries=st["block_entries"],
+                               exact_fallbacks=st["exact_fallbacks"])
+            if not to_host:
+                return frames[slot], stats
+            h = p["host"]
+            rec = opts.record_contributions
+            out = RenderOutput(image=h["image"].numpy(), final_transmittance=h["trans"].numpy(),
+                               contribution_max=h["contrib_max"].numpy()[:n_s].copy() if rec else None,
+                               contribution_sum=h["contrib_sum"].numpy() if rec else None,
+                               used_count=st["used"] if rec else None,
+                               passed_count=st["passed"], skipped_count=st["skipped"])
+            return out, stats
+
+        for i in range(min(F, len(cams))):
+            launch(i)
+        for i in range(len(cams)):
+            res = collect(i)
+            if i + F < len(cams):
+                if not to_host:
+                    yield res          # the caller reads the device frame before its slot is reused
+                    launch(i + F)
+                    continue
+                launch(i + F)
+            yield res
+        main.wait_stream(streams[0])
+        for st in streams[1:]:
+            main.wait_stream(st)
+
     def _payload_bytes_per_survivor(self, n_s, frame, have_surv):
         # instantiated x per-gaussian Asset payload (56 B at SH degree 0, SPEC.md:339)
         pb = self.dscene.payload_bytes
@@ -546,6 +644,25 @@ def render_composed(scene: ComposedScene, cam, opts: RenderOptions | None = None
             raise ValueError("pass either opts or keyword options, not both")
         opts = RenderOptions(**kw)
     return r.render(cam, opts, return_survivors=return_survivors)
+
+
+def render_path(scene: ComposedScene, cams, opts: RenderOptions | None = None, *, frames_in_flight: int = 2,
+                **kw):
+    """Render a camera path -> iterator of (RenderOutput, FrameStats), frames overlapped on the GPU.
+
+    Same per-frame results as ``render_composed`` (bit-identical images);
+    ``frames_in_flight`` frames are in flight on separate streams, so one
+    frame's device->host copy and its kernels' tails overlap the next frame.
+    """
+    r = scene._device
+    if r is None or r.dscene.scene_version != scene._version:
+        r = Renderer(scene)
+        scene._device = r
+    if kw:
+        if opts is not None:
+            raise ValueError("pass either opts or keyword options, not both")
+        opts = RenderOptions(**kw)
+    return r.render_path(cams, opts, frames_in_flight=frames_in_flight)
 
 
 def local_inputs(g_index: int, asset: Asset, inst: InstanceTransform, cam, model: VisibilityModel,

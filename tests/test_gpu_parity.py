@@ -527,3 +527,44 @@ def test_record_contributions_composed(cam_i):
     np.testing.assert_allclose(out.contribution_sum, ref.contribution_sum, atol=IMG_MAX_ABS)
     assert abs(out.used_count - ref.used_count) <= max(2, int(0.002 * len(s)))
     assert st.used == out.used_count
+
+
+@pytest.mark.parametrize("frames_in_flight", [1, 2, 3])
+def test_render_path_matches_render(frames_in_flight):
+    """Frames in flight on separate streams / workspaces: every frame of the
+    path equals the one-frame-at-a-time render bit for bit (images,
+    transmittance, counters, contributions), including a frame whose slot
+    workspace overflows and is regrown mid-path."""
+    from paper_2511_19202_b200.scene import RenderOptions, Renderer, Workspace
+    from paper_2511_19202_b200.workloads import config3
+
+    wl = config3(n_per=4_000, n_instances=60, width=320, height=180)
+    cams = [wl.cameras[i % 3] for i in range(7)]
+    opts = RenderOptions(record_contributions=True)
+    ref = Renderer(wl.scene)
+    want = [ref.render(c, opts) for c in cams]
+    r = Renderer(wl.scene)
+    c0 = cams[0]
+    # slot 1 starts far too small: its first frame overflows and is re-rendered
+    r.workspaces[(c0.width, c0.height, 1)] = Workspace(r.dscene, c0.width, c0.height, cap_s=512, cap_e=2048)
+    got = list(r.render_path(cams, opts, frames_in_flight=frames_in_flight))
+    assert len(got) == len(want)
+    for (go, gs), (wo, ws) in zip(got, want):
+        np.testing.assert_array_equal(go.image, wo.image)
+        np.testing.assert_array_equal(go.final_transmittance, wo.final_transmittance)
+        np.testing.assert_array_equal(go.contribution_max, wo.contribution_max)
+        np.testing.assert_array_equal(go.contribution_sum, wo.contribution_sum)
+        assert (gs.instantiated, gs.passed, gs.entries, gs.used) == (ws.instantiated, ws.passed, ws.entries, ws.used)
+
+
+def test_render_path_public_api():
+    import paper_2511_19202_b200 as pkg
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    cams = [look_at(*c) for c in CAMS]
+    got = list(pkg.render_path(sc, cams, frames_in_flight=2))
+    for cam, (out, st) in zip(cams, got):
+        ref, rst = pkg.render_composed(sc, cam)
+        np.testing.assert_array_equal(out.image, ref.image)
+        assert st.instantiated == rst.instantiated

@@ -197,6 +197,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
 }
 
 constexpr unsigned long long kFlagAgg = 1ull << 32, kFlagPre = 2ull << 32;
+constexpr int kCullCbSmem = 1024;   // instance chunk_begin table cached in shared memory up to this many
 
 // ---------------------------------------------------------------------------
 // Cull + MLP.  Persistent CTAs of 128 threads take chunks of kChunk pairs of
@@ -206,19 +207,20 @@ constexpr unsigned long long kFlagAgg = 1ull << 32, kFlagPre = 2ull << 32;
 // into the smem A tile, tcgen05 MLP, survivor ballot into an smem list kept
 // in pair order.  The chunk's list is placed after its predecessors'.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera cam, sc_opts opts, Ws ws,
+__global__ void __launch_bounds__(kCullThreads, 8) k_cull(sc_scene scene, sc_camera cam, sc_opts opts, Ws ws,
                                                        sc_survivor *out, long long cap, sc_frame_stats *stats)
 {
     __shared__ MlpSmem sm;
     __shared__ sc_instance_rec s_in;
     __shared__ sc_asset_rec s_as;
     __shared__ InstFrame s_fr;
-    __shared__ sc_survivor s_surv[kChunk];
+    __shared__ uint16_t s_surv[kChunk];   // survivors of the chunk: offset from the chunk start
     constexpr int kCullWarps = kCullThreads / 32;
     static_assert(kCullTilesPerChunk * kCullWarps == 32, "one warp scans the chunk's segment counts");
     __shared__ uint32_t s_wcnt[kCullTilesPerChunk * kCullWarps];   // survivors per (tile, warp) segment
     __shared__ uint32_t s_segoff[kCullTilesPerChunk * kCullWarps];
     __shared__ uint32_t s_chunk, s_inst, s_prefix, s_nc;
+    __shared__ uint32_t s_cb[kCullCbSmem];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     mlp_setup(sm, tid);
@@ -232,23 +234,46 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
     const bool banded = opts.band_y1 > 0;
     const double BY0 = (double)band.y0, BY1 = (double)band.y1;   // whole image: [0, TH)
 
+    // chunk -> instance: binary search over the instances' chunk_begin, from a
+    // shared-memory copy when the instance table is small (one load per
+    // instance per CTA), else from global memory
+    const int64_t n_inst = scene.n_instances;
+    const bool cb_smem = n_inst <= kCullCbSmem;
+    if (cb_smem)
+        for (int64_t i = tid; i < n_inst; i += kCullThreads) s_cb[i] = ws.inst[i].chunk_begin;
+    // (a ticket is taken only when its chunk starts: the look-back of a chunk waits
+    // for its predecessors, which must all be in progress)
     for (;;) {
         if (tid == 0) s_chunk = (uint32_t)atomicAdd(&ws.ctr->chunk_ticket, 1ull);
         __syncthreads();
         const uint32_t chunk = s_chunk;
         if (chunk >= total) break;
         if (tid < kCullTilesPerChunk * kCullWarps) s_wcnt[tid] = 0;   // tiles past the chunk end stay empty
-        if (tid == 0) {
-            // last instance with chunk_begin <= chunk
-            int64_t lo = 0, hi = scene.n_instances;
-            while (hi - lo > 1) {
-                int64_t mid = (lo + hi) >> 1;
-                if (ws.inst[mid].chunk_begin <= chunk) lo = mid; else hi = mid;
+        if (wid == 0) {
+            // last instance with chunk_begin <= chunk (lane 0), then the warp copies the
+            // instance, its asset and its frame records word by word (two load latencies)
+            int64_t lo = 0;
+            if (lane == 0) {
+                int64_t hi = n_inst;
+                while (hi - lo > 1) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    const uint32_t cb = cb_smem ? s_cb[mid] : ws.inst[mid].chunk_begin;
+                    if (cb <= chunk) lo = mid; else hi = mid;
+                }
             }
-            s_inst = (uint32_t)lo;
-            s_in = scene.instances[lo];
-            s_as = scene.assets[s_in.asset];
-            s_fr = ws.inst[lo];
+            lo = __shfl_sync(0xffffffffu, lo, 0);
+            static_assert(sizeof(sc_instance_rec) % 4 == 0 && sizeof(sc_asset_rec) % 4 == 0 &&
+                              sizeof(InstFrame) % 4 == 0, "word copies");
+            const uint32_t *gi = reinterpret_cast<const uint32_t *>(scene.instances + lo);
+            const uint32_t *gf = reinterpret_cast<const uint32_t *>(ws.inst + lo);
+            uint32_t *si = reinterpret_cast<uint32_t *>(&s_in), *sf = reinterpret_cast<uint32_t *>(&s_fr);
+            for (int w = lane; w < (int)(sizeof(sc_instance_rec) / 4); w += 32) si[w] = gi[w];
+            for (int w = lane; w < (int)(sizeof(InstFrame) / 4); w += 32) sf[w] = gf[w];
+            const int asset = scene.instances[lo].asset;
+            const uint32_t *ga = reinterpret_cast<const uint32_t *>(scene.assets + asset);
+            uint32_t *sa = reinterpret_cast<uint32_t *>(&s_as);
+            for (int w = lane; w < (int)(sizeof(sc_asset_rec) / 4); w += 32) sa[w] = ga[w];
+            if (lane == 0) s_inst = (uint32_t)lo;
         }
         __syncthreads();
         const int model = (opts.use_mlp && s_as.model >= 0) ? s_as.model : -1;
@@ -343,12 +368,7 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
             n_cull += (pass && !keep);
             // warp-local ordered compaction: segment (t, w) of the chunk, no CTA barrier
             const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                sc_survivor sv;
-                sv.inst = inst_id;
-                sv.gid = (uint32_t)j;
-                s_surv[t * kCullThreads + wid * 32 + __popc(bal & lanemask_lt())] = sv;
-            }
+            if (keep) s_surv[t * kCullThreads + wid * 32 + __popc(bal & lanemask_lt())] = (uint16_t)(j - j0);
             if (lane == 0) s_wcnt[t * kCullWarps + wid] = __popc(bal);
         }
         // chunk order = (tile, warp)-major: scan the 32 segment counts (one warp)
@@ -399,7 +419,12 @@ __global__ void __launch_bounds__(kCullThreads) k_cull(sc_scene scene, sc_camera
             const int seg = t * kCullWarps + wid;
             if ((uint32_t)lane < s_wcnt[seg]) {
                 const long long pos = (long long)prefix + s_segoff[seg] + lane;
-                if (pos < cap) out[pos] = s_surv[t * kCullThreads + wid * 32 + lane];
+                if (pos < cap) {
+                    sc_survivor sv;
+                    sv.inst = s_inst;
+                    sv.gid = (uint32_t)(j0 + s_surv[t * kCullThreads + wid * 32 + lane]);
+                    out[pos] = sv;
+                }
             }
         }
     }

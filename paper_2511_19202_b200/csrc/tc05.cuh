@@ -129,7 +129,9 @@ struct __align__(128) MlpSmem {
     __align__(128) __half a2[128 * 32];
     __align__(128) __half w1[32 * 16];
     __align__(128) __half w2[32 * 32];
-    float b1[32], b2[32], w3[32];
+    __align__(16) float b1[32];
+    __align__(16) float b2[32];
+    __align__(16) float w3[32];
     float b3;
     uint32_t tmem_base;
     __align__(8) uint64_t bar;
@@ -165,6 +167,14 @@ __device__ __forceinline__ void mlp_store_row(MlpSmem &sm, int row, uint4 lo, ui
     base[8] = hi;        // k 8..15  (+128 bytes)
 }
 
+// (a, b) -> fp16x2 {lo = relu(a), hi = relu(b)}, round to nearest (cvt.rn.relu.f16x2.f32)
+__device__ __forceinline__ uint32_t pack_h2_relu(float a, float b)
+{
+    uint32_t r;
+    asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t pack_h2(float a, float b)
 {
     __half2 h = __floats2half2_rn(a, b);
@@ -197,11 +207,12 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
         uint4 *dst = reinterpret_cast<uint4 *>(sm.a2 + (tid >> 3) * 256 + (tid & 7) * 8);
 #pragma unroll
         for (int kc = 0; kc < 4; kc++) {
-            float h[8];
-#pragma unroll
-            for (int e = 0; e < 8; e++) h[e] = fmaxf(v[kc * 8 + e] + sm.b1[kc * 8 + e], 0.0f);
-            dst[kc * 8] = make_uint4(pack_h2(h[0], h[1]), pack_h2(h[2], h[3]), pack_h2(h[4], h[5]),
-                                     pack_h2(h[6], h[7]));
+            // relu(acc + b1) rounded to fp16: the relu rides the f32 -> f16x2 conversion
+            const float4 ba = reinterpret_cast<const float4 *>(sm.b1)[2 * kc];
+            const float4 bb = reinterpret_cast<const float4 *>(sm.b1)[2 * kc + 1];
+            const float *u = v + kc * 8;
+            dst[kc * 8] = make_uint4(pack_h2_relu(u[0] + ba.x, u[1] + ba.y), pack_h2_relu(u[2] + ba.z, u[3] + ba.w),
+                                     pack_h2_relu(u[4] + bb.x, u[5] + bb.y), pack_h2_relu(u[6] + bb.z, u[7] + bb.w));
         }
     }
     fence_async_smem();
@@ -220,7 +231,14 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
     tmem_ld32(sm.tmem_base + lane_sel + 32, v);
     float logit = sm.b3;
 #pragma unroll
-    for (int n = 0; n < 32; n++) logit += fmaxf(v[n] + sm.b2[n], 0.0f) * sm.w3[n];
+    for (int n4 = 0; n4 < 8; n4++) {
+        const float4 b = reinterpret_cast<const float4 *>(sm.b2)[n4];
+        const float4 w = reinterpret_cast<const float4 *>(sm.w3)[n4];
+        logit += fmaxf(v[4 * n4] + b.x, 0.0f) * w.x;
+        logit += fmaxf(v[4 * n4 + 1] + b.y, 0.0f) * w.y;
+        logit += fmaxf(v[4 * n4 + 2] + b.z, 0.0f) * w.z;
+        logit += fmaxf(v[4 * n4 + 3] + b.w, 0.0f) * w.w;
+    }
     tc_fence_before();
     *logit_out = logit;
     return true;

@@ -537,7 +537,10 @@ cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_op
 {
     cudaError_t e = cudaMemsetAsync(ws.chunk_state, 0, sizeof(unsigned long long) * (size_t)ws.max_chunks, st);
     if (e != cudaSuccess) return e;
-    const int grid = sm_count() * 8;   // 8 x 64 TMEM columns = the whole TMEM of an SM
+#ifndef SC_CULL_CPS
+#define SC_CULL_CPS 8
+#endif
+    const int grid = sm_count() * SC_CULL_CPS;   // 8 x 64 TMEM columns = the whole TMEM of an SM
     SC_LAUNCH(k_cull, grid, kCullThreads, 0, st, scene, cam, opts, ws, out, (long long)cap, stats);
     return cudaGetLastError();
 }

@@ -410,7 +410,10 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 8);
+#ifndef SC_PROJ_GRID
+#define SC_PROJ_GRID 8
+#endif
+    const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * SC_PROJ_GRID);
     if (opts.exact_projection) {
         SC_LAUNCH(k_project<kProjExact>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
                   depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, nullptr);

@@ -440,7 +440,10 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
                   shift, ws.rs_counts, ntiles);
         e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;
-        const int grid = (int)std::min<int64_t>(ntiles, (int64_t)nsm * 2);
+#ifndef SC_RADIX_CPS
+#define SC_RADIX_CPS 2
+#endif
+        const int grid = (int)std::min<int64_t>(ntiles, (int64_t)nsm * SC_RADIX_CPS);
         if (last_match_any && p == npass - 1)
             SC_LAUNCH((k_radix_down<V, true>), grid, kOsThreads, sizeof(OsSmem<V>), st, ki, vi, ko, vo, n_dev, n_max,
                       shift, ws.rs_counts, ntiles);

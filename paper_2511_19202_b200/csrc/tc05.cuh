@@ -129,8 +129,12 @@ struct __align__(128) MlpSmem {
     __align__(128) __half a2[128 * 32];
     __align__(128) __half w1[32 * 16];
     __align__(128) __half w2[32 * 32];
-    __align__(16) float b1[32];
-    __align__(16) float b2[32];
+    // biases ride the MMAs: D += ONES . BIAS^T with ONES rows (1, 1, 0, ..) (one 8-row core
+    // matrix pair read by every row group: SBO = 0) and BIAS rows (b_hi, b_lo, 0, ..), b_hi
+    // = fp16(b), b_lo = fp16(b - b_hi): the f32 bias to ~2^-22 relative
+    __align__(128) __half ones[8 * 16];
+    __align__(128) __half bias1[32 * 16];
+    __align__(128) __half bias2[32 * 16];
     __align__(16) float w3[32];
     float b3;
     uint32_t tmem_base;
@@ -151,11 +155,19 @@ __device__ __forceinline__ void mlp_load_weights(MlpSmem &sm, const sc_vis_weigh
     const __half *w2 = reinterpret_cast<const __half *>(w->w2);
     for (int i = tid; i < 32 * 16; i += nthreads) sm.w1[core_off(i >> 4, i & 15, 2)] = w1[i];
     for (int i = tid; i < 32 * 32; i += nthreads) sm.w2[core_off(i >> 5, i & 31, 4)] = w2[i];
-    for (int i = tid; i < 32; i += nthreads) {
-        sm.b1[i] = w->b1[i];
-        sm.b2[i] = w->b2[i];
-        sm.w3[i] = w->w3[i];
+    for (int i = tid; i < 32 * 16; i += nthreads) {
+        const int n = i >> 4, k = i & 15;
+        __half v1 = __float2half_rn(0.0f), v2 = v1;
+        if (k < 2) {
+            const float b1 = w->b1[n], b2 = w->b2[n];
+            const __half h1 = __float2half_rn(b1), h2 = __float2half_rn(b2);
+            v1 = k == 0 ? h1 : __float2half_rn(b1 - __half2float(h1));
+            v2 = k == 0 ? h2 : __float2half_rn(b2 - __half2float(h2));
+        }
+        sm.bias1[core_off(n, k, 2)] = v1;
+        sm.bias2[core_off(n, k, 2)] = v2;
     }
+    for (int i = tid; i < 32; i += nthreads) sm.w3[i] = w->w3[i];
     if (tid == 0) sm.b3 = w->b3;
 }
 
@@ -195,6 +207,8 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
         tc_fence_after();
         mma_f16_ss(sm.tmem_base, smem_desc(smem_u32(sm.a1), 128, 256), smem_desc(smem_u32(sm.w1), 128, 256),
                    kIdesc, 0);
+        mma_f16_ss(sm.tmem_base, smem_desc(smem_u32(sm.ones), 128, 0), smem_desc(smem_u32(sm.bias1), 128, 256),
+                   kIdesc, 1);
         mma_commit(&sm.bar);
     }
     mbar_wait(&sm.bar, phase);
@@ -207,12 +221,10 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
         uint4 *dst = reinterpret_cast<uint4 *>(sm.a2 + (tid >> 3) * 256 + (tid & 7) * 8);
 #pragma unroll
         for (int kc = 0; kc < 4; kc++) {
-            // relu(acc + b1) rounded to fp16: the relu rides the f32 -> f16x2 conversion
-            const float4 ba = reinterpret_cast<const float4 *>(sm.b1)[2 * kc];
-            const float4 bb = reinterpret_cast<const float4 *>(sm.b1)[2 * kc + 1];
+            // relu(acc) rounded to fp16 (the bias is in acc): the relu rides the f32 -> f16x2 conversion
             const float *u = v + kc * 8;
-            dst[kc * 8] = make_uint4(pack_h2_relu(u[0] + ba.x, u[1] + ba.y), pack_h2_relu(u[2] + ba.z, u[3] + ba.w),
-                                     pack_h2_relu(u[4] + bb.x, u[5] + bb.y), pack_h2_relu(u[6] + bb.z, u[7] + bb.w));
+            dst[kc * 8] = make_uint4(pack_h2_relu(u[0], u[1]), pack_h2_relu(u[2], u[3]), pack_h2_relu(u[4], u[5]),
+                                     pack_h2_relu(u[6], u[7]));
         }
     }
     fence_async_smem();
@@ -223,6 +235,8 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
         const uint32_t a2 = smem_u32(sm.a2), w2 = smem_u32(sm.w2);
         mma_f16_ss(sm.tmem_base + 32, smem_desc(a2, 128, 512), smem_desc(w2, 128, 512), kIdesc, 0);
         mma_f16_ss(sm.tmem_base + 32, smem_desc(a2 + 256, 128, 512), smem_desc(w2 + 256, 128, 512), kIdesc, 1);
+        mma_f16_ss(sm.tmem_base + 32, smem_desc(smem_u32(sm.ones), 128, 0), smem_desc(smem_u32(sm.bias2), 128, 256),
+                   kIdesc, 1);
         mma_commit(&sm.bar);
     }
     mbar_wait(&sm.bar, phase);
@@ -232,12 +246,11 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
     float logit = sm.b3;
 #pragma unroll
     for (int n4 = 0; n4 < 8; n4++) {
-        const float4 b = reinterpret_cast<const float4 *>(sm.b2)[n4];
         const float4 w = reinterpret_cast<const float4 *>(sm.w3)[n4];
-        logit += fmaxf(v[4 * n4] + b.x, 0.0f) * w.x;
-        logit += fmaxf(v[4 * n4 + 1] + b.y, 0.0f) * w.y;
-        logit += fmaxf(v[4 * n4 + 2] + b.z, 0.0f) * w.z;
-        logit += fmaxf(v[4 * n4 + 3] + b.w, 0.0f) * w.w;
+        logit += fmaxf(v[4 * n4], 0.0f) * w.x;
+        logit += fmaxf(v[4 * n4 + 1], 0.0f) * w.y;
+        logit += fmaxf(v[4 * n4 + 2], 0.0f) * w.z;
+        logit += fmaxf(v[4 * n4 + 3], 0.0f) * w.w;
     }
     tc_fence_before();
     *logit_out = logit;
@@ -248,6 +261,7 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
 __device__ __forceinline__ void mlp_setup(MlpSmem &sm, int tid)
 {
     if (tid < 32) tmem_alloc(&sm.tmem_base, kTmemCols);
+    for (int i = tid; i < 8 * 16; i += blockDim.x) sm.ones[i] = __float2half_rn((i & 7) < 2 && i < 64 ? 1.0f : 0.0f);
     if (tid == 0) {
         mbar_init(&sm.bar, 1);
         mbar_fence_init();

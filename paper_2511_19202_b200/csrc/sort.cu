@@ -567,22 +567,132 @@ __device__ __forceinline__ uint32_t block_count(int x0, int x1, int y0, int y1)
     return (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
 }
 
-__global__ void k_bentry_count(const uint2 *pv, const sc_window *wins, const unsigned long long *n_dev,
-                               int64_t n_host, int width, int height, uint32_t *cnt)
+__device__ __forceinline__ uint32_t bentry_count(uint2 v, const sc_window *wins, int width, int height)
 {
+    int x0, x1, y0, y1;
+    return unpack_window(v.y, v.x, wins, width, height, x0, x1, y0, y1) ? block_count(x0, x1, y0, y1) : 0u;
+}
+
+// Emission tiles: kEmitTile consecutive passed splats (depth order) per CTA
+// iteration, warp w owning the contiguous kEmitPerWarp splats [w * 512, w * 512
+// + 512) of the tile.  Pass 1 writes per-tile entry totals, one exclusive scan
+// turns them into tile offsets, pass 2 recounts (the tile's payloads are in L1)
+// and emits: no per-splat count array round trip through HBM.
+constexpr int kEmitThreads = 256;
+constexpr int kEmitTile = 4096;
+constexpr int kEmitPerWarp = kEmitTile / (kEmitThreads / 32);
+
+__global__ void __launch_bounds__(kEmitThreads) k_bentry_tiles(const uint2 *__restrict__ pv, const sc_window *wins,
+                                                               const unsigned long long *n_dev, int64_t n_host,
+                                                               int64_t ntiles_max, int width, int height,
+                                                               uint32_t *tile_tot)
+{
+    __shared__ uint32_t s_w[kEmitThreads / 32];
     const int64_t n = dev_count(n_dev, n_host);
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const uint2 v = pv[k];
-        int x0, x1, y0, y1;
-        cnt[k] = unpack_window(v.y, v.x, wins, width, height, x0, x1, y0, y1) ? block_count(x0, x1, y0, y1) : 0u;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t = blockIdx.x; t < ntiles_max; t += gridDim.x) {
+        uint32_t c = 0;
+        const int64_t base = t * kEmitTile;
+        if (base < n) {
+#pragma unroll 4
+            for (int j = 0; j < kEmitTile / kEmitThreads; j++) {
+                const int64_t k = base + (int64_t)j * kEmitThreads + threadIdx.x;
+                if (k < n) c += bentry_count(__ldg(pv + k), wins, width, height);
+            }
+        }
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) s_w[wid] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < kEmitThreads / 32; w++) tot += s_w[w];
+            tile_tot[t] = tot;
+        }
+        __syncthreads();
     }
 }
 
-__global__ void k_bentry_emit(const uint2 *pv, const sc_window *wins, const uint32_t *off,
-                              const unsigned long long *n_dev, int64_t n_host, int width, int height, int n_tx,
-                              uint32_t *ekey, uint32_t *eval, const unsigned long long *e_total,
-                              unsigned long long *e_eff, int64_t cap_e, sc_frame_stats *stats)
+// one warp: the (contiguous) entries of 32 consecutive passed splats, starting
+// at output obase; returns their total
+__device__ __forceinline__ uint32_t emit_group(uint2 cv, bool valid, uint32_t obase, const sc_window *wins, int width,
+                                               int height, int n_tx, uint32_t *ekey, uint32_t *eval, int lane)
 {
+    // Warp-cooperative, load-balanced: lane l produces output o = step + l; the
+    // owning splat is found by an upper-bound search over the warp's exclusive
+    // counts (5 shuffles).  Splats covering thousands of blocks (close to the
+    // camera) do not serialise one thread, and the stores are coalesced.
+    int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
+    uint32_t sv = 0, cnt = 0;
+    if (valid) {
+        sv = cv.x;
+        if (unpack_window(cv.y, cv.x, wins, width, height, x0, x1, y0, y1)) cnt = block_count(x0, x1, y0, y1);
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
+        if (lane >= s) incl += y;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (__reduce_max_sync(0xffffffffu, cnt) <= 16u) {
+        // small splats (the common case): each lane writes its own entries, row by row;
+        // the warp's outputs are one contiguous range, so the stores stay within a few lines
+        uint32_t o = obase + excl;
+        if (cnt) {
+            for (int by = y0 / 4; by <= y1 / 4; by++) {
+                const int ry0 = max(y0 - 4 * by, 0), ry1 = min(y1 - 4 * by, 3);
+                const uint32_t row = (uint32_t)(((by >> 2) * n_tx) * 8 + (by & 3) * 2);
+                for (int bx = x0 / 8; bx <= x1 / 8; bx++) {
+                    const int rx0 = max(x0 - 8 * bx, 0), rx1 = min(x1 - 8 * bx, 7);
+                    const uint32_t id = row + (uint32_t)((bx >> 1) * 8 + (bx & 1));
+                    ekey[o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
+                    eval[o] = sv;
+                    o++;
+                }
+            }
+        }
+        return total;
+    }
+    for (uint32_t o0 = 0; o0 < total; o0 += 32) {
+        const uint32_t o = o0 + lane;
+        int s = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, excl, s + step);
+            if (e <= o) s += step;
+        }
+        const uint32_t li = o - __shfl_sync(0xffffffffu, excl, s);
+        const int X0 = __shfl_sync(0xffffffffu, x0, s), X1 = __shfl_sync(0xffffffffu, x1, s);
+        const int Y0 = __shfl_sync(0xffffffffu, y0, s), Y1 = __shfl_sync(0xffffffffu, y1, s);
+        const uint32_t v = __shfl_sync(0xffffffffu, sv, s);
+        if (o < total) {
+            const int w = X1 / 8 - X0 / 8 + 1;
+            // li / w without an integer division (li < 2^24: one correction step is exact)
+            int qy = (int)((float)li * __frcp_rn((float)w));
+            int rx = (int)li - qy * w;
+            if (rx < 0) { qy--; rx += w; } else if (rx >= w) { qy++; rx -= w; }
+            const int bx = X0 / 8 + rx, by = Y0 / 4 + qy;
+            const int rx0 = max(X0 - 8 * bx, 0), rx1 = min(X1 - 8 * bx, 7);
+            const int ry0 = max(Y0 - 4 * by, 0), ry1 = min(Y1 - 4 * by, 3);
+            const uint32_t id = (uint32_t)(((by >> 2) * n_tx + (bx >> 1)) * 8 + (by & 3) * 2 + (bx & 1));
+            ekey[obase + o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
+            eval[obase + o] = v;
+        }
+    }
+    return total;
+}
+
+__global__ void __launch_bounds__(kEmitThreads) k_bentry_emit(const uint2 *__restrict__ pv, const sc_window *wins,
+                                                              const uint32_t *tile_off, const unsigned long long *n_dev,
+                                                              int64_t n_host, int width, int height, int n_tx,
+                                                              uint32_t *ekey, uint32_t *eval,
+                                                              const unsigned long long *e_total,
+                                                              unsigned long long *e_eff, int64_t cap_e,
+                                                              sc_frame_stats *stats)
+{
+    __shared__ uint32_t s_w[kEmitThreads / 32];
     const int64_t n = dev_count(n_dev, n_host);
     const bool over = (int64_t)*e_total > cap_e;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -591,120 +701,49 @@ __global__ void k_bentry_emit(const uint2 *pv, const sc_window *wins, const uint
         if (over) atomicOr((unsigned long long *)&stats->overflow, 2ull);
     }
     if (over) return;
-    // Warp-cooperative, load-balanced: a warp owns 32 consecutive splats and
-    // emits their (contiguous) entries 32 at a time, lane l producing output
-    // o = step + l; the owning splat is found by an upper-bound search over the
-    // warp's exclusive counts (5 shuffles).  Splats covering thousands of
-    // blocks (close to the camera) no longer serialise one thread, and the
-    // stores are coalesced.
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    // one iteration ahead: the next 32 payloads and their output base are in flight
-    int64_t base = warp * 32;
-    uint2 nv = make_uint2(0u, kWinEmpty);
-    uint32_t noff = 0;
-    if (base < n) {
-        if (base + lane < n) nv = pv[base + lane];
-        noff = off[base];
-    }
-    for (; base < n; base += n_warps * 32) {
-        const int64_t k = base + lane;
-        const uint2 cv = nv;
-        const uint32_t obase = noff;
-        const int64_t nb = base + n_warps * 32;
-        if (nb < n) {
-            nv = nb + lane < n ? pv[nb + lane] : make_uint2(0u, kWinEmpty);
-            noff = off[nb];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t ntiles = (n + kEmitTile - 1) / kEmitTile;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t wbase = t * kEmitTile + (int64_t)wid * kEmitPerWarp;
+        // recount this warp's splats -> the warp's base inside the tile
+        uint32_t c = 0;
+#pragma unroll 4
+        for (int r = 0; r < kEmitPerWarp / 32; r++) {
+            const int64_t k = wbase + r * 32 + lane;
+            if (k < n) c += bentry_count(__ldg(pv + k), wins, width, height);
         }
-        int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
-        uint32_t sv = 0, cnt = 0;
-        if (k < n) {
-            sv = cv.x;
-            if (unpack_window(cv.y, cv.x, wins, width, height, x0, x1, y0, y1)) cnt = block_count(x0, x1, y0, y1);
-        }
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int s = 1; s < 32; s <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
-            if (lane >= s) incl += y;
-        }
-        const uint32_t excl = incl - cnt;
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        if (__reduce_max_sync(0xffffffffu, cnt) <= 16u) {
-            // small splats (the common case): each lane writes its own entries, row by row;
-            // the warp's outputs are one contiguous range, so the stores stay within a few lines
-            uint32_t o = obase + excl;
-            if (cnt) {
-                for (int by = y0 / 4; by <= y1 / 4; by++) {
-                    const int ry0 = max(y0 - 4 * by, 0), ry1 = min(y1 - 4 * by, 3);
-                    const uint32_t row = (uint32_t)(((by >> 2) * n_tx) * 8 + (by & 3) * 2);
-                    for (int bx = x0 / 8; bx <= x1 / 8; bx++) {
-                        const int rx0 = max(x0 - 8 * bx, 0), rx1 = min(x1 - 8 * bx, 7);
-                        const uint32_t id = row + (uint32_t)((bx >> 1) * 8 + (bx & 1));
-                        ekey[o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
-                        eval[o] = sv;
-                        o++;
-                    }
-                }
-            }
-            continue;
-        }
-        for (uint32_t o0 = 0; o0 < total; o0 += 32) {
-            const uint32_t o = o0 + lane;
-            int s = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint32_t e = __shfl_sync(0xffffffffu, excl, s + step);
-                if (e <= o) s += step;
-            }
-            const uint32_t li = o - __shfl_sync(0xffffffffu, excl, s);
-            const int X0 = __shfl_sync(0xffffffffu, x0, s), X1 = __shfl_sync(0xffffffffu, x1, s);
-            const int Y0 = __shfl_sync(0xffffffffu, y0, s), Y1 = __shfl_sync(0xffffffffu, y1, s);
-            const uint32_t v = __shfl_sync(0xffffffffu, sv, s);
-            if (o < total) {
-                const int w = X1 / 8 - X0 / 8 + 1;
-                // li / w without an integer division (li < 2^24: one correction step is exact)
-                int qy = (int)((float)li * __frcp_rn((float)w));
-                int rx = (int)li - qy * w;
-                if (rx < 0) { qy--; rx += w; } else if (rx >= w) { qy++; rx -= w; }
-                const int bx = X0 / 8 + rx, by = Y0 / 4 + qy;
-                const int rx0 = max(X0 - 8 * bx, 0), rx1 = min(X1 - 8 * bx, 7);
-                const int ry0 = max(Y0 - 4 * by, 0), ry1 = min(Y1 - 4 * by, 3);
-                const uint32_t id = (uint32_t)(((by >> 2) * n_tx + (bx >> 1)) * 8 + (by & 3) * 2 + (bx & 1));
-                ekey[obase + o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
-                eval[obase + o] = v;
-            }
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) s_w[wid] = c;
+        __syncthreads();
+        uint32_t o = tile_off[t];
+        for (int w = 0; w < wid; w++) o += s_w[w];
+        __syncthreads();
+        for (int r = 0; r < kEmitPerWarp / 32; r++) {
+            const int64_t g0 = wbase + r * 32;
+            if (g0 >= n) break;
+            const int64_t k = g0 + lane;
+            const uint2 cv = k < n ? __ldg(pv + k) : make_uint2(0u, kWinEmpty);
+            o += emit_group(cv, k < n, o, wins, width, height, n_tx, ekey, eval, lane);
         }
     }
 }
 
-// boff[b] = first entry with block id >= b, for b in [0, n_blocks]; thread
-// handles 4 consecutive entries (one uint4 load)
-__global__ void k_block_offsets(const uint32_t *ekey, const unsigned long long *e_dev, int64_t cap_e,
+// boff[b] = first entry with block id >= b, for b in [0, n_blocks]: one thread
+// per block, binary search over the sorted keys (~log2 E dependent loads whose
+// upper levels are shared through L1/L2): ~32 B per probe instead of a full read
+// of the E keys.
+__global__ void k_block_offsets(const uint32_t *__restrict__ ekey, const unsigned long long *e_dev, int64_t cap_e,
                                 int64_t n_blocks, uint32_t *boff)
 {
     const int64_t E = std::min<int64_t>((int64_t)*e_dev, cap_e);
-    const int64_t nq = E / 4 + 1;   // quads covering [0, E]
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i0 = 4 * q;
-        uint32_t kv[4];
-        if (i0 + 4 <= E) {
-            const uint4 x = __ldcs(reinterpret_cast<const uint4 *>(ekey) + q);
-            kv[0] = x.x; kv[1] = x.y; kv[2] = x.z; kv[3] = x.w;
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; j++) kv[j] = i0 + j < E ? ekey[i0 + j] : 0u;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= n_blocks;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = E;   // first i in [0, E] with block(i) >= b
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)(__ldg(ekey + mid) >> kCodeBits) < b) lo = mid + 1; else hi = mid;
         }
-        int64_t prev = i0 > 0 ? (int64_t)(ekey[i0 - 1] >> kCodeBits) : -1;
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int64_t i = i0 + j;
-            if (i > E) break;
-            const int64_t cur = i < E ? (int64_t)(kv[j] >> kCodeBits) : n_blocks;
-            for (int64_t t = prev + 1; t <= cur; t++) boff[t] = (uint32_t)i;
-            prev = cur;
-        }
+        boff[b] = (uint32_t)lo;
     }
 }
 
@@ -745,11 +784,14 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
     if (e != cudaSuccess) return e;
     uint32_t *ek = nullptr, *ev = nullptr;
     if (blocks) {
-        SC_LAUNCH(k_bentry_count, grid_for(n_max, 256), 256, 0, st, pv_s, wins, p_dev, n_max, cam.width, cam.height,
+        // per-tile entry totals (ws.ecount, free after the tie-fix) -> tile offsets -> emission
+        const int64_t etiles = std::max<int64_t>(1, (n_max + kEmitTile - 1) / kEmitTile);
+        const int egrid = (int)std::min<int64_t>(etiles, (int64_t)sm_count_sort() * 8);
+        SC_LAUNCH(k_bentry_tiles, egrid, kEmitThreads, 0, st, pv_s, wins, p_dev, n_max, etiles, cam.width, cam.height,
                   ws.ecount);
-        e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, nullptr, st);
+        e = scan_excl(ws.ecount, ws.ecount, nullptr, etiles, ws.scan_part, &ws.ctr->entries, nullptr, st);
         if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_bentry_emit, grid_for(n_max, 256), 256, 0, st, pv_s, wins, ws.ecount, p_dev, n_max, cam.width,
+        SC_LAUNCH(k_bentry_emit, egrid, kEmitThreads, 0, st, pv_s, wins, ws.ecount, p_dev, n_max, cam.width,
                   cam.height, ws.n_tx, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
         const int64_t n_blocks = 8 * ws.n_tiles;
         // last pass (block-id high byte ~ screen rows, which follow depth order): few distinct
@@ -757,8 +799,8 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
         e = radix_sort<uint32_t>(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, kCodeBits,
                                  kCodeBits + bits_for(n_blocks), ws, &ek, &ev, st, true);
         if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_block_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE, n_blocks,
-                  ws.boff);
+        SC_LAUNCH(k_block_offsets, (int)((n_blocks + 1 + 255) / 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE,
+                  n_blocks, ws.boff);
         if (order_out) *order_out = nullptr;
     } else {
         // free after the tie-fix: both key buffers and the other payload buffer

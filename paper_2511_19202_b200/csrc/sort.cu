@@ -16,6 +16,7 @@
 // Every kernel reads its element count from device memory, so the whole
 // frame stays asynchronous (and CUDA-graph capturable).
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -173,14 +174,22 @@ static_assert(kOsTile == kRadixTile, "matrix sizing in api.cu assumes kRadixTile
 
 // lanes of the warp holding the same 8-bit digit: 8 ballots, constant cost
 // (match.any's cost grows with the number of distinct values in the warp)
+// per bit: predicate straight from the digit, ballot, sign mask, one 3-input
+// logic op (m &= ~(ballot ^ mask)): 4 instructions
 __device__ __forceinline__ uint32_t match_digit8(uint32_t d)
 {
     uint32_t m = 0xffffffffu;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
-        const uint32_t bit = (d >> b) & 1u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-        m &= bit ? bal : ~bal;
+        uint32_t bal, sm;
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %2, %3;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+            "selp.b32 %1, -1, 0, p;\n\t}"
+            : "=r"(bal), "=r"(sm)
+            : "r"(d), "r"(1u << b));
+        m &= ~(bal ^ sm);
     }
     return m;
 }
@@ -328,29 +337,40 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
 
         // stable warp-private ranking: warp w owns the contiguous slice
         // [w * 256, (w + 1) * 256) and keeps running per-digit counts
-        uint32_t k[kOsItems], rk[kOsItems], peers[kOsItems];
+        uint32_t k[kOsItems], rk[kOsItems];
         V v[kOsItems];
+        auto rank = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;   // no bounds checks on full tiles
+            uint32_t peers[kOsItems];
 #pragma unroll
-        for (int j = 0; j < kOsItems; j++) {
-            const int i = wid * kPerWarp + j * 32 + lane;
-            k[j] = sm.in_k[b][i];
-            v[j] = sm.in_v[b][i];
-            if constexpr (MATCH_ANY)
-                peers[j] = __match_any_sync(0xffffffffu, i < cnt ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane);
-            else
-                peers[j] = match_digit8((k[j] >> shift) & 0xFFu) & __ballot_sync(0xffffffffu, i < cnt);
-        }
+            for (int j = 0; j < kOsItems; j++) {
+                const int i = wid * kPerWarp + j * 32 + lane;
+                k[j] = sm.in_k[b][i];
+                v[j] = sm.in_v[b][i];
+                const bool ok = FULL || i < cnt;
+                if constexpr (MATCH_ANY)
+                    peers[j] = __match_any_sync(0xffffffffu, ok ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane);
+                else if constexpr (FULL)
+                    peers[j] = match_digit8((k[j] >> shift) & 0xFFu);
+                else
+                    peers[j] = match_digit8((k[j] >> shift) & 0xFFu) & __ballot_sync(0xffffffffu, ok);
+            }
 #pragma unroll
-        for (int j = 0; j < kOsItems; j++) {
-            const bool ok = wid * kPerWarp + j * 32 + lane < cnt;
-            const uint32_t d = (k[j] >> shift) & 0xFFu;
-            const uint32_t r = __popc(peers[j] & lt);
-            const uint32_t prev = ok ? sm.wcnt[wid][d] : 0u;
-            __syncwarp();
-            if (ok && r == 0) sm.wcnt[wid][d] = (uint16_t)(prev + __popc(peers[j]));
-            __syncwarp();
-            rk[j] = prev + r;
-        }
+            for (int j = 0; j < kOsItems; j++) {
+                const bool ok = FULL || wid * kPerWarp + j * 32 + lane < cnt;
+                const uint32_t d = (k[j] >> shift) & 0xFFu;
+                const uint32_t r = __popc(peers[j] & lt);
+                const uint32_t prev = ok ? sm.wcnt[wid][d] : 0u;
+                __syncwarp();
+                if (ok && r == 0) sm.wcnt[wid][d] = (uint16_t)(prev + __popc(peers[j]));
+                __syncwarp();
+                rk[j] = prev + r;
+            }
+        };
+        if (cnt == kOsTile)
+            rank(std::true_type{});
+        else
+            rank(std::false_type{});
         __syncthreads();
         uint32_t tot = 0;
         if (tid < 256) {   // thread = digit: exclusive prefix over warps

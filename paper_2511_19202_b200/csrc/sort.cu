@@ -293,8 +293,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
     extern __shared__ __align__(128) uint4 s_dyn4[];
     OsSmem<V> &sm = *reinterpret_cast<OsSmem<V> *>(s_dyn4);
     __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ uint32_t s_dstart[256];   // tile-local start of each digit
-    __shared__ uint32_t s_gbase[256];    // global scatter base of each digit
+    __shared__ uint32_t s_gofs[256];     // global scatter base - tile-local start of each digit
     __shared__ uint32_t s_warp[32];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -372,27 +371,36 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
         else
             rank(std::false_type{});
         __syncthreads();
+        // thread = digit: its per-warp counts, the tile-local digit start (block scan), then
+        // wcnt[w][d] = digit start + exclusive prefix over warps (the scatter base of warp w)
+        uint32_t wc[kOsWarps];
         uint32_t tot = 0;
-        if (tid < 256) {   // thread = digit: exclusive prefix over warps
+        if (tid < 256) {
 #pragma unroll
             for (int w = 0; w < kOsWarps; w++) {
-                const uint32_t c = sm.wcnt[w][tid];
-                sm.wcnt[w][tid] = (uint16_t)tot;
-                tot += c;
+                wc[w] = sm.wcnt[w][tid];
+                tot += wc[w];
             }
-            s_gbase[tid] = gb;
         }
         {
             uint32_t total;
             const uint32_t ds = block_excl_scan<kOsThreads>(tid < 256 ? tot : 0u, s_warp, total);
-            if (tid < 256) s_dstart[tid] = ds;
+            if (tid < 256) {
+                uint32_t run = ds;
+#pragma unroll
+                for (int w = 0; w < kOsWarps; w++) {
+                    sm.wcnt[w][tid] = (uint16_t)run;
+                    run += wc[w];
+                }
+                s_gofs[tid] = gb - ds;   // output index = s_gofs[d] + tile position (mod 2^32)
+            }
         }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kOsItems; j++) {
             if (wid * kPerWarp + j * 32 + lane < cnt) {
                 const uint32_t d = (k[j] >> shift) & 0xFFu;
-                const uint32_t pos = s_dstart[d] + sm.wcnt[wid][d] + rk[j];
+                const uint32_t pos = sm.wcnt[wid][d] + rk[j];
                 sm.in_k[b][pos] = k[j];
                 sm.in_v[b][pos] = v[j];
             }
@@ -402,8 +410,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
 #pragma unroll 4
         for (int i = tid; i < cnt; i += kOsThreads) {
             const uint32_t key = sm.in_k[b][i];
-            const uint32_t d = (key >> shift) & 0xFFu;
-            const uint32_t dst = s_gbase[d] + (uint32_t)i - s_dstart[d];
+            const uint32_t dst = s_gofs[(key >> shift) & 0xFFu] + (uint32_t)i;
             keys_out[dst] = key;
             vals_out[dst] = sm.in_v[b][i];
         }

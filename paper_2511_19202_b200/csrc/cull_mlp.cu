@@ -197,7 +197,10 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
 }
 
 constexpr unsigned long long kFlagAgg = 1ull << 32, kFlagPre = 2ull << 32;
-constexpr int kCullCbSmem = 1024;   // instance chunk_begin table cached in shared memory up to this many
+#ifndef SC_CULL_CB
+#define SC_CULL_CB 0
+#endif
+constexpr int kCullCbSmem = SC_CULL_CB;   // instance chunk_begin table cached in shared memory up to this many
 
 // ---------------------------------------------------------------------------
 // Cull + MLP.  Persistent CTAs of 128 threads take chunks of kChunk pairs of
@@ -207,7 +210,10 @@ constexpr int kCullCbSmem = 1024;   // instance chunk_begin table cached in shar
 // into the smem A tile, tcgen05 MLP, survivor ballot into an smem list kept
 // in pair order.  The chunk's list is placed after its predecessors'.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCullThreads, 8) k_cull(sc_scene scene, sc_camera cam, sc_opts opts, Ws ws,
+#ifndef SC_CULL_CPS
+#define SC_CULL_CPS 12
+#endif
+__global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene scene, sc_camera cam, sc_opts opts, Ws ws,
                                                        sc_survivor *out, long long cap, sc_frame_stats *stats)
 {
     __shared__ MlpSmem sm;
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(kCullThreads, 8) k_cull(sc_scene scene, sc_cam
     __shared__ uint32_t s_wcnt[kCullTilesPerChunk * kCullWarps];   // survivors per (tile, warp) segment
     __shared__ uint32_t s_segoff[kCullTilesPerChunk * kCullWarps];
     __shared__ uint32_t s_chunk, s_inst, s_prefix, s_nc;
-    __shared__ uint32_t s_cb[kCullCbSmem];
+    __shared__ uint32_t s_cb[kCullCbSmem > 0 ? kCullCbSmem : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     mlp_setup(sm, tid);
@@ -537,10 +543,7 @@ cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_op
 {
     cudaError_t e = cudaMemsetAsync(ws.chunk_state, 0, sizeof(unsigned long long) * (size_t)ws.max_chunks, st);
     if (e != cudaSuccess) return e;
-#ifndef SC_CULL_CPS
-#define SC_CULL_CPS 8
-#endif
-    const int grid = sm_count() * SC_CULL_CPS;   // 8 x 64 TMEM columns = the whole TMEM of an SM
+    const int grid = sm_count() * SC_CULL_CPS;   // CTAs per SM (32 TMEM columns each)
     SC_LAUNCH(k_cull, grid, kCullThreads, 0, st, scene, cam, opts, ws, out, (long long)cap, stats);
     return cudaGetLastError();
 }

@@ -115,6 +115,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v)
     for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 consecutive columns (fewer live registers than x32: the cull kernel runs
+// 12 CTAs per SM)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v)
+{
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
+}
+
 // ---------------------------------------------------------------------------
 // Fused MLP tile: 128 rows x 16 fp16 inputs -> logit per row.
 //   layer 1: D1[128x32] = A1[128x16] . W1^T        (1 MMA, K = 16)   TMEM cols [0, 32)
@@ -125,8 +141,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v)
 //   byte(r, k) = (r / 8) * (KC * 128) + (k / 8) * 128 + (r % 8) * 16 + (k % 8) * 2
 // ---------------------------------------------------------------------------
 struct __align__(128) MlpSmem {
-    __align__(128) __half a1[128 * 16];
-    __align__(128) __half a2[128 * 32];
+    // a1 (layer-1 input) and a2 (layer-2 input) share storage: MMA 1 has completed
+    // before a2 is written, MMA 2 before the next tile's a1 is
+    union {
+        __align__(128) __half a1[128 * 16];
+        __align__(128) __half a2[128 * 32];
+    };
     __align__(128) __half w1[32 * 16];
     __align__(128) __half w2[32 * 32];
     // biases ride the MMAs: D += ONES . BIAS^T with ONES rows (1, 1, 0, ..) (one 8-row core
@@ -141,7 +161,7 @@ struct __align__(128) MlpSmem {
     __align__(8) uint64_t bar;
 };
 
-constexpr uint32_t kTmemCols = 64;
+constexpr uint32_t kTmemCols = 32;   // D1, then D2 in the same columns (D1 is read out before MMA 2)
 
 __device__ __forceinline__ int core_off(int r, int k, int kc_total)
 {
@@ -215,16 +235,19 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
     phase ^= 1u;
     tc_fence_after();
     const uint32_t lane_sel = (uint32_t)(tid & ~31) << 16;
-    float v[32];
-    tmem_ld32(sm.tmem_base + lane_sel, v);
+    float v[16];
     {
         uint4 *dst = reinterpret_cast<uint4 *>(sm.a2 + (tid >> 3) * 256 + (tid & 7) * 8);
 #pragma unroll
-        for (int kc = 0; kc < 4; kc++) {
-            // relu(acc) rounded to fp16 (the bias is in acc): the relu rides the f32 -> f16x2 conversion
-            const float *u = v + kc * 8;
-            dst[kc * 8] = make_uint4(pack_h2_relu(u[0], u[1]), pack_h2_relu(u[2], u[3]), pack_h2_relu(u[4], u[5]),
-                                     pack_h2_relu(u[6], u[7]));
+        for (int half = 0; half < 2; half++) {
+            tmem_ld16(sm.tmem_base + lane_sel + 16 * half, v);
+#pragma unroll
+            for (int kc = 0; kc < 2; kc++) {
+                // relu(acc) rounded to fp16 (the bias is in acc): the relu rides the f32 -> f16x2 conversion
+                const float *u = v + kc * 8;
+                dst[(2 * half + kc) * 8] = make_uint4(pack_h2_relu(u[0], u[1]), pack_h2_relu(u[2], u[3]),
+                                                      pack_h2_relu(u[4], u[5]), pack_h2_relu(u[6], u[7]));
+            }
         }
     }
     fence_async_smem();
@@ -233,24 +256,27 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
     if (tid == 0) {
         tc_fence_after();
         const uint32_t a2 = smem_u32(sm.a2), w2 = smem_u32(sm.w2);
-        mma_f16_ss(sm.tmem_base + 32, smem_desc(a2, 128, 512), smem_desc(w2, 128, 512), kIdesc, 0);
-        mma_f16_ss(sm.tmem_base + 32, smem_desc(a2 + 256, 128, 512), smem_desc(w2 + 256, 128, 512), kIdesc, 1);
-        mma_f16_ss(sm.tmem_base + 32, smem_desc(smem_u32(sm.ones), 128, 0), smem_desc(smem_u32(sm.bias2), 128, 256),
+        mma_f16_ss(sm.tmem_base, smem_desc(a2, 128, 512), smem_desc(w2, 128, 512), kIdesc, 0);
+        mma_f16_ss(sm.tmem_base, smem_desc(a2 + 256, 128, 512), smem_desc(w2 + 256, 128, 512), kIdesc, 1);
+        mma_f16_ss(sm.tmem_base, smem_desc(smem_u32(sm.ones), 128, 0), smem_desc(smem_u32(sm.bias2), 128, 256),
                    kIdesc, 1);
         mma_commit(&sm.bar);
     }
     mbar_wait(&sm.bar, phase);
     phase ^= 1u;
     tc_fence_after();
-    tmem_ld32(sm.tmem_base + lane_sel + 32, v);
     float logit = sm.b3;
 #pragma unroll
-    for (int n4 = 0; n4 < 8; n4++) {
-        const float4 w = reinterpret_cast<const float4 *>(sm.w3)[n4];
-        logit += fmaxf(v[4 * n4], 0.0f) * w.x;
-        logit += fmaxf(v[4 * n4 + 1], 0.0f) * w.y;
-        logit += fmaxf(v[4 * n4 + 2], 0.0f) * w.z;
-        logit += fmaxf(v[4 * n4 + 3], 0.0f) * w.w;
+    for (int half = 0; half < 2; half++) {
+        tmem_ld16(sm.tmem_base + lane_sel + 16 * half, v);
+#pragma unroll
+        for (int n4 = 0; n4 < 4; n4++) {
+            const float4 w = reinterpret_cast<const float4 *>(sm.w3)[4 * half + n4];
+            logit += fmaxf(v[4 * n4], 0.0f) * w.x;
+            logit += fmaxf(v[4 * n4 + 1], 0.0f) * w.y;
+            logit += fmaxf(v[4 * n4 + 2], 0.0f) * w.z;
+            logit += fmaxf(v[4 * n4 + 3], 0.0f) * w.w;
+        }
     }
     tc_fence_before();
     *logit_out = logit;

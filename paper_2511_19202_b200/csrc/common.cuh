@@ -68,6 +68,10 @@ struct Counters {
     unsigned long long tie_long;       // ... of which longer than 8 (one CTA each)
     unsigned long long proj_deferred;  // splats the f32 projection left to the exact kernel
     double key_dmin, key_scale;        // frame path: depth-key quantisation from the instance spheres (k_prep)
+    // dynamic tile tickets of the radix up/downsweeps (zero between launches: the last
+    // CTA to finish resets them), so a sweep sharing the GPU with another stream's
+    // kernels does not wait on CTAs that are not resident yet
+    unsigned long long rs_next, rs_done;
 };
 
 // Workspace carve-out (all offsets 256-byte aligned), see api.cu:carve().

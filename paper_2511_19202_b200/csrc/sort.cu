@@ -227,16 +227,35 @@ __device__ __forceinline__ void os_bulk_load(uint64_t *bar, void *dk, const void
                  : "memory");
 }
 
+// Tile tickets: tiles are handed out in order by an atomic counter; each CTA
+// ends by taking one ticket past the end; the last CTA to finish resets the
+// pair for the next sweep (kernels on a stream run one after the other).
+__device__ __forceinline__ void ticket_release(unsigned long long *next, unsigned long long *done)
+{
+    __threadfence();
+    if (atomicAdd(done, 1ull) == (unsigned long long)gridDim.x - 1) {
+        *next = 0;
+        *done = 0;
+        __threadfence();
+    }
+}
+
 // Upsweep: warp-private shared histograms (plain shared atomics, no ranking),
 // keys loaded 4 per thread per load (uint4, streaming).
 __global__ void __launch_bounds__(kOsThreads) k_radix_up(const uint32_t *__restrict__ keys,
                                                          const unsigned long long *n_dev, int64_t n_host, int shift,
-                                                         uint32_t *counts, int64_t ntiles_max)
+                                                         uint32_t *counts, int64_t ntiles_max,
+                                                         unsigned long long *tk_next, unsigned long long *tk_done)
 {
     __shared__ uint32_t h[kOsWarps][256];
+    __shared__ int64_t s_t;
     const int tid = threadIdx.x, wid = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host);
-    for (int64_t t = blockIdx.x; t < ntiles_max; t += gridDim.x) {
+    for (;;) {
+        if (tid == 0) s_t = (int64_t)atomicAdd(tk_next, 1ull);
+        __syncthreads();
+        const int64_t t = s_t;
+        if (t >= ntiles_max) break;
         for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&h[0][0])[i] = 0;
         __syncthreads();
         const int64_t base = t * kOsTile;
@@ -267,6 +286,7 @@ __global__ void __launch_bounds__(kOsThreads) k_radix_up(const uint32_t *__restr
         }
         __syncthreads();
     }
+    if (tid == 0) ticket_release(tk_next, tk_done);
 }
 
 // (the ranked tile is staged back into its own input buffer for the write-out)
@@ -287,7 +307,8 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
                                                               V *__restrict__ vals_out,
                                                               const unsigned long long *n_dev, int64_t n_host,
                                                               int shift, const uint32_t *__restrict__ bases,
-                                                              int64_t ntiles_max)
+                                                              int64_t ntiles_max, unsigned long long *tk_next,
+                                                              unsigned long long *tk_done)
 {
     constexpr int kPerWarp = kOsTile / kOsWarps;
     extern __shared__ __align__(128) uint4 s_dyn4[];
@@ -306,20 +327,25 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
         os_bulk_load(&s_bar[b], sm.in_k[b], keys_in + base, (c * 4u + 15u) & ~15u, sm.in_v[b], vals_in + base,
                      (c * (uint32_t)sizeof(V) + 15u) & ~15u);
     };
-    int64_t tile = blockIdx.x;
-    if (tile >= ntiles) return;
+    __shared__ int64_t s_tile;
     if (tid == 0) {
         os_mbar_init(&s_bar[0]);
         os_mbar_init(&s_bar[1]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        issue(tile, 0);
+        s_tile = (int64_t)atomicAdd(tk_next, 1ull);
+        if (s_tile < ntiles) issue(s_tile, 0);
     }
+    __syncthreads();
+    int64_t tile = s_tile;
     uint32_t phase0 = 0, phase1 = 0;
     int b = 0;
     const uint32_t lt = lanemask_lt();
-    for (; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();   // buffer b^1 (previous tile) fully written out
-        if (tid == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, b ^ 1);
+    while (tile < ntiles) {
+        __syncthreads();   // buffer b^1 (previous tile) fully written out; s_tile read by all
+        if (tid == 0) {   // the next tile's ticket and its TMA load, one tile ahead
+            s_tile = (int64_t)atomicAdd(tk_next, 1ull);
+            if (s_tile < ntiles) issue(s_tile, b ^ 1);
+        }
         for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&sm.wcnt[0][0])[i] = 0;
         uint32_t gb = 0;
         if (tid < 256) gb = bases[(int64_t)tid * ntiles_max + tile];
@@ -417,7 +443,9 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
         // generic-proxy writes to buffer b above; its next refill is a TMA (async-proxy) write
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         b ^= 1;
+        tile = s_tile;   // written by thread 0 before the tile's barriers
     }
+    if (tid == 0) ticket_release(tk_next, tk_done);
 }
 
 template <typename V>
@@ -464,7 +492,7 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
     for (int p = 0; p < npass; p++) {
         const int shift = bit_lo + 8 * p;
         SC_LAUNCH(k_radix_up, (int)std::min<int64_t>(ntiles, (int64_t)nsm * 4), kOsThreads, 0, st, ki, n_dev, n_max,
-                  shift, ws.rs_counts, ntiles);
+                  shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
         e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;
 #ifndef SC_RADIX_CPS
@@ -473,10 +501,10 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
         const int grid = (int)std::min<int64_t>(ntiles, (int64_t)nsm * SC_RADIX_CPS);
         if (last_match_any && p == npass - 1)
             SC_LAUNCH((k_radix_down<V, true>), grid, kOsThreads, sizeof(OsSmem<V>), st, ki, vi, ko, vo, n_dev, n_max,
-                      shift, ws.rs_counts, ntiles);
+                      shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
         else
             SC_LAUNCH((k_radix_down<V, false>), grid, kOsThreads, sizeof(OsSmem<V>), st, ki, vi, ko, vo, n_dev, n_max,
-                      shift, ws.rs_counts, ntiles);
+                      shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
         std::swap(ki, ko);
         std::swap(vi, vo);
     }

@@ -279,8 +279,8 @@ def main():
     F = max(1, args.frames_in_flight)
     streams = [torch.cuda.Stream() for _ in range(F)]
     pframes = [[None] * ncam for _ in range(F)]
-    if F > 1:   # size the extra slots' workspaces
-        for j in range(1, F):
+    if F > 1:   # size the extra slots' workspaces, allocate every slot's outputs
+        for j in range(F):
             for ci in range(ncam):
                 pframes[j][ci] = r.render_device(cams[ci], opts, slot=j)
         torch.cuda.synchronize()
@@ -307,6 +307,10 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
 
+    if F > 1 and not bands:   # untimed warm-up of the pipelined schedule itself
+        K_t, K = K, max(args.warmup, F)
+        pipelined_pass()
+        K = K_t
     launches0 = lib.sc_kernel_launches()
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
@@ -368,6 +372,10 @@ def main():
         if dist:
             dist.barrier()
         seq = [cams[(i + rank) % ncam] for i in range(ke)]
+        if F > 1:   # warm the path API (its streams, output frames and pinned host buffers)
+            for _ in pkg.render_path(wl.scene, seq[:2 * F], frames_in_flight=F):
+                pass
+            torch.cuda.synchronize()
         t0 = time.perf_counter()
         if F > 1:
             for out, fst in pkg.render_path(wl.scene, seq, frames_in_flight=F):

@@ -28,6 +28,8 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -395,11 +397,43 @@ class DeviceFrame:
     survivors: "torch.Tensor | None" = None
 
 
-def _to_pinned(t):
-    """Asynchronous device->host copy into a pinned tensor (caller synchronises)."""
-    import torch
+class _PinnedPool:
+    """Pinned host buffers for the per-frame device->host copies, recycled once
+    the numpy arrays handed out over them are garbage-collected (a fresh
+    pinned allocation of a 1080p image costs ~1.5 ms of host time, about what
+    the frame's GPU work leaves the host per frame)."""
 
-    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    def __init__(self):
+        self._free: dict = {}
+        self._lock = threading.Lock()
+
+    def take(self, shape, dtype):
+        import torch
+
+        key = (tuple(shape), dtype)
+        with self._lock:
+            lst = self._free.get(key)
+            if lst:
+                return lst.pop()
+        return torch.empty(tuple(shape), dtype=dtype, pin_memory=True)
+
+    def give(self, t) -> None:
+        with self._lock:
+            self._free.setdefault((tuple(t.shape), t.dtype), []).append(t)
+
+    def numpy(self, t):
+        """numpy view of pinned ``t``; ``t`` returns to the pool when the view is collected."""
+        a = t.numpy()
+        weakref.finalize(a, self.give, t)
+        return a
+
+
+_PINNED = _PinnedPool()
+
+
+def _to_pinned(t):
+    """Asynchronous device->host copy into a pooled pinned tensor (caller synchronises)."""
+    h = _PINNED.take(t.shape, t.dtype)
     h.copy_(t, non_blocking=True)
     return h
 
@@ -411,6 +445,8 @@ class Renderer:
         self.scene = scene
         self.dscene = DeviceScene(scene, device)
         self.workspaces: dict[tuple[int, int], Workspace] = {}
+        self._path_streams: list = []
+        self._path_frames: dict = {}
 
     def workspace(self, cam, slot: int = 0) -> Workspace:
         """The workspace of this resolution (``slot`` > 0: one more per frame in flight)."""
@@ -492,6 +528,7 @@ class Renderer:
                 host["trans"] = _to_pinned(frame.trans)
             torch.cuda.current_stream().synchronize()
             st = nat.stats_dict(host["stats"].numpy())
+            _PINNED.give(host["stats"])
             if not st["overflow"]:
                 break
             # the frame path bins (splat, 8x4 block) pairs: block_entries of them
@@ -512,8 +549,8 @@ class Renderer:
         if not to_host:
             return frame, stats
         out = RenderOutput(
-            image=host["image"].numpy(),
-            final_transmittance=host["trans"].numpy(),
+            image=_PINNED.numpy(host["image"]),
+            final_transmittance=_PINNED.numpy(host["trans"]),
             contribution_max=frame.contrib_max[:n_s].cpu().numpy() if opts.record_contributions else None,
             contribution_sum=frame.contrib_sum.cpu().numpy() if opts.record_contributions else None,
             used_count=st["used"] if opts.record_contributions else None,
@@ -542,8 +579,12 @@ class Renderer:
         F = max(1, int(frames_in_flight))
         cams = list(cams)
         main = torch.cuda.current_stream()
-        streams = [torch.cuda.Stream(device=self.dscene.device) for _ in range(F)]
-        frames: list[DeviceFrame | None] = [None] * F
+        # streams and per-slot output frames persist across calls: a new stream's first
+        # allocations would be fresh cudaMallocs (device-synchronising) inside the path
+        while len(self._path_streams) < F:
+            self._path_streams.append(torch.cuda.Stream(device=self.dscene.device))
+        streams = self._path_streams[:F]
+        frames: list[DeviceFrame | None] = [self._path_frames.get(j) for j in range(F)]
         pending: list[dict | None] = [None] * F
 
         def launch(i):
@@ -557,6 +598,7 @@ class Renderer:
                 frames[slot] = self.render_device(cams[i], opts, out=frames[slot], slot=slot)
                 ev1.record()
                 f = frames[slot]
+                self._path_frames[slot] = f
                 host = {"stats": _to_pinned(f.stats_raw)}
                 if to_host:
                     host["image"] = _to_pinned(f.image)
@@ -573,6 +615,7 @@ class Renderer:
             p = pending[slot]
             p["done"].synchronize()
             st = nat.stats_dict(p["host"]["stats"].numpy())
+            _PINNED.give(p["host"]["stats"])
             if st["overflow"]:
                 # regrow this slot's workspace and re-render the frame on its stream
                 torch.cuda.synchronize()
@@ -593,9 +636,13 @@ class Renderer:
                 return frames[slot], stats
             h = p["host"]
             rec = opts.record_contributions
-            out = RenderOutput(image=h["image"].numpy(), final_transmittance=h["trans"].numpy(),
-                               contribution_max=h["contrib_max"].numpy()[:n_s].copy() if rec else None,
-                               contribution_sum=h["contrib_sum"].numpy() if rec else None,
+            cmax = None
+            if rec:
+                cmax = h["contrib_max"].numpy()[:n_s].copy()
+                _PINNED.give(h["contrib_max"])
+            out = RenderOutput(image=_PINNED.numpy(h["image"]), final_transmittance=_PINNED.numpy(h["trans"]),
+                               contribution_max=cmax,
+                               contribution_sum=_PINNED.numpy(h["contrib_sum"]) if rec else None,
                                used_count=st["used"] if rec else None,
                                passed_count=st["passed"], skipped_count=st["skipped"])
             return out, stats

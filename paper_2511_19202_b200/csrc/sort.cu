@@ -242,6 +242,9 @@ __device__ __forceinline__ void ticket_release(unsigned long long *next, unsigne
 
 // Upsweep: warp-private shared histograms (plain shared atomics, no ranking),
 // keys loaded 4 per thread per load (uint4, streaming).
+// A ticket covers kUpTiles consecutive tiles whose keys are all loaded up front
+// (kUpTiles x 2 x 16 B per thread in flight), then histogrammed tile by tile.
+constexpr int kUpTiles = 4;
 __global__ void __launch_bounds__(kOsThreads) k_radix_up(const uint32_t *__restrict__ keys,
                                                          const unsigned long long *n_dev, int64_t n_host, int shift,
                                                          uint32_t *counts, int64_t ntiles_max,
@@ -251,40 +254,54 @@ __global__ void __launch_bounds__(kOsThreads) k_radix_up(const uint32_t *__restr
     __shared__ int64_t s_t;
     const int tid = threadIdx.x, wid = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host);
+    constexpr int kQ = kOsItems / 4;   // uint4 loads per thread per tile
+    for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&h[0][0])[i] = 0;
     for (;;) {
-        if (tid == 0) s_t = (int64_t)atomicAdd(tk_next, 1ull);
+        if (tid == 0) s_t = (int64_t)atomicAdd(tk_next, 1ull) * kUpTiles;
         __syncthreads();
-        const int64_t t = s_t;
-        if (t >= ntiles_max) break;
-        for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&h[0][0])[i] = 0;
-        __syncthreads();
-        const int64_t base = t * kOsTile;
-        if (base < n) {
-            const int cnt = (int)std::min<int64_t>(kOsTile, n - base);
-            uint32_t *hw = h[wid];
+        const int64_t t0 = s_t;
+        if (t0 >= ntiles_max) break;
+        uint4 kv[kUpTiles][kQ];
 #pragma unroll
-            for (int q = 0; q < kOsItems / 4; q++) {
-                const int i = 4 * (q * kOsThreads + tid);   // 4 consecutive keys
-                if (i + 4 <= cnt) {
-                    const uint4 k = __ldcs(reinterpret_cast<const uint4 *>(keys + base + i));
+        for (int u = 0; u < kUpTiles; u++)
+#pragma unroll
+            for (int q = 0; q < kQ; q++) {
+                const int64_t i = (t0 + u) * kOsTile + 4 * (q * kOsThreads + tid);   // 4 consecutive keys
+                kv[u][q] = i + 4 <= n ? __ldcs(reinterpret_cast<const uint4 *>(keys + i))
+                                      : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+            }
+        uint32_t *hw = h[wid];
+#pragma unroll
+        for (int u = 0; u < kUpTiles; u++) {
+            const int64_t t = t0 + u;
+            if (t >= ntiles_max) break;
+            const int64_t base = t * kOsTile;
+#pragma unroll
+            for (int q = 0; q < kQ; q++) {
+                const int64_t i = base + 4 * (q * kOsThreads + tid);
+                if (i + 4 <= n) {
+                    const uint4 k = kv[u][q];
                     atomicAdd(&hw[(k.x >> shift) & 0xFFu], 1u);
                     atomicAdd(&hw[(k.y >> shift) & 0xFFu], 1u);
                     atomicAdd(&hw[(k.z >> shift) & 0xFFu], 1u);
                     atomicAdd(&hw[(k.w >> shift) & 0xFFu], 1u);
                 } else {
-                    for (int e = i; e < cnt && e < i + 4; e++) atomicAdd(&hw[(keys[base + e] >> shift) & 0xFFu], 1u);
+                    for (int64_t e = i; e < n && e < i + 4; e++) atomicAdd(&hw[(keys[e] >> shift) & 0xFFu], 1u);
                 }
             }
-        }
-        __syncthreads();
-        // digit-major: the matrix's exclusive scan is every (digit, tile) base; empty tiles write zeros
-        if (tid < 256) {
-            uint32_t c = 0;
+            __syncthreads();
+            // digit-major: the matrix's exclusive scan is every (digit, tile) base; empty tiles write zeros
+            if (tid < 256) {
+                uint32_t c = 0;
 #pragma unroll
-            for (int w = 0; w < kOsWarps; w++) c += h[w][tid];
-            counts[(int64_t)tid * ntiles_max + t] = c;
+                for (int w = 0; w < kOsWarps; w++) {
+                    c += h[w][tid];
+                    h[w][tid] = 0;
+                }
+                counts[(int64_t)tid * ntiles_max + t] = c;
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     if (tid == 0) ticket_release(tk_next, tk_done);
 }
@@ -491,7 +508,8 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
     V *vi = va, *vo = vb;
     for (int p = 0; p < npass; p++) {
         const int shift = bit_lo + 8 * p;
-        SC_LAUNCH(k_radix_up, (int)std::min<int64_t>(ntiles, (int64_t)nsm * 4), kOsThreads, 0, st, ki, n_dev, n_max,
+        SC_LAUNCH(k_radix_up, (int)std::min<int64_t>((ntiles + kUpTiles - 1) / kUpTiles, (int64_t)nsm * 4), kOsThreads, 0,
+                  st, ki, n_dev, n_max,
                   shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
         e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;

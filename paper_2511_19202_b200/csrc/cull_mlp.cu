@@ -451,8 +451,8 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
 // ---------------------------------------------------------------------------
 // Batched forward on materialised fp32 inputs (config-4 sweep, nn.forward).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_vis_forward(const sc_vis_weights *w, const float *x, int64_t n,
-                                                     float *logits)
+__global__ void __launch_bounds__(128, 12) k_vis_forward(const sc_vis_weights *w, const float *x, int64_t n,
+                                                         float *logits)
 {
     __shared__ MlpSmem sm;
     const int tid = threadIdx.x;
@@ -461,16 +461,24 @@ __global__ void __launch_bounds__(128) k_vis_forward(const sc_vis_weights *w, co
     __syncthreads();
     uint32_t phase = 0;
     const int64_t n_tiles = (n + 127) / 128;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    // the next tile's row is loaded (and packed to fp16) while the current tile runs the MLP
+    auto load = [&](int64_t tile, uint4 &lo, uint4 &hi) {
         const int64_t r = tile * 128 + tid;
-        uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
-        if (r < n) {
+        lo = make_uint4(0, 0, 0, 0);
+        hi = lo;
+        if (tile < n_tiles && r < n) {
             const float4 *row = reinterpret_cast<const float4 *>(x + r * 16);
-            const float4 a = __ldg(row), b = __ldg(row + 1), c = __ldg(row + 2), d = __ldg(row + 3);
+            const float4 a = __ldcs(row), b = __ldcs(row + 1), c = __ldcs(row + 2), d = __ldcs(row + 3);
             lo = make_uint4(pack_h2(a.x, a.y), pack_h2(a.z, a.w), pack_h2(b.x, b.y), pack_h2(b.z, b.w));
             hi = make_uint4(pack_h2(c.x, c.y), pack_h2(c.z, c.w), pack_h2(d.x, d.y), pack_h2(d.z, d.w));
         }
+    };
+    uint4 lo, hi;
+    load(blockIdx.x, lo, hi);
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t r = tile * 128 + tid;
         mlp_store_row(sm, tid, lo, hi);
+        load(tile + gridDim.x, lo, hi);
         float lg = 0.0f;
         mlp_tile(sm, tid, phase, true, &lg);
         if (r < n) logits[r] = lg;
@@ -552,7 +560,7 @@ cudaError_t launch_vis_mlp(const sc_vis_weights *w, const float *x, int64_t n, f
 {
     if (n <= 0) return cudaSuccess;
     const int64_t tiles = (n + 127) / 128;
-    const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 8);
+    const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 12);
     SC_LAUNCH(k_vis_forward, grid, 128, 0, st, w, x, n, logits);
     return cudaGetLastError();
 }

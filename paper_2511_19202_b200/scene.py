@@ -401,11 +401,16 @@ class _PinnedPool:
     """Pinned host buffers for the per-frame device->host copies, recycled once
     the numpy arrays handed out over them are garbage-collected (a fresh
     pinned allocation of a 1080p image costs ~1.5 ms of host time, about what
-    the frame's GPU work leaves the host per frame)."""
+    the frame's GPU work leaves the host per frame).  At most ``limit_bytes``
+    of pinned memory stays handed out: beyond that (a caller keeping many
+    frames alive) the arrays are copied into pageable memory and the pinned
+    buffer returns to the pool at once."""
 
-    def __init__(self):
+    def __init__(self, limit_bytes: int = 2 << 30):
         self._free: dict = {}
         self._lock = threading.Lock()
+        self.limit_bytes = int(limit_bytes)
+        self.out_bytes = 0
 
     def take(self, shape, dtype):
         import torch
@@ -421,10 +426,25 @@ class _PinnedPool:
         with self._lock:
             self._free.setdefault((tuple(t.shape), t.dtype), []).append(t)
 
+    def _release(self, t, nbytes: int) -> None:
+        with self._lock:
+            self.out_bytes -= nbytes
+        self.give(t)
+
     def numpy(self, t):
-        """numpy view of pinned ``t``; ``t`` returns to the pool when the view is collected."""
+        """numpy view of pinned ``t`` (``t`` returns to the pool when the view is collected),
+        or a pageable copy once ``limit_bytes`` of pinned memory is handed out."""
+        nbytes = t.numel() * t.element_size()
+        with self._lock:
+            keep = self.out_bytes + nbytes <= self.limit_bytes
+            if keep:
+                self.out_bytes += nbytes
+        if not keep:
+            a = t.numpy().copy()
+            self.give(t)
+            return a
         a = t.numpy()
-        weakref.finalize(a, self.give, t)
+        weakref.finalize(a, self._release, t, nbytes)
         return a
 
 

@@ -136,3 +136,32 @@ def test_orbit_eval_slab_trained_model():
     ev = layout.orbit_eval(a, model, n_views=8, distance=dist, height_frac=0.8)
     assert ev["delta_passed_pct"] <= -40.0, ev
     assert ev["used_ours"] >= 0.98 * ev["used_gt"], ev
+
+
+def test_pinned_pool_recycles_and_caps():
+    """render()/render_path() host buffers: recycled when the returned arrays die,
+    pageable copies once the handed-out pinned bytes pass the cap (CPU-only check
+    with plain tensors standing in for pinned ones)."""
+    import gc
+
+    import torch
+
+    from paper_2511_19202_b200 import scene
+
+    pool = scene._PinnedPool(limit_bytes=3 * 4 * 100)
+    pool.take = lambda shape, dtype: torch.zeros(shape, dtype=dtype)   # no CUDA here
+    t1 = pool.take((100,), torch.float32)
+    a1 = pool.numpy(t1)
+    assert pool.out_bytes == 400 and a1.base is not None
+    del a1
+    gc.collect()
+    assert pool.out_bytes == 0 and pool._free[((100,), torch.float32)] == [t1]
+    kept = [pool.numpy(torch.zeros(100)) for _ in range(3)]
+    assert pool.out_bytes == 1200
+    t4 = torch.ones(100)
+    a4 = pool.numpy(t4)                  # over the cap: a pageable copy, t4 back in the pool at once
+    assert pool.out_bytes == 1200 and float(a4.sum()) == 100.0
+    assert any(x is t4 for x in pool._free[((100,), torch.float32)])
+    del kept
+    gc.collect()
+    assert pool.out_bytes == 0

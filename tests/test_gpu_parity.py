@@ -568,3 +568,57 @@ def test_render_path_public_api():
         ref, rst = pkg.render_composed(sc, cam)
         np.testing.assert_array_equal(out.image, ref.image)
         assert st.instantiated == rst.instantiated
+
+
+def test_nothing_visible_renders_background():
+    """A9 / sc/raster.py:284-285: with no splat in view (camera facing away from
+    every instance) the frame is the background with T = 1 and every count is 0."""
+    import paper_2511_19202_b200 as pkg
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    cam = look_at([0.0, -14.0, 4.0], [0.0, -30.0, 4.0], 45, 160, 120)   # looking away from the layout
+    out, st = pkg.render_composed(sc, cam, background=(0.25, 0.5, 0.75))
+    np.testing.assert_array_equal(out.final_transmittance, np.ones((120, 160), np.float32))
+    np.testing.assert_array_equal(out.image, np.broadcast_to(np.float32([0.25, 0.5, 0.75]), (120, 160, 3)))
+    assert st.instantiated == 0 and st.passed == 0 and st.frustum_passed == 0 and st.instances_visible == 0
+    ref = sr.render_composed(sc, cam)
+    assert ref.stats["frustum_passed"] == 0
+
+
+def test_everything_culled_by_the_mlp():
+    """Thresholds no logit reaches: every queried pair is culled, nothing is
+    instantiated, the frame is the background; the oracle agrees on the counts."""
+    import dataclasses
+
+    import paper_2511_19202_b200 as pkg
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    for k, sa in enumerate(sc.assets):
+        sc.set_model(k, dataclasses.replace(sa.model, threshold=1.0 - 1e-12))
+    cam = look_at(*CAMS[0])
+    out, st = pkg.render_composed(sc, cam)
+    assert st.mlp_queried > 0 and st.mlp_culled == st.mlp_queried
+    # pairs below d_near are not queried and survive (SPEC.md:356, :379)
+    assert st.instantiated == st.frustum_passed - st.mlp_culled
+    ref = sr.render_composed(sc, cam)
+    assert st.mlp_queried == ref.stats["mlp_queried"] and st.instantiated == ref.stats["instantiated"]
+    assert rr.psnr(out.image, ref.out.image, cap=None) >= 45.0
+
+
+def test_single_gaussian_dropin_vs_oracle():
+    """The smallest input: one Gaussian in front of the camera, render() vs the oracle."""
+    import paper_2511_19202_b200 as pkg
+    from paper_2511_19202_b200.asset import Asset
+    from conftest import look_at
+
+    a = Asset(means=np.float32([[0.1, 0.2, 0.0]]), log_scales=np.float32([[-1.0, -1.5, -2.0]]),
+              rotations=np.float32([[0.9, 0.1, 0.3, -0.2]]) / np.float32(np.linalg.norm([0.9, 0.1, 0.3, -0.2])),
+              opacity_logits=np.float32([1.5]), sh_coeffs=np.float32([[[0.3, -0.2, 0.5]]]), sh_degree=0)
+    cam = look_at([0.0, -3.0, 0.5], [0.0, 0.0, 0.0], 50, 96, 64)
+    out = pkg.render(a, cam, record_contributions=True)
+    ref = rr.render(a, cam, record_contributions=True)
+    _image_close(out.image, ref.image)
+    np.testing.assert_allclose(out.final_transmittance, ref.final_transmittance, atol=IMG_MAX_ABS)
+    assert out.passed_count == ref.passed_count == 1 and out.used_count == ref.used_count

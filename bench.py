@@ -396,6 +396,8 @@ def main():
                "api": (f"paper_2511_19202_b200.render_path(scene, cams, frames_in_flight={F}) -> RenderOutput per "
                        "frame (numpy image + transmittance)") if F > 1 else
                       "paper_2511_19202_b200.render_composed -> RenderOutput (numpy image + transmittance)"}
+        if bands:
+            e2e["sharding"] = "whole frames per rank (the banded path has no host-facing API of its own)"
 
     if rank != 0:
         if dist:

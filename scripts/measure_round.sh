@@ -19,6 +19,13 @@ for v in 0 1 2; do ./scripts/frame_profile.sh $v > /dev/null 2>&1; done
 timeout 900 ncu --set full --import-source on --nvtx --nvtx-include "frame/" -k regex:k_blend -c 3 --clock-control none \
     -o gpurun_out/ncu_blend python scripts/profile_frame.py cfg3 all > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --nvtx --nvtx-include "frame/" \
-    -k regex:"k_cull|k_project|k_radix_down|k_radix_up|k_bentry_emit" -c 6 --clock-control none \
+    -k regex:"k_cull|k_project|k_bentry_emit" -c 4 --clock-control none \
     -o gpurun_out/ncu_top python scripts/profile_frame.py cfg3 2 > /dev/null 2>&1
+# the sort: one depth upsweep, the last depth downsweep and both block-list downsweeps
+timeout 900 ncu --set full --import-source on --nvtx --nvtx-include "frame/" \
+    -k regex:"k_radix_down" --launch-skip 3 -c 3 --clock-control none \
+    -o gpurun_out/ncu_sort python scripts/profile_frame.py cfg3 2 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --nvtx --nvtx-include "frame/" \
+    -k regex:"k_radix_up" -c 1 --clock-control none \
+    -o gpurun_out/ncu_up python scripts/profile_frame.py cfg3 2 > /dev/null 2>&1
 ls gpurun_out

@@ -37,7 +37,7 @@ for v in (0, 1, 2):
     if os.path.exists(src):
         shutil.copy(src, os.path.join(P, f"{tag}_frame_view{v}_launches.txt"))
 summ = ""
-for rep in ("ncu_blend", "ncu_top"):
+for rep in ("ncu_blend", "ncu_top", "ncu_sort", "ncu_up"):
     path = os.path.join(G, rep + ".ncu-rep")
     if os.path.exists(path):
         summ += run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), path])

@@ -648,41 +648,33 @@ __device__ __forceinline__ uint32_t bentry_count(uint2 v, const sc_window *wins,
 
 // Emission tiles: kEmitTile consecutive passed splats (depth order) per CTA
 // iteration, warp w owning the contiguous kEmitPerWarp splats [w * 512, w * 512
-// + 512) of the tile.  Pass 1 writes per-tile entry totals, one exclusive scan
-// turns them into tile offsets, pass 2 recounts (the tile's payloads are in L1)
-// and emits: no per-splat count array round trip through HBM.
+// + 512) of the tile.  Pass 1 writes per-(tile, warp) entry totals, one
+// exclusive scan turns them into output bases, pass 2 emits (every warp on its
+// own, no CTA barrier): no per-splat count array round trip through HBM.
 constexpr int kEmitThreads = 256;
 constexpr int kEmitTile = 4096;
 constexpr int kEmitPerWarp = kEmitTile / (kEmitThreads / 32);
 
+// pass 1: the entry total of every (tile, warp) range of kEmitPerWarp splats
 __global__ void __launch_bounds__(kEmitThreads) k_bentry_tiles(const uint2 *__restrict__ pv, const sc_window *wins,
                                                                const unsigned long long *n_dev, int64_t n_host,
                                                                int64_t ntiles_max, int width, int height,
-                                                               uint32_t *tile_tot)
+                                                               uint32_t *warp_tot)
 {
-    __shared__ uint32_t s_w[kEmitThreads / 32];
     const int64_t n = dev_count(n_dev, n_host);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int64_t t = blockIdx.x; t < ntiles_max; t += gridDim.x) {
+        const int64_t wbase = t * kEmitTile + (int64_t)wid * kEmitPerWarp;
         uint32_t c = 0;
-        const int64_t base = t * kEmitTile;
-        if (base < n) {
+        if (wbase < n) {
 #pragma unroll 4
-            for (int j = 0; j < kEmitTile / kEmitThreads; j++) {
-                const int64_t k = base + (int64_t)j * kEmitThreads + threadIdx.x;
+            for (int r = 0; r < kEmitPerWarp / 32; r++) {
+                const int64_t k = wbase + r * 32 + lane;
                 if (k < n) c += bentry_count(__ldg(pv + k), wins, width, height);
             }
         }
         c = __reduce_add_sync(0xffffffffu, c);
-        if (lane == 0) s_w[wid] = c;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t tot = 0;
-#pragma unroll
-            for (int w = 0; w < kEmitThreads / 32; w++) tot += s_w[w];
-            tile_tot[t] = tot;
-        }
-        __syncthreads();
+        if (lane == 0) warp_tot[t * (kEmitThreads / 32) + wid] = c;
     }
 }
 
@@ -758,14 +750,13 @@ __device__ __forceinline__ uint32_t emit_group(uint2 cv, bool valid, uint32_t ob
 }
 
 __global__ void __launch_bounds__(kEmitThreads) k_bentry_emit(const uint2 *__restrict__ pv, const sc_window *wins,
-                                                              const uint32_t *tile_off, const unsigned long long *n_dev,
+                                                              const uint32_t *warp_off, const unsigned long long *n_dev,
                                                               int64_t n_host, int width, int height, int n_tx,
                                                               uint32_t *ekey, uint32_t *eval,
                                                               const unsigned long long *e_total,
                                                               unsigned long long *e_eff, int64_t cap_e,
                                                               sc_frame_stats *stats)
 {
-    __shared__ uint32_t s_w[kEmitThreads / 32];
     const int64_t n = dev_count(n_dev, n_host);
     const bool over = (int64_t)*e_total > cap_e;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -777,20 +768,9 @@ __global__ void __launch_bounds__(kEmitThreads) k_bentry_emit(const uint2 *__res
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t ntiles = (n + kEmitTile - 1) / kEmitTile;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        // this warp's range of the tile and its output base (scan of the (tile, warp) totals)
         const int64_t wbase = t * kEmitTile + (int64_t)wid * kEmitPerWarp;
-        // recount this warp's splats -> the warp's base inside the tile
-        uint32_t c = 0;
-#pragma unroll 4
-        for (int r = 0; r < kEmitPerWarp / 32; r++) {
-            const int64_t k = wbase + r * 32 + lane;
-            if (k < n) c += bentry_count(__ldg(pv + k), wins, width, height);
-        }
-        c = __reduce_add_sync(0xffffffffu, c);
-        if (lane == 0) s_w[wid] = c;
-        __syncthreads();
-        uint32_t o = tile_off[t];
-        for (int w = 0; w < wid; w++) o += s_w[w];
-        __syncthreads();
+        uint32_t o = warp_off[t * (kEmitThreads / 32) + wid];
         for (int r = 0; r < kEmitPerWarp / 32; r++) {
             const int64_t g0 = wbase + r * 32;
             if (g0 >= n) break;
@@ -862,7 +842,8 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
         const int egrid = (int)std::min<int64_t>(etiles, (int64_t)sm_count_sort() * 8);
         SC_LAUNCH(k_bentry_tiles, egrid, kEmitThreads, 0, st, pv_s, wins, p_dev, n_max, etiles, cam.width, cam.height,
                   ws.ecount);
-        e = scan_excl(ws.ecount, ws.ecount, nullptr, etiles, ws.scan_part, &ws.ctr->entries, nullptr, st);
+        e = scan_excl(ws.ecount, ws.ecount, nullptr, etiles * (kEmitThreads / 32), ws.scan_part, &ws.ctr->entries,
+                      nullptr, st);
         if (e != cudaSuccess) return e;
         SC_LAUNCH(k_bentry_emit, egrid, kEmitThreads, 0, st, pv_s, wins, ws.ecount, p_dev, n_max, cam.width,
                   cam.height, ws.n_tx, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);

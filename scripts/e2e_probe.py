@@ -12,7 +12,7 @@ from paper_2511_19202_b200 import workloads
 
 wl = workloads.config3()
 cams = wl.cameras
-for F in (1, 2, 3):
+for F in (1, 2, 2, 2, 2, 2, 3):
     seq = [cams[i % 3] for i in range(30)]
     list(pkg.render_path(wl.scene, seq[:6], frames_in_flight=F))   # warm (workspaces per slot)
     torch.cuda.synchronize()
@@ -23,12 +23,3 @@ for F in (1, 2, 3):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     print(f"F={F}: {n / dt:.1f} FPS e2e", flush=True)
-import cProfile
-import pstats
-seq = [cams[i % 3] for i in range(30)]
-pr = cProfile.Profile()
-pr.enable()
-for out, st in pkg.render_path(wl.scene, seq, frames_in_flight=2):
-    pass
-pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(14)

@@ -77,7 +77,9 @@ struct Counters {
 // Workspace carve-out (all offsets 256-byte aligned), see api.cu:carve().
 struct Ws {
     InstFrame *inst;                 // [n_instances]
-    unsigned long long *chunk_state; // [max_chunks] decoupled look-back
+    unsigned long long *chunk_state; // [max_chunks] (instance << 32) | chunk index within the instance
+    uint32_t *chunk_cnt;             // [max_chunks] survivors per chunk -> exclusive offsets
+    uint16_t *chunk_stage;           // [max_chunks][kChunk] survivors of each chunk (offset in the chunk)
     Counters *ctr;
     sc_survivor *surv;               // [capS]
     sc_splat *splats;                // [capS]
@@ -205,6 +207,9 @@ cudaError_t launch_prep(const sc_scene &scene, const sc_camera &cam, const sc_op
                         sc_frame_stats *stats, cudaStream_t st);
 cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
                         sc_survivor *out, int64_t cap, sc_frame_stats *stats, cudaStream_t st);
+// exclusive scan of uint32 (n from device or host); total -> *total_out (u64) / *stat_out (i64)
+cudaError_t scan_excl(const uint32_t *in, uint32_t *out, const unsigned long long *n_dev, int64_t n_max,
+                      uint32_t *part, unsigned long long *total_out, int64_t *stat_out, cudaStream_t st);
 cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                            int64_t n_max, const sc_camera &cam, const sc_opts &opts, sc_splat *splats,
                            sc_window *wins, double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,

@@ -1,6 +1,6 @@
 // Stages (a) + (b): per-instance bounding-sphere cull, per-(instance, gaussian)
 // frustum test, d_near gate and the fused tcgen05 visibility MLP, with an
-// order-preserving (decoupled look-back) compaction of survivors.
+// order-preserving compaction of survivors (per-chunk staging, scan, k_compact).
 //
 // Compiled with -fmad=false: the frustum / gate arithmetic is float64 and must
 // reproduce the oracle (oracle/sc_oracle.c:orc_scene_cull) bit for bit.
@@ -189,14 +189,6 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
     }
 }
 
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p)
-{
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-constexpr unsigned long long kFlagAgg = 1ull << 32, kFlagPre = 2ull << 32;
 #ifndef SC_CULL_CB
 #define SC_CULL_CB 0
 #endif
@@ -204,11 +196,12 @@ constexpr int kCullCbSmem = SC_CULL_CB;   // instance chunk_begin table cached i
 
 // ---------------------------------------------------------------------------
 // Cull + MLP.  Persistent CTAs of 128 threads take chunks of kChunk pairs of
-// one instance from an atomic ticket (so look-back never waits on an
-// unscheduled chunk).  Each 128-pair tile: thread = pair; f64 frustum test on
-// the f32-rounded instanced mean (B2/B3), Eq. 2 gate in f64, 16 fp16 inputs
-// into the smem A tile, tcgen05 MLP, survivor ballot into an smem list kept
-// in pair order.  The chunk's list is placed after its predecessors'.
+// one instance from an atomic ticket.  Each 128-pair tile: thread = pair; f64
+// frustum test on the f32-rounded instanced mean (B2/B3), Eq. 2 gate in f64, 16
+// fp16 inputs into the smem A tile, tcgen05 MLP, survivor ballot into an smem
+// list kept in pair order.  The chunk's list goes to its own staging slot;
+// k_compact places it after its predecessors' (scan of the chunk counts), so
+// no CTA waits on another (a decoupled look-back here stalled ~20 % of the time).
 // ---------------------------------------------------------------------------
 #ifndef SC_CULL_CPS
 #define SC_CULL_CPS 12
@@ -225,7 +218,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
     static_assert(kCullTilesPerChunk * kCullWarps == 32, "one warp scans the chunk's segment counts");
     __shared__ uint32_t s_wcnt[kCullTilesPerChunk * kCullWarps];   // survivors per (tile, warp) segment
     __shared__ uint32_t s_segoff[kCullTilesPerChunk * kCullWarps];
-    __shared__ uint32_t s_chunk, s_inst, s_prefix, s_nc;
+    __shared__ uint32_t s_chunk, s_inst, s_nc;
     __shared__ uint32_t s_cb[kCullCbSmem > 0 ? kCullCbSmem : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -247,8 +240,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
     const bool cb_smem = n_inst <= kCullCbSmem;
     if (cb_smem)
         for (int64_t i = tid; i < n_inst; i += kCullThreads) s_cb[i] = ws.inst[i].chunk_begin;
-    // (a ticket is taken only when its chunk starts: the look-back of a chunk waits
-    // for its predecessors, which must all be in progress)
+    // chunks are handed out by an atomic ticket (dynamic balance across CTAs)
     for (;;) {
         if (tid == 0) s_chunk = (uint32_t)atomicAdd(&ws.ctr->chunk_ticket, 1ull);
         __syncthreads();
@@ -393,45 +385,16 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
         __syncthreads();
         const uint32_t n_c = s_nc;
 
-        // decoupled look-back over chunk aggregates
+        // the chunk's survivors go to its staging slot (no wait on other chunks: their
+        // order-preserving placement is a scan over the chunk counts + k_compact)
         if (tid == 0) {
-            unsigned long long *st = ws.chunk_state;
-            uint32_t prefix = 0;
-            if (chunk == 0) {
-                atomicExch(&st[0], kFlagPre | n_c);
-            } else {
-                atomicExch(&st[chunk], kFlagAgg | n_c);
-                int64_t k = (int64_t)chunk - 1;
-                for (;;) {
-                    const unsigned long long v = ld_relaxed(&st[k]);
-                    const unsigned long long flag = v & (3ull << 32);
-                    if (flag == 0) continue;
-                    prefix += (uint32_t)v;
-                    if (flag == kFlagPre) break;
-                    k--;
-                }
-                atomicExch(&st[chunk], kFlagPre | (unsigned long long)(prefix + n_c));
-            }
-            s_prefix = prefix;
-            if (chunk == total - 1) {
-                stats->survivors = (int64_t)prefix + n_c;
-                ws.ctr->survivors = (unsigned long long)prefix + n_c;
-                if ((long long)prefix + n_c > cap) atomicOr((unsigned long long *)&stats->overflow, 1ull);
-            }
+            ws.chunk_cnt[chunk] = n_c;
+            ws.chunk_state[chunk] = ((unsigned long long)s_inst << 32) | (uint32_t)(chunk - s_fr.chunk_begin);
         }
-        __syncthreads();
-        const uint32_t prefix = s_prefix;
+        uint16_t *stage = ws.chunk_stage + (size_t)chunk * kChunk;
         for (int t = 0; t < kCullTilesPerChunk; t++) {   // warp w copies its segments
             const int seg = t * kCullWarps + wid;
-            if ((uint32_t)lane < s_wcnt[seg]) {
-                const long long pos = (long long)prefix + s_segoff[seg] + lane;
-                if (pos < cap) {
-                    sc_survivor sv;
-                    sv.inst = s_inst;
-                    sv.gid = (uint32_t)(j0 + s_surv[t * kCullThreads + wid * 32 + lane]);
-                    out[pos] = sv;
-                }
-            }
+            if ((uint32_t)lane < s_wcnt[seg]) stage[s_segoff[seg] + lane] = s_surv[t * kCullThreads + wid * 32 + lane];
         }
     }
     // stats
@@ -446,6 +409,40 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
         if (n_cull) atomicAdd((unsigned long long *)&stats->mlp_culled, n_cull);
     }
     mlp_teardown(sm, tid);
+}
+
+// ---------------------------------------------------------------------------
+// Survivor placement: chunk c's staged survivors land at the exclusive scan of
+// the chunk counts (chunk order = pair order, so the list is the flat
+// (asset, instance, gaussian) order of B1).  One warp per chunk.
+// ---------------------------------------------------------------------------
+__global__ void k_compact(const unsigned long long *__restrict__ chunk_state, const uint32_t *__restrict__ chunk_off,
+                          const uint16_t *__restrict__ stage, const unsigned long long *n_chunks_dev,
+                          const unsigned long long *total_dev, sc_survivor *out, long long cap,
+                          sc_frame_stats *stats)
+{
+    const int64_t n_chunks = (int64_t)*n_chunks_dev;
+    const int64_t total = (int64_t)*total_dev;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && total > cap) atomicOr((unsigned long long *)&stats->overflow, 1ull);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < n_chunks; c += n_warps) {
+        const int64_t o0 = chunk_off[c];
+        const int64_t n = (c + 1 < n_chunks ? (int64_t)chunk_off[c + 1] : total) - o0;
+        const unsigned long long cs = chunk_state[c];
+        const uint32_t inst = (uint32_t)(cs >> 32);
+        const uint32_t j0 = (uint32_t)cs * (uint32_t)kChunk;
+        const uint16_t *src = stage + (size_t)c * kChunk;
+        for (int64_t i = lane; i < n; i += 32) {
+            if (o0 + i < cap) {
+                sc_survivor sv;
+                sv.inst = inst;
+                sv.gid = j0 + src[i];
+                out[o0 + i] = sv;
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -549,10 +546,13 @@ cudaError_t launch_prep(const sc_scene &scene, const sc_camera &cam, const sc_op
 cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
                         sc_survivor *out, int64_t cap, sc_frame_stats *stats, cudaStream_t st)
 {
-    cudaError_t e = cudaMemsetAsync(ws.chunk_state, 0, sizeof(unsigned long long) * (size_t)ws.max_chunks, st);
-    if (e != cudaSuccess) return e;
     const int grid = sm_count() * SC_CULL_CPS;   // CTAs per SM (32 TMEM columns each)
     SC_LAUNCH(k_cull, grid, kCullThreads, 0, st, scene, cam, opts, ws, out, (long long)cap, stats);
+    cudaError_t e = scan_excl(ws.chunk_cnt, ws.chunk_cnt, &ws.ctr->total_chunks, ws.max_chunks, ws.scan_part,
+                              &ws.ctr->survivors, &stats->survivors, st);
+    if (e != cudaSuccess) return e;
+    SC_LAUNCH(k_compact, sm_count() * 16, 256, 0, st, ws.chunk_state, ws.chunk_cnt, ws.chunk_stage,
+              &ws.ctr->total_chunks, &ws.ctr->survivors, out, (long long)cap, stats);
     return cudaGetLastError();
 }
 

@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t *in, 
     }
 }
 
-static cudaError_t scan_excl(const uint32_t *in, uint32_t *out, const unsigned long long *n_dev, int64_t n_max,
-                             uint32_t *part, unsigned long long *total_out, int64_t *stat_out, cudaStream_t st)
+cudaError_t scan_excl(const uint32_t *in, uint32_t *out, const unsigned long long *n_dev, int64_t n_max,
+                      uint32_t *part, unsigned long long *total_out, int64_t *stat_out, cudaStream_t st)
 {
     const int64_t nblk = std::max<int64_t>(1, (n_max + kScanTile - 1) / kScanTile);
     SC_LAUNCH(k_scan_reduce, (int)nblk, kScanThreads, 0, st, in, n_dev, n_max, part);

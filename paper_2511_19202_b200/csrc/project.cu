@@ -19,6 +19,14 @@ __constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539
 __constant__ double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
                                 -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
 
+__device__ __forceinline__ sc_survivor make_survivor(uint32_t inst, uint32_t gid)
+{
+    sc_survivor s;
+    s.inst = inst;
+    s.gid = gid;
+    return s;
+}
+
 __device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // sqrt.approx (rel. error < 2^-22): only where the result is widened by a margin far larger
@@ -70,9 +78,16 @@ __global__ void __launch_bounds__(256, 2) k_project(
                 r4 = (float)cam.rot[4], r5 = (float)cam.rot[5], r6 = (float)cam.rot[6], r7 = (float)cam.rot[7],
                 r8 = (float)cam.rot[8];
 
-    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n; it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // the survivor record is loaded one iteration ahead (the instance / Gaussian loads of an
+    // iteration then start without waiting on it)
+    int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    sc_survivor sv_next = make_survivor(0u, 0u);
+    if (it < n) sv_next = surv[from_list ? (int64_t)list[it] : it];
+    for (; it < n; it += stride) {
         const int64_t k = from_list ? (int64_t)list[it] : it;
-        const sc_survivor sv = surv[k];
+        const sc_survivor sv = sv_next;
+        if (it + stride < n) sv_next = surv[from_list ? (int64_t)list[it + stride] : it + stride];
         const sc_instance_rec &in = scene.instances[sv.inst];
         const sc_asset_rec &as = scene.assets[in.asset];
         const int64_t g = as.offset + sv.gid;

@@ -55,6 +55,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--frames-in-flight", type=int, default=2,
                    help="frames rendered concurrently on separate streams (own workspaces); 1 = serial")
+    p.add_argument("--e2e-frames-in-flight", type=int, default=3,
+                   help="frames in flight for the end-to-end pass through render_path (one more than the device "
+                        "pass: the host's wake-up after each frame's copy then never leaves the GPU one frame)")
     return p.parse_args()
 
 
@@ -373,15 +376,17 @@ def main():
         if dist:
             dist.barrier()
         seq = [cams[(i + rank) % ncam] for i in range(ke)]
-        if F > 1:   # warm the path API (its streams, output frames and pinned host buffers)
-            for _ in pkg.render_path(wl.scene, seq[:2 * F], frames_in_flight=F):
+        FE = max(1, args.e2e_frames_in_flight) if F > 1 else 1
+        if FE > 1:   # warm the path API (its streams, output frames and pinned host buffers)
+            for _ in pkg.render_path(wl.scene, seq[:2 * FE], frames_in_flight=FE):
                 pass
             torch.cuda.synchronize()
         gc.collect()
         gc.disable()   # no cyclic-GC pause inside the timed host loop
+        r.path_wait_s = 0.0
         t0 = time.perf_counter()
-        if F > 1:
-            for out, fst in pkg.render_path(wl.scene, seq, frames_in_flight=F):
+        if FE > 1:
+            for out, fst in pkg.render_path(wl.scene, seq, frames_in_flight=FE):
                 pass
         else:
             for cam in seq:
@@ -389,6 +394,7 @@ def main():
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         gc.enable()
+        host_busy = e2e_s - r.path_wait_s
         if dist:
             t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -397,9 +403,12 @@ def main():
         e2e = {"value": world * ke / e2e_s, "unit": "FPS",
                "h2d_bytes_per_step": 136 + 80,
                "d2h_bytes_per_step": h * w * 3 * 4 + h * w * 4 + nat.STATS_BYTES,
-               "api": (f"paper_2511_19202_b200.render_path(scene, cams, frames_in_flight={F}) -> RenderOutput per "
-                       "frame (numpy image + transmittance)") if F > 1 else
+               "api": (f"paper_2511_19202_b200.render_path(scene, cams, frames_in_flight={FE}) -> RenderOutput per "
+                       "frame (numpy image + transmittance)") if FE > 1 else
                       "paper_2511_19202_b200.render_composed -> RenderOutput (numpy image + transmittance)"}
+        e2e["peak_vram_gb"] = torch.cuda.max_memory_allocated() / 1e9   # includes the e2e pass's frame slots
+        if FE > 1:   # host time per frame not spent waiting on the GPU (render_path's own accounting)
+            e2e["host_busy_ms_per_step"] = 1e3 * host_busy / ke
         if bands:
             e2e["sharding"] = "whole frames per rank (the banded path has no host-facing API of its own)"
 

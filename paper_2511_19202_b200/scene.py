@@ -29,6 +29,7 @@ from __future__ import annotations
 import ctypes
 import math
 import threading
+import time
 import weakref
 from dataclasses import dataclass, field
 
@@ -467,6 +468,7 @@ class Renderer:
         self.workspaces: dict[tuple[int, int], Workspace] = {}
         self._path_streams: list = []
         self._path_frames: dict = {}
+        self.path_wait_s = 0.0   # host time render_path spent waiting on frames (diagnostics)
 
     def workspace(self, cam, slot: int = 0) -> Workspace:
         """The workspace of this resolution (``slot`` > 0: one more per frame in flight)."""
@@ -633,7 +635,9 @@ class Renderer:
         def collect(i):
             slot = i % F
             p = pending[slot]
+            t_sync = time.perf_counter()
             p["done"].synchronize()
+            self.path_wait_s += time.perf_counter() - t_sync
             st = nat.stats_dict(p["host"]["stats"].numpy())
             _PINNED.give(p["host"]["stats"])
             if st["overflow"]:

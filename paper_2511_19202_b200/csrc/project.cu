@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(256, 2) k_project(
             // re-ordered by (tz, index) in the tie-fix; non-passed splats sink to the end
             constexpr double kTop = 4294967040.0;
             keys[k] = passed ? (uint32_t)fmin(floor(fmax(tz - key_dmin, 0.0) * key_scale), kTop) : 0xFFFFFFFFu;
-            pv[k] = make_uint2((uint32_t)k, packed);
+            reinterpret_cast<uint32_t *>(pv)[k] = packed;   // the first depth pass adds the index (= k)
         }
         if (rect) rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0, (unsigned short)ty1);
         if (dbg_f64) {

@@ -317,7 +317,10 @@ struct OsSmem {
 // MATCH_ANY: rank with match.any (fast when a warp holds few distinct digits,
 // e.g. the block sort's high byte: screen rows follow depth order) instead of
 // the constant-cost 8-ballot match.
-template <typename V, bool MATCH_ANY>
+// IDX_IN (first depth pass of the frame path, V = uint2): the input values are the
+// packed pixel windows alone (u32, the projection writes no index) and the output
+// value is (input position = survivor index, window).
+template <typename V, bool MATCH_ANY, bool IDX_IN = false>
 __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__restrict__ keys_in,
                                                               const V *__restrict__ vals_in,
                                                               uint32_t *__restrict__ keys_out,
@@ -341,8 +344,12 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
         const int64_t base = t * kOsTile;
         const uint32_t c = (uint32_t)std::min<int64_t>(kOsTile, n - base);
         // sizes rounded up to 16 B (the key / value buffers carry 16 bytes of slack)
-        os_bulk_load(&s_bar[b], sm.in_k[b], keys_in + base, (c * 4u + 15u) & ~15u, sm.in_v[b], vals_in + base,
-                     (c * (uint32_t)sizeof(V) + 15u) & ~15u);
+        if constexpr (IDX_IN)
+            os_bulk_load(&s_bar[b], sm.in_k[b], keys_in + base, (c * 4u + 15u) & ~15u, sm.in_v[b],
+                         reinterpret_cast<const uint32_t *>(vals_in) + base, (c * 4u + 15u) & ~15u);
+        else
+            os_bulk_load(&s_bar[b], sm.in_k[b], keys_in + base, (c * 4u + 15u) & ~15u, sm.in_v[b], vals_in + base,
+                         (c * (uint32_t)sizeof(V) + 15u) & ~15u);
     };
     __shared__ int64_t s_tile;
     if (tid == 0) {
@@ -388,7 +395,10 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
             for (int j = 0; j < kOsItems; j++) {
                 const int i = wid * kPerWarp + j * 32 + lane;
                 k[j] = sm.in_k[b][i];
-                v[j] = sm.in_v[b][i];
+                if constexpr (IDX_IN)
+                    v[j] = make_uint2((uint32_t)(base + i), reinterpret_cast<const uint32_t *>(sm.in_v[b])[i]);
+                else
+                    v[j] = sm.in_v[b][i];
                 const bool ok = FULL || i < cnt;
                 if constexpr (MATCH_ANY)
                     peers[j] = __match_any_sync(0xffffffffu, ok ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane);
@@ -475,6 +485,10 @@ static cudaError_t radix_down_attr()
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_radix_down<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(OsSmem<V>));
+    if constexpr (std::is_same<V, uint2>::value)
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_radix_down<V, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(OsSmem<V>));
     if (e == cudaSuccess) done = true;
     return e;
 }
@@ -497,7 +511,7 @@ static int sm_count_sort()
 template <typename V>
 static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const unsigned long long *n_dev, int64_t n_max,
                               int bit_lo, int bit_hi, const Ws &ws, uint32_t **keys_res, V **vals_res, cudaStream_t st,
-                              bool last_match_any = false)
+                              bool last_match_any = false, bool first_idx_in = false)
 {
     cudaError_t e = radix_down_attr<V>();
     if (e != cudaSuccess) return e;
@@ -520,6 +534,9 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
         if (last_match_any && p == npass - 1)
             SC_LAUNCH((k_radix_down<V, true>), grid, kOsThreads, sizeof(OsSmem<V>), st, ki, vi, ko, vo, n_dev, n_max,
                       shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
+        else if (first_idx_in && p == 0)   // input values: u32 windows at va (index = position)
+            SC_LAUNCH((k_radix_down<V, false, std::is_same<V, uint2>::value>), grid, kOsThreads, sizeof(OsSmem<V>), st,
+                      ki, vi, ko, vo, n_dev, n_max, shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
         else
             SC_LAUNCH((k_radix_down<V, false>), grid, kOsThreads, sizeof(OsSmem<V>), st, ki, vi, ko, vo, n_dev, n_max,
                       shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
@@ -828,7 +845,9 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
     uint2 *pv_s = nullptr;
     if (!blocks)   // stage-level API: keys from the exact depth range (the frame path's come from the projection)
         SC_LAUNCH(k_depth_keys, grid_for(n_max, 256), 256, 0, st, ws.depth64, n_dev, n_max, ws.ctr, ws.key_a, ws.pv_a);
-    e = radix_sort<uint2>(ws.key_a, ws.pv_a, ws.key_b, ws.pv_b, n_dev, n_max, 0, 32, ws, &keys_s, &pv_s, st);
+    // frame path: the projection wrote u32 windows at pv_a (the survivor index is the position)
+    e = radix_sort<uint2>(ws.key_a, ws.pv_a, ws.key_b, ws.pv_b, n_dev, n_max, 0, 32, ws, &keys_s, &pv_s, st, false,
+                          blocks);
     if (e != cudaSuccess) return e;
     const unsigned long long *p_dev = &ws.ctr->passed;   // passed splats lead the sorted order
     // ws.ecount is free until the entry counts: it holds the tie-run list

@@ -425,7 +425,8 @@ def main():
         per_view.setdefault(i % ncam if bands else (i + rank) % ncam, []).append(dev_ms[i])
     n_gauss = sum(len(a.asset) for a in wl.scene.assets)
     pixels = int(cams[0].width) * int(cams[0].height)
-    alg = [algorithmic_bytes(stats[ci], n_gauss, wl.scene.n_instances, pixels) for ci in range(ncam)]
+    # views rendered in the serial pass (all of them unless K < the number of cameras)
+    alg = [algorithmic_bytes(st_, n_gauss, wl.scene.n_instances, pixels) for st_ in stats if st_]
     def stage_roof(name):
         b = float(np.mean([a[name][0] for a in alg]))
         f = float(np.mean([a[name][1] for a in alg]))

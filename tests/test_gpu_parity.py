@@ -622,3 +622,41 @@ def test_single_gaussian_dropin_vs_oracle():
     _image_close(out.image, ref.image)
     np.testing.assert_allclose(out.final_transmittance, ref.final_transmittance, atol=IMG_MAX_ABS)
     assert out.passed_count == ref.passed_count == 1 and out.used_count == ref.used_count
+
+
+def test_config3_full_size_properties():
+    """BASELINE config 3 at full size (~1,000 instances, 100M pairs, 1080p), the
+    properties that do not need a full CPU render: the far view's frustum / gate
+    counts equal the oracle's over all 100M pairs and the MLP decisions differ
+    only within the logit margin; every view renders deterministically and
+    bit-identically with two frames in flight; T in [0, 1], colours in [0, 1]
+    (white background), survivors = frustum-passed - MLP-culled."""
+    import torch
+
+    from paper_2511_19202_b200.scene import Renderer, RenderOptions
+    from paper_2511_19202_b200.workloads import config3
+
+    wl = config3()
+    r = Renderer(wl.scene)
+    serial = [r.render(c, RenderOptions()) for c in wl.cameras]
+    again = r.render(wl.cameras[0], RenderOptions())
+    np.testing.assert_array_equal(again[0].image, serial[0][0].image)
+    piped = list(r.render_path(wl.cameras, RenderOptions(), frames_in_flight=2))
+    for (a, sa), (b, sb) in zip(serial, piped):
+        np.testing.assert_array_equal(a.image, b.image)
+        np.testing.assert_array_equal(a.final_transmittance, b.final_transmittance)
+        assert (sa.instantiated, sa.passed, sa.entries) == (sb.instantiated, sb.passed, sb.entries)
+        assert sa.instantiated == sa.frustum_passed - sa.mlp_culled and sa.passed <= sa.instantiated
+        assert float(a.final_transmittance.min()) >= 0.0 and float(a.final_transmittance.max()) <= 1.0
+        assert float(a.image.min()) >= 0.0 and float(a.image.max()) <= 1.0 + 1e-5
+    far = wl.cameras[2]
+    c = sr.cull(_oracle_tables(wl.scene), far)
+    st = serial[2][1]
+    assert st.frustum_passed == int(np.count_nonzero(c.flags & 1))
+    assert st.mlp_queried == int(np.count_nonzero(c.flags & 2))
+    queried = (c.flags & 2) != 0
+    n_ref_culled = int(np.count_nonzero(queried & ~c.keep.astype(bool)))
+    near_threshold = int(np.count_nonzero(queried & (np.abs(c.logit) < LOGIT_MARGIN)))
+    assert abs(st.mlp_culled - n_ref_culled) <= near_threshold
+    del c
+    torch.cuda.empty_cache()

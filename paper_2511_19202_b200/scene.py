@@ -632,7 +632,7 @@ class Renderer:
                 done.record()
             pending[slot] = {"i": i, "ev0": ev0, "ev1": ev1, "host": host, "done": done}
 
-        def collect(i):
+        def collect(i, attempt=0):
             slot = i % F
             p = pending[slot]
             t_sync = time.perf_counter()
@@ -641,11 +641,13 @@ class Renderer:
             st = nat.stats_dict(p["host"]["stats"].numpy())
             _PINNED.give(p["host"]["stats"])
             if st["overflow"]:
+                if attempt >= 3:
+                    raise nat.NativeError("workspace overflow persists after regrowing")
                 # regrow this slot's workspace and re-render the frame on its stream
                 torch.cuda.synchronize()
                 self.workspace(cams[i], slot).grow(st["survivors"], max(st["entries"], st["block_entries"]))
                 launch(i)
-                return collect(i)
+                return collect(i, attempt + 1)
             n_s = st["survivors"]
             stats = FrameStats(frustum_passed=st["frustum_passed"], mlp_culled=st["mlp_culled"], instantiated=n_s,
                                used=st["used"] if opts.record_contributions else None,

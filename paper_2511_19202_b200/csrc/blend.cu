@@ -454,11 +454,24 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_
                                                      int stride, uint32_t *order)
 {
     __shared__ uint32_t hist[33], base[33];
+    constexpr int kPer = 16;   // tiles per thread kept in registers (one weight pass)
     if (threadIdx.x < 33) hist[threadIdx.x] = 0;
     __syncthreads();
-    for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-        const uint32_t c = tile_weight(off, tile_base + t, stride);
-        atomicAdd(&hist[c ? 32 - __clz(c) : 0], 1u);
+    uint32_t bucket[kPer];
+    for (int64_t t0 = 0; t0 < n_tiles; t0 += (int64_t)blockDim.x * kPer) {
+#pragma unroll
+        for (int q = 0; q < kPer; q++) {
+            const int64_t t = t0 + (int64_t)q * blockDim.x + threadIdx.x;
+            uint32_t b = 0xFFFFFFFFu;
+            if (t < n_tiles) {
+                const uint32_t c = tile_weight(off, tile_base + t, stride);
+                b = c ? 32 - __clz(c) : 0;
+            }
+            bucket[q] = b;
+            // warp-aggregated histogram: one shared atomic per distinct bucket in the warp
+            const uint32_t peers = __match_any_sync(0xffffffffu, b);
+            if (b != 0xFFFFFFFFu && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -469,9 +482,27 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_
         }
     }
     __syncthreads();
-    for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-        const uint32_t c = tile_weight(off, tile_base + t, stride);
-        order[atomicAdd(&base[c ? 32 - __clz(c) : 0], 1u)] = (uint32_t)(tile_base + t);
+    for (int64_t t0 = 0; t0 < n_tiles; t0 += (int64_t)blockDim.x * kPer) {
+        const bool single = n_tiles <= (int64_t)blockDim.x * kPer;   // weights still in registers
+#pragma unroll
+        for (int q = 0; q < kPer; q++) {
+            const int64_t t = t0 + (int64_t)q * blockDim.x + threadIdx.x;
+            uint32_t b = 0xFFFFFFFFu;
+            if (t < n_tiles) {
+                if (single) {
+                    b = bucket[q];
+                } else {
+                    const uint32_t c = tile_weight(off, tile_base + t, stride);
+                    b = c ? 32 - __clz(c) : 0;
+                }
+            }
+            const uint32_t peers = __match_any_sync(0xffffffffu, b);
+            uint32_t slot = 0;
+            const int leader = __ffs(peers) - 1;
+            if (b != 0xFFFFFFFFu && (int)(threadIdx.x & 31) == leader) slot = atomicAdd(&base[b], __popc(peers));
+            slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(peers & lanemask_lt());
+            if (b != 0xFFFFFFFFu) order[slot] = (uint32_t)(tile_base + t);
+        }
     }
 }
 

@@ -42,6 +42,8 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
     for (int64_t base = 0; base < scene.n_instances; base += 1024) {
         const int64_t i = base + tid;
         uint32_t nch = 0;
+        unsigned long long t_dlo = (unsigned long long)__double_as_longlong(INFINITY), t_dhi = 0ull, t_pairs = 0ull,
+                           t_vis = 0ull;
         if (i < scene.n_instances) {
             const sc_instance_rec &in = scene.instances[i];
             const sc_asset_rec &a = scene.assets[in.asset];
@@ -139,8 +141,8 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
             if (vis) {   // depth range of every instanced mean of a visible instance (frame-path sort keys)
                 const double lo = fmax(cz - rho * (1.0 + 1e-9), d_floor);
                 const double hi = fmax(cz + rho * (1.0 + 1e-9), lo);
-                atomicMin(&s_dlo, (unsigned long long)__double_as_longlong(lo));
-                atomicMax(&s_dhi, (unsigned long long)__double_as_longlong(hi));
+                t_dlo = (unsigned long long)__double_as_longlong(lo);
+                t_dhi = (unsigned long long)__double_as_longlong(hi);
             }
             fr.visible = vis;
             nch = vis ? (uint32_t)((a.count + kChunk - 1) / kChunk) : 0u;
@@ -148,8 +150,24 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
             fr.chunk_begin = 0;
             ws.inst[i] = fr;
             if (vis) {
-                atomicAdd(&s_pairs, (unsigned long long)a.count);
-                atomicAdd(&s_vis, 1ull);
+                t_pairs = (unsigned long long)a.count;
+                t_vis = 1ull;
+            }
+        }
+        // warp reductions, one shared atomic per warp (1,000 threads on one address serialise)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            t_dlo = min(t_dlo, __shfl_xor_sync(0xffffffffu, t_dlo, o));
+            t_dhi = max(t_dhi, __shfl_xor_sync(0xffffffffu, t_dhi, o));
+            t_pairs += __shfl_xor_sync(0xffffffffu, t_pairs, o);
+            t_vis += __shfl_xor_sync(0xffffffffu, t_vis, o);
+        }
+        if (lane == 0) {
+            if (t_vis) {
+                atomicMin(&s_dlo, t_dlo);
+                atomicMax(&s_dhi, t_dhi);
+                atomicAdd(&s_pairs, t_pairs);
+                atomicAdd(&s_vis, t_vis);
             }
         }
         // block exclusive scan of nch

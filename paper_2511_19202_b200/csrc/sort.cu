@@ -77,38 +77,30 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *in
     if (threadIdx.x == 0) part[blockIdx.x] = total;
 }
 
-// single block: exclusive scan of the block partials, total -> *total_out
-__global__ void __launch_bounds__(1024) k_scan_partials(uint32_t *part, int64_t nblk, unsigned long long *total_out,
-                                                        int64_t *stat_out)
-{
-    __shared__ uint32_t s_warp[32];
-    __shared__ uint32_t s_run;
-    if (threadIdx.x == 0) s_run = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < nblk; base += 1024) {
-        const int64_t i = base + threadIdx.x;
-        const uint32_t x = i < nblk ? part[i] : 0u;
-        uint32_t total;
-        const uint32_t e = block_excl_scan<1024>(x, s_warp, total);
-        if (i < nblk) part[i] = s_run + e;
-        __syncthreads();
-        if (threadIdx.x == 0) s_run += total;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        if (total_out) *total_out = s_run;
-        if (stat_out) *stat_out = (int64_t)s_run;
-    }
-}
-
+// Each block adds up the raw sums of the blocks before it (a few thousand L2-resident
+// words at most), so no single-CTA pass over the partials sits between the two kernels;
+// the last active block writes the total.
 __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t *in, uint32_t *out,
                                                             const unsigned long long *n_dev, int64_t n_host,
-                                                            const uint32_t *part)
+                                                            const uint32_t *part, unsigned long long *total_out,
+                                                            int64_t *stat_out)
 {
     __shared__ uint32_t s_warp[32];
     const int64_t n = dev_count(n_dev, n_host);
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    if (base >= n) return;
+    if (base >= n) {
+        if (n <= 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+            if (total_out) *total_out = 0;
+            if (stat_out) *stat_out = 0;
+        }
+        return;
+    }
+    uint32_t pre = 0;
+    {
+        uint32_t acc = 0;
+        for (int64_t i = threadIdx.x; i < (int64_t)blockIdx.x; i += kScanThreads) acc += __ldcg(part + i);
+        block_excl_scan<kScanThreads>(acc, s_warp, pre);   // pre = total over the block
+    }
     // blocked arrangement: thread t owns items [base + t*16, base + t*16 + 16), moved as 4 x uint4
     static_assert(kScanItems == 16, "vector path assumes 16 items per thread");
     uint32_t v[kScanItems];
@@ -128,7 +120,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t *in, 
 #pragma unroll
     for (int j = 0; j < kScanItems; j++) sum += v[j];
     uint32_t total;
-    uint32_t run = block_excl_scan<kScanThreads>(sum, s_warp, total) + part[blockIdx.x];
+    uint32_t run = block_excl_scan<kScanThreads>(sum, s_warp, total) + pre;
+    if (threadIdx.x == 0 && base + kScanTile >= n) {   // the last active block
+        if (total_out) *total_out = (unsigned long long)pre + total;
+        if (stat_out) *stat_out = (int64_t)pre + total;
+    }
 #pragma unroll
     for (int j = 0; j < kScanItems; j++) {
         const uint32_t x = v[j];
@@ -151,8 +147,7 @@ cudaError_t scan_excl(const uint32_t *in, uint32_t *out, const unsigned long lon
 {
     const int64_t nblk = std::max<int64_t>(1, (n_max + kScanTile - 1) / kScanTile);
     SC_LAUNCH(k_scan_reduce, (int)nblk, kScanThreads, 0, st, in, n_dev, n_max, part);
-    SC_LAUNCH(k_scan_partials, 1, 1024, 0, st, part, nblk, total_out, stat_out);
-    SC_LAUNCH(k_scan_down, (int)nblk, kScanThreads, 0, st, in, out, n_dev, n_max, part);
+    SC_LAUNCH(k_scan_down, (int)nblk, kScanThreads, 0, st, in, out, n_dev, n_max, part, total_out, stat_out);
     return cudaGetLastError();
 }
 

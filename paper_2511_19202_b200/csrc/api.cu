@@ -48,7 +48,7 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
-    size_t inst, chunk_state, chunk_cnt, chunk_stage, ctr, surv, splats, wins, key_a, key_b, pv_a, pv_b, depth64, rect, ecount, ekey_a, ekey_b,
+    size_t inst, chunk_state, chunk_cnt, chunk_inst, chunk_stage, ctr, surv, splats, wins, key_a, key_b, pv_a, pv_b, depth64, rect, ecount, ekey_a, ekey_b,
         eval_a, eval_b, tile_off, task_order, boff, rs_counts, scan_part, total;
     int64_t max_chunks, nblk_max, n_tiles;
     int n_tx, n_ty;
@@ -73,6 +73,7 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.inst = take(sizeof(sc::InstFrame) * (size_t)std::max<int64_t>(n_inst, 1));
     L.chunk_state = take(sizeof(unsigned long long) * (size_t)L.max_chunks);
     L.chunk_cnt = take(sizeof(uint32_t) * (size_t)L.max_chunks);
+    L.chunk_inst = take(sizeof(uint32_t) * (size_t)L.max_chunks);
     L.chunk_stage = take(sizeof(uint16_t) * (size_t)L.max_chunks * sc::kChunk);
     L.ctr = take(sizeof(sc::Counters));
     L.surv = take(sizeof(sc_survivor) * (size_t)capS);
@@ -111,6 +112,7 @@ int carve(const sc_workspace *ws, int32_t w, int32_t h, sc::Ws &out)
     out.inst = reinterpret_cast<sc::InstFrame *>(b + L.inst);
     out.chunk_state = reinterpret_cast<unsigned long long *>(b + L.chunk_state);
     out.chunk_cnt = reinterpret_cast<uint32_t *>(b + L.chunk_cnt);
+    out.chunk_inst = reinterpret_cast<uint32_t *>(b + L.chunk_inst);
     out.chunk_stage = reinterpret_cast<uint16_t *>(b + L.chunk_stage);
     out.ctr = reinterpret_cast<sc::Counters *>(b + L.ctr);
     out.surv = reinterpret_cast<sc_survivor *>(b + L.surv);

@@ -79,6 +79,7 @@ struct Ws {
     InstFrame *inst;                 // [n_instances]
     unsigned long long *chunk_state; // [max_chunks] (instance << 32) | chunk index within the instance
     uint32_t *chunk_cnt;             // [max_chunks] survivors per chunk -> exclusive offsets
+    uint32_t *chunk_inst;            // [max_chunks] the instance owning each chunk (k_chunk_map)
     uint16_t *chunk_stage;           // [max_chunks][kChunk] survivors of each chunk (offset in the chunk)
     Counters *ctr;
     sc_survivor *surv;               // [capS]

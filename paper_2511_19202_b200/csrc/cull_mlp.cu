@@ -207,10 +207,23 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
     }
 }
 
-#ifndef SC_CULL_CB
-#define SC_CULL_CB 0
-#endif
-constexpr int kCullCbSmem = SC_CULL_CB;   // instance chunk_begin table cached in shared memory up to this many
+
+// chunk -> owning instance: the last instance with chunk_begin <= chunk (one thread
+// per chunk, binary search; invisible instances own no chunk and share their
+// successor's chunk_begin, so "last" is the owner)
+__global__ void k_chunk_map(const InstFrame *__restrict__ inst, int64_t n_inst, const Counters *ctr,
+                            uint32_t *chunk_inst)
+{
+    const int64_t total = (int64_t)ctr->total_chunks;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < total; c += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = n_inst;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (inst[mid].chunk_begin <= (uint32_t)c) lo = mid; else hi = mid;
+        }
+        chunk_inst[c] = (uint32_t)lo;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Cull + MLP.  Persistent CTAs of 128 threads take chunks of kChunk pairs of
@@ -237,7 +250,6 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
     __shared__ uint32_t s_wcnt[kCullTilesPerChunk * kCullWarps];   // survivors per (tile, warp) segment
     __shared__ uint32_t s_segoff[kCullTilesPerChunk * kCullWarps];
     __shared__ uint32_t s_chunk, s_inst, s_nc;
-    __shared__ uint32_t s_cb[kCullCbSmem > 0 ? kCullCbSmem : 1];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     mlp_setup(sm, tid);
@@ -251,13 +263,6 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
     const bool banded = opts.band_y1 > 0;
     const double BY0 = (double)band.y0, BY1 = (double)band.y1;   // whole image: [0, TH)
 
-    // chunk -> instance: binary search over the instances' chunk_begin, from a
-    // shared-memory copy when the instance table is small (one load per
-    // instance per CTA), else from global memory
-    const int64_t n_inst = scene.n_instances;
-    const bool cb_smem = n_inst <= kCullCbSmem;
-    if (cb_smem)
-        for (int64_t i = tid; i < n_inst; i += kCullThreads) s_cb[i] = ws.inst[i].chunk_begin;
     // chunks are handed out by an atomic ticket (dynamic balance across CTAs)
     for (;;) {
         if (tid == 0) s_chunk = (uint32_t)atomicAdd(&ws.ctr->chunk_ticket, 1ull);
@@ -266,18 +271,9 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
         if (chunk >= total) break;
         if (tid < kCullTilesPerChunk * kCullWarps) s_wcnt[tid] = 0;   // tiles past the chunk end stay empty
         if (wid == 0) {
-            // last instance with chunk_begin <= chunk (lane 0), then the warp copies the
-            // instance, its asset and its frame records word by word (two load latencies)
-            int64_t lo = 0;
-            if (lane == 0) {
-                int64_t hi = n_inst;
-                while (hi - lo > 1) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    const uint32_t cb = cb_smem ? s_cb[mid] : ws.inst[mid].chunk_begin;
-                    if (cb <= chunk) lo = mid; else hi = mid;
-                }
-            }
-            lo = __shfl_sync(0xffffffffu, lo, 0);
+            // the chunk's instance (k_chunk_map), then the warp copies the instance, its asset
+            // and its frame records word by word (two load latencies)
+            const int64_t lo = (int64_t)ws.chunk_inst[chunk];
             static_assert(sizeof(sc_instance_rec) % 4 == 0 && sizeof(sc_asset_rec) % 4 == 0 &&
                               sizeof(InstFrame) % 4 == 0, "word copies");
             const uint32_t *gi = reinterpret_cast<const uint32_t *>(scene.instances + lo);
@@ -564,6 +560,8 @@ cudaError_t launch_prep(const sc_scene &scene, const sc_camera &cam, const sc_op
 cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
                         sc_survivor *out, int64_t cap, sc_frame_stats *stats, cudaStream_t st)
 {
+    SC_LAUNCH(k_chunk_map, (int)std::max<int64_t>(1, std::min<int64_t>((ws.max_chunks + 255) / 256, sm_count() * 8)),
+              256, 0, st, ws.inst, scene.n_instances, ws.ctr, ws.chunk_inst);
     const int grid = sm_count() * SC_CULL_CPS;   // CTAs per SM (32 TMEM columns each)
     SC_LAUNCH(k_cull, grid, kCullThreads, 0, st, scene, cam, opts, ws, out, (long long)cap, stats);
     cudaError_t e = scan_excl(ws.chunk_cnt, ws.chunk_cnt, &ws.ctr->total_chunks, ws.max_chunks, ws.scan_part,

@@ -47,6 +47,22 @@ def main():
     cases.append(("cloud_clip_112x80", d, ref.Camera.look_at([0.2, 1.2 * d.d_near, -0.4], [0, 0, 0],
                                                              math.radians(60), 112, 80),
                   dict(radius_clip=2.0, stop_transmittance=0.02)))
+    # higher SH degrees (the synthetic generators emit degree 0): the same assets with seeded
+    # degree-3 / degree-2 coefficients, rendered in full and with sh_degree_eval truncation
+    import dataclasses
+    rng = np.random.default_rng(11)
+    e0 = ref.prepare(synth.make_shell(2500, seed=6))
+    e = dataclasses.replace(e0, sh_degree=3, sh_coeffs=np.concatenate(
+        [e0.sh_coeffs, rng.normal(0.0, 0.25, (len(e0), 15, 3)).astype(np.float32)], axis=1))
+    cases.append(("shell_sh3_144x112", e, ref.Camera.look_at([0.6, -1.8 * e.d_near, 0.9], [0, 0, 0],
+                                                             math.radians(50), 144, 112),
+                  dict(record_contributions=True)))
+    f0 = ref.prepare(synth.make_random_cloud(2000, seed=7))
+    f = dataclasses.replace(f0, sh_degree=2, sh_coeffs=np.concatenate(
+        [f0.sh_coeffs, rng.normal(0.0, 0.3, (len(f0), 8, 3)).astype(np.float32)], axis=1))
+    cases.append(("cloud_sh2_eval1_120x90", f, ref.Camera.look_at([-1.4 * f.d_near, 0.5, 0.7], [0, 0, 0],
+                                                                  math.radians(55), 120, 90),
+                  dict(sh_degree_eval=1)))
     for name, asset, cam, kw in cases:
         out = ref.render(asset, cam, **kw)
         proj = raster.project_gaussians(asset, cam)

@@ -660,3 +660,28 @@ def test_config3_full_size_properties():
     assert abs(st.mlp_culled - n_ref_culled) <= near_threshold
     del c
     torch.cuda.empty_cache()
+
+
+def test_composed_sh3_instances_vs_oracle():
+    """Rotated, scaled instances of a degree-3 SH asset (the reference golden asset),
+    composed render vs the oracle's restatement: SH evaluated with the world-space
+    view direction on the stored coefficients, same survivors on both
+    sides (MLP off), image within the drop-in tolerance."""
+    import paper_2511_19202_b200 as pkg
+    from conftest import load_golden, look_at
+    from paper_2511_19202_b200.asset import prepare
+    from paper_2511_19202_b200.scene import ComposedScene, InstanceTransform
+    from paper_2511_19202_b200.workloads import random_unit_quats
+
+    asset, _cam, _opts, _z = load_golden("shell_sh3_144x112")
+    asset = prepare(asset)
+    sc = ComposedScene()
+    sc.add_asset(asset, None)
+    q = random_unit_quats(np.random.default_rng(3), 5)
+    for k in range(5):
+        sc.add_instance(0, InstanceTransform([2.5 * k - 5.0, 0.3 * k, 0.1 * k], q[k], 0.6 + 0.2 * k))
+    cam = look_at([0.0, -9.0, 3.0], [0.0, 0.5, 0.0], 55, 200, 140)
+    out, st = pkg.render_composed(sc, cam)
+    ref = sr.render_composed(sc, cam)
+    assert st.instantiated == ref.stats["instantiated"] and st.passed == ref.stats["passed"]
+    _image_close(out.image, ref.out.image)

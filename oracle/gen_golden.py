@@ -63,9 +63,13 @@ def main():
     cases.append(("cloud_sh2_eval1_120x90", f, ref.Camera.look_at([-1.4 * f.d_near, 0.5, 0.7], [0, 0, 0],
                                                                   math.radians(55), 120, 90),
                   dict(sh_degree_eval=1)))
+    g = ref.prepare(synth.make_random_cloud(1800, seed=8))
+    cases.append(("cloud_bg_dil_100x70", g, ref.Camera.look_at([0.9, -1.3 * g.d_near, -0.5], [0, 0, 0],
+                                                               math.radians(48), 100, 70),
+                  dict(background=(0.1, 0.2, 0.3), dilation=0.5)))
     for name, asset, cam, kw in cases:
         out = ref.render(asset, cam, **kw)
-        proj = raster.project_gaussians(asset, cam)
+        proj = raster.project_gaussians(asset, cam, kw.get("dilation", 0.3))
         valid = proj.valid.copy()
         if kw.get("radius_clip"):
             det = proj.cov2d[:, 0] * proj.cov2d[:, 2] - proj.cov2d[:, 1] ** 2

@@ -18,7 +18,7 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 GOLDEN_CASES = ["cloud3k_128", "shell4k_160x96", "slab_headon_96", "cloud_clip_112x80", "shell_sh3_144x112",
-                "cloud_sh2_eval1_120x90"]
+                "cloud_sh2_eval1_120x90", "cloud_bg_dil_100x70"]
 
 
 def pytest_configure(config):

@@ -156,10 +156,12 @@ cudaError_t scan_excl(const uint32_t *in, uint32_t *out, const unsigned long lon
 //   upsweep:   per 4096-key tile, digit counts -> counts[digit][tile]
 //   scan:      one exclusive scan over the digit-major matrix = every
 //              (digit, tile) global scatter base (no inter-tile chains)
-//   downsweep: persistent CTAs; a tile's keys/values arrive by TMA bulk copy
-//              into one of two shared buffers while the previous tile is
-//              ranked and scattered; stable warp-private ranking (match.any),
-//              staging in shared memory, digit-run coalesced write-out.
+//   downsweep: persistent CTAs taking tiles from an atomic ticket; a tile's
+//              keys/values arrive by TMA bulk copy into one of two shared
+//              buffers while the previous tile is ranked and scattered; stable
+//              warp-private ranking (8-ballot match, or match.any for the
+//              block sort's last pass), staging in shared memory, digit-run
+//              coalesced write-out.
 // ---------------------------------------------------------------------------
 constexpr int kOsThreads = 512;
 constexpr int kOsItems = 8;

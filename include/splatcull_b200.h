@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SC_ABI_VERSION 2
+#define SC_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define SC_API __attribute__((visibility("default")))
@@ -82,7 +82,9 @@ typedef struct sc_camera {
 
 /* Render options (reference render() keywords, sc/raster.py:240-251). Host struct. */
 typedef struct sc_opts {
-    int32_t tile_size;            /* must be 16 (the oracle's semantics depend on it) */
+    int32_t tile_size;            /* reference tile edge in pixels, 1..65535 (default 16; the image
+                                     depends on it, sc/raster.py:297-311, sc/_kernels.py:224-227);
+                                     screen bands need 16 */
     int32_t sh_degree_eval;       /* -1: use each asset's degree */
     int32_t record_contributions; /* per-splat max contribution + per-pixel sum */
     int32_t use_mlp;              /* 0: no MLP gate ("Ours w/o MLP") */
@@ -94,7 +96,7 @@ typedef struct sc_opts {
     double background[3];         /* (1, 1, 1) */
     double dilation;              /* 0.3 */
     double frustum_G;             /* Jacobian bound factor */
-    /* screen band [band_y0, band_y1) in pixel rows, multiples of the tile size
+    /* screen band [band_y0, band_y1) in pixel rows, band_y0 a multiple of 16
      * (band_y1 may be the image height); band_y1 <= 0: the whole image.  Only
      * the band's pixels are written; they are identical to the whole-image
      * render (the band's sub-frustum is a conservative superset). */
@@ -156,6 +158,7 @@ typedef struct sc_scene {
     const sc_vis_weights *vis_weights; /* [n_models] */
     int32_t n_models;
     int32_t reserved0;
+    int64_t n_pairs;             /* sum over instances of their asset's count (workspace check) */
 } sc_scene;
 
 /* Device-side counters of one frame (copy back with the stream). */
@@ -171,7 +174,8 @@ typedef struct sc_frame_stats {
     int64_t entries;             /* tile entries E */
     int64_t used;                /* splats with contribution_max > 0 (record mode) */
     int64_t max_tie_run;         /* longest run of equal f32 depth keys (tie-fix work) */
-    int64_t overflow;            /* bit0 survivors, bit1 entries, bit2 block lists: re-render with more capacity */
+    int64_t overflow;            /* bit0 survivors, bit1 entries, bit2 block lists, bit3 scene pairs beyond
+                                    the workspace's max_pairs: re-render with more capacity */
     int64_t block_entries;       /* frame path: (splat, 8x4 pixel block) entries binned for the blend */
     int64_t exact_fallbacks;     /* projections that fell back to the all-f64 path (exact_projection = 0) */
     int64_t reserved[2];
@@ -200,6 +204,18 @@ typedef struct sc_window { int16_t x0, x1, y0, y1; } sc_window;
 SC_API size_t sc_workspace_bytes(int64_t n_instances, int64_t max_pairs, int64_t cap_survivors,
                           int64_t cap_entries, int32_t width, int32_t height, int32_t tile_size);
 
+/* Optional frame-path internals copied out for parity tests (all device, NULL
+ * to skip each): the depth order and the per-(16x16 tile, 8x4 block) lists
+ * the blend walks.  Block b of tile t has id 8 t + b, b = 2 row + col (x in
+ * [8 col, 8 col + 7], y in [4 row, 4 row + 3] inside the 16x16 tile). */
+typedef struct sc_frame_debug {
+    uint32_t *order;          /* [cap_survivors]: passed survivors in (depth, index) order (stats.passed) */
+    uint32_t *block_offsets;  /* [8 n_tiles16 + 1]: list of block id k = [offsets[k], offsets[k + 1]) */
+    uint32_t *block_entries;  /* [cap_entries]: survivor index per block entry (stats.block_entries) */
+    uint32_t *block_codes;    /* [cap_entries]: block id << 10 | block-relative window
+                                 x0 | x1 << 3 | y0 << 6 | y1 << 8 */
+} sc_frame_debug;
+
 typedef struct sc_frame_out {
     float *image;                /* [H][W][3] f32, background composited */
     float *trans;                /* [H][W] f32 final transmittance */
@@ -213,6 +229,7 @@ typedef struct sc_frame_out {
     void *const *stage_events;
     int32_t n_stage_events;
     int32_t reserved0;
+    const sc_frame_debug *debug; /* optional (NULL) */
 } sc_frame_out;
 
 #define SC_STAGE_EVENTS 5
@@ -227,6 +244,13 @@ typedef struct sc_workspace {
 /* Whole frame: cull + MLP -> project -> sort/bin -> blend. */
 SC_API int sc_render_composed(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts,
                        const sc_workspace *ws, const sc_frame_out *out, void *stream);
+
+/* Stages (c)-(e) of the frame path on an explicit survivor list (device,
+ * n <= ws->cap_survivors, e.g. the oracle's cull): the same kernels as
+ * sc_render_composed after its cull, so stage-level parity tests can inject
+ * survivors into the benchmarked path. */
+SC_API int sc_render_survivors(const sc_scene *scene, const sc_survivor *survivors, int64_t n, const sc_camera *cam,
+                        const sc_opts *opts, const sc_workspace *ws, const sc_frame_out *out, void *stream);
 
 /* Stage (a)+(b): survivors in flat (instance, gaussian) order + stats. */
 SC_API int sc_cull_mlp(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts,

@@ -2,7 +2,7 @@
 container only; /root/reference does not exist on the GPU box).
 
     PYTHONDONTWRITEBYTECODE=1 NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python oracle/gen_golden.py
+        python oracle/gen_golden.py [case names]   (no names: every case)
 
 Writes tests/golden/*.npz: the inputs (asset arrays + camera) and the
 reference's outputs of project_kernel, the (depth, index) order, bin_tiles
@@ -67,7 +67,29 @@ def main():
     cases.append(("cloud_bg_dil_100x70", g, ref.Camera.look_at([0.9, -1.3 * g.d_near, -0.5], [0, 0, 0],
                                                                math.radians(48), 100, 70),
                   dict(background=(0.1, 0.2, 0.3), dilation=0.5)))
+    # tile sizes other than 16 (the image depends on the tile size: the composite window
+    # reaches one pixel past the tile rect, sc/_kernels.py:224-227), a non-power-of-two
+    # size, and a large dilation with splats straddling the image border
+    h = ref.prepare(synth.make_random_cloud(2200, seed=9))
+    cases.append(("cloud_ts8_120x88", h, ref.Camera.look_at([1.3 * h.d_near, -0.6, 0.4], [0, 0, 0],
+                                                            math.radians(52), 120, 88),
+                  dict(tile_size=8, record_contributions=True)))
+    k = ref.prepare(synth.make_shell(3000, seed=10))
+    cases.append(("shell_ts32_150x100", k, ref.Camera.look_at([0.2, 1.9 * k.d_near, -0.7], [0, 0, 0],
+                                                              math.radians(45), 150, 100),
+                  dict(tile_size=32)))
+    m = ref.prepare(synth.make_random_cloud(2000, seed=12))
+    cases.append(("cloud_ts12_100x76", m, ref.Camera.look_at([-0.9, -1.2 * m.d_near, 0.6], [0, 0, 0],
+                                                             math.radians(50), 100, 76),
+                  dict(tile_size=12, stop_transmittance=0.01)))
+    q = ref.prepare(synth.make_random_cloud(2400, seed=13))
+    cases.append(("cloud_dil15_border_96x72", q, ref.Camera.look_at([0.7 * q.d_near, 0.3, -0.2], [0, 0, 0],
+                                                                    math.radians(40), 96, 72),
+                  dict(dilation=1.5)))
+    only = set(sys.argv[1:])
     for name, asset, cam, kw in cases:
+        if only and name not in only:
+            continue
         out = ref.render(asset, cam, **kw)
         proj = raster.project_gaussians(asset, cam, kw.get("dilation", 0.3))
         valid = proj.valid.copy()
@@ -76,7 +98,7 @@ def main():
             valid &= ~(det < kw["radius_clip"])
         n = len(asset)
         idx = np.flatnonzero(valid)
-        ts = 16
+        ts = kw.get("tile_size", 16)
         n_tx = (cam.width + ts - 1) // ts
         n_ty = (cam.height + ts - 1) // ts
         tx0 = np.zeros(n, np.int64); tx1 = np.zeros(n, np.int64)
@@ -107,6 +129,8 @@ def main():
             passed_count=out.passed_count, skipped_count=out.skipped_count,
             asset_hash=np.uint64(ref.asset_hash(asset)))
         print(name, n, "passed", out.passed_count, "entries", entry_idx.size)
+    if only:
+        return
     # generator hashes (tests/test_synth.py pins the product generators to them)
     gens = {
         "shell_1000_s0": ref.asset_hash(synth.make_shell(1000, seed=0)),

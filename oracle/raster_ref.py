@@ -71,8 +71,10 @@ def lib():
         L.orc_instantiate.restype = None
         L.orc_instantiate.argtypes = [i64, P, P, P, P, P, P, P, P, i64, P, P, P, P, P]
         L.orc_scene_cull.restype = None
-        L.orc_scene_cull.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, i64, f64, i32, i32, f64,
+        L.orc_scene_cull.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, i64, f64, f64, i32, i32, f64,
                                      P, P, P]
+        L.orc_margin_pad.restype = f64
+        L.orc_margin_pad.argtypes = [f64]
         L.orc_mlp_forward.restype = None
         L.orc_mlp_forward.argtypes = [i64, P, P, i64, P, P]
         _lib = L

@@ -325,9 +325,18 @@ EXPORT void orc_instantiate(int64_t n_surv, const int64_t *surv_inst, const int6
     }
 }
 
+/* B3 margin pad in pixels: radius = ceil(3 sqrt(lambda)) <= 3 sigma (f / tz) G + 3 sqrt(dilation) + 1,
+ * so max(3, 3 sqrt(dilation) + 1 + 1e-6) covers every splat the rasterizer can pass (3 px at the
+ * default dilation 0.3).  Same expression as the device (common.cuh margin_pad). */
+EXPORT double orc_margin_pad(double dilation)
+{
+    double p = 3.0 * sqrt(dilation > 0.0 ? dilation : 0.0) + 1.0 + 1e-6;
+    return p > 3.0 ? p : 3.0;
+}
+
 /* B3 frustum predicate on the f32-rounded instanced mean (see scene_ref.py). */
-static inline int frustum_pass(const orc_camera *cam, const double mw[3], double sigma_w, double G, int strict,
-                               double *out_t /* tx, ty, tz */)
+static inline int frustum_pass(const orc_camera *cam, const double mw[3], double sigma_w, double G, double pad,
+                               int strict, double *out_t /* tx, ty, tz */)
 {
     const double *R = cam->rot;
     const double *c = cam->pos;
@@ -341,7 +350,7 @@ static inline int frustum_pass(const orc_camera *cam, const double mw[3], double
     if (strict) {
         return mx >= 0.0 && mx <= (double)(cam->width - 1) && my >= 0.0 && my <= (double)(cam->height - 1);
     }
-    double rb = 3.0 * (cam->focal / tz) * sigma_w * G + 3.0;
+    double rb = 3.0 * (cam->focal / tz) * sigma_w * G + pad;
     double tw = (double)(cam->tile_size * ((cam->width + cam->tile_size - 1) / cam->tile_size));
     double th = (double)(cam->tile_size * ((cam->height + cam->tile_size - 1) / cam->tile_size));
     return (mx + rb >= 0.0) && (mx - rb < tw) && (my + rb >= 0.0) && (my - rb < th);
@@ -383,9 +392,10 @@ EXPORT void orc_scene_cull(int64_t n_inst, const orc_instance *inst, const int64
                            const orc_asset *assets, const orc_camera *cam, const float *means,
                            const float *sigma_max, const double *features, const double *model_params,
                            const int64_t *model_param_offset, const int64_t *vis_widths, int64_t vis_layers,
-                           double G, int32_t strict, int32_t use_models, double logit_threshold,
-                           uint8_t *keep, uint8_t *flags, double *logit)
+                           double G, double dilation, int32_t strict, int32_t use_models,
+                           double logit_threshold, uint8_t *keep, uint8_t *flags, double *logit)
 {
+    const double pad = orc_margin_pad(dilation);
     for (int64_t i = 0; i < n_inst; i++) {
         const orc_instance *in = inst + i;
         const orc_asset *a = assets + in->asset;
@@ -403,7 +413,7 @@ EXPORT void orc_scene_cull(int64_t n_inst, const orc_instance *inst, const int64
             keep[pair] = 0;
             flags[pair] = 0;
             logit[pair] = NAN;
-            if (!frustum_pass(cam, mw, sigma_w, G, strict, tcam)) continue;
+            if (!frustum_pass(cam, mw, sigma_w, G, pad, strict, tcam)) continue;
             flags[pair] = 1;
             if (params == NULL) { keep[pair] = 1; continue; }
             double dx = mw[0] - cam->pos[0], dy = mw[1] - cam->pos[1], dz = mw[2] - cam->pos[2];

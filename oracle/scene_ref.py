@@ -16,8 +16,10 @@ Pinned decisions
   B3  frustum: on the f32 instanced mean, camera-space (tx, ty, tz) as the
       reference projection; cull if tz <= near; "margin" mode keeps a pair iff
       mx + Rb >= 0, mx - Rb < 16 n_tx, my + Rb >= 0, my - Rb < 16 n_ty with
-      Rb = 3 (f / tz) s sigma_max G + 3 px — a superset of the splats the
-      rasterizer passes, so culling never changes the image; "strict" mode
+      Rb = 3 (f / tz) s sigma_max G + pad, pad = max(3, 3 sqrt(dilation) + 1 +
+      1e-6) px (3 px at the default dilation), and 16 = the render tile size —
+      a superset of the splats the rasterizer passes, so culling never changes
+      the image; "strict" mode
       keeps a pair iff the mean projects inside [0, W-1] x [0, H-1].
   B4  direction input: R_i^T (m' - c) / |m' - c| (camera -> gaussian, local);
       forward input: R_i^T cam.forward.
@@ -188,10 +190,10 @@ def camera_record(cam, tile_size=16):
     return c
 
 
-def cull(tables: SceneTables, cam, frustum="margin", use_mlp=True) -> CullResult:
+def cull(tables: SceneTables, cam, frustum="margin", use_mlp=True, tile_size=16, dilation=0.3) -> CullResult:
     """Stages (a)+(b) for every (instance, gaussian) pair."""
     inst = tables.instances(cam)
-    camr = camera_record(cam)
+    camr = camera_record(cam, tile_size)
     n_pairs = int(tables.pair_offset[-1])
     keep = np.zeros(n_pairs, np.uint8)
     flags = np.zeros(n_pairs, np.uint8)
@@ -207,7 +209,8 @@ def cull(tables: SceneTables, cam, frustum="margin", use_mlp=True) -> CullResult
     rr.lib().orc_scene_cull(len(inst), _p(inst), _p(tables.pair_offset), _p(tables.asset_tab), _p(camr),
                             _p(tables.means), _p(tables.sigma_max), _p(tables.features), _p(tables.params),
                             _p(tables.param_offsets), _p(tables.vis_widths), len(tables.vis_widths) - 1,
-                            jacobian_bound(tx, ty), 1 if frustum == "strict" else 0, 1 if use_mlp else 0, thr,
+                            jacobian_bound(tx, ty), float(dilation), 1 if frustum == "strict" else 0,
+                            1 if use_mlp else 0, thr,
                             _p(keep), _p(flags), _p(logit))
     counts = np.array([len(tables.assets[a].means) for a, _ in tables.flat], dtype=np.int64)
     pair_inst = np.repeat(np.arange(len(tables.flat), dtype=np.int64), counts)
@@ -256,7 +259,8 @@ def render_composed(scene, cam, *, frustum="margin", use_mlp=True, tables: Scene
                     **render_kw) -> ComposedResult:
     """Oracle render_composed: cull + MLP, instantiate survivors, raster_ref.render."""
     tables = tables or SceneTables(scene)
-    c = cull(tables, cam, frustum=frustum, use_mlp=use_mlp)
+    c = cull(tables, cam, frustum=frustum, use_mlp=use_mlp, tile_size=render_kw.get("tile_size", 16),
+             dilation=render_kw.get("dilation", rr.COV_DILATION))
     m, ls, q, op, sh, deg = instantiate(tables, cam, c.surv_inst, c.surv_gid)
     stages = rr.Stages()
     out = rr.render_arrays(m, ls, q, op, sh, deg, cam, stages=stages, **render_kw)

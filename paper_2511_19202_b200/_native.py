@@ -22,7 +22,7 @@ if os.environ.get("SPLATCULL_B200_VARIANT"):         # A/B builds of kernel vari
     LIB_PATH = os.path.abspath(os.environ["SPLATCULL_B200_VARIANT"])
 
 SC_OK = 0
-ABI_VERSION = 2   # include/splatcull_b200.h SC_ABI_VERSION
+ABI_VERSION = 3   # include/splatcull_b200.h SC_ABI_VERSION
 SC_FRUSTUM_MARGIN, SC_FRUSTUM_STRICT, SC_FRUSTUM_OFF = 0, 1, 2
 
 c_f64, c_i32, c_i64, c_f32, c_u32, c_u16 = (ctypes.c_double, ctypes.c_int32, ctypes.c_int64,
@@ -63,7 +63,7 @@ class ScScene(ctypes.Structure):
     _fields_ = [("mean_opa", P), ("quat", P), ("scale_smax", P), ("sh", P), ("features", P),
                 ("n_gauss", c_i64), ("sh_stride", c_i32), ("n_assets", c_i32), ("assets", P),
                 ("instances", P), ("n_instances", c_i64), ("vis_weights", P), ("n_models", c_i32),
-                ("reserved0", c_i32)]
+                ("reserved0", c_i32), ("n_pairs", c_i64)]
 
 
 STATS_FIELDS = ("instances_visible", "pairs_tested", "frustum_passed", "mlp_queried", "mlp_culled",
@@ -88,9 +88,14 @@ class ScWindow(ctypes.Structure):
     _fields_ = [("x0", ctypes.c_int16), ("x1", ctypes.c_int16), ("y0", ctypes.c_int16), ("y1", ctypes.c_int16)]
 
 
+class ScFrameDebug(ctypes.Structure):
+    _fields_ = [("order", P), ("block_offsets", P), ("block_entries", P), ("block_codes", P)]
+
+
 class ScFrameOut(ctypes.Structure):
     _fields_ = [("image", P), ("trans", P), ("contrib_sum", P), ("contrib_max", P), ("stats", P),
-                ("survivors", P), ("stage_events", P), ("n_stage_events", c_i32), ("reserved0", c_i32)]
+                ("survivors", P), ("stage_events", P), ("n_stage_events", c_i32), ("reserved0", c_i32),
+                ("debug", P)]
 
 
 N_STAGE_EVENTS = 5
@@ -114,6 +119,7 @@ SIGNATURES = {
     "sc_kernel_launches": (c_i64, []),
     "sc_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32]),
     "sc_render_composed": (c_i32, [P, P, P, P, P, P]),
+    "sc_render_survivors": (c_i32, [P, P, c_i64, P, P, P, P, P]),
     "sc_cull_mlp": (c_i32, [P, P, P, P, P, c_i64, P, P]),
     "sc_project": (c_i32, [P, P, c_i64, P, P, P, P, P, P, P, P, P]),
     "sc_bin_sort": (c_i32, [P, P, c_i64, P, P, P, P, P, P, P, P, P, P]),

@@ -121,6 +121,7 @@ struct WalkCtx {
     const sc_window *__restrict__ wins;
     int blocks;
     int gx0, gy0;       // warp block origin, absolute pixels
+    int bx1, by1;       // last pixel column / row of the block inside its tile (tile lists)
     float fpx, fpy;     // this lane's pixel
     float stop_t;
     int record;
@@ -172,8 +173,8 @@ __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint
         if ((int64_t)v >= c.n_splats) return 0u;
         if (c.blocks) return code_mask(k & 0x3FFu);
         const uint2 w = __ldg(reinterpret_cast<const uint2 *>(c.wins + v));
-        const int x0 = max(lo16(w.x), c.gx0), x1 = min(hi16(w.x), c.gx0 + 7);
-        const int y0 = max(lo16(w.y), c.gy0), y1 = min(hi16(w.y), c.gy0 + 3);
+        const int x0 = max(lo16(w.x), c.gx0), x1 = min(hi16(w.x), c.bx1);
+        const int y0 = max(lo16(w.y), c.gy0), y1 = min(hi16(w.y), c.by1);
         if (x0 > x1 || y0 > y1) return 0u;
         return code_mask((uint32_t)((x0 - c.gx0) | ((x1 - c.gx0) << 3) | ((y0 - c.gy0) << 6) | ((y1 - c.gy0) << 8)));
     };
@@ -367,17 +368,19 @@ __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint
     __syncwarp();
 }
 
-// One CTA per 16x16 tile, warp w = 8x4 block w.  Frame path: the warp walks its
-// own (tile, block) list; stage-level API (tile lists): every warp walks the
-// whole tile list, clipping each record's window to its block.
+// Frame path: one CTA per 16x16 tile, warp w = 8x4 block w, walking its own
+// (tile, block) list.  Stage-level API (tile lists of ts x ts tiles): a tile is
+// covered by ceil(ts / 8) x ceil(ts / 4) 8x4 blocks (the last ones clipped to
+// the tile), 8 per CTA; every warp walks the whole tile list, clipping each
+// record's window to its block.
 __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
                                                       const uint32_t *__restrict__ offsets,
                                                       const uint32_t *__restrict__ vals,
                                                       const uint32_t *__restrict__ keys,
                                                       const sc_window *__restrict__ wins, int blocks,
                                                       const uint32_t *__restrict__ task_order, int tile_base,
-                                                      int width, int height,
-                                                      int n_tx, float stop_t, float bg_r, float bg_g, float bg_b,
+                                                      int width, int height, int n_tx, int ts, int nbx, int nblk,
+                                                      int ngroups, float stop_t, float bg_r, float bg_g, float bg_b,
                                                       int record, float *image, float *trans, float *csum,
                                                       float *cmax)
 {
@@ -403,13 +406,18 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     WalkStats d{0, 0, 0, 0};
     const long long d_t0 = clock64();
 #endif
-    const int tile = (int)(task_order ? task_order[blockIdx.x] : tile_base + (int)blockIdx.x);
-    const int b = wid;   // block within the tile
+    const int cta = (int)blockIdx.x / ngroups;
+    const int tile = (int)(task_order ? task_order[cta] : tile_base + cta);
+    const int b = ((int)blockIdx.x - cta * ngroups) * kBlendWarps + wid;   // block within the tile
+    if (b >= nblk) return;   // (no CTA barrier in this kernel)
     const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
-    c.gx0 = txi * kTile + (b & 1) * 8;
-    c.gy0 = tyi * kTile + (b >> 1) * 4;
+    const int byi = b / nbx, bxi = b - byi * nbx;
+    c.gx0 = txi * ts + bxi * 8;
+    c.gy0 = tyi * ts + byi * 4;
+    c.bx1 = min(c.gx0 + 7, txi * ts + ts - 1);
+    c.by1 = min(c.gy0 + 3, tyi * ts + ts - 1);
     const int px = c.gx0 + (lane & 7), py = c.gy0 + (lane >> 3);
-    const bool inside = px < width && py < height;
+    const bool inside = px <= c.bx1 && py <= c.by1 && px < width && py < height;
     c.fpx = (float)px;
     c.fpy = (float)py;
     PixAcc a{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, !inside};
@@ -521,20 +529,24 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
     constexpr int kSmem = (int)(kBlendWarps * kWarpSmem);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_blend, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    {
+        cudaError_t e = smem_attr_once(reinterpret_cast<const void *>(k_blend), kSmem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
-    const int n_tx = (cam.width + kTile - 1) / kTile;
-    const Band band = band_of(opts, cam.height);   // only the band's tiles are blended (and written)
+    // frame path: 16x16 CTA tiles of 8 blocks; tile lists: the reference's tile size
+    const int ts = lists.blocks ? kTile : opts.tile_size;
+    const int n_tx = (cam.width + ts - 1) / ts;
+    const int nbx = (ts + 7) / 8, nblk = nbx * ((ts + 3) / 4);
+    const int ngroups = (nblk + kBlendWarps - 1) / kBlendWarps;
+    const Band band = band_of(opts, cam.height, ts);   // only the band's tiles are blended (and written)
     const int64_t tile_base = (int64_t)band.t0 * n_tx, n_tiles = (int64_t)(band.t1 - band.t0) * n_tx;
     if (n_tiles <= 0) return cudaSuccess;
+    if (n_tiles * ngroups > 0x7FFFFFFFll) return cudaErrorInvalidValue;
     if (task_order)
         SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, tile_base, n_tiles, lists.blocks ? 8 : 1, task_order);
-    SC_LAUNCH(k_blend, (int)n_tiles, kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
+    SC_LAUNCH(k_blend, (int)(n_tiles * ngroups), kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
               lists.keys, lists.wins, lists.blocks ? 1 : 0, task_order, (int)tile_base, cam.width, cam.height, n_tx,
+              ts, nbx, nblk, ngroups,
               (float)opts.stop_transmittance, (float)opts.background[0], (float)opts.background[1],
               (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image, out.trans, out.contrib_sum,
               out.contrib_max);
@@ -557,10 +569,7 @@ __global__ void k_labels_or(const float *cmax, int64_t n, uint32_t *bits)
 cudaError_t launch_labels_or(const float *cmax, int64_t n, uint32_t *bits, cudaStream_t st)
 {
     if (n <= 0) return cudaSuccess;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)nsm * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8));
     SC_LAUNCH(k_labels_or, grid, 256, 0, st, cmax, n, bits);
     return cudaGetLastError();
 }
@@ -568,10 +577,7 @@ cudaError_t launch_labels_or(const float *cmax, int64_t n, uint32_t *bits, cudaS
 cudaError_t launch_count_used(const float *cmax, const unsigned long long *n_dev, int64_t n_max,
                               sc_frame_stats *stats, cudaStream_t st)
 {
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_max + 255) / 256, (int64_t)sm_count() * 8));
     SC_LAUNCH(k_count_used, grid, 256, 0, st, cmax, n_dev, n_max, stats);
     return cudaGetLastError();
 }

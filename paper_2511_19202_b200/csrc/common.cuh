@@ -8,7 +8,7 @@
 
 namespace sc {
 
-constexpr int kTile = 16;              // pixel tile edge (the oracle's tile_size)
+constexpr int kTile = 16;              // blend CTA tile edge (frame path; 8 warps of 8x4 pixel blocks)
 constexpr int kCullThreads = 128;      // one MLP row per thread (tcgen05 M = 128)
 constexpr int kCullTilesPerChunk = 8;  // chunk = 1024 (instance, gaussian) pairs
 constexpr int kChunk = kCullThreads * kCullTilesPerChunk;
@@ -35,23 +35,36 @@ struct InstFrame {
     int32_t gate;         // 1: every pair is queried (d_t >= d_near), 0: none, -1: per-pair f64 test
 };
 
-// Screen band of a render in pixel rows [y0, y1) and tile rows [t0, t1)
-// (sc_opts.band_*; the whole image when band_y1 <= 0).
+// Screen band of a render in pixel rows [y0, y1) and tile rows [t0, t1) of
+// `ts`-pixel tiles (sc_opts.band_*; the whole image [0, ts n_ty) when
+// band_y1 <= 0).  Bands need tile_size 16 (api.cu check_opts), so the band's
+// tile rows are also blend-CTA rows.
 struct Band {
     int y0, y1, t0, t1;
 };
-__host__ __device__ __forceinline__ Band band_of(const sc_opts &o, int height)
+__host__ __device__ __forceinline__ Band band_of(const sc_opts &o, int height, int ts)
 {
-    const int n_ty = (height + kTile - 1) / kTile;
-    Band b{0, n_ty * kTile, 0, n_ty};
+    const int n_ty = (height + ts - 1) / ts;
+    Band b{0, n_ty * ts, 0, n_ty};
     if (o.band_y1 > 0) {
-        b.t0 = o.band_y0 / kTile;
-        b.t1 = (o.band_y1 + kTile - 1) / kTile;
+        b.t0 = o.band_y0 / ts;
+        b.t1 = (o.band_y1 + ts - 1) / ts;
         b.t1 = b.t1 < n_ty ? b.t1 : n_ty;
-        b.y0 = b.t0 * kTile;
-        b.y1 = b.t1 * kTile;
+        b.y0 = b.t0 * ts;
+        b.y1 = b.t1 * ts;
     }
     return b;
+}
+
+// Margin-mode frustum pad in pixels (B3, oracle/sc_oracle.c:margin_pad): the
+// projected radius is ceil(3 sqrt(lambda)) with lambda <= (3 sigma f G / tz)^2
+// / 9 + dilation, so radius <= 3 sigma (f / tz) G + 3 sqrt(dilation) + 1;
+// at the default dilation 0.3 the pad is 3 px.  IEEE sqrt: identical on host
+// and device.
+__host__ __device__ __forceinline__ double margin_pad(double dilation)
+{
+    const double p = 3.0 * sqrt(dilation > 0.0 ? dilation : 0.0) + 1.0 + 1e-6;
+    return p > 3.0 ? p : 3.0;
 }
 
 // Internal counters block (device), zeroed per frame together with the stats.
@@ -92,13 +105,15 @@ struct Ws {
     uint32_t *ecount;                // [capS]  tile count -> exclusive offsets
     uint32_t *ekey_a, *ekey_b;       // [capE]
     uint32_t *eval_a, *eval_b;       // [capE]
-    uint32_t *tile_off;              // [n_tiles + 1]
+    uint32_t *tile_off;              // [n_tiles_ref + 1] stage API: reference tile offsets
     uint32_t *task_order;            // [n_tiles] blend dispatch order (heavy tiles first)
     uint32_t *boff;                  // [8 n_tiles + 1] offsets of the per-(tile, 8x4 block) entry lists
     uint32_t *rs_counts;             // radix pass digit counts -> bases, digit-major [256][nblk_max]
     uint32_t *scan_part;             // scan partials
-    int64_t capS, capE, max_chunks, nblk_max, n_tiles;
+    int64_t capS, capE, max_chunks, nblk_max, n_tiles;   // n_tiles: 16x16 blend tiles (frame path)
     int n_tx, n_ty;
+    int ts, n_tx_ref;                // reference tile size (sc_opts.tile_size) and its tile columns
+    int64_t n_tiles_ref;             // reference tiles (stage API binning)
 };
 
 // ------------------------------------------------------------------------
@@ -204,6 +219,11 @@ extern "C" void sc_note_launch(void);
 
 // internal launchers (host)
 namespace sc {
+// SM count of the current device (cached per device)
+int sm_count();
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the current device,
+// set once per device (the attribute is per device context)
+cudaError_t smem_attr_once(const void *func, int bytes);
 cudaError_t launch_prep(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
                         sc_frame_stats *stats, cudaStream_t st);
 cudaError_t launch_cull(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
@@ -223,7 +243,8 @@ cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const 
                           uint32_t *run_list, Counters *ctr, sc_frame_stats *stats, cudaStream_t st);
 cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                        int64_t n_max, const sc_camera &cam, const sc_window *wins, sc_frame_stats *stats, bool blocks,
-                       uint32_t **order_out, uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st);
+                       uint32_t **order_out, uint32_t **entries_out, uint32_t **keys_out, uint32_t *dbg_order,
+                       cudaStream_t st);
 // Blend input, one of:
 //  * block lists (frame path): boff [8 n_tiles + 1], vals = survivor per entry,
 //    keys = block id << 10 | block-relative window;

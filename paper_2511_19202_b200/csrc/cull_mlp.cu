@@ -36,9 +36,11 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
     __syncthreads();
     const double f = cam.focal;
     const double cxp = (double)(cam.width - 1) / 2.0, cyp = (double)(cam.height - 1) / 2.0;
-    const double TW = (double)(kTile * ((cam.width + kTile - 1) / kTile));
-    const Band band = band_of(opts, cam.height);
+    const int ts = opts.tile_size;
+    const double TW = (double)(ts * ((cam.width + ts - 1) / ts));
+    const Band band = band_of(opts, cam.height, ts);
     const bool banded = opts.band_y1 > 0;
+    const double PAD = margin_pad(opts.dilation);
     for (int64_t base = 0; base < scene.n_instances; base += 1024) {
         const int64_t i = base + tid;
         uint32_t nch = 0;
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
                        yhi = (double)(cam.height - 1);
                 if (opts.frustum_mode == SC_FRUSTUM_MARGIN) {
                     mg = 3.0 * f * opts.frustum_G * in.s * a.sigma_max * (1.0 + 1e-6);
-                    pad = 3.0;
+                    pad = PAD;
                     xhi = TW;
                     ylo = (double)band.y0;
                     yhi = (double)band.y1;
@@ -90,9 +92,9 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
             if (banded && opts.frustum_mode != SC_FRUSTUM_MARGIN && vis) {   // band rows, margin style
                 const double mgb = 3.0 * f * opts.frustum_G * in.s * a.sigma_max * (1.0 + 1e-6);
                 if (cz + rho <= cam.near_) vis = 0;
-                double kl = cyp + 3.0 - (double)band.y0;
+                double kl = cyp + PAD - (double)band.y0;
                 if (f * cy + kl * cz + mgb + rho * sqrt(f * f + kl * kl) < 0.0) vis = 0;
-                double kh = cyp - 3.0 - (double)band.y1;
+                double kh = cyp - PAD - (double)band.y1;
                 if (f * cy + kh * cz - mgb - rho * sqrt(f * f + kh * kh) > 0.0) vis = 0;
             }
             // Uniform instances (every pair decided the same way) skip the per-pair f64
@@ -196,7 +198,11 @@ __global__ void __launch_bounds__(1024) k_prep(sc_scene scene, sc_camera cam, sc
         __syncthreads();
     }
     if (tid == 0) {
-        ws.ctr->total_chunks = s_running;
+        // a scene with more pairs than the workspace was sized for (sc_scene.n_pairs
+        // understated): cull nothing rather than write past the chunk arrays
+        const bool fits = (int64_t)s_running <= ws.max_chunks;
+        if (!fits) atomicOr((unsigned long long *)&stats->overflow, 8ull);
+        ws.ctr->total_chunks = fits ? s_running : 0u;
         ws.ctr->chunk_ticket = 0;
         stats->instances_visible = (int64_t)s_vis;
         // frame-path depth keys: floor((tz - dmin) * scale) over [dmin, dmax] (k_project)
@@ -258,9 +264,11 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
     unsigned long long n_pass = 0, n_query = 0, n_cull = 0;
     const unsigned long long total = ws.ctr->total_chunks;
     const double cxp = (double)(cam.width - 1) / 2.0, cyp = (double)(cam.height - 1) / 2.0;
-    const double TW = (double)(kTile * ((cam.width + kTile - 1) / kTile));
-    const Band band = band_of(opts, cam.height);
+    const int ts = opts.tile_size;
+    const double TW = (double)(ts * ((cam.width + ts - 1) / ts));
+    const Band band = band_of(opts, cam.height, ts);
     const bool banded = opts.band_y1 > 0;
+    const double PAD = margin_pad(opts.dilation);
     const double BY0 = (double)band.y0, BY1 = (double)band.y1;   // whole image: [0, TH)
 
     // chunks are handed out by an atomic ticket (dynamic balance across CTAs)
@@ -328,7 +336,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
                                    my <= (double)(cam.height - 1);
                         } else {
                             const double sigma_w = s_in.s * (double)smax;
-                            const double rb = 3.0 * (cam.focal / tz) * sigma_w * opts.frustum_G + 3.0;
+                            const double rb = 3.0 * (cam.focal / tz) * sigma_w * opts.frustum_G + PAD;
                             pass = (mx + rb >= 0.0) && (mx - rb < TW) && (my + rb >= BY0) && (my - rb < BY1);
                         }
                     }
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
                         pass = false;
                         if (tz > cam.near_) {
                             const double my = cam.focal * (ty / tz) + cyp;
-                            const double rb = 3.0 * (cam.focal / tz) * (s_in.s * (double)smax) * opts.frustum_G + 3.0;
+                            const double rb = 3.0 * (cam.focal / tz) * (s_in.s * (double)smax) * opts.frustum_G + PAD;
                             pass = (my + rb >= BY0) && (my - rb < BY1);
                         }
                     }
@@ -538,18 +546,6 @@ __global__ void __launch_bounds__(256) k_encode_features(const float *params, co
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-static int sm_count()
-{
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
-
 cudaError_t launch_prep(const sc_scene &scene, const sc_camera &cam, const sc_opts &opts, const Ws &ws,
                         sc_frame_stats *stats, cudaStream_t st)
 {

@@ -68,8 +68,10 @@ __global__ void __launch_bounds__(256, 2) k_project(
     const int64_t n = from_list ? (int64_t)ctr->proj_deferred : n_surv;
     const double lim_x = 1.3 * cam.tan_x, lim_y = 1.3 * cam.tan_y;
     const double focal = cam.focal;
-    const int n_tx = (cam.width + kTile - 1) / kTile;
-    const Band band = band_of(opts, cam.height);
+    const int ts = opts.tile_size;
+    const int tsh = (ts & (ts - 1)) == 0 ? __ffs(ts) - 1 : -1;   // log2 of a power-of-two tile size
+    const int n_tx = (cam.width + ts - 1) / ts;
+    const Band band = band_of(opts, cam.height, ts);
     const double log_min_alpha = log(1.0 / 255.0);
     unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0, n_exact = 0;
     const bool fast = MODE == kProjFast || (MODE == kProjMixed && opts.exact_projection == 0);
@@ -251,22 +253,31 @@ __global__ void __launch_bounds__(256, 2) k_project(
             }
         }
         // --- tile rectangle (sc/raster.py:307-314) ---
-        // floor((m -+ r) / 16) == floor(m -+ r) >> 4: the f64 difference is rounded once
-        // either way, /16 is exact, and floor(floor(x) / 16) == floor(x / 16); the int
-        // conversions saturate, which the clamps below absorb
+        // power-of-two tile sizes: floor((m -+ r) / ts) == floor(m -+ r) >> log2(ts) (the
+        // f64 difference is rounded once either way, / 2^k is exact, and floor(floor(x) /
+        // 2^k) == floor(x / 2^k)); other sizes divide in f64 exactly as the reference.
+        // The int conversions saturate, which the clamps below absorb.
         int tx0 = 0, tx1 = 0, ty0 = 0, ty1 = 0;
         int fx0 = 0, fx1 = 0, fy0 = 0, fy1 = 0;   // floor(m - r), floor(m + r)
         bool passed = false;
         if (valid) {
-            fx0 = ifloor(mx - radius);
-            fx1 = ifloor(mx + radius);
-            fy0 = ifloor(my - radius);
-            fy1 = ifloor(my + radius);
-            tx0 = iclamp(fx0 >> 4, 0, n_tx);
-            tx1 = iclamp((fx1 >> 4) + 1, 0, n_tx);
+            const double vx0 = mx - radius, vx1 = mx + radius, vy0 = my - radius, vy1 = my + radius;
+            fx0 = ifloor(vx0);
+            fx1 = ifloor(vx1);
+            fy0 = ifloor(vy0);
+            fy1 = ifloor(vy1);
+            int qx0, qx1, qy0, qy1;
+            if (tsh >= 0) {
+                qx0 = fx0 >> tsh; qx1 = fx1 >> tsh; qy0 = fy0 >> tsh; qy1 = fy1 >> tsh;
+            } else {
+                const double dts = (double)ts;
+                qx0 = ifloor(vx0 / dts); qx1 = ifloor(vx1 / dts); qy0 = ifloor(vy0 / dts); qy1 = ifloor(vy1 / dts);
+            }
+            tx0 = iclamp(qx0, 0, n_tx);
+            tx1 = iclamp(min(qx1, 0x7FFFFFFE) + 1, 0, n_tx);
             // tile rows clamp to the band (the whole image: [0, n_ty))
-            ty0 = iclamp(fy0 >> 4, band.t0, band.t1);
-            ty1 = iclamp((fy1 >> 4) + 1, band.t0, band.t1);
+            ty0 = iclamp(qy0, band.t0, band.t1);
+            ty1 = iclamp(min(qy1, 0x7FFFFFFE) + 1, band.t0, band.t1);
             passed = tx1 > tx0 && ty1 > ty0;
         }
         n_passed += passed;
@@ -361,10 +372,10 @@ __global__ void __launch_bounds__(256, 2) k_project(
             }
             // integer form of max(floor(m - r), ceil(m - e), 16 t0) / min(floor(m + r) + 1,
             // floor(m + e), 16 t1 - 1), clamped to the int16 window range [-1, 32767]
-            win.x0 = (int16_t)iclamp(max(max(fx0, iceil(mx - ex)), kTile * tx0), -1, 32767);
-            win.x1 = (int16_t)iclamp(min(min(min(fx1, 0x7FFFFFFE) + 1, ifloor(mx + ex)), kTile * tx1 - 1), -1, 32767);
-            win.y0 = (int16_t)iclamp(max(max(fy0, iceil(my - ey)), kTile * ty0), -1, 32767);
-            win.y1 = (int16_t)iclamp(min(min(min(fy1, 0x7FFFFFFE) + 1, ifloor(my + ey)), kTile * ty1 - 1), -1, 32767);
+            win.x0 = (int16_t)iclamp(max(max(fx0, iceil(mx - ex)), ts * tx0), -1, 32767);
+            win.x1 = (int16_t)iclamp(min(min(min(fx1, 0x7FFFFFFE) + 1, ifloor(mx + ex)), ts * tx1 - 1), -1, 32767);
+            win.y0 = (int16_t)iclamp(max(max(fy0, iceil(my - ey)), ts * ty0), -1, 32767);
+            win.y1 = (int16_t)iclamp(min(min(min(fy1, 0x7FFFFFFE) + 1, ifloor(my + ey)), ts * ty1 - 1), -1, 32767);
         } else {   // never composited
             win.x0 = 1;
             win.x1 = 0;
@@ -422,9 +433,7 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
                            Counters *ctr, uint32_t *defer_list, cudaStream_t st)
 {
     if (n_max <= 0) return cudaSuccess;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int nsm = sm_count();
 #ifndef SC_PROJ_GRID
 #define SC_PROJ_GRID 8
 #endif
@@ -674,9 +683,7 @@ cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const 
                           uint32_t *run_list, Counters *ctr, sc_frame_stats *stats, cudaStream_t st)
 {
     if (n_max <= 0) return cudaSuccess;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int nsm = sm_count();
     const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * 16);
     const int64_t hblocks = std::min<int64_t>((n_max + 2047) / 2048, (int64_t)nsm * 8);
     SC_LAUNCH(k_tie_heads, (int)std::max<int64_t>(1, hblocks), 256, 0, st, keys, n_dev, n_max, run_list, ctr);

@@ -475,32 +475,15 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
 template <typename V>
 static cudaError_t radix_down_attr()
 {
-    static bool done = false;
-    if (done) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_radix_down<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(OsSmem<V>));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_radix_down<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(OsSmem<V>));
+    const int bytes = (int)sizeof(OsSmem<V>);
+    cudaError_t e = smem_attr_once(reinterpret_cast<const void *>(k_radix_down<V, false>), bytes);
+    if (e == cudaSuccess) e = smem_attr_once(reinterpret_cast<const void *>(k_radix_down<V, true>), bytes);
     if constexpr (std::is_same<V, uint2>::value)
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_radix_down<V, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(OsSmem<V>));
-    if (e == cudaSuccess) done = true;
+        if (e == cudaSuccess) e = smem_attr_once(reinterpret_cast<const void *>(k_radix_down<V, false, true>), bytes);
     return e;
 }
 
-static int sm_count_sort()
-{
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+static int sm_count_sort() { return sm_count(); }
 
 // Sorts (keys, vals) on key bits [bit_lo, bit_hi) (bits below bit_lo ride
 // along); the result ends in the buffers returned through keys_res / vals_res
@@ -835,7 +818,8 @@ static int bits_for(int64_t n)
 // exactly bin_tiles' output.
 cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                        int64_t n_max, const sc_camera &cam, const sc_window *wins, sc_frame_stats *stats, bool blocks,
-                       uint32_t **order_out, uint32_t **entries_out, uint32_t **keys_out, cudaStream_t st)
+                       uint32_t **order_out, uint32_t **entries_out, uint32_t **keys_out, uint32_t *dbg_order,
+                       cudaStream_t st)
 {
     cudaError_t e;
     uint32_t *keys_s = nullptr;
@@ -851,6 +835,8 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
     e = launch_tiefix(scene, surv, cam, keys_s, pv_s, blocks ? nullptr : ws.depth64, p_dev, n_max, ws.ecount, ws.ctr,
                       stats, st);
     if (e != cudaSuccess) return e;
+    if (dbg_order)   // debug copy-out of the (depth, index) order of the passed survivors
+        SC_LAUNCH(k_extract_order, grid_for(n_max, 256), 256, 0, st, pv_s, p_dev, n_max, dbg_order);
     uint32_t *ek = nullptr, *ev = nullptr;
     if (blocks) {
         // per-tile entry totals (ws.ecount, free after the tie-fix) -> tile offsets -> emission
@@ -880,13 +866,13 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
         SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, ws.ecount, rlo, rhi);
         e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, &stats->entries, st);
         if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max, ws.n_tx,
-                  ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
+        SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max,
+                  ws.n_tx_ref, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
         e = radix_sort<uint32_t>(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, 0,
-                                 std::max(1, bits_for(ws.n_tiles)), ws, &ek, &ev, st);
+                                 std::max(1, bits_for(ws.n_tiles_ref)), ws, &ek, &ev, st);
         if (e != cudaSuccess) return e;
         SC_LAUNCH(k_tile_offsets, grid_for(ws.capE + 1, 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE,
-                  ws.n_tiles, ws.tile_off);
+                  ws.n_tiles_ref, ws.tile_off);
         if (order_out) *order_out = order;
     }
     *entries_out = ev;

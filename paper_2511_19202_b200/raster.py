@@ -38,15 +38,55 @@ class RenderOutput:
     skipped_count: int
 
 
+_RENDERERS: list = []   # [(weakref(asset), fingerprint, Renderer)], most recent last
+_MAX_CACHED = 4
+
+
+def _asset_fingerprint(asset) -> tuple:
+    arrs = (asset.means, asset.log_scales, asset.rotations, asset.opacity_logits, asset.sh_coeffs)
+    return tuple((a.__array_interface__["data"][0], a.shape, a.dtype.str) for a in map(np.asarray, arrs)) + \
+        (int(asset.sh_degree),)
+
+
+def _renderer_for(asset):
+    """The cached single-instance Renderer of ``asset`` (device scene + workspaces), built
+    on first use.  Like the reference an Asset is immutable once rendered:
+    the cache is keyed by the asset object and its array buffers, not their contents."""
+    import weakref
+
+    import torch
+
+    from .scene import ComposedScene, InstanceTransform, Renderer
+
+    fp = _asset_fingerprint(asset)
+    dev = torch.cuda.current_device()
+    for k, (ref, f, r) in enumerate(_RENDERERS):
+        if ref() is asset and f == fp and r.dscene.device.index == dev:
+            _RENDERERS.append(_RENDERERS.pop(k))
+            return r
+    scene = ComposedScene()
+    scene.add_asset(asset)
+    scene.add_instance(0, InstanceTransform.identity())
+    r = Renderer(scene)
+    _RENDERERS.append((weakref.ref(asset), fp, r))
+    while len(_RENDERERS) > _MAX_CACHED or (_RENDERERS and _RENDERERS[0][0]() is None):
+        _RENDERERS.pop(0)
+    return r
+
+
 def render(asset, cam, *, sh_degree_eval: int | None = None, record_contributions: bool = False,
            radius_clip: float | None = None, tile_size: int = 16,
            stop_transmittance: float = STOP_TRANSMITTANCE, background=(1.0, 1.0, 1.0),
            dilation: float = COV_DILATION) -> RenderOutput:
-    """Rasterize one asset on the GPU (reference signature, sc/raster.py:240-251)."""
-    from .scene import ComposedScene, InstanceTransform, Renderer, RenderOptions
+    """Rasterize one asset on the GPU (reference signature, sc/raster.py:240-251).
 
-    if tile_size != 16:
-        raise ValueError("tile_size must be 16 (the reference's default; tile size changes the image)")
+    Any positive ``tile_size`` (the image depends on it, as in the reference).
+    The uploaded asset and the frame workspace are cached across calls on the
+    same Asset object.
+    """
+    from .scene import RenderOptions, check_tile_size
+
+    tile_size = check_tile_size(tile_size)
     if len(asset) == 0:
         h, w = int(cam.height), int(cam.width)
         bg = np.asarray(background, dtype=np.float32)
@@ -54,13 +94,10 @@ def render(asset, cam, *, sh_degree_eval: int | None = None, record_contribution
                             np.zeros(0, np.float32) if record_contributions else None,
                             np.zeros((h, w), np.float32) if record_contributions else None,
                             0 if record_contributions else None, 0, 0)
-    scene = ComposedScene()
-    scene.add_asset(asset)
-    scene.add_instance(0, InstanceTransform.identity())
     opts = RenderOptions(sh_degree_eval=sh_degree_eval, record_contributions=record_contributions,
                          radius_clip=radius_clip, tile_size=tile_size, stop_transmittance=stop_transmittance,
                          background=tuple(background), dilation=dilation, use_mlp=False, frustum="off")
-    out, _stats = Renderer(scene).render(cam, opts)
+    out, _stats = _renderer_for(asset).render(cam, opts)
     return out
 
 

@@ -178,18 +178,19 @@ class RenderOptions:
     band: tuple | None = None        # (y0, y1) pixel rows, y0 a multiple of 16: render only this screen band
 
     def struct(self, cam) -> nat.ScOpts:
-        if self.tile_size != 16:
-            raise ValueError("tile_size must be 16 (the oracle's tile semantics; see DESIGN.md)")
+        ts = check_tile_size(self.tile_size)
         if self.frustum not in FRUSTUM_MODES:
             raise ValueError(f"frustum must be one of {sorted(FRUSTUM_MODES)}")
         o = nat.ScOpts()
-        o.tile_size = 16
+        o.tile_size = ts
         o.sh_degree_eval = -1 if self.sh_degree_eval is None else int(self.sh_degree_eval)
         o.record_contributions = 1 if self.record_contributions else 0
         o.use_mlp = 1 if self.use_mlp else 0
         o.frustum_mode = FRUSTUM_MODES[self.frustum]
         o.exact_projection = 1 if self.exact_projection else 0
         if self.band is not None:
+            if ts != 16:
+                raise ValueError("screen bands need tile_size 16")
             y0, y1 = int(self.band[0]), int(self.band[1])
             if y0 < 0 or y0 % 16 or y1 <= y0 or y0 >= int(cam.height):
                 raise ValueError(f"band must be (y0, y1) with 0 <= y0 < height, y0 % 16 == 0, y1 > y0; got {self.band}")
@@ -200,6 +201,16 @@ class RenderOptions:
         o.dilation = float(self.dilation)
         o.frustum_G = frustum_G(cam)
         return o
+
+
+def check_tile_size(tile_size) -> int:
+    """The reference accepts any positive tile size (sc/raster.py:245, :297-311); the image depends on it."""
+    if isinstance(tile_size, bool) or int(tile_size) != tile_size:
+        raise ValueError(f"tile_size must be an integer, got {tile_size!r}")
+    ts = int(tile_size)
+    if not 1 <= ts <= 65535:
+        raise ValueError(f"tile_size must be in [1, 65535], got {ts}")
+    return ts
 
 
 def frustum_G(cam) -> float:
@@ -247,6 +258,9 @@ class DeviceScene:
 
         nat.load()
         self.device = torch.device(device or "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self._scene_version = scene._version
         assets = scene.assets
         if not assets:
             raise ValueError("scene has no assets")
@@ -309,6 +323,15 @@ class DeviceScene:
             wrecs[k] = vis_weights_struct(m)
 
         dev = self.device
+        with torch.cuda.device(dev):
+            self._upload(mean_opa, quat, scale_smax, sh, arecs, irecs, wrecs, n, flat, models, counts, offsets,
+                         sh_stride, feat_jobs, assets)
+
+    def _upload(self, mean_opa, quat, scale_smax, sh, arecs, irecs, wrecs, n, flat, models, counts, offsets,
+                sh_stride, feat_jobs, assets):
+        import torch
+
+        dev = self.device
         T = torch.from_numpy
         self.mean_opa = T(mean_opa).to(dev)
         self.quat = T(quat).to(dev)
@@ -323,7 +346,7 @@ class DeviceScene:
         self.sh_stride = sh_stride
         self.asset_offsets = offsets
         self.inst_asset = np.array([ai for ai, _ in flat], dtype=np.int64)
-        self.scene_version = scene._version
+        self.scene_version = self._scene_version
         for lo, hi, m, a in feat_jobs:
             self.features[lo:hi] = encode_features_device(m, a, dev)
         self.struct = nat.ScScene()
@@ -333,6 +356,7 @@ class DeviceScene:
         s.n_gauss, s.sh_stride, s.n_assets = n, sh_stride, len(assets)
         s.assets, s.instances, s.n_instances = nat.ptr(self.assets_t), nat.ptr(self.instances_t), len(flat)
         s.vis_weights, s.n_models = nat.ptr(self.weights_t), len(models)
+        s.n_pairs = self.max_pairs
         self.payload_bytes = [44 + 12 * (a.asset.sh_degree + 1) ** 2 for a in assets]
 
 
@@ -353,8 +377,9 @@ class Workspace:
     """Device workspace sized from the previous frame's counts (grows on overflow)."""
 
     def __init__(self, dscene: DeviceScene, width: int, height: int, cap_s: int | None = None,
-                 cap_e: int | None = None):
+                 cap_e: int | None = None, tile_size: int = 16):
         self.dscene, self.width, self.height = dscene, int(width), int(height)
+        self.tile_size = check_tile_size(tile_size)
         mp = max(1, dscene.max_pairs)
         self.cap_s = int(cap_s if cap_s is not None else min(mp, 1 << 24))
         self.cap_e = int(cap_e if cap_e is not None else max(4 * self.cap_s, 1 << 16))
@@ -365,7 +390,7 @@ class Workspace:
 
         lib = nat.load()
         nbytes = lib.sc_workspace_bytes(self.dscene.n_instances, self.dscene.max_pairs, self.cap_s, self.cap_e,
-                                        self.width, self.height, 16)
+                                        self.width, self.height, self.tile_size)
         if nbytes == 0:
             raise ValueError("invalid workspace request")
         self.buf = torch.empty(int(nbytes), dtype=torch.uint8, device=self.dscene.device)
@@ -459,139 +484,237 @@ def _to_pinned(t):
     return h
 
 
+class _StageEvents:
+    """Five timing events the library records at the stage boundaries of one frame
+    (frame start, after cull + MLP, projection, sort / binning, blend), reused
+    frame after frame by one workspace slot."""
+
+    def __init__(self):
+        import torch
+
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(nat.N_STAGE_EVENTS)]
+        for ev in self.events:
+            ev.record()   # torch creates the CUDA event lazily
+        self.handles = (ctypes.c_void_p * nat.N_STAGE_EVENTS)(*[ev.cuda_event for ev in self.events])
+
+    def timings(self) -> tuple[float, float, float]:
+        """(render_ms, mlp_ms, preprocess_ms) of the last recorded frame (its events have completed):
+        the whole frame, the cull + MLP stage, and projection + sort / binning."""
+        e = self.events
+        return (float(e[0].elapsed_time(e[4])), float(e[0].elapsed_time(e[1])), float(e[1].elapsed_time(e[3])))
+
+
+def _frame_stats(st: dict, timings, payload: int, record: bool) -> FrameStats:
+    render_ms, mlp_ms, pre_ms = timings
+    return FrameStats(frustum_passed=st["frustum_passed"], mlp_culled=st["mlp_culled"], instantiated=st["survivors"],
+                      used=st["used"] if record else None, mem_bytes_instantiated=payload, render_ms=render_ms,
+                      mlp_ms=mlp_ms, preprocess_ms=pre_ms, mlp_queried=st["mlp_queried"],
+                      instances_visible=st["instances_visible"], pairs_tested=st["pairs_tested"], passed=st["passed"],
+                      skipped=st["skipped"], entries=st["entries"], max_tie_run=st["max_tie_run"],
+                      block_entries=st["block_entries"], exact_fallbacks=st["exact_fallbacks"])
+
+
+class FrameDebug:
+    """Device buffers for the frame path's internals (sc_frame_debug): the
+    (depth, index) order of the passed survivors and the per-(16x16 tile, 8x4
+    block) entry lists the blend walks.  Parity tests only."""
+
+    def __init__(self, ws: Workspace):
+        import torch
+
+        dev = ws.dscene.device
+        n_tiles16 = ((ws.width + 15) // 16) * ((ws.height + 15) // 16)
+        self.order = torch.empty(max(ws.cap_s, 1), dtype=torch.int32, device=dev)
+        self.block_offsets = torch.empty(8 * n_tiles16 + 1, dtype=torch.int32, device=dev)
+        self.block_entries = torch.empty(max(ws.cap_e, 1), dtype=torch.int32, device=dev)
+        self.block_codes = torch.empty(max(ws.cap_e, 1), dtype=torch.int32, device=dev)
+        self.struct = nat.ScFrameDebug()
+        d = self.struct
+        d.order, d.block_offsets = nat.ptr(self.order), nat.ptr(self.block_offsets)
+        d.block_entries, d.block_codes = nat.ptr(self.block_entries), nat.ptr(self.block_codes)
+
+    def host(self, stats: dict) -> dict:
+        """numpy copies: order [passed], block offsets, entries / codes [block_entries] (uint32 as int64)."""
+        u = lambda t, n: t[:n].cpu().numpy().view(np.uint32).astype(np.int64)   # noqa: E731
+        nb = stats["block_entries"]
+        return {"order": u(self.order, stats["passed"]),
+                "block_offsets": u(self.block_offsets, self.block_offsets.numel()),
+                "block_entries": u(self.block_entries, nb), "block_codes": u(self.block_codes, nb)}
+
+
 class Renderer:
-    """Renders frames of one ComposedScene on one GPU."""
+    """Renders frames of one ComposedScene on one GPU (the scene's device)."""
 
     def __init__(self, scene: ComposedScene, device=None):
         self.scene = scene
         self.dscene = DeviceScene(scene, device)
-        self.workspaces: dict[tuple[int, int], Workspace] = {}
+        self.workspaces: dict[tuple, Workspace] = {}
         self._path_streams: list = []
         self._path_frames: dict = {}
+        self._events: dict = {}
         self.path_wait_s = 0.0   # host time render_path spent waiting on frames (diagnostics)
 
-    def workspace(self, cam, slot: int = 0) -> Workspace:
-        """The workspace of this resolution (``slot`` > 0: one more per frame in flight)."""
-        key = (int(cam.width), int(cam.height)) + ((int(slot),) if slot else ())
+    @staticmethod
+    def ws_key(cam, slot: int = 0, tile_size: int = 16) -> tuple:
+        return (int(cam.width), int(cam.height), int(slot), int(tile_size))
+
+    def workspace(self, cam, slot: int = 0, tile_size: int = 16) -> Workspace:
+        """The workspace of this resolution / tile size (``slot`` > 0: one more per frame in flight)."""
+        key = self.ws_key(cam, slot, tile_size)
         if key not in self.workspaces:
-            base = self.workspaces.get(key[:2]) if slot else None   # extra slots start at slot 0's capacities
+            base = self.workspaces.get(self.ws_key(cam, 0, tile_size)) if slot else None   # extra slots start at slot 0's
             self.workspaces[key] = Workspace(self.dscene, int(cam.width), int(cam.height),
-                                             cap_s=base.cap_s if base else None, cap_e=base.cap_e if base else None)
+                                             cap_s=base.cap_s if base else None, cap_e=base.cap_e if base else None,
+                                             tile_size=tile_size)
         return self.workspaces[key]
 
-    def render_device(self, cam, opts: RenderOptions | None = None, out: DeviceFrame | None = None,
-                      return_survivors: bool = False, stage_events=None, slot: int = 0) -> DeviceFrame:
-        """Enqueue one frame on the current stream; no host synchronisation.
+    def stage_events(self, slot: int = 0) -> _StageEvents:
+        if slot not in self._events:
+            import torch
 
-        ``stage_events``: optional 5 timing-enabled torch.cuda.Event objects,
-        recorded by the library at the stage boundaries (frame start, after
-        cull+MLP, projection, sort/binning, blend).  ``slot``: which of the
-        per-frame-in-flight workspaces to use (frames rendered concurrently on
-        different streams need different slots).
+            with torch.cuda.device(self.dscene.device):
+                self._events[slot] = _StageEvents()
+        return self._events[slot]
+
+    def render_device(self, cam, opts: RenderOptions | None = None, out: DeviceFrame | None = None,
+                      return_survivors: bool = False, stage_events=None, slot: int = 0,
+                      survivors=None, debug: FrameDebug | None = None) -> DeviceFrame:
+        """Enqueue one frame on the current stream of the scene's device; no host synchronisation.
+
+        ``stage_events``: optional 5 timing-enabled torch.cuda.Event objects (or a
+        _StageEvents), recorded by the library at the stage boundaries (frame
+        start, after cull+MLP, projection, sort/binning, blend).  ``slot``: which
+        of the per-frame-in-flight workspaces to use (frames rendered
+        concurrently on different streams need different slots).
+        ``survivors``: an explicit (S, 2) int32 [instance, gaussian] device list
+        rendered through stages (c)-(e) of the frame path instead of the cull
+        (sc_render_survivors).  ``debug``: FrameDebug buffers to copy the depth
+        order and block lists into.
         """
         import torch
 
         opts = opts or RenderOptions()
         lib = nat.load()
-        ws = self.workspace(cam, slot)
         dev = self.dscene.device
-        h, w = int(cam.height), int(cam.width)
-        if out is None or out.image.shape != (h, w, 3):
-            out = DeviceFrame(torch.empty((h, w, 3), dtype=torch.float32, device=dev),
-                              torch.empty((h, w), dtype=torch.float32, device=dev),
-                              torch.empty(nat.STATS_BYTES, dtype=torch.uint8, device=dev))
-        if opts.record_contributions:
-            if out.contrib_sum is None or out.contrib_sum.shape != (h, w):
-                out.contrib_sum = torch.empty((h, w), dtype=torch.float32, device=dev)
-            if out.contrib_max is None or out.contrib_max.numel() != ws.cap_s:
-                out.contrib_max = torch.empty(ws.cap_s, dtype=torch.float32, device=dev)
-        if return_survivors and (out.survivors is None or out.survivors.shape[0] != ws.cap_s):
-            out.survivors = torch.empty((ws.cap_s, 2), dtype=torch.int32, device=dev)
-        fo = nat.ScFrameOut()
-        fo.image, fo.trans, fo.stats = nat.ptr(out.image), nat.ptr(out.trans), nat.ptr(out.stats_raw)
-        fo.contrib_sum = nat.ptr(out.contrib_sum) if opts.record_contributions else 0
-        fo.contrib_max = nat.ptr(out.contrib_max) if opts.record_contributions else 0
-        fo.survivors = nat.ptr(out.survivors) if return_survivors else 0
-        if stage_events is not None:
-            handles = (ctypes.c_void_p * nat.N_STAGE_EVENTS)()
-            for i, ev in enumerate(stage_events[:nat.N_STAGE_EVENTS]):
-                if not ev.cuda_event:
-                    ev.record()            # torch creates the CUDA event lazily
-                handles[i] = ev.cuda_event
-            fo.stage_events = ctypes.cast(handles, ctypes.c_void_p)
-            fo.n_stage_events = nat.N_STAGE_EVENTS
-            self._event_handles = handles  # keep alive until the call returns
-        camc = nat.camera_struct(cam)
-        optc = opts.struct(cam)
-        nat.check(lib.sc_render_composed(ctypes.byref(self.dscene.struct), ctypes.byref(camc), ctypes.byref(optc),
-                                         ctypes.byref(ws.struct), ctypes.byref(fo), nat.stream_handle()),
-                  "sc_render_composed")
+        with torch.cuda.device(dev):
+            ws = self.workspace(cam, slot, opts.tile_size)
+            h, w = int(cam.height), int(cam.width)
+            if out is None or out.image.shape != (h, w, 3):
+                out = DeviceFrame(torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                                  torch.empty((h, w), dtype=torch.float32, device=dev),
+                                  torch.empty(nat.STATS_BYTES, dtype=torch.uint8, device=dev))
+            if opts.record_contributions:
+                if out.contrib_sum is None or out.contrib_sum.shape != (h, w):
+                    out.contrib_sum = torch.empty((h, w), dtype=torch.float32, device=dev)
+                if out.contrib_max is None or out.contrib_max.numel() != ws.cap_s:
+                    out.contrib_max = torch.empty(ws.cap_s, dtype=torch.float32, device=dev)
+            if return_survivors and (out.survivors is None or out.survivors.shape[0] != ws.cap_s):
+                out.survivors = torch.empty((ws.cap_s, 2), dtype=torch.int32, device=dev)
+            fo = nat.ScFrameOut()
+            fo.image, fo.trans, fo.stats = nat.ptr(out.image), nat.ptr(out.trans), nat.ptr(out.stats_raw)
+            fo.contrib_sum = nat.ptr(out.contrib_sum) if opts.record_contributions else 0
+            fo.contrib_max = nat.ptr(out.contrib_max) if opts.record_contributions else 0
+            fo.survivors = nat.ptr(out.survivors) if return_survivors else 0
+            handles = None
+            if isinstance(stage_events, _StageEvents):
+                handles = stage_events.handles
+            elif stage_events is not None:
+                handles = (ctypes.c_void_p * nat.N_STAGE_EVENTS)()
+                for i, ev in enumerate(stage_events[:nat.N_STAGE_EVENTS]):
+                    if not ev.cuda_event:
+                        ev.record()            # torch creates the CUDA event lazily
+                    handles[i] = ev.cuda_event
+            if handles is not None:
+                fo.stage_events = ctypes.cast(handles, ctypes.c_void_p)
+                fo.n_stage_events = nat.N_STAGE_EVENTS
+            if debug is not None:
+                if debug.order.numel() < ws.cap_s or debug.block_entries.numel() < ws.cap_e:
+                    raise ValueError("FrameDebug buffers are smaller than the workspace capacities")
+                fo.debug = ctypes.addressof(debug.struct)
+            camc = nat.camera_struct(cam)
+            optc = opts.struct(cam)
+            if survivors is not None:
+                n = int(survivors.shape[0])
+                if n > ws.cap_s:
+                    if debug is not None:
+                        raise ValueError("survivor list exceeds the workspace capacity (grow it before FrameDebug)")
+                    ws.grow(n, ws.cap_e)
+                nat.check(lib.sc_render_survivors(ctypes.byref(self.dscene.struct), nat.ptr(survivors), n,
+                                                  ctypes.byref(camc), ctypes.byref(optc), ctypes.byref(ws.struct),
+                                                  ctypes.byref(fo), nat.stream_handle()), "sc_render_survivors")
+            else:
+                nat.check(lib.sc_render_composed(ctypes.byref(self.dscene.struct), ctypes.byref(camc),
+                                                 ctypes.byref(optc), ctypes.byref(ws.struct), ctypes.byref(fo),
+                                                 nat.stream_handle()), "sc_render_composed")
         return out
 
     def render(self, cam, opts: RenderOptions | None = None, return_survivors: bool = False,
-               to_host: bool = True):
-        """One frame -> (RenderOutput, FrameStats); regrows the workspace on overflow."""
+               to_host: bool = True, survivors=None, debug: bool = False):
+        """One frame -> (RenderOutput, FrameStats); regrows the workspace on overflow.
+
+        ``debug=True`` also returns the frame path's depth order and block lists
+        (a dict of numpy arrays, FrameDebug.host) as a third element.
+        """
         import torch
 
         from .raster import RenderOutput
 
         opts = opts or RenderOptions()
-        for _attempt in range(4):
-            ev0 = torch.cuda.Event(enable_timing=True)
-            ev1 = torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            frame = self.render_device(cam, opts, return_survivors=return_survivors)
-            ev1.record()
-            # one batch of asynchronous copies into pinned host memory (torch's caching host
-            # allocator), then a single synchronisation
-            host = {"stats": _to_pinned(frame.stats_raw)}
-            if to_host:
-                host["image"] = _to_pinned(frame.image)
-                host["trans"] = _to_pinned(frame.trans)
-            torch.cuda.current_stream().synchronize()
-            st = nat.stats_dict(host["stats"].numpy())
-            _PINNED.give(host["stats"])
-            if not st["overflow"]:
-                break
-            # the frame path bins (splat, 8x4 block) pairs: block_entries of them
-            self.workspace(cam).grow(st["survivors"], max(st["entries"], st["block_entries"]))
-        else:
-            raise nat.NativeError("workspace overflow persists after regrowing")
-        render_ms = float(ev0.elapsed_time(ev1))
-        n_s = st["survivors"]
-        payload = self._payload_bytes_per_survivor(n_s, frame, return_survivors)
-        stats = FrameStats(frustum_passed=st["frustum_passed"], mlp_culled=st["mlp_culled"], instantiated=n_s,
-                           used=st["used"] if opts.record_contributions else None,
-                           mem_bytes_instantiated=payload, render_ms=render_ms, mlp_ms=float("nan"),
-                           preprocess_ms=float("nan"), mlp_queried=st["mlp_queried"],
-                           instances_visible=st["instances_visible"], pairs_tested=st["pairs_tested"],
-                           passed=st["passed"], skipped=st["skipped"], entries=st["entries"],
-                           max_tie_run=st["max_tie_run"], block_entries=st["block_entries"],
-                           exact_fallbacks=st["exact_fallbacks"])
-        if not to_host:
-            return frame, stats
-        out = RenderOutput(
-            image=_PINNED.numpy(host["image"]),
-            final_transmittance=_PINNED.numpy(host["trans"]),
-            contribution_max=frame.contrib_max[:n_s].cpu().numpy() if opts.record_contributions else None,
-            contribution_sum=frame.contrib_sum.cpu().numpy() if opts.record_contributions else None,
-            used_count=st["used"] if opts.record_contributions else None,
-            passed_count=st["passed"], skipped_count=st["skipped"])
-        if return_survivors:
-            out.survivors = frame.survivors[:n_s].cpu().numpy().astype(np.int64)
-        return out, stats
+        with torch.cuda.device(self.dscene.device):
+            evs = self.stage_events(0)
+            if survivors is not None:
+                ws = self.workspace(cam, 0, opts.tile_size)
+                if int(survivors.shape[0]) > ws.cap_s:
+                    ws.grow(int(survivors.shape[0]), ws.cap_e)
+            for _attempt in range(4):
+                dbg = FrameDebug(self.workspace(cam, 0, opts.tile_size)) if debug else None
+                frame = self.render_device(cam, opts, return_survivors=return_survivors, stage_events=evs,
+                                           survivors=survivors, debug=dbg)
+                # one batch of asynchronous copies into pinned host memory (torch's caching host
+                # allocator), then a single synchronisation
+                host = {"stats": _to_pinned(frame.stats_raw)}
+                if to_host:
+                    host["image"] = _to_pinned(frame.image)
+                    host["trans"] = _to_pinned(frame.trans)
+                torch.cuda.current_stream().synchronize()
+                st = nat.stats_dict(host["stats"].numpy())
+                _PINNED.give(host["stats"])
+                if not st["overflow"]:
+                    break
+                # the frame path bins (splat, 8x4 block) pairs: block_entries of them
+                self.workspace(cam, 0, opts.tile_size).grow(st["survivors"], max(st["entries"], st["block_entries"]))
+            else:
+                raise nat.NativeError("workspace overflow persists after regrowing")
+            n_s = st["survivors"]
+            payload = self._payload_bytes_per_survivor(n_s, frame, return_survivors)
+            stats = _frame_stats(st, evs.timings(), payload, opts.record_contributions)
+            extra = (dbg.host(st),) if debug else ()
+            if not to_host:
+                return (frame, stats) + extra
+            out = RenderOutput(
+                image=_PINNED.numpy(host["image"]),
+                final_transmittance=_PINNED.numpy(host["trans"]),
+                contribution_max=frame.contrib_max[:n_s].cpu().numpy() if opts.record_contributions else None,
+                contribution_sum=frame.contrib_sum.cpu().numpy() if opts.record_contributions else None,
+                used_count=st["used"] if opts.record_contributions else None,
+                passed_count=st["passed"], skipped_count=st["skipped"])
+            if return_survivors:
+                out.survivors = frame.survivors[:n_s].cpu().numpy().astype(np.int64)
+            return (out, stats) + extra
 
     def render_path(self, cams, opts: RenderOptions | None = None, frames_in_flight: int = 2,
                     to_host: bool = True):
         """Render a camera path; yields (RenderOutput, FrameStats) per camera, in order.
 
-        Frame i is rendered on stream i % F with its own workspace and output
-        buffers (F = ``frames_in_flight``), so the kernels of consecutive
-        frames overlap on the GPU and the device->host copies of frame i run
-        while frame i + 1 renders.  Each frame is bit-identical to
-        ``render(cam, opts)``.  ``to_host=False`` yields (DeviceFrame,
-        FrameStats); a DeviceFrame stays valid until F further frames have
-        been yielded.
+        Frame i is rendered on stream i % F with workspace slot i % F (F =
+        ``frames_in_flight``), so the kernels of consecutive frames overlap on
+        the GPU and the device->host copies of frame i run while frame i + 1
+        renders.  Each frame is bit-identical to ``render(cam, opts)``.
+        ``to_host=False`` yields (DeviceFrame, FrameStats); the device frames
+        rotate through F + 1 output buffers, so a DeviceFrame stays valid until
+        the caller requests the frame after next (two consecutive frames can be
+        held at once; work the caller enqueues on its current stream before
+        that request is ordered before the buffer's reuse).
         """
         import torch
 
@@ -599,41 +722,43 @@ class Renderer:
 
         opts = opts or RenderOptions()
         F = max(1, int(frames_in_flight))
+        R = F + 1   # output frames in the ring
         cams = list(cams)
-        main = torch.cuda.current_stream()
-        # streams and per-slot output frames persist across calls: a new stream's first
-        # allocations would be fresh cudaMallocs (device-synchronising) inside the path
-        while len(self._path_streams) < F:
-            self._path_streams.append(torch.cuda.Stream(device=self.dscene.device))
+        dev = self.dscene.device
+        with torch.cuda.device(dev):
+            main = torch.cuda.current_stream()
+            # streams, per-slot events and the output ring persist across calls: a new stream's
+            # first allocations would be fresh cudaMallocs (device-synchronising) inside the path
+            while len(self._path_streams) < F:
+                self._path_streams.append(torch.cuda.Stream(device=dev))
         streams = self._path_streams[:F]
-        frames: list[DeviceFrame | None] = [self._path_frames.get(j) for j in range(F)]
+        events = [self.stage_events(j) for j in range(F)]
+        frames: list[DeviceFrame | None] = [self._path_frames.get(j) for j in range(R)]
         pending: list[dict | None] = [None] * F
 
         def launch(i):
-            slot = i % F
+            slot, ring = i % F, i % R
             st = streams[slot]
-            st.wait_stream(main)
-            with torch.cuda.stream(st):
-                ev0 = torch.cuda.Event(enable_timing=True)
-                ev1 = torch.cuda.Event(enable_timing=True)
-                ev0.record()
-                frames[slot] = self.render_device(cams[i], opts, out=frames[slot], slot=slot)
-                ev1.record()
-                f = frames[slot]
-                self._path_frames[slot] = f
-                host = {"stats": _to_pinned(f.stats_raw)}
-                if to_host:
-                    host["image"] = _to_pinned(f.image)
-                    host["trans"] = _to_pinned(f.trans)
-                    if opts.record_contributions:
-                        host["contrib_sum"] = _to_pinned(f.contrib_sum)
-                        host["contrib_max"] = _to_pinned(f.contrib_max)
-                done = torch.cuda.Event()
-                done.record()
-            pending[slot] = {"i": i, "ev0": ev0, "ev1": ev1, "host": host, "done": done}
+            with torch.cuda.device(dev):
+                st.wait_stream(main)
+                with torch.cuda.stream(st):
+                    frames[ring] = self.render_device(cams[i], opts, out=frames[ring], slot=slot,
+                                                      stage_events=events[slot])
+                    f = frames[ring]
+                    self._path_frames[ring] = f
+                    host = {"stats": _to_pinned(f.stats_raw)}
+                    if to_host:
+                        host["image"] = _to_pinned(f.image)
+                        host["trans"] = _to_pinned(f.trans)
+                        if opts.record_contributions:
+                            host["contrib_sum"] = _to_pinned(f.contrib_sum)
+                            host["contrib_max"] = _to_pinned(f.contrib_max)
+                    done = torch.cuda.Event()
+                    done.record()
+            pending[slot] = {"i": i, "host": host, "done": done}
 
         def collect(i, attempt=0):
-            slot = i % F
+            slot, ring = i % F, i % R
             p = pending[slot]
             t_sync = time.perf_counter()
             p["done"].synchronize()
@@ -644,22 +769,16 @@ class Renderer:
                 if attempt >= 3:
                     raise nat.NativeError("workspace overflow persists after regrowing")
                 # regrow this slot's workspace and re-render the frame on its stream
-                torch.cuda.synchronize()
-                self.workspace(cams[i], slot).grow(st["survivors"], max(st["entries"], st["block_entries"]))
+                torch.cuda.synchronize(dev)
+                self.workspace(cams[i], slot, opts.tile_size).grow(st["survivors"],
+                                                                   max(st["entries"], st["block_entries"]))
                 launch(i)
                 return collect(i, attempt + 1)
             n_s = st["survivors"]
-            stats = FrameStats(frustum_passed=st["frustum_passed"], mlp_culled=st["mlp_culled"], instantiated=n_s,
-                               used=st["used"] if opts.record_contributions else None,
-                               mem_bytes_instantiated=self._payload_bytes_per_survivor(n_s, frames[slot], False),
-                               render_ms=float(p["ev0"].elapsed_time(p["ev1"])), mlp_ms=float("nan"),
-                               preprocess_ms=float("nan"), mlp_queried=st["mlp_queried"],
-                               instances_visible=st["instances_visible"], pairs_tested=st["pairs_tested"],
-                               passed=st["passed"], skipped=st["skipped"], entries=st["entries"],
-                               max_tie_run=st["max_tie_run"], block_entries=st["block_entries"],
-                               exact_fallbacks=st["exact_fallbacks"])
+            stats = _frame_stats(st, events[slot].timings(),
+                                 self._payload_bytes_per_survivor(n_s, frames[ring], False), opts.record_contributions)
             if not to_host:
-                return frames[slot], stats
+                return frames[ring], stats
             h = p["host"]
             rec = opts.record_contributions
             cmax = None
@@ -684,9 +803,9 @@ class Renderer:
                     continue
                 launch(i + F)
             yield res
-        main.wait_stream(streams[0])
-        for st in streams[1:]:
-            main.wait_stream(st)
+        with torch.cuda.device(dev):
+            for st in streams:
+                main.wait_stream(st)
 
     def _payload_bytes_per_survivor(self, n_s, frame, have_surv):
         # instantiated x per-gaussian Asset payload (56 B at SH degree 0)

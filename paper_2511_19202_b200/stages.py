@@ -29,7 +29,7 @@ def cull_mlp(dscene: DeviceScene, cam, opts: RenderOptions, cap: int | None = No
 
     lib = nat.load()
     cap = int(cap if cap is not None else max(1, dscene.max_pairs))
-    ws = Workspace(dscene, cam.width, cam.height, cap_s=1, cap_e=1)
+    ws = Workspace(dscene, cam.width, cam.height, cap_s=1, cap_e=1, tile_size=opts.tile_size)
     surv = torch.empty((cap, 2), dtype=torch.int32, device=dscene.device)
     stats = torch.empty(nat.STATS_BYTES, dtype=torch.uint8, device=dscene.device)
     camc, optc = nat.camera_struct(cam), opts.struct(cam)
@@ -75,8 +75,9 @@ def bin_sort(dscene: DeviceScene, surv_inst, surv_gid, cam, opts: RenderOptions,
     sv = _survivor_tensor(surv_inst, surv_gid, dev)
     n = int(sv.shape[0])
     cap_e = int(cap_entries if cap_entries is not None else max(1 << 16, 64 * n))
-    ws = Workspace(dscene, cam.width, cam.height, cap_s=max(n, 1), cap_e=cap_e)
-    n_tiles = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    ws = Workspace(dscene, cam.width, cam.height, cap_s=max(n, 1), cap_e=cap_e, tile_size=opts.tile_size)
+    ts = int(opts.tile_size)
+    n_tiles = ((cam.width + ts - 1) // ts) * ((cam.height + ts - 1) // ts)
     splats = torch.empty((max(n, 1), nat.SPLAT_BYTES), dtype=torch.uint8, device=dev)
     wins = torch.empty((max(n, 1), nat.WINDOW_BYTES), dtype=torch.uint8, device=dev)
     entries = torch.empty(max(cap_e, 1), dtype=torch.int32, device=dev)

@@ -18,7 +18,8 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 GOLDEN_CASES = ["cloud3k_128", "shell4k_160x96", "slab_headon_96", "cloud_clip_112x80", "shell_sh3_144x112",
-                "cloud_sh2_eval1_120x90", "cloud_bg_dil_100x70"]
+                "cloud_sh2_eval1_120x90", "cloud_bg_dil_100x70", "cloud_ts8_120x88", "shell_ts32_150x100",
+                "cloud_ts12_100x76", "cloud_dil15_border_96x72"]
 
 
 def pytest_configure(config):

@@ -23,7 +23,8 @@ pytestmark = pytest.mark.gpu
 
 IMG_MAX_ABS = 5e-3
 IMG_PSNR = 80.0
-LOGIT_MARGIN = 0.01
+LOGIT_MARGIN = 0.0025          # SURVEY §8c fp16 margin (measured flips: |logit_ref| < 8.3e-4)
+LOGIT_MAX_ABS = 5e-3           # fp16 forward vs f64 (measured max |dlogit| 2.4e-3)
 
 
 def _single_scene(asset):
@@ -137,7 +138,7 @@ def test_mlp_forward_vs_f64():
     diff = np.abs(got - ref)
     flips = (got >= 0) != (ref >= 0)
     assert np.all(np.abs(ref[flips]) < LOGIT_MARGIN), f"decision flip at |logit| {np.abs(ref[flips]).max()}"
-    assert diff.max() < 0.05, diff.max()
+    assert diff.max() < LOGIT_MAX_ABS, diff.max()
     assert 0.5 < (ref >= 0).mean() < 0.8
 
 
@@ -422,7 +423,7 @@ def test_mlp_sweep_config4_16m():
     got = out[:n, 0].cpu().numpy()
     flips = (got >= 0) != (ref >= 0)
     assert np.all(np.abs(ref[flips]) < LOGIT_MARGIN)
-    assert np.abs(got - ref).max() < 0.05
+    assert np.abs(got - ref).max() < LOGIT_MAX_ABS
 
 
 @pytest.mark.parametrize("view", [0, 2], ids=["near", "far"])
@@ -501,9 +502,10 @@ def test_workspace_regrows_on_overflow():
     big = Renderer(wl.scene)
     ref, rst = big.render(cam, RenderOptions(), to_host=False)
     small = Renderer(wl.scene)
-    small.workspaces[(cam.width, cam.height)] = Workspace(small.dscene, cam.width, cam.height, cap_s=1024, cap_e=4096)
+    key = Renderer.ws_key(cam)
+    small.workspaces[key] = Workspace(small.dscene, cam.width, cam.height, cap_s=1024, cap_e=4096)
     got, gst = small.render(cam, RenderOptions(), to_host=False)
-    assert small.workspaces[(cam.width, cam.height)].cap_s >= gst.instantiated > 1024
+    assert small.workspaces[key].cap_s >= gst.instantiated > 1024
     assert gst.instantiated == rst.instantiated and gst.passed == rst.passed
     assert torch.equal(got.image, ref.image)
 
@@ -546,7 +548,7 @@ def test_render_path_matches_render(frames_in_flight):
     r = Renderer(wl.scene)
     c0 = cams[0]
     # slot 1 starts far too small: its first frame overflows and is re-rendered
-    r.workspaces[(c0.width, c0.height, 1)] = Workspace(r.dscene, c0.width, c0.height, cap_s=512, cap_e=2048)
+    r.workspaces[Renderer.ws_key(c0, 1)] = Workspace(r.dscene, c0.width, c0.height, cap_s=512, cap_e=2048)
     got = list(r.render_path(cams, opts, frames_in_flight=frames_in_flight))
     assert len(got) == len(want)
     for (go, gs), (wo, ws) in zip(got, want):
@@ -685,3 +687,135 @@ def test_composed_sh3_instances_vs_oracle():
     ref = sr.render_composed(sc, cam)
     assert st.instantiated == ref.stats["instantiated"] and st.passed == ref.stats["passed"]
     _image_close(out.image, ref.out.image)
+
+
+def test_margin_cull_large_dilation_equals_unculled():
+    """the margin frustum's pad follows the dilation (3 sqrt(dilation) + 1 px).
+    Golden asset with dilation 1.5 and splats straddling the image border: the
+    margin-culled instanced render equals the unculled drop-in render bit for bit,
+    and the drop-in render matches the reference golden."""
+    import paper_2511_19202_b200 as pkg
+    from conftest import load_golden
+    from paper_2511_19202_b200.scene import ComposedScene, InstanceTransform
+
+    asset, cam, opts, z = load_golden("cloud_dil15_border_96x72")
+    sc = ComposedScene()
+    sc.add_asset(asset)
+    sc.add_instance(0, InstanceTransform())
+    culled, st = pkg.render_composed(sc, cam, use_mlp=False, **opts)
+    plain = pkg.render(asset, cam, **opts)
+    np.testing.assert_array_equal(culled.image, plain.image)
+    np.testing.assert_array_equal(culled.final_transmittance, plain.final_transmittance)
+    _image_close(plain.image, z["image"])
+    ref = sr.render_composed(sc, cam, use_mlp=False, **opts)
+    assert st.frustum_passed == ref.stats["frustum_passed"]
+
+
+@pytest.mark.parametrize("ts", [8, 12, 32])
+def test_composed_tile_size(ts):
+    """Composed scene (rotated / scaled instances, MLP on) at a non-default tile size:
+    the oracle rendering the GPU's own survivors with the same tile size matches."""
+    import paper_2511_19202_b200 as pkg
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    cam = look_at(*CAMS[0])
+    out, st = pkg.render_composed(sc, cam, tile_size=ts, return_survivors=True)
+    s = out.survivors
+    m, ls, q, op, sh, deg = sr.instantiate(sr.SceneTables(sc), cam, s[:, 0], s[:, 1])
+    own = rr.render_arrays(m, ls, q, op, sh, deg, cam, tile_size=ts)
+    _image_close(out.image, own.image)
+    assert out.passed_count == own.passed_count
+    ref = sr.render_composed(sc, cam, tile_size=ts)
+    assert st.frustum_passed == ref.stats["frustum_passed"]
+
+
+def test_frame_stats_timings():
+    """SPEC.md:339 FrameStats timings come from the library's stage events:
+    render_ms = whole frame, mlp_ms = cull + MLP, preprocess_ms = projection + sort."""
+    import paper_2511_19202_b200 as pkg
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=True)
+    for cam in (look_at(*c) for c in CAMS):
+        _out, st = pkg.render_composed(sc, cam)
+        assert 0.0 < st.mlp_ms and 0.0 < st.preprocess_ms
+        assert st.mlp_ms + st.preprocess_ms <= st.render_ms + 1e-3
+    for _out, st in pkg.render_path(sc, [look_at(*c) for c in CAMS], frames_in_flight=2):
+        assert 0.0 < st.mlp_ms <= st.render_ms and 0.0 < st.preprocess_ms <= st.render_ms
+
+
+def test_render_reuses_device_asset():
+    """render() keeps the uploaded asset and its workspace across calls on the same Asset."""
+    import dataclasses
+
+    import paper_2511_19202_b200 as pkg
+    from conftest import load_golden
+    from paper_2511_19202_b200 import raster
+
+    asset, cam, opts, z = load_golden("cloud3k_128")
+    a = pkg.render(asset, cam)
+    r1 = raster._renderer_for(asset)
+    b = pkg.render(asset, cam)
+    assert raster._renderer_for(asset) is r1
+    np.testing.assert_array_equal(a.image, b.image)
+    other = dataclasses.replace(asset, means=asset.means.copy())
+    assert raster._renderer_for(other) is not r1
+    _image_close(pkg.render(other, cam).image, z["image"])
+
+
+def test_encode_features_vs_f64():
+    """sc_encode_features (fp32 CUDA cores, fp16 out) against the f64 oracle."""
+    from paper_2511_19202_b200 import nn, synth
+    from paper_2511_19202_b200.asset import prepare
+    from paper_2511_19202_b200.workloads import calibrated_model
+
+    a = prepare(synth.make_shell(20_000, seed=4))
+    m = calibrated_model(a, seed=4)
+    got = nn.encode_features(m, a)
+    ref = sr.encode_features(m, a)
+    assert got.shape == ref.shape == (len(a), 6)
+    err = np.abs(got - ref)
+    # fp16 storage: half an ulp of the magnitude, plus fp32 accumulation
+    assert np.all(err <= np.abs(ref) * 2.0 ** -10 + 1e-4), float((err - np.abs(ref) * 2.0 ** -10).max())
+
+
+def test_render_path_device_frames_hold_two():
+    """with to_host=False a DeviceFrame stays valid until the frame after
+    next is requested, so a caller can hold two consecutive frames."""
+    import torch
+
+    from paper_2511_19202_b200.scene import RenderOptions, Renderer
+    from paper_2511_19202_b200.workloads import config3
+
+    wl = config3(n_per=3_000, n_instances=40, width=256, height=144)
+    cams = [wl.cameras[i % 3] for i in range(6)]
+    ref = Renderer(wl.scene)
+    want = [ref.render(c, RenderOptions())[0].image for c in cams]
+    r = Renderer(wl.scene)
+    prev = None
+    for i, (f, _st) in enumerate(r.render_path(cams, RenderOptions(), frames_in_flight=2, to_host=False)):
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(f.image.cpu().numpy(), want[i])
+        if prev is not None:   # frame i - 1 is still intact while frame i is held
+            np.testing.assert_array_equal(prev.image.cpu().numpy(), want[i - 1])
+        prev = f
+
+
+def test_workspace_too_small_for_scene_is_rejected():
+    """a workspace sized for fewer instances / pairs than the scene is refused."""
+    from paper_2511_19202_b200.scene import RenderOptions, Renderer, Workspace
+    from conftest import look_at
+
+    sc = _multi_scene(with_model=False)
+    r = Renderer(sc)
+    cam = look_at(*CAMS[0])
+    ws = Workspace(r.dscene, cam.width, cam.height)
+    ws.struct.max_pairs = r.dscene.max_pairs - 1
+    r.workspaces[Renderer.ws_key(cam)] = ws
+    with pytest.raises(ValueError, match="smaller scene"):
+        r.render(cam, RenderOptions())
+    ws.struct.max_pairs = r.dscene.max_pairs
+    ws.struct.n_instances = r.dscene.n_instances - 1
+    with pytest.raises(ValueError, match="smaller scene"):
+        r.render(cam, RenderOptions())

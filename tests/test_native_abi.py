@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
         assert name in _native.SIGNATURES, f"{name} has no ctypes signature"
-    assert lib.sc_abi_version() == _native.ABI_VERSION == 2
+    assert lib.sc_abi_version() == _native.ABI_VERSION == 3
 
 
 def test_workspace_bytes_is_host_computable():
@@ -38,11 +38,15 @@ def test_workspace_bytes_is_host_computable():
     small = lib.sc_workspace_bytes(1, 10_000, 10_000, 40_000, 256, 256, 16)
     big = lib.sc_workspace_bytes(1000, 100_000_000, 60_000_000, 180_000_000, 1920, 1080, 16)
     assert 0 < small < big
-    assert lib.sc_workspace_bytes(1, 1, 1, 1, 256, 256, 8) == 0     # tile_size must be 16
+    # any tile size in [1, 65535] (the reference's tile_size keyword); smaller tiles need more offsets
+    assert lib.sc_workspace_bytes(1, 1, 1, 1, 256, 256, 8) > lib.sc_workspace_bytes(1, 1, 1, 1, 256, 256, 32) > 0
+    assert lib.sc_workspace_bytes(1, 1, 1, 1, 256, 256, 0) == 0
+    assert lib.sc_workspace_bytes(1, 1, 1, 1, 256, 256, 65536) == 0
 
 
 STRUCTS = ["sc_camera", "sc_opts", "sc_asset_rec", "sc_instance_rec", "sc_vis_weights", "sc_scene",
-           "sc_frame_stats", "sc_survivor", "sc_splat", "sc_window", "sc_frame_out", "sc_workspace"]
+           "sc_frame_stats", "sc_survivor", "sc_splat", "sc_window", "sc_frame_out", "sc_workspace",
+           "sc_frame_debug"]
 
 
 @pytest.mark.parametrize("name", STRUCTS)
@@ -52,7 +56,7 @@ def test_struct_layout_matches_c(name, tmp_path):
     py = {"sc_camera": nat.ScCamera, "sc_opts": nat.ScOpts, "sc_asset_rec": nat.ScAssetRec,
           "sc_instance_rec": nat.ScInstanceRec, "sc_vis_weights": nat.ScVisWeights, "sc_scene": nat.ScScene,
           "sc_frame_stats": nat.ScFrameStats, "sc_survivor": nat.ScSurvivor, "sc_splat": nat.ScSplat, "sc_window": nat.ScWindow,
-          "sc_frame_out": nat.ScFrameOut, "sc_workspace": nat.ScWorkspace}[name]
+          "sc_frame_out": nat.ScFrameOut, "sc_workspace": nat.ScWorkspace, "sc_frame_debug": nat.ScFrameDebug}[name]
     lines = [f'printf("%zu\\n", sizeof({name}));']
     for fname, _t in py._fields_:
         lines.append(f'printf("%zu\\n", offsetof({name}, {fname}));')

@@ -159,6 +159,12 @@ typedef struct sc_scene {
     int32_t n_models;
     int32_t reserved0;
     int64_t n_pairs;             /* sum over instances of their asset's count (workspace check) */
+    /* [n_gauss] float4 per gaussian, view-independent appearance computed once
+     * in f64 like the reference and rounded: x = p_min = ln(1/255) - ln(sigmoid(
+     * opacity_logit)), +inf when opacity < 1/255 (sc/_kernels.py:215-219);
+     * y, z = the degree-0 colour clip(C0 f_dc + 0.5, 0, 1) as fp16 bits (r | g << 16,
+     * b); w = 0 */
+    const float *appear;
 } sc_scene;
 
 /* Device-side counters of one frame (copy back with the stream). */

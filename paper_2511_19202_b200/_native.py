@@ -63,7 +63,7 @@ class ScScene(ctypes.Structure):
     _fields_ = [("mean_opa", P), ("quat", P), ("scale_smax", P), ("sh", P), ("features", P),
                 ("n_gauss", c_i64), ("sh_stride", c_i32), ("n_assets", c_i32), ("assets", P),
                 ("instances", P), ("n_instances", c_i64), ("vis_weights", P), ("n_models", c_i32),
-                ("reserved0", c_i32), ("n_pairs", c_i64)]
+                ("reserved0", c_i32), ("n_pairs", c_i64), ("appear", P)]
 
 
 STATS_FIELDS = ("instances_visible", "pairs_tested", "frustum_passed", "mlp_queried", "mlp_culled",

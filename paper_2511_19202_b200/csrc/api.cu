@@ -133,7 +133,7 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.eval_a = take(4 * (size_t)capE + 16);
     L.eval_b = take(4 * (size_t)capE + 16);
     L.tile_off = take(4 * (size_t)(L.n_tiles_ref + 1));
-    L.task_order = take(4 * (size_t)L.n_tiles);   // blend dispatch order over tiles
+    L.task_order = take(4 * (size_t)(8 * L.n_tiles));   // blend dispatch order over (tile, block) lists
     L.boff = take(4 * (size_t)(8 * L.n_tiles + 1));
     L.rs_counts = take(4 * (size_t)(256 * L.nblk_max));
     L.scan_part = take(4 * (size_t)part);
@@ -221,7 +221,7 @@ int check_scene(const sc_scene *s)
         return fail(SC_ERR_INVALID, "negative scene sizes%s");
     if (s->n_instances > 0 && (!s->instances || !s->assets))
         return fail(SC_ERR_INVALID, "scene tables are NULL%s");
-    if (s->n_gauss > 0 && (!s->mean_opa || !s->quat || !s->scale_smax || !s->sh))
+    if (s->n_gauss > 0 && (!s->mean_opa || !s->quat || !s->scale_smax || !s->sh || !s->appear))
         return fail(SC_ERR_INVALID, "scene gaussian arrays are NULL%s");
     if (s->sh_stride < 3) return fail(SC_ERR_INVALID, "sh_stride must be >= 3%s");
     return SC_OK;
@@ -278,7 +278,7 @@ int frame_tail(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts,
     }
     if (opts->record_contributions && w.capS > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
-    const sc::BlendLists lists{w.boff, entries, bkeys, nullptr, true};
+    const sc::BlendLists lists{w.boff, entries, bkeys, nullptr, true, &w.ctr->blend_next};
     SC_TRY(sc::launch_blend(w.splats, lists, *cam, *opts, *out, w.capS, w.task_order, st), "blend");
     SC_TRY(mark(4), "event");
     if (opts->record_contributions)
@@ -397,7 +397,7 @@ int sc_blend(const sc_splat *splats, const sc_window *windows, int64_t n_splats,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (opts->record_contributions && n_splats > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)n_splats, st), "memset contrib_max");
-    const sc::BlendLists lists{tile_offsets, entry_idx, nullptr, windows, false};
+    const sc::BlendLists lists{tile_offsets, entry_idx, nullptr, windows, false, nullptr};
     SC_TRY(sc::launch_blend(splats, lists, *cam, *opts, *out, n_splats, nullptr, st), "blend");
     return SC_OK;
 }

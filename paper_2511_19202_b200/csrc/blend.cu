@@ -48,7 +48,11 @@ constexpr int kBlendWarps = 8;           // warps per CTA (one 16x16 tile)
 constexpr int kG = 32;                   // hits per record stage
 constexpr int kStep = 128;               // meta entries per stream step (4 per lane)
 constexpr int kHQ = 256;                 // hit queue capacity (>= kG + kStep)
-constexpr int kRecStages = 4;            // record stages: up to 3 in flight while the oldest is blended
+#ifndef SC_BLEND_STAGES
+#define SC_BLEND_STAGES 3
+#endif
+constexpr int kRecStages = SC_BLEND_STAGES;   // record stages: up to kRecStages - 1 in flight while the oldest
+                                              // is blended (3: 5.9 KB per warp, 4 CTAs = 32 warps per SM)
 constexpr int kMaxHeavyPixels = 8;       // ... and at most this many such pixels in the stage
 constexpr int kHeavyHits = 12;           // a pixel covered by >= this many entries of a stage: entry-parallel
 constexpr size_t kHQBytesW = sizeof(uint2) * kHQ;
@@ -448,6 +452,68 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     }
 }
 
+// Frame path, persistent: every warp repeatedly takes the next (16x16 tile, 8x4
+// block) list from an atomic ticket over the LPT order (longest lists first) and
+// walks it.  No CTA barrier and no CTA-wide lifetime: a warp whose list is short
+// takes the next one at once, so the SM's warp slots stay busy until the queue
+// drains (one CTA per tile kept a CTA resident until its longest list ended:
+// ~17 % warps active).  Per list the walk is the same as k_blend's, so images
+// are bit-identical.
+__global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
+    const sc_splat *__restrict__ splats, int64_t n_splats, const uint32_t *__restrict__ boff,
+    const uint32_t *__restrict__ vals, const uint32_t *__restrict__ keys, const uint32_t *__restrict__ task_order,
+    int64_t n_tasks, unsigned long long *ticket, int width, int height, int n_tx, float stop_t, float bg_r,
+    float bg_g, float bg_b, int record, float *image, float *trans, float *csum, float *cmax)
+{
+    extern __shared__ float4 s_dyn[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    WalkCtx c;
+    c.splats = splats;
+    c.n_splats = n_splats;
+    c.vals = vals;
+    c.keys = keys;
+    c.wins = nullptr;
+    c.blocks = 1;
+    c.stop_t = stop_t;
+    c.record = record;
+    c.cmax = cmax;
+    c.lane = lane;
+    char *wbase = reinterpret_cast<char *>(s_dyn) + wid * kWarpSmem;
+    c.hq = reinterpret_cast<uint2 *>(wbase);
+    c.stage = reinterpret_cast<uint2 *>(wbase + kHQBytesW);
+    c.recs = reinterpret_cast<float4 *>(wbase + kHQBytesW + kStageMetaBytesW);
+#ifdef SC_BLEND_STATS
+    WalkStats d{0, 0, 0, 0};
+#endif
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(ticket, 1ull);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if ((int64_t)t >= n_tasks) break;
+        const uint32_t blk = __ldg(task_order + t);   // block id = 8 tile + b
+        const int tile = (int)(blk >> 3), b = (int)(blk & 7u);
+        const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
+        c.gx0 = txi * kTile + (b & 1) * 8;
+        c.gy0 = tyi * kTile + (b >> 1) * 4;
+        c.bx1 = c.gx0 + 7;
+        c.by1 = c.gy0 + 3;
+        const int px = c.gx0 + (lane & 7), py = c.gy0 + (lane >> 3);
+        const bool inside = px < width && py < height;
+        c.fpx = (float)px;
+        c.fpy = (float)py;
+        PixAcc a{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, !inside};
+        walk_list(c, __ldg(boff + blk), __ldg(boff + blk + 1), a SC_WS_ARG);
+        if (inside) {
+            const int64_t p = (int64_t)py * width + px;
+            image[3 * p + 0] = a.cr + a.T * bg_r;
+            image[3 * p + 1] = a.cg + a.T * bg_g;
+            image[3 * p + 2] = a.cb + a.T * bg_b;
+            trans[p] = a.T;
+            if (record && csum) csum[p] = a.cs;
+        }
+    }
+}
+
 // LPT dispatch order: heavier tiles first, bucketed by floor(log2(weight)),
 // weight = the longest list among the tile's `stride` lists (the tile's
 // critical path); the order inside a bucket is irrelevant to the result.
@@ -541,6 +607,33 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
     const Band band = band_of(opts, cam.height, ts);   // only the band's tiles are blended (and written)
     const int64_t tile_base = (int64_t)band.t0 * n_tx, n_tiles = (int64_t)(band.t1 - band.t0) * n_tx;
     if (n_tiles <= 0) return cudaSuccess;
+#ifndef SC_BLEND_PERSIST
+#define SC_BLEND_PERSIST 1
+#endif
+    if (SC_BLEND_PERSIST && lists.blocks && task_order && lists.ticket) {
+        // frame path: persistent warps over the (tile, block) lists, longest first
+        cudaError_t e = smem_attr_once(reinterpret_cast<const void *>(k_blend_blocks), kSmem);
+        if (e != cudaSuccess) return e;
+        static int cps_cache[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int cps = (dev >= 0 && dev < 64) ? cps_cache[dev] : 0;
+        if (cps <= 0) {
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_blend_blocks, kBlendWarps * 32, kSmem);
+            if (e != cudaSuccess) return e;
+            cps = std::max(cps, 1);
+            if (dev >= 0 && dev < 64) cps_cache[dev] = cps;
+        }
+        const int64_t n_tasks = 8 * n_tiles;
+        SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, 8 * tile_base, n_tasks, 1, task_order);
+        const int grid = (int)std::min<int64_t>((n_tasks + kBlendWarps - 1) / kBlendWarps, (int64_t)sm_count() * cps);
+        SC_LAUNCH(k_blend_blocks, grid, kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
+                  lists.keys, task_order, n_tasks, lists.ticket, cam.width, cam.height, n_tx,
+                  (float)opts.stop_transmittance, (float)opts.background[0], (float)opts.background[1],
+                  (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image, out.trans,
+                  out.contrib_sum, out.contrib_max);
+        return cudaGetLastError();
+    }
     if (n_tiles * ngroups > 0x7FFFFFFFll) return cudaErrorInvalidValue;
     if (task_order)
         SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, tile_base, n_tiles, lists.blocks ? 8 : 1, task_order);

@@ -85,6 +85,7 @@ struct Counters {
     // CTA to finish resets them), so a sweep sharing the GPU with another stream's
     // kernels does not wait on CTAs that are not resident yet
     unsigned long long rs_next, rs_done;
+    unsigned long long blend_next;     // persistent blend warps: next (tile, block) list of the LPT order
 };
 
 // Workspace carve-out (all offsets 256-byte aligned), see api.cu:carve().
@@ -106,7 +107,7 @@ struct Ws {
     uint32_t *ekey_a, *ekey_b;       // [capE]
     uint32_t *eval_a, *eval_b;       // [capE]
     uint32_t *tile_off;              // [n_tiles_ref + 1] stage API: reference tile offsets
-    uint32_t *task_order;            // [n_tiles] blend dispatch order (heavy tiles first)
+    uint32_t *task_order;            // [8 n_tiles] blend dispatch order over (tile, block) lists (longest first)
     uint32_t *boff;                  // [8 n_tiles + 1] offsets of the per-(tile, 8x4 block) entry lists
     uint32_t *rs_counts;             // radix pass digit counts -> bases, digit-major [256][nblk_max]
     uint32_t *scan_part;             // scan partials
@@ -256,6 +257,7 @@ struct BlendLists {
     const uint32_t *keys;
     const sc_window *wins;   // tile lists only: windows to clip per warp block
     bool blocks;
+    unsigned long long *ticket;   // block lists: persistent-warp task ticket (zeroed per frame), else NULL
 };
 cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st);

@@ -27,7 +27,6 @@ __device__ __forceinline__ sc_survivor make_survivor(uint32_t inst, uint32_t gid
     return s;
 }
 
-__device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // sqrt.approx (rel. error < 2^-22): only where the result is widened by a margin far larger
 __device__ __forceinline__ float sqrt_approx(float x)
@@ -72,10 +71,11 @@ __global__ void __launch_bounds__(256, 2) k_project(
     const int tsh = (ts & (ts - 1)) == 0 ? __ffs(ts) - 1 : -1;   // log2 of a power-of-two tile size
     const int n_tx = (cam.width + ts - 1) / ts;
     const Band band = band_of(opts, cam.height, ts);
-    const double log_min_alpha = log(1.0 / 255.0);
     unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0, n_exact = 0;
     const bool fast = MODE == kProjFast || (MODE == kProjMixed && opts.exact_projection == 0);
     // camera rotation in f32 for the f32 covariance path (loop invariant)
+    const float clip_f = opts.radius_clip > 0.0 ? (float)opts.radius_clip : 0.0f;
+    const float pos_x = (float)cam.pos[0], pos_y = (float)cam.pos[1], pos_z = (float)cam.pos[2];
     const float r0 = (float)cam.rot[0], r1 = (float)cam.rot[1], r2 = (float)cam.rot[2], r3 = (float)cam.rot[3],
                 r4 = (float)cam.rot[4], r5 = (float)cam.rot[5], r6 = (float)cam.rot[6], r7 = (float)cam.rot[7],
                 r8 = (float)cam.rot[8];
@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(256, 2) k_project(
         cam_xyz(cam, m0, m1, m2, tx, ty, tz);
         bool valid = false;
         double mx = 0.0, my = 0.0, ca = 0.0, cb = 0.0, cc = 0.0, radius = 0.0, det = 0.0, cov_a = 0.0, cov_c = 0.0;
-        float ex_f = 0.0f, ey_f = 0.0f;   // fast path: conservative support half-widths (before the L factor)
+        // fast path (f32 end to end): half conic a / c, b, det and the conservative a, c of the support box
+        float f_ha = 0.0f, f_b = 0.0f, f_hc = 0.0f, f_det = 0.0f, f_sa = 0.0f, f_sc = 0.0f;
         bool fast_done = false;
         if (tz > cam.near_) {
             const double txz = tx / tz, tyz = ty / tz;
@@ -167,24 +168,27 @@ __global__ void __launch_bounds__(256, 2) k_project(
                 const float hi = lam * (1.0f + 16.0f * kEps) + 2.0f * err;
                 const float rlo = ceilf(3.0f * sqrtf(lo) * (1.0f - 4.0f * kEps));
                 const float rhi = ceilf(3.0f * sqrtf(hi) * (1.0f + 4.0f * kEps));
-                const double fdet = (double)fa * (double)fc - (double)fb * (double)fb;
-                const double det_err = 4.0 * (double)err * ((double)fa + (double)fc + 2.0 * (double)err) + 1e-30;
-                const bool clip_ok = !(opts.radius_clip > 0.0) || fabs(fdet - opts.radius_clip) > det_err;
-                if (rlo == rhi && fdet - det_err > 1e-12 && clip_ok) {
+                // det = a c - b^2 in f32 with one FMA-exact square (Kahan): |error| <= 2 eps |det|,
+                // added to the bound below together with the f32 rounding of radius_clip
+                const float bb = fb * fb;
+                const float fdet = fmaf(fa, fc, -bb) - fmaf(fb, fb, -bb);
+                const float det_err = 4.0f * err * (fa + fc + 2.0f * err) + 4.0f * kEps * fabsf(fdet) +
+                                      2.0f * kEps * clip_f + 1e-30f;
+                const bool clip_ok = !(clip_f > 0.0f) || fabsf(fdet - clip_f) > det_err;
+                if (rlo == rhi && fdet - det_err > 1e-12f && clip_ok) {
                     fast_done = true;
                     radius = (double)rlo;
-                    det = fdet;
-                    const float inv = 1.0f / (float)fdet;
-                    ca = (double)(fc * inv);
-                    cb = (double)(-fb * inv);
-                    cc = (double)(fa * inv);
-                    valid = radius > 0.0;
-                    if (valid && opts.radius_clip > 0.0 && det < opts.radius_clip) valid = false;
-                    // support half-widths from conservative a, c (times sqrt(2 L) later)
-                    ex_f = sqrt_approx(fa + err);
-                    ey_f = sqrt_approx(fc + err);
-                    cov_a = (double)fa;
-                    cov_c = (double)fc;
+                    f_det = fdet;
+                    det = (double)fdet;
+                    const float inv = 1.0f / fdet;
+                    f_ha = 0.5f * (fc * inv);
+                    f_b = -fb * inv;
+                    f_hc = 0.5f * (fa * inv);
+                    valid = rlo > 0.0f;
+                    if (valid && clip_f > 0.0f && fdet < clip_f) valid = false;
+                    // support box from the conservative a, c (times 2 L later)
+                    f_sa = fa + err;
+                    f_sc = fc + err;
                 }
             }
             if constexpr (MODE == kProjFast) {
@@ -289,93 +293,110 @@ __global__ void __launch_bounds__(256, 2) k_project(
         }
 
         // --- colour (sc/raster.py:198-226) and opacity (sc/asset.py:44-51) ---
+        // Per-gaussian, view-independent parts come precomputed (DeviceScene, f64 like the
+        // reference, rounded once): p_min = ln(1/255) - ln(sigmoid(logit)) (+inf when the
+        // reference skips the splat, opacity < 1/255) and the degree-0 colour in fp16.
+        // Higher degrees are evaluated here in f32 (the colour is stored as fp16).
+        const float4 ap = __ldg(reinterpret_cast<const float4 *>(scene.appear) + g);
+        const float p_min = ap.x;
+        const bool skip = !(p_min < __int_as_float(0x7f800000));
         int deg = as.sh_degree;
         if (opts.sh_degree_eval >= 0 && opts.sh_degree_eval < deg) deg = opts.sh_degree_eval;
-        const float *shp = scene.sh + g * (int64_t)scene.sh_stride;
-        double col[3];
-        for (int ch = 0; ch < 3; ch++) col[ch] = kShC0 * (double)__ldg(shp + ch);
-        if (deg >= 1) {
-            double dx = m0 - cam.pos[0], dy = m1 - cam.pos[1], dz = m2 - cam.pos[2];
-            const double nrm = sqrt(dx * dx + dy * dy + dz * dz);
-            dx /= nrm;
-            dy /= nrm;
-            dz /= nrm;
+        sc_splat sp;
+        if (deg == 0) {
+            const uint32_t rg = __float_as_uint(ap.y), bz = __float_as_uint(ap.z);
+            sp.rgb[0] = (uint16_t)(rg & 0xFFFFu);
+            sp.rgb[1] = (uint16_t)(rg >> 16);
+            sp.rgb[2] = (uint16_t)(bz & 0xFFFFu);
+        } else {
+            const float *shp = scene.sh + g * (int64_t)scene.sh_stride;
+            float dx = mw.x - pos_x, dy = mw.y - pos_y, dz = mw.z - pos_z;
+            const float rn = rsqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+            dx *= rn;
+            dy *= rn;
+            dz *= rn;
+            const float C0 = (float)kShC0, C1 = (float)kShC1;
+            float col[3];
             for (int ch = 0; ch < 3; ch++) {
-                const double s1 = __ldg(shp + 3 + ch), s2 = __ldg(shp + 6 + ch), s3 = __ldg(shp + 9 + ch);
-                col[ch] = col[ch] - kShC1 * dy * s1 + kShC1 * dz * s2 - kShC1 * dx * s3;
+                col[ch] = C0 * __ldg(shp + ch) - C1 * dy * __ldg(shp + 3 + ch) + C1 * dz * __ldg(shp + 6 + ch) -
+                          C1 * dx * __ldg(shp + 9 + ch);
             }
             if (deg >= 2) {
-                const double xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yz = dy * dz, xz = dx * dz;
+                const float xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yz = dy * dz, xz = dx * dz;
                 for (int ch = 0; ch < 3; ch++) {
                     const float *c = shp + ch;
-                    col[ch] = col[ch] + kShC2[0] * xy * (double)c[12] + kShC2[1] * yz * (double)c[15] +
-                              kShC2[2] * (2.0 * zz - xx - yy) * (double)c[18] + kShC2[3] * xz * (double)c[21] +
-                              kShC2[4] * (xx - yy) * (double)c[24];
+                    col[ch] += (float)kShC2[0] * xy * __ldg(c + 12) + (float)kShC2[1] * yz * __ldg(c + 15) +
+                               (float)kShC2[2] * (2.0f * zz - xx - yy) * __ldg(c + 18) +
+                               (float)kShC2[3] * xz * __ldg(c + 21) + (float)kShC2[4] * (xx - yy) * __ldg(c + 24);
                 }
                 if (deg >= 3) {
                     for (int ch = 0; ch < 3; ch++) {
                         const float *c = shp + ch;
-                        col[ch] = col[ch] + kShC3[0] * dy * (3.0 * xx - yy) * (double)c[27] +
-                                  kShC3[1] * xy * dz * (double)c[30] +
-                                  kShC3[2] * dy * (4.0 * zz - xx - yy) * (double)c[33] +
-                                  kShC3[3] * dz * (2.0 * zz - 3.0 * xx - 3.0 * yy) * (double)c[36] +
-                                  kShC3[4] * dx * (4.0 * zz - xx - yy) * (double)c[39] +
-                                  kShC3[5] * dz * (xx - yy) * (double)c[42] +
-                                  kShC3[6] * dx * (xx - 3.0 * yy) * (double)c[45];
+                        col[ch] += (float)kShC3[0] * dy * (3.0f * xx - yy) * __ldg(c + 27) +
+                                   (float)kShC3[1] * xy * dz * __ldg(c + 30) +
+                                   (float)kShC3[2] * dy * (4.0f * zz - xx - yy) * __ldg(c + 33) +
+                                   (float)kShC3[3] * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy) * __ldg(c + 36) +
+                                   (float)kShC3[4] * dx * (4.0f * zz - xx - yy) * __ldg(c + 39) +
+                                   (float)kShC3[5] * dz * (xx - yy) * __ldg(c + 42) +
+                                   (float)kShC3[6] * dx * (xx - 3.0f * yy) * __ldg(c + 45);
                     }
                 }
             }
+            for (int ch = 0; ch < 3; ch++)
+                sp.rgb[ch] = __half_as_ushort(__float2half_rn(fminf(fmaxf(col[ch] + 0.5f, 0.0f), 1.0f)));
         }
-        // opacity = sigmoid(logit) (sc/asset.py:44-51) in fp32: it only feeds the
-        // fp32 blend (alpha, p_min) and the widened support box below
-        const float xl = mo.w;
-        float op;
-        if (xl >= 0.0f) {
-            op = __fdividef(1.0f, 1.0f + __expf(-xl));
-        } else {
-            const float e = __expf(xl);
-            op = __fdividef(e, 1.0f + e);
-        }
-        const bool skip = !(op >= 1.0f / 255.0f);   // reference: `op < min_alpha: continue`
-        const float p_min = skip ? __int_as_float(0x7f800000) : (float)log_min_alpha - __logf(op);
-
-        sc_splat sp;
         sp.mx = (float)mx;
         sp.my = (float)my;
-        sp.half_a = (float)(0.5 * ca);
-        sp.b = (float)cb;
-        sp.half_c = (float)(0.5 * cc);
+        if (fast_done) {
+            sp.half_a = f_ha;
+            sp.b = f_b;
+            sp.half_c = f_hc;
+        } else {
+            sp.half_a = (float)(0.5 * ca);
+            sp.b = (float)cb;
+            sp.half_c = (float)(0.5 * cc);
+        }
         sp.p_min = p_min;
-        for (int ch = 0; ch < 3; ch++)
-            sp.rgb[ch] = __half_as_ushort(__float2half_rn((float)clampd(col[ch] + 0.5, 0.0, 1.0)));
         sp.reserved = 0;
         sc_window win;
         if (passed && !skip) {
             // reference pixel window (sc/_kernels.py:224-227), intersected with the
             // bounding box of the alpha >= 1/255 support {1/2 d^T cov^-1 d <= L},
-            // L = log(op) - log(1/255): |dx| <= sqrt(2 L cov_xx).  Pixels outside the
-            // box fail the reference's `power < p_min` test, so the image is
-            // unchanged; the box is widened by 1e-6 relative + 1e-3 px for safety.
-            // Also clipped to the splat's tile rectangle in pixels: the reference only
-            // composites a splat inside tiles whose list holds it, and its window can
-            // reach one pixel past the rect (A8 step 3).
-            // L = -p_min; the fp32 opacity's error is far inside the widening
-            const double L = -(double)p_min;
-            double ex, ey;
-            if (fast_done) {   // f32: a, c widened by their error bound, then 1e-4 relative + 1e-2 px
-                const float sl = sqrt_approx(2.0f * (float)L);
-                ex = (double)(sl * ex_f) * (1.0 + 1e-4) + 1e-2;
-                ey = (double)(sl * ey_f) * (1.0 + 1e-4) + 1e-2;
+            // L = log(op) - log(1/255) = -p_min: |dx| <= sqrt(2 L cov_xx).  Pixels
+            // outside the box fail the reference's `power < p_min` test, so the image
+            // is unchanged; the box is widened for safety.  Also clipped to the
+            // splat's tile rectangle in pixels: the reference only composites a splat
+            // inside tiles whose list holds it, and its window can reach one pixel
+            // past the rect (A8 step 3).  Integer form of max(floor(m - r), ceil(m -
+            // e), ts t0) / min(floor(m + r) + 1, floor(m + e), ts t1 - 1), clamped to
+            // the int16 window range [-1, 32767].
+            int bx0, bx1, by0, by1;
+            if (fast_done) {
+                // f32: a, c widened by their error bound, then 1e-4 relative + 1e-2 px, plus the
+                // f32 rounding of m and of the sums (1e-3 px + 2.4e-7 relative)
+                const float l2 = -2.0f * p_min;
+                const float ex = fmaf(sqrt_approx(l2 * f_sa), 1.0001f, 0.01f);
+                const float ey = fmaf(sqrt_approx(l2 * f_sc), 1.0001f, 0.01f);
+                const float mxf = sp.mx, myf = sp.my;
+                const float gx = ex + 1e-3f + 2.4e-7f * (fabsf(mxf) + ex);
+                const float gy = ey + 1e-3f + 2.4e-7f * (fabsf(myf) + ey);
+                bx0 = __float2int_ru(mxf - gx);
+                bx1 = __float2int_rd(mxf + gx);
+                by0 = __float2int_ru(myf - gy);
+                by1 = __float2int_rd(myf + gy);
             } else {
-                ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-5) + 1e-3;
-                ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-5) + 1e-3;
+                const double L = -(double)p_min;
+                const double ex = sqrt(2.0 * L * cov_a) * (1.0 + 1e-5) + 1e-3;
+                const double ey = sqrt(2.0 * L * cov_c) * (1.0 + 1e-5) + 1e-3;
+                bx0 = iceil(mx - ex);
+                bx1 = ifloor(mx + ex);
+                by0 = iceil(my - ey);
+                by1 = ifloor(my + ey);
             }
-            // integer form of max(floor(m - r), ceil(m - e), 16 t0) / min(floor(m + r) + 1,
-            // floor(m + e), 16 t1 - 1), clamped to the int16 window range [-1, 32767]
-            win.x0 = (int16_t)iclamp(max(max(fx0, iceil(mx - ex)), ts * tx0), -1, 32767);
-            win.x1 = (int16_t)iclamp(min(min(min(fx1, 0x7FFFFFFE) + 1, ifloor(mx + ex)), ts * tx1 - 1), -1, 32767);
-            win.y0 = (int16_t)iclamp(max(max(fy0, iceil(my - ey)), ts * ty0), -1, 32767);
-            win.y1 = (int16_t)iclamp(min(min(min(fy1, 0x7FFFFFFE) + 1, ifloor(my + ey)), ts * ty1 - 1), -1, 32767);
+            win.x0 = (int16_t)iclamp(max(max(fx0, bx0), ts * tx0), -1, 32767);
+            win.x1 = (int16_t)iclamp(min(min(min(fx1, 0x7FFFFFFE) + 1, bx1), ts * tx1 - 1), -1, 32767);
+            win.y0 = (int16_t)iclamp(max(max(fy0, by0), ts * ty0), -1, 32767);
+            win.y1 = (int16_t)iclamp(min(min(min(fy1, 0x7FFFFFFE) + 1, by1), ts * ty1 - 1), -1, 32767);
         } else {   // never composited
             win.x0 = 1;
             win.x1 = 0;
@@ -396,6 +417,11 @@ __global__ void __launch_bounds__(256, 2) k_project(
         if (rect) rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0, (unsigned short)ty1);
         if (dbg_f64) {
             double *d = dbg_f64 + 8 * k;
+            if (fast_done) {   // the f32 conic (0.5 a and 0.5 c are exact halvings)
+                ca = 2.0 * (double)f_ha;
+                cb = (double)f_b;
+                cc = 2.0 * (double)f_hc;
+            }
             d[0] = mx; d[1] = my; d[2] = ca; d[3] = cb; d[4] = cc; d[5] = tz; d[6] = radius; d[7] = det;
         }
         if (dbg_rect) {

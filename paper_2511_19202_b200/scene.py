@@ -219,6 +219,28 @@ def frustum_G(cam) -> float:
     return math.sqrt(1.0 + 1.69 * (tx * tx + ty * ty)) * 1.00001
 
 
+def appearance(asset: Asset) -> np.ndarray:
+    """(n, 4) float32 per-gaussian view-independent appearance (sc_scene.appear), computed
+    in f64 with the reference's formulas and rounded once:
+    [p_min = ln(1/255) - ln(sigmoid(logit)) (+inf when opacity < 1/255: the reference
+    skips the splat, sc/_kernels.py:215-219; sigmoid sc/asset.py:44-51),
+    fp16 bits r | g << 16, fp16 bits b, 0] with the degree-0 colour
+    clip(C0 f_dc + 0.5, 0, 1) (sc/raster.py:198-226 at degree 0)."""
+    from .asset import SH_C0, sigmoid
+
+    n = len(asset)
+    out = np.zeros((n, 4), np.float32)
+    op = sigmoid(asset.opacity_logits)
+    with np.errstate(divide="ignore"):
+        p_min = math.log(1.0 / 255.0) - np.log(np.maximum(op, 1e-300))
+    out[:, 0] = np.where(op < 1.0 / 255.0, np.inf, p_min).astype(np.float32)
+    rgb = np.clip(SH_C0 * asset.sh_coeffs[:, 0, :].astype(np.float64) + 0.5, 0.0, 1.0).astype(np.float16)
+    bits = rgb.view(np.uint16).astype(np.uint32)
+    out[:, 1] = (bits[:, 0] | (bits[:, 1] << 16)).view(np.float32)
+    out[:, 2] = bits[:, 2].view(np.float32)
+    return out
+
+
 def sigma_max(asset: Asset) -> np.ndarray:
     """Per-gaussian largest std-dev exp(max log_scale), f32 (frustum margin input)."""
     return np.exp(asset.log_scales.max(axis=1).astype(np.float64)).astype(np.float32)
@@ -273,6 +295,7 @@ class DeviceScene:
         quat = np.empty((n, 4), np.float32)
         scale_smax = np.empty((n, 4), np.float32)
         sh = np.zeros((n, sh_stride), np.float32)
+        appear = np.zeros((n, 4), np.float32)
         arecs = (nat.ScAssetRec * len(assets))()
         models: list[VisibilityModel] = []
         feat_jobs = []
@@ -287,6 +310,7 @@ class DeviceScene:
             scale_smax[lo:hi, 3] = smax
             k = 3 * (a.sh_degree + 1) ** 2
             sh[lo:hi, :k] = a.sh_coeffs.reshape(hi - lo, k)
+            appear[lo:hi] = appearance(a)
             r = arecs[i]
             r.offset, r.count = lo, hi - lo
             r.bound_local = float(np.sqrt((a.means.astype(np.float64) ** 2).sum(axis=1)).max())
@@ -324,10 +348,10 @@ class DeviceScene:
 
         dev = self.device
         with torch.cuda.device(dev):
-            self._upload(mean_opa, quat, scale_smax, sh, arecs, irecs, wrecs, n, flat, models, counts, offsets,
-                         sh_stride, feat_jobs, assets)
+            self._upload(mean_opa, quat, scale_smax, sh, appear, arecs, irecs, wrecs, n, flat, models, counts,
+                         offsets, sh_stride, feat_jobs, assets)
 
-    def _upload(self, mean_opa, quat, scale_smax, sh, arecs, irecs, wrecs, n, flat, models, counts, offsets,
+    def _upload(self, mean_opa, quat, scale_smax, sh, appear, arecs, irecs, wrecs, n, flat, models, counts, offsets,
                 sh_stride, feat_jobs, assets):
         import torch
 
@@ -337,6 +361,7 @@ class DeviceScene:
         self.quat = T(quat).to(dev)
         self.scale_smax = T(scale_smax).to(dev)
         self.sh = T(sh).to(dev)
+        self.appear = T(appear).to(dev)
         self.features = torch.zeros((max(n, 1), 8), dtype=torch.float16, device=dev)
         self.assets_t = nat.struct_tensor(arecs, dev)
         self.instances_t = nat.struct_tensor(irecs, dev)
@@ -357,6 +382,7 @@ class DeviceScene:
         s.assets, s.instances, s.n_instances = nat.ptr(self.assets_t), nat.ptr(self.instances_t), len(flat)
         s.vis_weights, s.n_models = nat.ptr(self.weights_t), len(models)
         s.n_pairs = self.max_pairs
+        s.appear = nat.ptr(self.appear)
         self.payload_bytes = [44 + 12 * (a.asset.sh_degree + 1) ** 2 for a in assets]
 
 

@@ -239,9 +239,10 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
                            Counters *ctr, uint32_t *defer_list, cudaStream_t st);
 // equal depth keys -> (f64 depth, survivor index) order; depth from depth64 or
 // recomputed from the survivor (project.cu, -fmad=false)
+// scratch: n_max doubles, free during the tie-fix (long runs sort their f64 depths there)
 cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const sc_camera &cam, const uint32_t *keys,
                           uint2 *pv, const double *depth64, const unsigned long long *n_dev, int64_t n_max,
-                          uint32_t *run_list, Counters *ctr, sc_frame_stats *stats, cudaStream_t st);
+                          uint32_t *run_list, double *scratch, Counters *ctr, sc_frame_stats *stats, cudaStream_t st);
 cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *surv, const unsigned long long *n_dev,
                        int64_t n_max, const sc_camera &cam, const sc_window *wins, sc_frame_stats *stats, bool blocks,
                        uint32_t **order_out, uint32_t **entries_out, uint32_t **keys_out, uint32_t *dbg_order,

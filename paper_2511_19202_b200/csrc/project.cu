@@ -12,12 +12,13 @@
 
 namespace sc {
 
-__constant__ double kShC0 = 0.28209479177387814;
-__constant__ double kShC1 = 0.4886025119029199;
-__constant__ double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
-                                -1.0925484305920792, 0.5462742152960396};
-__constant__ double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
-                                -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
+// real SH basis constants (sc/raster.py:30-37), f32: degrees >= 1 are evaluated in f32 (fp16 colours)
+constexpr float kShC0 = 0.28209479177387814f;
+constexpr float kShC1 = 0.4886025119029199f;
+__constant__ float kShC2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                               -1.0925484305920792f, 0.5462742152960396f};
+__constant__ float kShC3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f, 0.3731763325901154f,
+                               -0.4570457994644658f, 1.445305721320277f, -0.5900435899266435f};
 
 __device__ __forceinline__ sc_survivor make_survivor(uint32_t inst, uint32_t gid)
 {
@@ -157,17 +158,24 @@ __global__ void __launch_bounds__(256, 2) k_project(
                 const float fa = fdot3(u0, u1, u2, j00, j01, j02) + dil;
                 const float fb = fdot3(u0, u1, u2, j10, j11, j12);
                 const float fc = fdot3(v0, v1, v2, j10, j11, j12) + dil;
-                const float sg0 = sqrt_approx(g00), sg1 = sqrt_approx(g11), sg2 = sqrt_approx(g22);   // bound only
-                const float na = fdot3(fabsf(j00), fabsf(j01), fabsf(j02), sg0, sg1, sg2);
-                const float nc = fdot3(fabsf(j10), fabsf(j11), fabsf(j12), sg0, sg1, sg2);
+                // (na + nc)^2 with na = sum |j0i| sqrt(g_ii) (nc likewise) is bounded without a
+                // square root by Cauchy-Schwarz: <= 2 tr(Sigma) (|J0|^2 + |J1|^2), tr(Sigma) =
+                // s0 + s1 + s2 (rotation invariant; 1e-3 slack for the f32 rotation's norm)
+                const float jn = fdot3(j00, j01, j02, j00, j01, j02) + fdot3(j10, j11, j12, j10, j11, j12);
+                const float nn = 2.002f * (s0 + s1 + s2) * jn;
                 constexpr float kEps = 5.9604645e-08f, K = 64.0f;
-                const float err = K * kEps * (na + nc) * (na + nc) + 4.0f * kEps * fabsf(dil);
+                const float err = K * kEps * nn + 4.0f * kEps * fabsf(dil);
                 const float hd = 0.5f * (fa - fc);
                 const float lam = 0.5f * (fa + fc) + sqrtf(hd * hd + fb * fb);
                 const float lo = fmaxf(lam * (1.0f - 16.0f * kEps) - 2.0f * err, 0.0f);
                 const float hi = lam * (1.0f + 16.0f * kEps) + 2.0f * err;
-                const float rlo = ceilf(3.0f * sqrtf(lo) * (1.0f - 4.0f * kEps));
-                const float rhi = ceilf(3.0f * sqrtf(hi) * (1.0f + 4.0f * kEps));
+                // radius = ceil(3 sqrt(lambda)) is the same integer rc for every lambda in [lo, hi] iff
+                // (rc - 1)^2 < 9 lo and 9 hi <= rc^2 (squares exact in f32 below 4096; 9 x rounded
+                // with margin): one square root instead of one per interval end
+                const float rc = ceilf(3.0f * sqrtf(lam));
+                const bool r_ok = rc >= 1.0f && rc <= 4000.0f && (rc - 1.0f) * (rc - 1.0f) < 9.0f * lo * (1.0f - 8.0f * kEps) &&
+                                  9.0f * hi * (1.0f + 8.0f * kEps) <= rc * rc;
+                const float rlo = r_ok ? rc : 0.0f, rhi = r_ok ? rc : -1.0f;
                 // det = a c - b^2 in f32 with one FMA-exact square (Kahan): |error| <= 2 eps |det|,
                 // added to the bound below together with the f32 rounding of radius_clip
                 const float bb = fb * fb;
@@ -179,13 +187,12 @@ __global__ void __launch_bounds__(256, 2) k_project(
                     fast_done = true;
                     radius = (double)rlo;
                     f_det = fdet;
-                    det = (double)fdet;
                     const float inv = 1.0f / fdet;
                     f_ha = 0.5f * (fc * inv);
                     f_b = -fb * inv;
                     f_hc = 0.5f * (fa * inv);
                     valid = rlo > 0.0f;
-                    if (valid && clip_f > 0.0f && fdet < clip_f) valid = false;
+                    if (valid && clip_f > 0.0f && fdet < clip_f) valid = false;   // det == fdet (dbg only)
                     // support box from the conservative a, c (times 2 L later)
                     f_sa = fa + err;
                     f_sc = fc + err;
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(256, 2) k_project(
             dx *= rn;
             dy *= rn;
             dz *= rn;
-            const float C0 = (float)kShC0, C1 = (float)kShC1;
+            const float C0 = kShC0, C1 = kShC1;
             float col[3];
             for (int ch = 0; ch < 3; ch++) {
                 col[ch] = C0 * __ldg(shp + ch) - C1 * dy * __ldg(shp + 3 + ch) + C1 * dz * __ldg(shp + 6 + ch) -
@@ -325,20 +332,20 @@ __global__ void __launch_bounds__(256, 2) k_project(
                 const float xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yz = dy * dz, xz = dx * dz;
                 for (int ch = 0; ch < 3; ch++) {
                     const float *c = shp + ch;
-                    col[ch] += (float)kShC2[0] * xy * __ldg(c + 12) + (float)kShC2[1] * yz * __ldg(c + 15) +
-                               (float)kShC2[2] * (2.0f * zz - xx - yy) * __ldg(c + 18) +
-                               (float)kShC2[3] * xz * __ldg(c + 21) + (float)kShC2[4] * (xx - yy) * __ldg(c + 24);
+                    col[ch] += kShC2[0] * xy * __ldg(c + 12) + kShC2[1] * yz * __ldg(c + 15) +
+                               kShC2[2] * (2.0f * zz - xx - yy) * __ldg(c + 18) +
+                               kShC2[3] * xz * __ldg(c + 21) + kShC2[4] * (xx - yy) * __ldg(c + 24);
                 }
                 if (deg >= 3) {
                     for (int ch = 0; ch < 3; ch++) {
                         const float *c = shp + ch;
-                        col[ch] += (float)kShC3[0] * dy * (3.0f * xx - yy) * __ldg(c + 27) +
-                                   (float)kShC3[1] * xy * dz * __ldg(c + 30) +
-                                   (float)kShC3[2] * dy * (4.0f * zz - xx - yy) * __ldg(c + 33) +
-                                   (float)kShC3[3] * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy) * __ldg(c + 36) +
-                                   (float)kShC3[4] * dx * (4.0f * zz - xx - yy) * __ldg(c + 39) +
-                                   (float)kShC3[5] * dz * (xx - yy) * __ldg(c + 42) +
-                                   (float)kShC3[6] * dx * (xx - 3.0f * yy) * __ldg(c + 45);
+                        col[ch] += kShC3[0] * dy * (3.0f * xx - yy) * __ldg(c + 27) +
+                                   kShC3[1] * xy * dz * __ldg(c + 30) +
+                                   kShC3[2] * dy * (4.0f * zz - xx - yy) * __ldg(c + 33) +
+                                   kShC3[3] * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy) * __ldg(c + 36) +
+                                   kShC3[4] * dx * (4.0f * zz - xx - yy) * __ldg(c + 39) +
+                                   kShC3[5] * dz * (xx - yy) * __ldg(c + 42) +
+                                   kShC3[6] * dx * (xx - 3.0f * yy) * __ldg(c + 45);
                     }
                 }
             }
@@ -417,10 +424,11 @@ __global__ void __launch_bounds__(256, 2) k_project(
         if (rect) rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0, (unsigned short)ty1);
         if (dbg_f64) {
             double *d = dbg_f64 + 8 * k;
-            if (fast_done) {   // the f32 conic (0.5 a and 0.5 c are exact halvings)
+            if (fast_done) {   // the f32 conic (0.5 a and 0.5 c are exact halvings) and det
                 ca = 2.0 * (double)f_ha;
                 cb = (double)f_b;
                 cc = 2.0 * (double)f_hc;
+                det = (double)f_det;
             }
             d[0] = mx; d[1] = my; d[2] = ca; d[3] = cb; d[4] = cc; d[5] = tz; d[6] = radius; d[7] = det;
         }
@@ -612,13 +620,35 @@ __global__ void k_tie_runs(sc_scene scene, const sc_survivor *surv, sc_camera ca
 // pass 3: runs longer than kTieRegs, one CTA each: depths computed in parallel;
 // runs already in (depth, index) order (e.g. a planar asset facing the camera:
 // all depths equal) are left alone, others up to kTieSmem elements are
-// bitonic-sorted in shared memory, longer unsorted ones insertion-sorted by one
-// thread (never seen in practice).
+// bitonic-sorted in shared memory; longer ones are sorted by a CTA-wide
+// ascending-only bitonic network (mirror first step per merge size, so the
+// virtual +inf padding past the run never moves): merge steps with partner
+// distance >= kTieSmem run in global memory over the run's own slice of the
+// depth-sort ping-pong buffer (f64 depths, free after the depth sort), the
+// shorter ones chunk by chunk in shared memory.
 constexpr int kTieSmem = 2048;
+
+__device__ __forceinline__ bool tie_less(double da, uint32_t ia, double db, uint32_t ib)
+{
+    return da < db || (da == db && ia < ib);
+}
+
+// one compare-exchange of positions lo < hi (min to lo) in global memory
+__device__ __forceinline__ void tie_ce_global(double *d, uint2 *v, int64_t lo, int64_t hi)
+{
+    const double dl = d[lo], dh = d[hi];
+    const uint2 vl = v[lo], vh = v[hi];
+    if (tie_less(dh, vh.x, dl, vl.x)) {
+        d[lo] = dh; d[hi] = dl;
+        v[lo] = vh; v[hi] = vl;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_tie_long(sc_scene scene, const sc_survivor *surv, sc_camera cam,
                                                   const uint32_t *keys, uint2 *pv, const double *depth64,
                                                   const unsigned long long *n_dev, int64_t n_host,
-                                                  const uint32_t *long_list, const Counters *ctr, sc_frame_stats *stats)
+                                                  const uint32_t *long_list, const Counters *ctr, sc_frame_stats *stats,
+                                                  double *scratch)
 {
     __shared__ double s_d[kTieSmem];
     __shared__ uint2 s_v[kTieSmem];
@@ -685,19 +715,60 @@ __global__ void __launch_bounds__(256) k_tie_long(sc_scene scene, const sc_survi
                     __syncthreads();
                 }
             for (int a = tid; a < len; a += 256) pv[i + a] = s_v[a];
-        } else if (tid == 0) {
-            for (int64_t a = i + 1; a < e; a++) {
-                const uint2 va = pv[a];
-                const double da = tie_depth(scene, surv, cam, depth64, va.x);
-                int64_t b = a - 1;
-                while (b >= i) {
-                    const uint2 vb = pv[b];
-                    const double db = tie_depth(scene, surv, cam, depth64, vb.x);
-                    if (db < da || (db == da && vb.x < va.x)) break;
-                    pv[b + 1] = vb;
-                    b--;
+        } else {
+            double *gd = scratch + i;   // this run's slice: runs are disjoint
+            uint2 *gv = pv + i;
+            for (int64_t a = tid; a < len; a += 256) gd[a] = tie_depth(scene, surv, cam, depth64, gv[a].x);
+            __syncthreads();
+            int64_t p2 = 1;
+            while (p2 < len) p2 <<= 1;
+            // chunk-local steps (partner distance < kTieSmem) of merge size k in shared memory;
+            // kfull: the whole network up to merge size kTieSmem (first phase)
+            auto smem_steps = [&](int64_t k, bool kfull) {
+                for (int64_t c0 = 0; c0 < len; c0 += kTieSmem) {
+                    const int cl = (int)min((int64_t)kTieSmem, len - c0);
+                    for (int a = tid; a < kTieSmem; a += 256) {
+                        s_d[a] = a < cl ? gd[c0 + a] : INFINITY;
+                        s_v[a] = a < cl ? gv[c0 + a] : make_uint2(0xFFFFFFFFu, 0u);
+                    }
+                    __syncthreads();
+                    const int k0 = kfull ? 2 : (int)kTieSmem;   // merge sizes handled here
+                    for (int kk = k0; kk <= (kfull ? kTieSmem : kTieSmem); kk <<= 1) {
+                        const bool mirror_here = kfull;
+                        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                            if (!kfull && jj >= kTieSmem) continue;
+                            for (int a = tid; a < kTieSmem; a += 256) {
+                                int b;
+                                if (mirror_here && jj == (kk >> 1)) b = (a & ~(kk - 1)) + (kk - 1 - (a & (kk - 1)));
+                                else b = a ^ jj;
+                                if (b > a && tie_less(s_d[b], s_v[b].x, s_d[a], s_v[a].x)) {
+                                    const double td = s_d[a]; s_d[a] = s_d[b]; s_d[b] = td;
+                                    const uint2 tv = s_v[a]; s_v[a] = s_v[b]; s_v[b] = tv;
+                                }
+                            }
+                            __syncthreads();
+                        }
+                        if (!kfull) break;
+                    }
+                    for (int a = tid; a < cl; a += 256) {
+                        gd[c0 + a] = s_d[a];
+                        gv[c0 + a] = s_v[a];
+                    }
+                    __syncthreads();
                 }
-                pv[b + 1] = va;
+                (void)k;
+            };
+            smem_steps(kTieSmem, true);   // every chunk sorted
+            for (int64_t k = 2 * kTieSmem; k <= p2; k <<= 1) {
+                for (int64_t jj = k >> 1; jj >= kTieSmem; jj >>= 1) {
+                    const bool mirror = jj == (k >> 1);
+                    for (int64_t a = tid; a < p2; a += 256) {
+                        const int64_t b = mirror ? (a & ~(k - 1)) + (k - 1 - (a & (k - 1))) : (a ^ jj);
+                        if (b > a && b < len) tie_ce_global(gd, gv, a, b);
+                    }
+                    __syncthreads();
+                }
+                smem_steps(k, false);   // steps jj = kTieSmem / 2 .. 1, chunk by chunk
             }
         }
         __syncthreads();
@@ -706,7 +777,7 @@ __global__ void __launch_bounds__(256) k_tie_long(sc_scene scene, const sc_survi
 
 cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const sc_camera &cam, const uint32_t *keys,
                           uint2 *pv, const double *depth64, const unsigned long long *n_dev, int64_t n_max,
-                          uint32_t *run_list, Counters *ctr, sc_frame_stats *stats, cudaStream_t st)
+                          uint32_t *run_list, double *scratch, Counters *ctr, sc_frame_stats *stats, cudaStream_t st)
 {
     if (n_max <= 0) return cudaSuccess;
     const int nsm = sm_count();
@@ -717,7 +788,8 @@ cudaError_t launch_tiefix(const sc_scene &scene, const sc_survivor *surv, const 
     uint32_t *long_list = run_list + (n_max + 1) / 2;
     SC_LAUNCH(k_tie_runs, (int)std::max<int64_t>(1, blocks / 8), 256, 0, st, scene, surv, cam, keys, pv, depth64, n_dev,
               n_max, run_list, long_list, ctr, stats);
-    SC_LAUNCH(k_tie_long, nsm * 2, 256, 0, st, scene, surv, cam, keys, pv, depth64, n_dev, n_max, long_list, ctr, stats);
+    SC_LAUNCH(k_tie_long, nsm * 2, 256, 0, st, scene, surv, cam, keys, pv, depth64, n_dev, n_max, long_list, ctr, stats,
+              scratch);
     return cudaGetLastError();
 }
 

@@ -832,8 +832,10 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
     if (e != cudaSuccess) return e;
     const unsigned long long *p_dev = &ws.ctr->passed;   // passed splats lead the sorted order
     // ws.ecount is free until the entry counts: it holds the tie-run list
-    e = launch_tiefix(scene, surv, cam, keys_s, pv_s, blocks ? nullptr : ws.depth64, p_dev, n_max, ws.ecount, ws.ctr,
-                      stats, st);
+    // the other payload buffer of the depth sort is free now: long tie runs sort f64 depths there
+    double *tie_scratch = reinterpret_cast<double *>(pv_s == ws.pv_a ? ws.pv_b : ws.pv_a);
+    e = launch_tiefix(scene, surv, cam, keys_s, pv_s, blocks ? nullptr : ws.depth64, p_dev, n_max, ws.ecount,
+                      tie_scratch, ws.ctr, stats, st);
     if (e != cudaSuccess) return e;
     if (dbg_order)   // debug copy-out of the (depth, index) order of the passed survivors
         SC_LAUNCH(k_extract_order, grid_for(n_max, 256), 256, 0, st, pv_s, p_dev, n_max, dbg_order);

@@ -134,27 +134,24 @@ def forward(model: VisibilityModel, inputs) -> np.ndarray:
     """Batched visibility MLP on the GPU: (B, 16) -> (B, 1) logits.
 
     Inputs are materialised fp32 rows; the kernel converts them to fp16 and
-    runs the 16->32->32 layers on tcgen05 tensor cores (sc_vis_mlp_forward).
+    runs the 16->32->32 layers on tcgen05 tensor cores (torch.ops.splatcull.vis_mlp_forward).
     Accepts a numpy array or a CUDA torch tensor (then returns a tensor).
     """
-    import ctypes
-
     import torch
 
     from . import _native as nat
+    from . import ops
     from .scene import vis_weights_struct
 
-    lib = nat.load()
+    nat.load()
     is_tensor = isinstance(inputs, torch.Tensor)
     x = inputs if is_tensor else torch.from_numpy(np.ascontiguousarray(inputs, dtype=np.float32))
     if x.ndim != 2 or x.shape[1] != 16:
         raise ValueError(f"visibility MLP expects (B, 16) inputs, got {tuple(x.shape)}")
-    x = x.to("cuda", torch.float32).contiguous()
+    x = x.to("cuda" if not x.is_cuda else x.device, torch.float32).contiguous()
     w = nat.struct_tensor(vis_weights_struct(model), x.device)
-    out = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
-    nat.check(lib.sc_vis_mlp_forward(nat.ptr(w), nat.ptr(x), int(x.shape[0]), nat.ptr(out), nat.stream_handle()),
-              "sc_vis_mlp_forward")
-    out = out.view(-1, 1)
+    with torch.cuda.device(x.device):
+        out = ops.vis_mlp_forward(w, x).view(-1, 1)
     return out if is_tensor else out.cpu().numpy()
 
 

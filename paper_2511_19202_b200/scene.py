@@ -36,6 +36,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
+from . import ops
 from .asset import Asset
 from .nn import VisibilityModel, feature_inputs
 
@@ -383,20 +384,22 @@ class DeviceScene:
         s.vis_weights, s.n_models = nat.ptr(self.weights_t), len(models)
         s.n_pairs = self.max_pairs
         s.appear = nat.ptr(self.appear)
+        # packed form for torch.ops.splatcull (ops.py)
+        self.op_scene = [self.mean_opa, self.quat, self.scale_smax, self.sh, self.features, self.appear,
+                         self.assets_t, self.instances_t, self.weights_t]
+        self.op_meta = [n, sh_stride, len(assets), len(flat), len(models), self.max_pairs]
         self.payload_bytes = [44 + 12 * (a.asset.sh_degree + 1) ** 2 for a in assets]
 
 
 def encode_features_device(model: VisibilityModel, asset: Asset, device) -> "torch.Tensor":
-    """nn.encode_features on the GPU: (n, 8) fp16 (6 used)."""
+    """nn.encode_features on the GPU (torch.ops.splatcull.encode_features): (n, 8) fp16 (6 used)."""
     import torch
 
-    lib = nat.load()
+    nat.load()
     x = torch.from_numpy(feature_inputs(asset, model.mean_scale)).to(device)
     p = torch.from_numpy(feature_params(model)).to(device)
-    out = torch.empty((len(asset), 8), dtype=torch.float16, device=device)
-    nat.check(lib.sc_encode_features(nat.ptr(p), nat.ptr(x), len(asset), nat.ptr(out), nat.stream_handle()),
-              "sc_encode_features")
-    return out
+    with torch.cuda.device(x.device):
+        return ops.encode_features(p, x)
 
 
 class Workspace:
@@ -435,6 +438,11 @@ class Workspace:
     @property
     def nbytes(self) -> int:
         return int(self.buf.numel())
+
+    @property
+    def op_meta(self) -> list[int]:
+        w = self.struct
+        return [int(w.n_instances), int(w.max_pairs), int(w.cap_survivors), int(w.cap_entries)]
 
 
 @dataclass
@@ -554,10 +562,6 @@ class FrameDebug:
         self.block_offsets = torch.empty(8 * n_tiles16 + 1, dtype=torch.int32, device=dev)
         self.block_entries = torch.empty(max(ws.cap_e, 1), dtype=torch.int32, device=dev)
         self.block_codes = torch.empty(max(ws.cap_e, 1), dtype=torch.int32, device=dev)
-        self.struct = nat.ScFrameDebug()
-        d = self.struct
-        d.order, d.block_offsets = nat.ptr(self.order), nat.ptr(self.block_offsets)
-        d.block_entries, d.block_codes = nat.ptr(self.block_entries), nat.ptr(self.block_codes)
 
     def host(self, stats: dict) -> dict:
         """numpy copies: order [passed], block offsets, entries / codes [block_entries] (uint32 as int64)."""
@@ -615,12 +619,12 @@ class Renderer:
         ``survivors``: an explicit (S, 2) int32 [instance, gaussian] device list
         rendered through stages (c)-(e) of the frame path instead of the cull
         (sc_render_survivors).  ``debug``: FrameDebug buffers to copy the depth
-        order and block lists into.
+        order and block lists into.  Calls torch.ops.splatcull.render_frame_.
         """
         import torch
 
         opts = opts or RenderOptions()
-        lib = nat.load()
+        nat.load()
         dev = self.dscene.device
         with torch.cuda.device(dev):
             ws = self.workspace(cam, slot, opts.tile_size)
@@ -636,42 +640,30 @@ class Renderer:
                     out.contrib_max = torch.empty(ws.cap_s, dtype=torch.float32, device=dev)
             if return_survivors and (out.survivors is None or out.survivors.shape[0] != ws.cap_s):
                 out.survivors = torch.empty((ws.cap_s, 2), dtype=torch.int32, device=dev)
-            fo = nat.ScFrameOut()
-            fo.image, fo.trans, fo.stats = nat.ptr(out.image), nat.ptr(out.trans), nat.ptr(out.stats_raw)
-            fo.contrib_sum = nat.ptr(out.contrib_sum) if opts.record_contributions else 0
-            fo.contrib_max = nat.ptr(out.contrib_max) if opts.record_contributions else 0
-            fo.survivors = nat.ptr(out.survivors) if return_survivors else 0
-            handles = None
+            handles: list[int] = []
             if isinstance(stage_events, _StageEvents):
-                handles = stage_events.handles
+                handles = [int(h) for h in stage_events.handles]
             elif stage_events is not None:
-                handles = (ctypes.c_void_p * nat.N_STAGE_EVENTS)()
-                for i, ev in enumerate(stage_events[:nat.N_STAGE_EVENTS]):
+                for ev in stage_events[:nat.N_STAGE_EVENTS]:
                     if not ev.cuda_event:
                         ev.record()            # torch creates the CUDA event lazily
-                    handles[i] = ev.cuda_event
-            if handles is not None:
-                fo.stage_events = ctypes.cast(handles, ctypes.c_void_p)
-                fo.n_stage_events = nat.N_STAGE_EVENTS
+                    handles.append(int(ev.cuda_event))
+            dbg: list = []
             if debug is not None:
                 if debug.order.numel() < ws.cap_s or debug.block_entries.numel() < ws.cap_e:
                     raise ValueError("FrameDebug buffers are smaller than the workspace capacities")
-                fo.debug = ctypes.addressof(debug.struct)
-            camc = nat.camera_struct(cam)
-            optc = opts.struct(cam)
-            if survivors is not None:
-                n = int(survivors.shape[0])
-                if n > ws.cap_s:
-                    if debug is not None:
-                        raise ValueError("survivor list exceeds the workspace capacity (grow it before FrameDebug)")
-                    ws.grow(n, ws.cap_e)
-                nat.check(lib.sc_render_survivors(ctypes.byref(self.dscene.struct), nat.ptr(survivors), n,
-                                                  ctypes.byref(camc), ctypes.byref(optc), ctypes.byref(ws.struct),
-                                                  ctypes.byref(fo), nat.stream_handle()), "sc_render_survivors")
-            else:
-                nat.check(lib.sc_render_composed(ctypes.byref(self.dscene.struct), ctypes.byref(camc),
-                                                 ctypes.byref(optc), ctypes.byref(ws.struct), ctypes.byref(fo),
-                                                 nat.stream_handle()), "sc_render_composed")
+                dbg = [debug.order, debug.block_offsets, debug.block_entries, debug.block_codes]
+            if survivors is not None and int(survivors.shape[0]) > ws.cap_s:
+                if debug is not None:
+                    raise ValueError("survivor list exceeds the workspace capacity (grow it before FrameDebug)")
+                ws.grow(int(survivors.shape[0]), ws.cap_e)
+            cam_f, cam_i = ops.pack_camera(cam)
+            opt_f, opt_i = ops.pack_opts(opts.struct(cam))
+            rec = opts.record_contributions
+            ops.render_frame_(self.dscene.op_scene, self.dscene.op_meta, cam_f, cam_i, opt_f, opt_i, ws.buf,
+                              ws.op_meta, out.image, out.trans, out.stats_raw, out.contrib_sum if rec else None,
+                              out.contrib_max if rec else None, out.survivors if return_survivors else None,
+                              survivors, handles, dbg)
         return out
 
     def render(self, cam, opts: RenderOptions | None = None, return_survivors: bool = False,

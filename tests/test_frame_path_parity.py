@@ -234,7 +234,8 @@ def test_frame_path_config3_views(view):
     check_frame_path(wl.scene, cam, c.surv_inst, c.surv_gid)
 
 
-@pytest.mark.parametrize("tilt, n", [(2e-12, 1_500), (0.0, 20_000)], ids=["tilted-unsorted-run", "head-on-equal-run"])
+@pytest.mark.parametrize("tilt, n", [(2e-12, 1_500), (0.0, 20_000), (2e-12, 60_000)],
+                         ids=["tilted-unsorted-run", "head-on-equal-run", "tilted-unsorted-60k-run"])
 def test_frame_path_tie_runs(tilt, n):
     from paper_2511_19202_b200.camera import Camera
     from test_gpu_parity import _plane_asset

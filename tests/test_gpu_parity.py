@@ -465,12 +465,14 @@ def _plane_asset(n, seed):
                  sh_coeffs=rng.uniform(-1, 1, (n, 1, 3)).astype(np.float32), sh_degree=0)
 
 
-@pytest.mark.parametrize("tilt, n", [(2e-12, 1_500), (0.0, 60_000)], ids=["tilted-unsorted-run", "head-on-equal-run"])
+@pytest.mark.parametrize("tilt, n", [(2e-12, 1_500), (0.0, 60_000), (2e-12, 60_000)],
+                         ids=["tilted-unsorted-run", "head-on-equal-run", "tilted-unsorted-60k-run"])
 def test_long_depth_tie_runs(tilt, n):
     """A plane facing the camera: every splat's depth key is equal (the frame
     path quantises over the instance sphere), so the whole asset is one tie run.
     Tilted by ~1e-12 the f64 depths differ and the run must be re-ordered
-    (CTA bitonic sort); head-on they are equal and the run stays in index order.
+    (CTA bitonic sort; beyond 2,048 splats a CTA-wide network over global
+    memory); head-on they are equal and the run stays in index order.
     Image against the f64 oracle rendering the same splats."""
     import paper_2511_19202_b200 as pkg
     from paper_2511_19202_b200.camera import Camera

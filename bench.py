@@ -371,6 +371,13 @@ def main():
                 for j, name in enumerate(nat.STAGE_NAMES)}
     total_ms = float(sum(dev_ms))   # serial pass
     peak_gb = torch.cuda.max_memory_allocated() / 1e9
+    # per frame slot: its workspace (sized on the largest view) + its output frame; the scene is shared
+    slot_ws = {k[2]: w.nbytes for k, w in r.workspaces.items() if k[3] == 16}
+    frame_bytes = int(cams[0].width) * int(cams[0].height) * 16 + nat.STATS_BYTES
+    vram = {"scene_gb": r.dscene.nbytes / 1e9,
+            "per_frame_slot_gb": [round((slot_ws[j] + frame_bytes) / 1e9, 3) for j in sorted(slot_ws)],
+            "frame_slots": len(slot_ws), "peak_allocated_gb": peak_gb,
+            "note": "per slot = workspace (capacities from the largest view, +5 % headroom) + image/T/stats buffers"}
     stats = [nat.stats_dict(f.stats_raw.cpu().numpy()) if f is not None else None for f in frames]
     if any(s and s["overflow"] for s in stats):
         raise RuntimeError("workspace overflow inside the timed region")
@@ -497,7 +504,7 @@ def main():
         "dtype": "f64 (cull, projection, keys) + fp16/f32 tensor-core MLP + fp32 blend",
         "data": "synthetic (seeded reference generators, random-init visibility MLPs)",
         "config": describe(wl, args, world),
-        "peak_vram_gb": peak_gb,
+        "peak_vram_gb": peak_gb, "vram": vram,
         "psnr_vs_cpu_oracle": quality,
         "per_view_ms": {["near", "mid", "far"][k] if ncam == 3 else str(k): float(np.mean(v))
                         for k, v in sorted(per_view.items())},

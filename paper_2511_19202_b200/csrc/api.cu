@@ -85,7 +85,7 @@ constexpr size_t kAlign = 256;
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
-    size_t inst, chunk_state, chunk_cnt, chunk_inst, chunk_stage, ctr, surv, splats, wins, key_a, key_b, pv_a, pv_b, depth64, rect, ecount, ekey_a, ekey_b,
+    size_t inst, chunk_state, chunk_cnt, chunk_inst, chunk_stage, ctr, surv, splats, wins, key_a, key_b, pv_a, pv_b, depth64, rect, ekey_a, ekey_b,
         eval_a, eval_b, tile_off, task_order, boff, rs_counts, scan_part, total;
     int64_t max_chunks, nblk_max, n_tiles, n_tiles_ref;
     int n_tx, n_ty, n_tx_ref;
@@ -93,6 +93,16 @@ struct Layout {
 
 constexpr int kMaxTileSize = 65535;
 
+// Workspace layout.  Two regions are unions of buffers with disjoint lifetimes
+// (stream order within one frame):
+//   U = [surv | key_a | key_b | pv_b]          cull -> projection -> depth sort -> tie-fix
+//     = [ekey_b | eval_b]                      block / entry sort ping-pong (after the emission)
+//   V = [chunk_stage]                          cull staging
+//     = [depth64 | rect]                       stage API: projection -> tie-fix / entry counts
+//     = [ekey_a | eval_a]                      emission -> block sort -> blend
+// key_b doubles as the projection's deferred-splat list, the tie-run list and the
+// emission's per-warp totals; pv_b (the depth sort's other payload) holds the
+// f64 depths of long tie runs.  Per survivor: splats 32 + wins 8 + pv_a 8 + U 24 B.
 Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int32_t w, int32_t h, int32_t ts)
 {
     Layout L{};
@@ -105,6 +115,8 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     const int64_t big = std::max<int64_t>(std::max<int64_t>(capS, capE), 1);
     L.nblk_max = (big + sc::kRadixTile - 1) / sc::kRadixTile;
     const int64_t part = (std::max<int64_t>(256 * L.nblk_max, big) + sc::kScanTile - 1) / sc::kScanTile + 1;
+    // key buffers also hold small per-tile lists: at least 4096 words
+    const int64_t capK = std::max<int64_t>(capS, 4096);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
@@ -115,23 +127,42 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.chunk_state = take(sizeof(unsigned long long) * (size_t)L.max_chunks);
     L.chunk_cnt = take(sizeof(uint32_t) * (size_t)L.max_chunks);
     L.chunk_inst = take(sizeof(uint32_t) * (size_t)L.max_chunks);
-    L.chunk_stage = take(sizeof(uint16_t) * (size_t)L.max_chunks * sc::kChunk);
     L.ctr = take(sizeof(sc::Counters));
-    L.surv = take(sizeof(sc_survivor) * (size_t)capS);
     L.splats = take(sizeof(sc_splat) * (size_t)capS);
     L.wins = take(sizeof(sc_window) * (size_t)capS);
-    // +16 bytes: onesweep bulk copies round the last tile up to 16 bytes
-    L.key_a = take(4 * (size_t)capS + 16);
-    L.key_b = take(4 * (size_t)capS + 16);
+    // +16 bytes: radix bulk copies round the last tile up to 16 bytes
     L.pv_a = take(8 * (size_t)capS + 16);
-    L.pv_b = take(8 * (size_t)capS + 16);
-    L.depth64 = take(8 * (size_t)capS);
-    L.rect = take(8 * (size_t)capS);
-    L.ecount = take(4 * (size_t)capS);
-    L.ekey_a = take(4 * (size_t)capE + 16);
-    L.ekey_b = take(4 * (size_t)capE + 16);
-    L.eval_a = take(4 * (size_t)capE + 16);
-    L.eval_b = take(4 * (size_t)capE + 16);
+    // region U
+    {
+        const size_t u0 = off;
+        size_t o = 0;
+        auto sub = [&](size_t bytes) { size_t r = o; o = align_up(o + std::max<size_t>(bytes, 1)); return u0 + r; };
+        L.surv = sub(sizeof(sc_survivor) * (size_t)capS);
+        L.key_a = sub(4 * (size_t)capK + 16);
+        L.key_b = sub(4 * (size_t)capK + 16);
+        L.pv_b = sub(8 * (size_t)capS + 16);
+        const size_t u_a = o;
+        o = 0;
+        L.ekey_b = sub(4 * (size_t)capE + 16);
+        L.eval_b = sub(4 * (size_t)capE + 16);
+        off = align_up(u0 + std::max(u_a, o));
+    }
+    // region V
+    {
+        const size_t v0 = off;
+        size_t o = 0;
+        auto sub = [&](size_t bytes) { size_t r = o; o = align_up(o + std::max<size_t>(bytes, 1)); return v0 + r; };
+        L.chunk_stage = sub(sizeof(uint16_t) * (size_t)L.max_chunks * sc::kChunk);
+        const size_t v_a = o;
+        o = 0;
+        L.depth64 = sub(8 * (size_t)capS);
+        L.rect = sub(8 * (size_t)capS);
+        const size_t v_b = o;
+        o = 0;
+        L.ekey_a = sub(4 * (size_t)capE + 16);
+        L.eval_a = sub(4 * (size_t)capE + 16);
+        off = align_up(v0 + std::max(std::max(v_a, v_b), o));
+    }
     L.tile_off = take(4 * (size_t)(L.n_tiles_ref + 1));
     L.task_order = take(4 * (size_t)(8 * L.n_tiles));   // blend dispatch order over (tile, block) lists
     L.boff = take(4 * (size_t)(8 * L.n_tiles + 1));
@@ -165,7 +196,6 @@ int carve(const sc_workspace *ws, int32_t w, int32_t h, int32_t ts, sc::Ws &out)
     out.pv_b = reinterpret_cast<uint2 *>(b + L.pv_b);
     out.depth64 = reinterpret_cast<double *>(b + L.depth64);
     out.rect = reinterpret_cast<ushort4 *>(b + L.rect);
-    out.ecount = reinterpret_cast<uint32_t *>(b + L.ecount);
     out.ekey_a = reinterpret_cast<uint32_t *>(b + L.ekey_a);
     out.ekey_b = reinterpret_cast<uint32_t *>(b + L.ekey_b);
     out.eval_a = reinterpret_cast<uint32_t *>(b + L.eval_a);
@@ -244,6 +274,25 @@ __global__ void k_set_survivors(Counters *ctr, sc_frame_stats *stats, int64_t n)
     ctr->survivors = (unsigned long long)n;
     stats->survivors = n;
 }
+
+// dst[i] = src[i] for i < min(*n_dev, cap) (words; copy-outs of device-counted lists)
+__global__ void k_copy_words(const uint32_t *__restrict__ src, uint32_t *__restrict__ dst,
+                             const unsigned long long *n_dev, int64_t cap, int words_per_item)
+{
+    const int64_t n = std::min<int64_t>((int64_t)*n_dev, cap) * words_per_item;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t copy_counted(const void *src, void *dst, const unsigned long long *n_dev, int64_t cap, int words,
+                         cudaStream_t st)
+{
+    if (cap <= 0) return cudaSuccess;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cap * words + 255) / 256, (int64_t)sm_count() * 8));
+    SC_LAUNCH(k_copy_words, grid, 256, 0, st, static_cast<const uint32_t *>(src), static_cast<uint32_t *>(dst), n_dev,
+              cap, words);
+    return cudaGetLastError();
+}
 }  // namespace sc
 
 namespace {
@@ -255,8 +304,11 @@ int frame_tail(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts,
 {
     sc_frame_stats *stats = out->stats;
     const sc_frame_debug *dbg = out->debug;
+    // the survivor list shares region U with the block sort: copy it out now
+    if (out->survivors)
+        SC_TRY(sc::copy_counted(w.surv, out->survivors, &w.ctr->survivors, w.capS, 2, st), "copy survivors");
     SC_TRY(sc::launch_project(*scene, w.surv, &w.ctr->survivors, w.capS, *cam, *opts, w.splats, w.wins, nullptr,
-                              nullptr, w.key_a, w.pv_a, nullptr, nullptr, nullptr, stats, w.ctr, w.ecount, st),
+                              nullptr, w.key_a, w.pv_a, nullptr, nullptr, nullptr, stats, w.ctr, w.key_b, st),
            "project");
     SC_TRY(mark(2), "event");
     uint32_t *order = nullptr, *entries = nullptr;
@@ -269,12 +321,10 @@ int frame_tail(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts,
         if (dbg->block_offsets)
             SC_TRY(cudaMemcpyAsync(dbg->block_offsets, w.boff, 4 * (size_t)(8 * w.n_tiles + 1), cudaMemcpyDeviceToDevice,
                                    st), "copy block offsets");
-        if (dbg->block_entries && w.capE > 0)
-            SC_TRY(cudaMemcpyAsync(dbg->block_entries, entries, 4 * (size_t)w.capE, cudaMemcpyDeviceToDevice, st),
-                   "copy block entries");
-        if (dbg->block_codes && w.capE > 0)
-            SC_TRY(cudaMemcpyAsync(dbg->block_codes, bkeys, 4 * (size_t)w.capE, cudaMemcpyDeviceToDevice, st),
-                   "copy block codes");
+        if (dbg->block_entries)
+            SC_TRY(sc::copy_counted(entries, dbg->block_entries, &w.ctr->entries_eff, w.capE, 1, st), "copy block entries");
+        if (dbg->block_codes)
+            SC_TRY(sc::copy_counted(bkeys, dbg->block_codes, &w.ctr->entries_eff, w.capE, 1, st), "copy block codes");
     }
     if (opts->record_contributions && w.capS > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
@@ -283,10 +333,6 @@ int frame_tail(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts,
     SC_TRY(mark(4), "event");
     if (opts->record_contributions)
         SC_TRY(sc::launch_count_used(out->contrib_max, &w.ctr->survivors, w.capS, stats, st), "count used");
-    if (out->survivors && w.capS > 0)
-        SC_TRY(cudaMemcpyAsync(out->survivors, w.surv, sizeof(sc_survivor) * (size_t)w.capS, cudaMemcpyDeviceToDevice,
-                               st),
-               "copy survivors");
     return SC_OK;
 }
 
@@ -369,15 +415,14 @@ int sc_bin_sort(const sc_scene *scene, const sc_survivor *survivors, int64_t n, 
     SC_TRY(cudaMemsetAsync(w.ctr, 0, sizeof(sc::Counters), st), "memset counters");
     uint32_t *order = nullptr, *entries = nullptr;
     SC_TRY(sc::launch_project(*scene, survivors, nullptr, n, *cam, *opts, splats, wins, w.depth64, w.rect, nullptr,
-                              nullptr, nullptr, nullptr, nullptr, stats, w.ctr, w.ecount, st),
+                              nullptr, nullptr, nullptr, nullptr, stats, w.ctr, w.key_b, st),
            "project");
-    // reference tile binning (bin_tiles semantics) for parity with the oracle
+    // reference tile binning (bin_tiles semantics) for parity with the oracle; the order is
+    // extracted into order_idx inside (its buffer is reused by the entry sort)
     SC_TRY(sc::launch_bin(w, *scene, survivors, nullptr, n, *cam, wins, stats, false, &order, &entries, nullptr,
-                          nullptr, st),
+                          n > 0 ? order_idx : nullptr, st),
            "bin/sort");
-    if (order_idx && n > 0) SC_TRY(cudaMemcpyAsync(order_idx, order, 4 * (size_t)n, cudaMemcpyDeviceToDevice, st), "copy order");
-    if (entry_idx && w.capE > 0)
-        SC_TRY(cudaMemcpyAsync(entry_idx, entries, 4 * (size_t)w.capE, cudaMemcpyDeviceToDevice, st), "copy entries");
+    if (entry_idx) SC_TRY(sc::copy_counted(entries, entry_idx, &w.ctr->entries_eff, w.capE, 1, st), "copy entries");
     if (tile_offsets)
         SC_TRY(cudaMemcpyAsync(tile_offsets, w.tile_off, 4 * (size_t)(w.n_tiles_ref + 1), cudaMemcpyDeviceToDevice, st),
                "copy tile offsets");

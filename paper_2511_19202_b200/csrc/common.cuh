@@ -99,12 +99,12 @@ struct Ws {
     sc_survivor *surv;               // [capS]
     sc_splat *splats;                // [capS]
     sc_window *wins;                 // [capS]
-    uint32_t *key_a, *key_b;         // [capS]  depth keys (ping-pong)
+    uint32_t *key_a, *key_b;         // [max(capS, 4096)]  depth keys (ping-pong); key_b also the deferred /
+                                     // tie-run / emission-total lists
     uint2 *pv_a, *pv_b;              // [capS]  (survivor index, packed pixel window) riding the depth sort
     double *depth64;                 // [capS]  stage-level API only
-    ushort4 *rect;                   // [capS]  tx0, tx1, ty0, ty1
-    uint32_t *ecount;                // [capS]  tile count -> exclusive offsets
-    uint32_t *ekey_a, *ekey_b;       // [capE]
+    ushort4 *rect;                   // [capS]  tx0, tx1, ty0, ty1 (stage-level API only)
+    uint32_t *ekey_a, *ekey_b;       // [capE]   (aliases: see api.cu layout())
     uint32_t *eval_a, *eval_b;       // [capE]
     uint32_t *tile_off;              // [n_tiles_ref + 1] stage API: reference tile offsets
     uint32_t *task_order;            // [8 n_tiles] blend dispatch order over (tile, block) lists (longest first)

@@ -831,25 +831,26 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
                           blocks);
     if (e != cudaSuccess) return e;
     const unsigned long long *p_dev = &ws.ctr->passed;   // passed splats lead the sorted order
-    // ws.ecount is free until the entry counts: it holds the tie-run list
-    // the other payload buffer of the depth sort is free now: long tie runs sort f64 depths there
-    double *tie_scratch = reinterpret_cast<double *>(pv_s == ws.pv_a ? ws.pv_b : ws.pv_a);
-    e = launch_tiefix(scene, surv, cam, keys_s, pv_s, blocks ? nullptr : ws.depth64, p_dev, n_max, ws.ecount,
-                      tie_scratch, ws.ctr, stats, st);
+    // the depth sort's other key / payload buffers are free now: the tie-run list and the
+    // f64 depths of long tie runs go there
+    uint32_t *key_free = keys_s == ws.key_a ? ws.key_b : ws.key_a;
+    uint2 *pv_free = pv_s == ws.pv_a ? ws.pv_b : ws.pv_a;
+    e = launch_tiefix(scene, surv, cam, keys_s, pv_s, blocks ? nullptr : ws.depth64, p_dev, n_max, key_free,
+                      reinterpret_cast<double *>(pv_free), ws.ctr, stats, st);
     if (e != cudaSuccess) return e;
     if (dbg_order)   // debug copy-out of the (depth, index) order of the passed survivors
         SC_LAUNCH(k_extract_order, grid_for(n_max, 256), 256, 0, st, pv_s, p_dev, n_max, dbg_order);
     uint32_t *ek = nullptr, *ev = nullptr;
     if (blocks) {
-        // per-tile entry totals (ws.ecount, free after the tie-fix) -> tile offsets -> emission
+        // per-(tile, warp) entry totals (free key buffer) -> output bases -> emission
         const int64_t etiles = std::max<int64_t>(1, (n_max + kEmitTile - 1) / kEmitTile);
         const int egrid = (int)std::min<int64_t>(etiles, (int64_t)sm_count_sort() * 8);
+        uint32_t *wtot = key_free;   // etiles x 8 words <= max(capS, 4096)
         SC_LAUNCH(k_bentry_tiles, egrid, kEmitThreads, 0, st, pv_s, wins, p_dev, n_max, etiles, cam.width, cam.height,
-                  ws.ecount);
-        e = scan_excl(ws.ecount, ws.ecount, nullptr, etiles * (kEmitThreads / 32), ws.scan_part, &ws.ctr->entries,
-                      nullptr, st);
+                  wtot);
+        e = scan_excl(wtot, wtot, nullptr, etiles * (kEmitThreads / 32), ws.scan_part, &ws.ctr->entries, nullptr, st);
         if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_bentry_emit, egrid, kEmitThreads, 0, st, pv_s, wins, ws.ecount, p_dev, n_max, cam.width,
+        SC_LAUNCH(k_bentry_emit, egrid, kEmitThreads, 0, st, pv_s, wins, wtot, p_dev, n_max, cam.width,
                   cam.height, ws.n_tx, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
         const int64_t n_blocks = 8 * ws.n_tiles;
         // last pass (block-id high byte ~ screen rows, which follow depth order): few distinct
@@ -861,14 +862,16 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
                   n_blocks, ws.boff);
         if (order_out) *order_out = nullptr;
     } else {
-        // free after the tie-fix: both key buffers and the other payload buffer
-        uint32_t *order = reinterpret_cast<uint32_t *>(pv_s == ws.pv_a ? ws.pv_b : ws.pv_a);
+        // free after the tie-fix: both key buffers and the other payload buffer; after the
+        // order is extracted the sorted payload buffer holds the per-splat entry counts
+        uint32_t *order = reinterpret_cast<uint32_t *>(pv_free);
+        uint32_t *cnt = reinterpret_cast<uint32_t *>(pv_s);
         uint32_t *rlo = ws.key_a, *rhi = ws.key_b;
         SC_LAUNCH(k_extract_order, grid_for(n_max, 256), 256, 0, st, pv_s, p_dev, n_max, order);
-        SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, ws.ecount, rlo, rhi);
-        e = scan_excl(ws.ecount, ws.ecount, p_dev, n_max, ws.scan_part, &ws.ctr->entries, &stats->entries, st);
+        SC_LAUNCH(k_entry_count, grid_for(n_max, 256), 256, 0, st, order, ws.rect, p_dev, n_max, cnt, rlo, rhi);
+        e = scan_excl(cnt, cnt, p_dev, n_max, ws.scan_part, &ws.ctr->entries, &stats->entries, st);
         if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, ws.ecount, p_dev, n_max,
+        SC_LAUNCH(k_entry_emit, grid_for(n_max, 256), 256, 0, st, order, rlo, rhi, cnt, p_dev, n_max,
                   ws.n_tx_ref, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
         e = radix_sort<uint32_t>(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, 0,
                                  std::max(1, bits_for(ws.n_tiles_ref)), ws, &ek, &ev, st);

@@ -384,6 +384,9 @@ class DeviceScene:
         s.vis_weights, s.n_models = nat.ptr(self.weights_t), len(models)
         s.n_pairs = self.max_pairs
         s.appear = nat.ptr(self.appear)
+        self.nbytes = sum(int(t.numel() * t.element_size()) for t in
+                          (self.mean_opa, self.quat, self.scale_smax, self.sh, self.features, self.appear,
+                           self.assets_t, self.instances_t, self.weights_t))
         # packed form for torch.ops.splatcull (ops.py)
         self.op_scene = [self.mean_opa, self.quat, self.scale_smax, self.sh, self.features, self.appear,
                          self.assets_t, self.instances_t, self.weights_t]
@@ -430,8 +433,10 @@ class Workspace:
         w.cap_survivors, w.cap_entries = self.cap_s, self.cap_e
 
     def grow(self, need_s: int, need_e: int) -> None:
-        self.cap_s = max(self.cap_s, int(need_s * 1.15) + 1024)
-        self.cap_e = max(self.cap_e, int(need_e * 1.15) + 4096)
+        # 5 % headroom: a camera path's next frames rarely need more, and an overflow only
+        # costs one re-render of that frame
+        self.cap_s = max(self.cap_s, int(need_s * 1.05) + 4096)
+        self.cap_e = max(self.cap_e, int(need_e * 1.05) + 16384)
         self.buf = None
         self._alloc()
 

@@ -232,8 +232,8 @@ def instantiate(tables: SceneTables, cam, surv_inst, surv_gid):
     sh = np.zeros((len(means), k, 3), np.float32)
     for i, a in enumerate(tables.assets):
         sh[tables.offsets[i]:tables.offsets[i + 1], :a.sh_coeffs.shape[1]] = a.sh_coeffs
-    gid_global = (np.asarray(surv_gid, np.int64) +
-                  tables.offsets[np.asarray([tables.flat[i][0] for i in surv_inst], dtype=np.int64)]
+    inst_asset = np.asarray([a for a, _ in tables.flat], dtype=np.int64)
+    gid_global = (np.asarray(surv_gid, np.int64) + tables.offsets[inst_asset[np.asarray(surv_inst, np.int64)]]
                   if n else np.zeros(0, np.int64))
     si = np.ascontiguousarray(surv_inst, dtype=np.int64)
     sg = np.ascontiguousarray(gid_global, dtype=np.int64)

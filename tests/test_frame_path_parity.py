@@ -289,3 +289,45 @@ def test_frame_path_record_and_image_match_oracle():
     _image_close(out.image, ref.image)
     np.testing.assert_allclose(out.contribution_max, ref.contribution_max, atol=5e-3)
     assert st.passed == ref.passed_count
+
+
+_CFG2 = {}
+
+
+def _cfg2():
+    if "wl" not in _CFG2:
+        from paper_2511_19202_b200.workloads import config2
+
+        _CFG2["wl"] = config2()
+    return _CFG2["wl"]
+
+
+@pytest.mark.parametrize("frame", [0, 24, 48, 72, 96])
+def test_config2_full_size(frame):
+    """BASELINE config 2 at full size (100K shell x 16 instances, 1080p, orbit frames;
+    SURVEY §4 / §8d): with the oracle's survivors injected, order and (tile, block)
+    lists are bit-exact (i)-(iv) and the image is within the blend tolerance of the
+    oracle rendering the same survivors; the whole pipeline (GPU cull + MLP) is
+    >= 45 dB against the oracle's whole pipeline."""
+    import torch
+
+    import paper_2511_19202_b200 as pkg
+    from paper_2511_19202_b200.scene import RenderOptions, Renderer
+    from test_gpu_parity import _image_close
+
+    wl = _cfg2()
+    cam = wl.cameras[frame]
+    tabs = sr.SceneTables(wl.scene)
+    c = sr.cull(tabs, cam)
+    assert c.surv_inst.size > 100_000
+    ref, _st = check_frame_path(wl.scene, cam, c.surv_inst, c.surv_gid)
+    r = Renderer(wl.scene)
+    surv = torch.from_numpy(np.stack([c.surv_inst, c.surv_gid], 1).astype(np.int32)).to(r.dscene.device)
+    out, _fst = r.render(cam, RenderOptions(), survivors=surv)
+    _image_close(out.image, ref.image)
+    whole, st = pkg.render_composed(wl.scene, cam)
+    assert st.frustum_passed == int(np.count_nonzero(c.flags & 1))
+    # MLP decisions may differ only within the fp16 logit margin of the threshold
+    assert abs(st.instantiated - c.surv_inst.size) <= max(3, int(1e-4 * c.surv_inst.size))
+    assert rr.psnr(whole.image, ref.image, cap=None) >= 45.0
+    assert rr.ssim(whole.image, ref.image) >= 0.995

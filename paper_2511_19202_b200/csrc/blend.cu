@@ -32,6 +32,7 @@
 // (-> hit compaction: in the heaviest tiles ~80 % of entries miss every alive
 // pixel because a few pixels never saturate).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -151,6 +152,139 @@ struct WalkStats { unsigned long long slots, hits, evals, iters; };
 #define SC_WS_ARG
 #endif
 
+// Entry-parallel compositing of one pixel pl over a record stage (grp: lane j's
+// entry at grp[2 j]; cov bit j: entry j covers pl; T_in: pl's transmittance before
+// the stage).  Lane j evaluates entry j's alpha at the pixel (alphas do not depend
+// on T), an in-order warp prefix product of (1 - alpha) gives T before every
+// entry, the reference's retirement cut (first T < stop after a composite) is a
+// ballot and the colour a warp sum.  Same terms as the serial walk, products in
+// tree order (fp32 rounding only).  Warp-uniform results: colour sums and T_out.
+__device__ __forceinline__ void pixel_entry_parallel(const WalkCtx &c, const float4 *grp, uint32_t cov, float T_in,
+                                                     float qx, float qy, uint32_t sidx, float &sr, float &sg,
+                                                     float &sb, float &sc, float &T_out)
+{
+    const int lane = c.lane;
+    float alpha = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+    if ((cov >> lane) & 1u) {
+        const float4 *r = grp + lane * 2;
+        const float4 g = r[0];
+        const float4 p = r[1];
+        const float dx = qx - g.x, dy = qy - g.y;
+        const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
+        if (!(power > 0.0f || power < p.y)) {
+            alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
+            const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
+            const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
+            cr = __low2float(rg);
+            cg = __high2float(rg);
+            cb = __low2float(bx);
+        }
+    }
+    // inclusive prefix product of (1 - alpha) over lanes 0..j
+    float incl = 1.0f - alpha;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl *= y;
+    }
+    float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = 1.0f;
+    const float t_before = T_in * excl, t_after = T_in * incl;
+    // composited: a valid entry reached before the pixel retired
+    const bool comp = alpha > 0.0f && t_before >= c.stop_t;
+    const float contrib = comp ? alpha * t_before : 0.0f;
+    if (c.record && contrib > 0.0f) atomicMax(reinterpret_cast<int *>(c.cmax) + sidx, __float_as_int(contrib));
+    sr = contrib * cr;
+    sg = contrib * cg;
+    sb = contrib * cb;
+    sc = contrib;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, o);
+        sg += __shfl_xor_sync(0xffffffffu, sg, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    }
+    const uint32_t compm = __ballot_sync(0xffffffffu, comp);
+    T_out = compm ? __shfl_sync(0xffffffffu, t_after, 31 - __clz(compm)) : T_in;
+}
+
+// Blend one record stage onto the lanes' pixels: lane j holds entry j's splat
+// index sidx and footprint fp (already masked by the alive pixels), its record at
+// grp[2 j].  The warp transposes the 32 footprints so each lane walks only the
+// entries covering its own pixel (max-over-lanes iterations); pixels covered by
+// >= kHeavyHits of the stage's entries (when at most kMaxHeavyPixels) go
+// entry-parallel instead -- the serial per-pixel chain (~150-200 cycles per
+// composite) was the tail of the heaviest lists.
+__device__ __forceinline__ void blend_stage(const WalkCtx &c, const float4 *grp, uint32_t sidx_lane, uint32_t fp,
+                                            PixAcc &a SC_WS_PARAM)
+{
+    const int lane = c.lane;
+    const uint32_t covers = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
+    uint32_t heavy = __ballot_sync(0xffffffffu, __popc(covers) >= kHeavyHits);
+    // when many pixels are heavy the lane-per-pixel loop is already busy on every lane
+    if (__popc(heavy) > kMaxHeavyPixels) heavy = 0u;
+    uint32_t mine = ((heavy >> lane) & 1u) ? 0u : covers;
+    while (__any_sync(0xffffffffu, mine != 0u)) {
+        const bool act = mine != 0u;
+        const int j = act ? __ffs(mine) - 1 : lane;
+        mine &= mine - 1u;
+        const uint32_t sidx = c.record ? __shfl_sync(0xffffffffu, sidx_lane, j) : 0u;
+#ifdef SC_BLEND_STATS
+        d.evals += act;
+        d.iters += (lane == 0);
+#endif
+        if (act) {
+            const float4 *r = grp + j * 2;
+            const float4 g = r[0];   // mx, my, 0.5 a, b
+            const float4 p = r[1];   // 0.5 c, p_min, rgb (fp16 x3)
+            const float dx = c.fpx - g.x, dy = c.fpy - g.y;
+            const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
+            if (!(power > 0.0f || power < p.y)) {
+                // opacity * e^power == e^(power - p_min) / 255
+                const float alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
+                const float contrib = alpha * a.T;
+                const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
+                const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
+                a.cr += contrib * __low2float(rg);
+                a.cg += contrib * __high2float(rg);
+                a.cb += contrib * __low2float(bx);
+                a.T = a.T * (1.0f - alpha);
+                if (c.record) {
+                    a.cs += contrib;
+                    if (contrib > 0.0f) atomicMax(reinterpret_cast<int *>(c.cmax) + sidx, __float_as_int(contrib));
+                }
+                if (a.T < c.stop_t) {
+                    a.done = true;
+                    mine = 0u;
+                }
+            }
+        }
+    }
+    uint32_t hv = heavy;
+    while (hv) {
+        const int pl = __ffs(hv) - 1;
+        hv &= hv - 1u;
+        const uint32_t cov = __shfl_sync(0xffffffffu, covers, pl);
+        const float T_in = __shfl_sync(0xffffffffu, a.T, pl);
+        const float qx = __shfl_sync(0xffffffffu, c.fpx, pl), qy = __shfl_sync(0xffffffffu, c.fpy, pl);
+        float sr, sg, sb, sc, T_out;
+        pixel_entry_parallel(c, grp, cov, T_in, qx, qy, sidx_lane, sr, sg, sb, sc, T_out);
+        if (lane == pl) {
+            a.cr += sr;
+            a.cg += sg;
+            a.cb += sb;
+            a.cs += sc;
+            a.T = T_out;
+            if (T_out < c.stop_t) a.done = true;
+        }
+#ifdef SC_BLEND_STATS
+        d.evals += __popc(cov) * (lane == pl);
+        d.iters += (lane == 0);
+#endif
+    }
+}
+
 // Front-to-back compositing of entries [start, end) of the warp's stream onto
 // the lanes that are not done (reference semantics, sc/_kernels.py:190-275).
 __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint32_t end, PixAcc &a SC_WS_PARAM)
@@ -253,118 +387,7 @@ __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint
         d.slots++;
         d.hits += __popc(__ballot_sync(0xffffffffu, fp != 0u)) * (lane == 0);
 #endif
-        if (__any_sync(0xffffffffu, fp != 0u)) {
-            const float4 *grp = c.recs + slot * kG * 2;
-            const uint32_t covers = transpose32(fp, lane);   // bit j: entry of lane j covers my pixel
-            // pixels covered by many of this stage's entries are composited entry-parallel below
-            uint32_t heavy = __ballot_sync(0xffffffffu, __popc(covers) >= kHeavyHits);
-            // when many pixels are heavy the lane-per-pixel loop is already busy on every lane
-            if (__popc(heavy) > kMaxHeavyPixels) heavy = 0u;
-            uint32_t mine = ((heavy >> lane) & 1u) ? 0u : covers;
-            while (__any_sync(0xffffffffu, mine != 0u)) {
-                const bool act = mine != 0u;
-                const int j = act ? __ffs(mine) - 1 : lane;
-                mine &= mine - 1u;
-                const uint32_t sidx = c.record ? __shfl_sync(0xffffffffu, m.x, j) : 0u;
-#ifdef SC_BLEND_STATS
-                d.evals += act;
-                d.iters += (lane == 0);
-#endif
-                if (act) {
-                    const float4 *r = grp + j * 2;
-                    const float4 g = r[0];   // mx, my, 0.5 a, b
-                    const float4 p = r[1];   // 0.5 c, p_min, rgb (fp16 x3)
-                    const float dx = c.fpx - g.x, dy = c.fpy - g.y;
-                    const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
-                    if (!(power > 0.0f || power < p.y)) {
-                        // opacity * e^power == e^(power - p_min) / 255
-                        const float alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
-                        const float contrib = alpha * a.T;
-                        const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
-                        const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
-                        a.cr += contrib * __low2float(rg);
-                        a.cg += contrib * __high2float(rg);
-                        a.cb += contrib * __low2float(bx);
-                        a.T = a.T * (1.0f - alpha);
-                        if (c.record) {
-                            a.cs += contrib;
-                            if (contrib > 0.0f)
-                                atomicMax(reinterpret_cast<int *>(c.cmax) + sidx, __float_as_int(contrib));
-                        }
-                        if (a.T < c.stop_t) {
-                            a.done = true;
-                            mine = 0u;
-                        }
-                    }
-                }
-            }
-            // Entry-parallel compositing of one heavy pixel at a time: lane j evaluates
-            // entry j's alpha at the pixel (alphas do not depend on T), an in-order warp
-            // prefix product of (1 - alpha) gives T before every entry, the reference's
-            // retirement cut (first T < stop after a composite) is a ballot, and the
-            // colour a warp sum.  Same terms as the serial walk, products in tree order
-            // (fp32 rounding only).
-            uint32_t hv = heavy;
-            while (hv) {
-                const int pl = __ffs(hv) - 1;
-                hv &= hv - 1u;
-                const uint32_t cov = __shfl_sync(0xffffffffu, covers, pl);
-                const float T_in = __shfl_sync(0xffffffffu, a.T, pl);
-                const float qx = __shfl_sync(0xffffffffu, c.fpx, pl), qy = __shfl_sync(0xffffffffu, c.fpy, pl);
-                float alpha = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-                if ((cov >> lane) & 1u) {
-                    const float4 *r = grp + lane * 2;
-                    const float4 g = r[0];
-                    const float4 p = r[1];
-                    const float dx = qx - g.x, dy = qy - g.y;
-                    const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
-                    if (!(power > 0.0f || power < p.y)) {
-                        alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
-                        const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
-                        const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
-                        cr = __low2float(rg);
-                        cg = __high2float(rg);
-                        cb = __low2float(bx);
-                    }
-                }
-                // inclusive prefix product of (1 - alpha) over lanes 0..j
-                float incl = 1.0f - alpha;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const float y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl *= y;
-                }
-                float excl = __shfl_up_sync(0xffffffffu, incl, 1);
-                if (lane == 0) excl = 1.0f;
-                const float t_before = T_in * excl, t_after = T_in * incl;
-                // composited: a valid entry reached before the pixel retired
-                const bool comp = alpha > 0.0f && t_before >= c.stop_t;
-                const float contrib = comp ? alpha * t_before : 0.0f;
-                if (c.record && contrib > 0.0f) atomicMax(reinterpret_cast<int *>(c.cmax) + m.x, __float_as_int(contrib));
-                float sr = contrib * cr, sg = contrib * cg, sb = contrib * cb, sc = contrib;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    sr += __shfl_xor_sync(0xffffffffu, sr, o);
-                    sg += __shfl_xor_sync(0xffffffffu, sg, o);
-                    sb += __shfl_xor_sync(0xffffffffu, sb, o);
-                    sc += __shfl_xor_sync(0xffffffffu, sc, o);
-                }
-                const uint32_t compm = __ballot_sync(0xffffffffu, comp);
-                const float T_out = compm ? __shfl_sync(0xffffffffu, t_after, 31 - __clz(compm)) : T_in;
-                if (lane == pl) {
-                    a.cr += sr;
-                    a.cg += sg;
-                    a.cb += sb;
-                    a.cs += sc;
-                    a.T = T_out;
-                    if (T_out < c.stop_t) a.done = true;
-                }
-#ifdef SC_BLEND_STATS
-                d.evals += __popc(cov) * (lane == pl);
-                d.iters += (lane == 0);
-#endif
-            }
-        }
+        if (__any_sync(0xffffffffu, fp != 0u)) blend_stage(c, c.recs + slot * kG * 2, m.x, fp, a SC_WS_ARG);
         __syncwarp();   // the slot is refilled by a later stage
         blended++;
     }
@@ -452,6 +475,187 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     }
 }
 
+// ---- long lists: one CTA per (tile, block) list (frame path) ----
+//
+// A few very long lists set the blend's tail (config-3 far view: 8.9K non-empty
+// lists of mean 20K entries, the longest 137K; near view: one warp walking a
+// 141K-entry list was the whole kernel's duration).  Lists of at least
+// 2^SC_COOP_LOG2 entries are therefore walked by a whole CTA, exactly.
+#ifndef SC_COOP_LOG2
+#define SC_COOP_LOG2 12
+#endif
+constexpr int kCoopQ = 2048;                     // CTA hit queue (ring; >= 2 chunks + one stream step)
+constexpr int kCoopChunk = kBlendWarps * kG;     // 256 hits per chunk, 32 per warp
+constexpr int kCoopStep = kBlendWarps * kStep;   // 1024 meta entries per CTA stream step
+struct CoopSmem {
+    uint2 q[kCoopQ];                        // (splat index, footprint) of queued hits, list order
+    uint2 stage[kBlendWarps][2][kG];        // per warp: the hits of its segment of the current / next chunk
+    float4 recs[kBlendWarps][2][kG * 2];    // ... and their 32-byte splat records
+    float4 seg[kBlendWarps][32];            // per segment, per pixel: (P, r, g, b) composited from T = 1
+    float4 fin[32];                         // (T, r, g, b) of pixels retired by a segment re-composite
+    uint32_t cnt[2][kBlendWarps];           // stream step: hits per warp (double-buffered by step parity)
+    uint32_t ticket[2];
+};
+static_assert(sizeof(CoopSmem) <= kBlendWarps * kWarpSmem, "the CTA layout reuses the per-warp queues' bytes");
+static_assert(kCoopQ >= 2 * kCoopChunk + kCoopStep, "queue holds two chunks plus one stream step");
+
+// One list walked by the whole CTA.  The meta streams 1024 entries per step (128
+// per warp) and hits (entries touching a still-alive pixel) are compacted in
+// order into the CTA queue.  Each chunk of 256 queued hits is cut into 8
+// consecutive segments of 32, one per warp; a warp composites its segment onto
+// the alive pixels from T = 1 (blend_stage), giving per pixel the segment's
+// transmittance product P_w and colour C_w.  After a barrier every warp combines
+// the 8 segments in order (C += T C_w, T *= P_w) as long as T P_w >= stop: T is
+// non-increasing along the list, so no pixel retired inside such a segment.  A
+// pixel whose T would fall below stop inside segment w retires there: warp w
+// re-composites that segment for it from its true T (pixel_entry_parallel: the
+// reference's exact cut).  Alive shrinks chunk by chunk as in the serial walk, so
+// entries behind retired pixels still never reach the queue.  Every CTA-level
+// decision derives from state all warps hold identically (alive, counters).
+// Accumulation order differs from the serial walk (fp32 rounding only).
+__device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start, uint32_t end, PixAcc &a,
+                          bool &retired_here SC_WS_PARAM)
+{
+    const int lane = c.lane;
+    const uint32_t lt = lanemask_lt();
+    uint32_t va[4], ka[4], vb[4], kb[4];
+    auto load_step = [&](uint32_t base, uint32_t *v, uint32_t *k) {   // this warp's 128 entries of a step
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t e = base + (uint32_t)(kStep * wid + 32 * j + lane);
+            v[j] = kNoEntry;
+            k[j] = kEmptyCode;
+            if (e < end) {
+                v[j] = __ldg(c.vals + e);
+                k[j] = __ldg(c.keys + e);
+            }
+        }
+    };
+    uint32_t mbase = start;
+    load_step(mbase, va, ka);
+    if (mbase + kCoopStep < end) load_step(mbase + kCoopStep, vb, kb);
+    bool meta_done = false;
+    uint32_t qi = 0, qtail = 0;            // queue: next hit to issue, tail
+    uint32_t issued = 0, blended = 0, step = 0;
+    for (;;) {
+        const uint32_t alive = __ballot_sync(0xffffffffu, !a.done);
+        if (!alive) break;
+        // 1. stream meta until two chunks are queued (or the list ends)
+        while (!meta_done && qtail - qi < 2u * kCoopChunk) {
+            uint32_t fp[4], bal[4], nw = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                fp[j] = (int64_t)va[j] < c.n_splats ? code_mask(ka[j] & 0x3FFu) & alive : 0u;
+                bal[j] = __ballot_sync(0xffffffffu, fp[j] != 0u);
+                nw += __popc(bal[j]);
+            }
+            if (lane == 0) s.cnt[step & 1][wid] = nw;
+            __syncthreads();
+            const uint32_t cw = lane < kBlendWarps ? s.cnt[step & 1][lane] : 0u;
+            uint32_t off = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kBlendWarps; w++) {
+                const uint32_t x = __shfl_sync(0xffffffffu, cw, w);
+                off += w < wid ? x : 0u;
+                tot += x;
+            }
+            uint32_t pos = qtail + off;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                if (fp[j]) s.q[(pos + __popc(bal[j] & lt)) & (kCoopQ - 1)] = make_uint2(va[j], fp[j]);
+                pos += __popc(bal[j]);
+            }
+            qtail += tot;
+            step++;
+            mbase += kCoopStep;
+            if (mbase >= end) {
+                meta_done = true;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    va[j] = vb[j];
+                    ka[j] = kb[j];
+                }
+                if (mbase + kCoopStep < end) load_step(mbase + kCoopStep, vb, kb);
+            }
+        }
+        __syncthreads();   // queued hits visible to every warp; the last chunk's seg / fin consumed
+        // 2. record stages of the next chunks (one chunk in flight while one is blended)
+        while (issued - blended < 2u) {
+            const uint32_t avail = qtail - qi;
+            if (avail == 0u || (!meta_done && avail < (uint32_t)kCoopChunk)) break;
+            const uint32_t n = avail < (uint32_t)kCoopChunk ? avail : (uint32_t)kCoopChunk;
+            const int slot = (int)(issued & 1u);
+            const uint32_t k = 32u * (uint32_t)wid + (uint32_t)lane;
+            uint2 h = make_uint2(kNoEntry, 0u);
+            if (k < n) {
+                h = s.q[(qi + k) & (kCoopQ - 1)];
+                h.y &= alive;
+            }
+            s.stage[wid][slot][lane] = h;
+            if (h.y) {
+                const float4 *src = reinterpret_cast<const float4 *>(c.splats + h.x);
+                float4 *dst = &s.recs[wid][slot][2 * lane];
+                cp_async16(dst, src);
+                cp_async16(dst + 1, src + 1);
+            }
+            cp_async_commit();
+            qi += n;
+            issued++;
+        }
+        if (issued == blended) break;   // the list is exhausted
+        // 3. this warp's segment of the oldest chunk, composited from T = 1
+        cp_async_wait_dyn(issued - blended - 1);
+        __syncwarp();
+        const int slot = (int)(blended & 1u);
+        const uint2 m = s.stage[wid][slot][lane];
+        const uint32_t fp = m.y & alive;
+        PixAcc loc{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, a.done};
+        if (__any_sync(0xffffffffu, fp != 0u)) blend_stage(c, s.recs[wid][slot], m.x, fp, loc SC_WS_ARG);
+        s.seg[wid][lane] = make_float4(loc.T, loc.cr, loc.cg, loc.cb);
+        __syncthreads();
+        // 4. combine the segments in list order (every warp, identical results)
+        int rw = -1;
+        float tin = 0.0f;
+        if (!a.done) {
+#pragma unroll
+            for (int w = 0; w < kBlendWarps; w++) {
+                const float4 g = s.seg[w][lane];
+                const float tn = a.T * g.x;
+                if (tn < c.stop_t) {
+                    rw = w;
+                    tin = a.T;
+                    break;
+                }
+                a.cr += a.T * g.y;
+                a.cg += a.T * g.z;
+                a.cb += a.T * g.w;
+                a.T = tn;
+            }
+        }
+        // 5. pixels retiring inside this warp's segment: exact re-composite from their true T
+        uint32_t mine = __ballot_sync(0xffffffffu, rw == wid);
+        while (mine) {
+            const int pl = __ffs(mine) - 1;
+            mine &= mine - 1u;
+            const uint32_t cov = __ballot_sync(0xffffffffu, (fp >> pl) & 1u);
+            const float T_in = __shfl_sync(0xffffffffu, tin, pl);
+            const float qx = __shfl_sync(0xffffffffu, c.fpx, pl), qy = __shfl_sync(0xffffffffu, c.fpy, pl);
+            float sr, sg, sb, sc, T_out;
+            pixel_entry_parallel(c, s.recs[wid][slot], cov, T_in, qx, qy, m.x, sr, sg, sb, sc, T_out);
+            if (lane == pl) s.fin[pl] = make_float4(T_out, a.cr + sr, a.cg + sg, a.cb + sb);
+        }
+        if (rw >= 0) {
+            a.done = true;
+            retired_here = true;
+        }
+        __syncwarp();   // the slot is refilled by a later chunk
+        blended++;
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
 // Frame path, persistent: every warp repeatedly takes the next (16x16 tile, 8x4
 // block) list from an atomic ticket over the LPT order (longest lists first) and
 // walks it.  No CTA barrier and no CTA-wide lifetime: a warp whose list is short
@@ -485,9 +689,50 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
 #ifdef SC_BLEND_STATS
     WalkStats d{0, 0, 0, 0};
 #endif
+    // phase 1: the long lists at the head of the LPT order, one CTA each
+    const int64_t n_coop = (int64_t)*reinterpret_cast<volatile unsigned long long *>(ticket + 2);
+    if (n_coop > 0) {
+        CoopSmem &s = *reinterpret_cast<CoopSmem *>(s_dyn);
+        for (int it = 0;; it++) {
+            if (threadIdx.x == 0) s.ticket[it & 1] = (uint32_t)atomicAdd(ticket + 1, 1ull);
+            __syncthreads();
+            const int64_t t = s.ticket[it & 1];
+            if (t >= n_coop) break;
+            const uint32_t blk = __ldg(task_order + t);
+            const int tile = (int)(blk >> 3), b = (int)(blk & 7u);
+            const int tyi = tile / n_tx, txi = tile - tyi * n_tx;
+            c.gx0 = txi * kTile + (b & 1) * 8;
+            c.gy0 = tyi * kTile + (b >> 1) * 4;
+            c.bx1 = c.gx0 + 7;
+            c.by1 = c.gy0 + 3;
+            const int px = c.gx0 + (lane & 7), py = c.gy0 + (lane >> 3);
+            const bool inside = px < width && py < height;
+            c.fpx = (float)px;
+            c.fpy = (float)py;
+            PixAcc a{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, !inside};
+            bool retired_here = false;
+            coop_list(c, s, wid, __ldg(boff + blk), __ldg(boff + blk + 1), a, retired_here SC_WS_ARG);
+            __syncthreads();   // s.fin complete
+            if (wid == 0 && inside) {
+                if (retired_here) {
+                    const float4 f = s.fin[lane];
+                    a.T = f.x;
+                    a.cr = f.y;
+                    a.cg = f.z;
+                    a.cb = f.w;
+                }
+                const int64_t p = (int64_t)py * width + px;
+                image[3 * p + 0] = a.cr + a.T * bg_r;
+                image[3 * p + 1] = a.cg + a.T * bg_g;
+                image[3 * p + 2] = a.cb + a.T * bg_b;
+                trans[p] = a.T;
+            }
+        }
+    }
+    // phase 2: the remaining lists, one warp each
     for (;;) {
         unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(ticket, 1ull);
+        if (lane == 0) t = (unsigned long long)n_coop + atomicAdd(ticket, 1ull);
         t = __shfl_sync(0xffffffffu, t, 0);
         if ((int64_t)t >= n_tasks) break;
         const uint32_t blk = __ldg(task_order + t);   // block id = 8 tile + b
@@ -525,7 +770,8 @@ __device__ __forceinline__ uint32_t tile_weight(const uint32_t *off, int64_t t, 
 }
 
 __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_t tile_base, int64_t n_tiles,
-                                                     int stride, uint32_t *order)
+                                                     int stride, uint32_t *order, unsigned long long *n_long,
+                                                     int long_log2)
 {
     __shared__ uint32_t hist[33], base[33];
     constexpr int kPer = 16;   // tiles per thread kept in registers (one weight pass)
@@ -554,6 +800,8 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_
             base[b] = run;
             run += hist[b];
         }
+        // lists of >= 2^long_log2 entries (buckets > long_log2) lead the order
+        if (n_long) *n_long = long_log2 >= 0 && long_log2 < 32 ? base[long_log2] : 0;
     }
     __syncthreads();
     for (int64_t t0 = 0; t0 < n_tiles; t0 += (int64_t)blockDim.x * kPer) {
@@ -591,6 +839,15 @@ __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev,
     if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)&stats->used, c);
 }
 
+// Threshold (log2 entries) of the lists walked by a whole CTA; the environment
+// variable SPLATCULL_B200_LONG_LIST_LOG2 overrides it (tests force the CTA walk on
+// small scenes with it; a value >= 32 disables it).
+static int long_list_log2()
+{
+    const char *e = getenv("SPLATCULL_B200_LONG_LIST_LOG2");
+    return e && *e ? atoi(e) : SC_COOP_LOG2;
+}
+
 cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
@@ -625,7 +882,9 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
             if (dev >= 0 && dev < 64) cps_cache[dev] = cps;
         }
         const int64_t n_tasks = 8 * n_tiles;
-        SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, 8 * tile_base, n_tasks, 1, task_order);
+        // ticket[0]: next short list (per warp), [1]: next long list (per CTA), [2]: number of long lists
+        SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, 8 * tile_base, n_tasks, 1, task_order,
+                  lists.ticket + 2, opts.record_contributions ? -1 : long_list_log2());
         const int grid = (int)std::min<int64_t>((n_tasks + kBlendWarps - 1) / kBlendWarps, (int64_t)sm_count() * cps);
         SC_LAUNCH(k_blend_blocks, grid, kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
                   lists.keys, task_order, n_tasks, lists.ticket, cam.width, cam.height, n_tx,
@@ -636,7 +895,8 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
     }
     if (n_tiles * ngroups > 0x7FFFFFFFll) return cudaErrorInvalidValue;
     if (task_order)
-        SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, tile_base, n_tiles, lists.blocks ? 8 : 1, task_order);
+        SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, tile_base, n_tiles, lists.blocks ? 8 : 1, task_order,
+                  (unsigned long long *)nullptr, -1);
     SC_LAUNCH(k_blend, (int)(n_tiles * ngroups), kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
               lists.keys, lists.wins, lists.blocks ? 1 : 0, task_order, (int)tile_base, cam.width, cam.height, n_tx,
               ts, nbx, nblk, ngroups,

@@ -14,6 +14,19 @@ if len(sys.argv) > 1 and sys.argv[1] != "--child":
         env = dict(os.environ, SPLATCULL_B200_VARIANT=lib)
         r = subprocess.run([sys.executable, __file__, "--child"], env=env, capture_output=True, text=True)
         print(os.path.basename(lib), r.stdout.strip() or r.stderr[-2000:], flush=True)
+    # images of every variant against the first one's (same survivors and lists: blend differences only)
+    import numpy as np
+    first = sys.argv[1]
+    for lib in sys.argv[2:]:
+        d = []
+        for vi in range(3):
+            try:
+                a, b = np.load(first + f".v{vi}.npy"), np.load(lib + f".v{vi}.npy")
+            except OSError:
+                continue
+            mse = float(np.mean((a.astype(np.float64) - b) ** 2))
+            d.append((float(np.abs(a - b).max()), 10 * np.log10(1.0 / mse) if mse > 0 else float("inf")))
+        print("images", os.path.basename(lib), "vs", os.path.basename(first), "(max-abs, PSNR dB) per view:", d)
     sys.exit(0)
 
 sys.path.insert(0, ROOT)
@@ -41,6 +54,7 @@ for vi, cam in enumerate(wl.cameras):
         torch.cuda.synchronize()
         per.append([ev[j].elapsed_time(ev[j + 1]) for j in range(nat.N_STAGE_EVENTS - 1)])
     per = np.median(np.array(per), axis=0)
+    np.save(os.environ["SPLATCULL_B200_VARIANT"] + f".v{vi}.npy", frame.image.cpu().numpy())
     res[("near", "mid", "far")[vi]] = [round(float(x), 3) for x in per] + [round(float(per.sum()), 3)]
 tot = np.mean([v[-1] for v in res.values()])
 print(json.dumps({"views(cull,proj,sort,blend,total)": res, "mean_ms": round(float(tot), 3),

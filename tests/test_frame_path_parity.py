@@ -331,3 +331,52 @@ def test_config2_full_size(frame):
     assert abs(st.instantiated - c.surv_inst.size) <= max(3, int(1e-4 * c.surv_inst.size))
     assert rr.psnr(whole.image, ref.image, cap=None) >= 45.0
     assert rr.ssim(whole.image, ref.image) >= 0.995
+
+
+@pytest.mark.parametrize("log2", [0, 5, 9])
+@pytest.mark.parametrize("view", [0, 2], ids=["near", "far"])
+def test_long_lists_cta_walk(monkeypatch, log2, view):
+    """Lists of >= 2^log2 entries are walked by a whole CTA (segments composited
+    from T = 1, combined in order, the retiring segment re-composited exactly;
+    blend.cu coop_list).  Forced onto every list of a small config-3 view with
+    SPLATCULL_B200_LONG_LIST_LOG2: the image equals the per-warp serial walk within
+    fp32 reassociation, and the oracle (sc/_kernels.py:190-275 on the same
+    survivors) within the blend tolerance; bands stay bit-identical to the whole
+    frame; record mode keeps the serial walk (its contributions need the true T)."""
+    import torch
+
+    from test_gpu_parity import _image_close
+
+    from paper_2511_19202_b200 import sharding
+    from paper_2511_19202_b200.scene import RenderOptions, Renderer
+    from paper_2511_19202_b200.workloads import config3
+
+    wl = config3(n_per=6_000, n_instances=150, width=480, height=270)
+    cam = wl.cameras[view]
+    r = Renderer(wl.scene)
+    monkeypatch.setenv("SPLATCULL_B200_LONG_LIST_LOG2", "40")
+    serial, sst = r.render(cam, return_survivors=True)
+    monkeypatch.setenv("SPLATCULL_B200_LONG_LIST_LOG2", str(log2))
+    coop, cst = r.render(cam, return_survivors=True)
+    assert cst.block_entries == sst.block_entries and cst.passed == sst.passed
+    d = np.abs(coop.image.astype(np.float64) - serial.image)
+    assert d.max() <= 2e-4, d.max()
+    assert np.abs(coop.final_transmittance.astype(np.float64) - serial.final_transmittance).max() <= 2e-4
+    s = coop.survivors
+    m, ls, q, op, sh, deg = sr.instantiate(sr.SceneTables(wl.scene), cam, s[:, 0], s[:, 1])
+    ref = rr.render_arrays(m, ls, q, op, sh, deg, cam)
+    _image_close(coop.image, ref.image)
+    # bands: the same lists, so the same walk decisions
+    full, _ = r.render(cam, RenderOptions(), to_host=False)
+    img = full.image.clone()
+    bounds = sharding.split_rows(sharding.tile_rows(cam.height), 3)
+    for b in range(len(bounds) - 1):
+        y0, y1 = sharding.band_pixels(bounds, b, cam.height)
+        band, _ = r.render(cam, RenderOptions(band=(y0, y1)), to_host=False)
+        assert torch.equal(band.image[y0:y1], img[y0:y1]), b
+    # record mode: serial walk whatever the threshold
+    rec, _ = r.render(cam, RenderOptions(record_contributions=True))
+    monkeypatch.setenv("SPLATCULL_B200_LONG_LIST_LOG2", "40")
+    rec40, _ = r.render(cam, RenderOptions(record_contributions=True))
+    np.testing.assert_array_equal(rec.image, rec40.image)
+    np.testing.assert_array_equal(rec.contribution_max, rec40.contribution_max)

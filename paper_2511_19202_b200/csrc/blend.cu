@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
 // 141K-entry list was the whole kernel's duration).  Lists of at least
 // 2^SC_COOP_LOG2 entries are therefore walked by a whole CTA, exactly.
 #ifndef SC_COOP_LOG2
-#define SC_COOP_LOG2 12
+#define SC_COOP_LOG2 10
 #endif
 constexpr int kCoopQ = 2048;                     // CTA hit queue (ring; >= 2 chunks + one stream step)
 constexpr int kCoopChunk = kBlendWarps * kG;     // 256 hits per chunk, 32 per warp

@@ -54,8 +54,14 @@ constexpr int kHQ = 256;                 // hit queue capacity (>= kG + kStep)
 #endif
 constexpr int kRecStages = SC_BLEND_STAGES;   // record stages: up to kRecStages - 1 in flight while the oldest
                                               // is blended (3: 5.9 KB per warp, 4 CTAs = 32 warps per SM)
-constexpr int kMaxHeavyPixels = 8;       // ... and at most this many such pixels in the stage
-constexpr int kHeavyHits = 12;           // a pixel covered by >= this many entries of a stage: entry-parallel
+#ifndef SC_HEAVY_PIXELS
+#define SC_HEAVY_PIXELS 8
+#endif
+#ifndef SC_HEAVY_HITS
+#define SC_HEAVY_HITS 8
+#endif
+constexpr int kMaxHeavyPixels = SC_HEAVY_PIXELS;   // ... and at most this many such pixels in the stage
+constexpr int kHeavyHits = SC_HEAVY_HITS;          // a pixel covered by >= this many entries of a stage: entry-parallel
 constexpr size_t kHQBytesW = sizeof(uint2) * kHQ;
 constexpr size_t kStageMetaBytesW = sizeof(uint2) * kG * kRecStages;
 constexpr size_t kRecBytesW = sizeof(float4) * 2 * kG * kRecStages;   // 32-byte sc_splat records
@@ -203,7 +209,7 @@ __device__ __forceinline__ void pixel_entry_parallel(const WalkCtx &c, const flo
         sr += __shfl_xor_sync(0xffffffffu, sr, o);
         sg += __shfl_xor_sync(0xffffffffu, sg, o);
         sb += __shfl_xor_sync(0xffffffffu, sb, o);
-        sc += __shfl_xor_sync(0xffffffffu, sc, o);
+        if (c.record) sc += __shfl_xor_sync(0xffffffffu, sc, o);   // the contribution sum is a record output
     }
     const uint32_t compm = __ballot_sync(0xffffffffu, comp);
     T_out = compm ? __shfl_sync(0xffffffffu, t_after, 31 - __clz(compm)) : T_in;
@@ -400,6 +406,7 @@ __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint
 // covered by ceil(ts / 8) x ceil(ts / 4) 8x4 blocks (the last ones clipped to
 // the tile), 8 per CTA; every warp walks the whole tile list, clipping each
 // record's window to its block.
+template <int REC>
 __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__restrict__ splats, int64_t n_splats,
                                                       const uint32_t *__restrict__ offsets,
                                                       const uint32_t *__restrict__ vals,
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
                                                       const uint32_t *__restrict__ task_order, int tile_base,
                                                       int width, int height, int n_tx, int ts, int nbx, int nblk,
                                                       int ngroups, float stop_t, float bg_r, float bg_g, float bg_b,
-                                                      int record, float *image, float *trans, float *csum,
+                                                      float *image, float *trans, float *csum,
                                                       float *cmax)
 {
     extern __shared__ float4 s_dyn[];
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     c.wins = wins;
     c.blocks = blocks;
     c.stop_t = stop_t;
-    c.record = record;
+    c.record = REC;   // compile-time: the non-recording kernels carry no contribution code
     c.cmax = cmax;
     c.lane = lane;
     // this warp's private queues: hits [kHQ], stage metas [kRecStages][32], records [kRecStages][32][2]
@@ -471,7 +478,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
         image[3 * p + 1] = a.cg + a.T * bg_g;
         image[3 * p + 2] = a.cb + a.T * bg_b;
         trans[p] = a.T;
-        if (record && csum) csum[p] = a.cs;
+        if (REC && csum) csum[p] = a.cs;
     }
 }
 
@@ -663,11 +670,12 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
 // drains (one CTA per tile kept a CTA resident until its longest list ended:
 // ~17 % warps active).  Per list the walk is the same as k_blend's, so images
 // are bit-identical.
+template <int REC>
 __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
     const sc_splat *__restrict__ splats, int64_t n_splats, const uint32_t *__restrict__ boff,
     const uint32_t *__restrict__ vals, const uint32_t *__restrict__ keys, const uint32_t *__restrict__ task_order,
     int64_t n_tasks, unsigned long long *ticket, int width, int height, int n_tx, float stop_t, float bg_r,
-    float bg_g, float bg_b, int record, float *image, float *trans, float *csum, float *cmax)
+    float bg_g, float bg_b, float *image, float *trans, float *csum, float *cmax)
 {
     extern __shared__ float4 s_dyn[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -679,7 +687,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
     c.wins = nullptr;
     c.blocks = 1;
     c.stop_t = stop_t;
-    c.record = record;
+    c.record = REC;   // compile-time: the non-recording kernels carry no contribution code
     c.cmax = cmax;
     c.lane = lane;
     char *wbase = reinterpret_cast<char *>(s_dyn) + wid * kWarpSmem;
@@ -754,7 +762,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
             image[3 * p + 1] = a.cg + a.T * bg_g;
             image[3 * p + 2] = a.cb + a.T * bg_b;
             trans[p] = a.T;
-            if (record && csum) csum[p] = a.cs;
+            if (REC && csum) csum[p] = a.cs;
         }
     }
 }
@@ -848,12 +856,13 @@ static int long_list_log2()
     return e && *e ? atoi(e) : SC_COOP_LOG2;
 }
 
-cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
-                         const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
+template <int REC>
+static cudaError_t blend_impl(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
+                              const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
 {
     constexpr int kSmem = (int)(kBlendWarps * kWarpSmem);
     {
-        cudaError_t e = smem_attr_once(reinterpret_cast<const void *>(k_blend), kSmem);
+        cudaError_t e = smem_attr_once(reinterpret_cast<const void *>(k_blend<REC>), kSmem);
         if (e != cudaSuccess) return e;
     }
     // frame path: 16x16 CTA tiles of 8 blocks; tile lists: the reference's tile size
@@ -869,14 +878,14 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
 #endif
     if (SC_BLEND_PERSIST && lists.blocks && task_order && lists.ticket) {
         // frame path: persistent warps over the (tile, block) lists, longest first
-        cudaError_t e = smem_attr_once(reinterpret_cast<const void *>(k_blend_blocks), kSmem);
+        cudaError_t e = smem_attr_once(reinterpret_cast<const void *>(k_blend_blocks<REC>), kSmem);
         if (e != cudaSuccess) return e;
         static int cps_cache[64];
         int dev = 0;
         cudaGetDevice(&dev);
         int cps = (dev >= 0 && dev < 64) ? cps_cache[dev] : 0;
         if (cps <= 0) {
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_blend_blocks, kBlendWarps * 32, kSmem);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, k_blend_blocks<REC>, kBlendWarps * 32, kSmem);
             if (e != cudaSuccess) return e;
             cps = std::max(cps, 1);
             if (dev >= 0 && dev < 64) cps_cache[dev] = cps;
@@ -884,12 +893,12 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
         const int64_t n_tasks = 8 * n_tiles;
         // ticket[0]: next short list (per warp), [1]: next long list (per CTA), [2]: number of long lists
         SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, 8 * tile_base, n_tasks, 1, task_order,
-                  lists.ticket + 2, opts.record_contributions ? -1 : long_list_log2());
+                  lists.ticket + 2, REC ? -1 : long_list_log2());
         const int grid = (int)std::min<int64_t>((n_tasks + kBlendWarps - 1) / kBlendWarps, (int64_t)sm_count() * cps);
-        SC_LAUNCH(k_blend_blocks, grid, kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
+        SC_LAUNCH(k_blend_blocks<REC>, grid, kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
                   lists.keys, task_order, n_tasks, lists.ticket, cam.width, cam.height, n_tx,
                   (float)opts.stop_transmittance, (float)opts.background[0], (float)opts.background[1],
-                  (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image, out.trans,
+                  (float)opts.background[2], out.image, out.trans,
                   out.contrib_sum, out.contrib_max);
         return cudaGetLastError();
     }
@@ -897,13 +906,20 @@ cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const 
     if (task_order)
         SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, tile_base, n_tiles, lists.blocks ? 8 : 1, task_order,
                   (unsigned long long *)nullptr, -1);
-    SC_LAUNCH(k_blend, (int)(n_tiles * ngroups), kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
+    SC_LAUNCH(k_blend<REC>, (int)(n_tiles * ngroups), kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
               lists.keys, lists.wins, lists.blocks ? 1 : 0, task_order, (int)tile_base, cam.width, cam.height, n_tx,
               ts, nbx, nblk, ngroups,
               (float)opts.stop_transmittance, (float)opts.background[0], (float)opts.background[1],
-              (float)opts.background[2], opts.record_contributions ? 1 : 0, out.image, out.trans, out.contrib_sum,
+              (float)opts.background[2], out.image, out.trans, out.contrib_sum,
               out.contrib_max);
     return cudaGetLastError();
+}
+
+cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
+                         const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st)
+{
+    return opts.record_contributions ? blend_impl<1>(splats, lists, cam, opts, out, n_splats, task_order, st)
+                                     : blend_impl<0>(splats, lists, cam, opts, out, n_splats, task_order, st);
 }
 
 // Visibility labels (sc/sampling.py:206-213): bit i of the little-endian word

@@ -113,9 +113,7 @@ Layout layout(int64_t n_inst, int64_t max_pairs, int64_t capS, int64_t capE, int
     L.n_tiles_ref = (int64_t)L.n_tx_ref * ((h + ts - 1) / ts);
     L.max_chunks = max_pairs / sc::kChunk + n_inst + 1;
     const int64_t big = std::max<int64_t>(std::max<int64_t>(capS, capE), 1);
-    // count-matrix columns: radix tiles of the largest sort, or the block-entry groups of the survivors
-    L.nblk_max = std::max<int64_t>((big + sc::kRadixTile - 1) / sc::kRadixTile,
-                                   (std::max<int64_t>(capS, 1) + sc::kSplitGroup - 1) / sc::kSplitGroup);
+    L.nblk_max = (big + sc::kRadixTile - 1) / sc::kRadixTile;
     const int64_t part = (std::max<int64_t>(256 * L.nblk_max, big) + sc::kScanTile - 1) / sc::kScanTile + 1;
     // key buffers also hold small per-tile lists: at least 4096 words
     const int64_t capK = std::max<int64_t>(capS, 4096);

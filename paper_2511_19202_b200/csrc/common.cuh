@@ -15,7 +15,6 @@ constexpr int kChunk = kCullThreads * kCullTilesPerChunk;
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
 constexpr int kRadixTile = 4096;                          // radix sort tile (count matrix sizing)
-constexpr int kSplitGroup = 1024;                         // passed splats per block-entry group (count matrix sizing)
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;

@@ -311,106 +311,6 @@ struct OsSmem {
     uint16_t wcnt[kOsWarps][256];
 };
 
-// Stable rank + scatter of one staged tile: sm.in_k[b] / sm.in_v[b] hold cnt keys
-// (sm.wcnt zeroed, all visible after a barrier); digit = bits [shift, shift + 8).
-// Thread d < 256 passes gb = the global output base of digit d for this tile and
-// gets back the tile's count of digit d.  Warp w ranks the contiguous slice [w *
-// 256, (w + 1) * 256) with running per-digit counts; the ranked tile is staged back
-// into its own buffer and written out digit-run by digit-run (coalesced).
-template <typename V, bool MATCH_ANY, bool IDX_IN>
-__device__ __forceinline__ uint32_t os_rank_scatter(OsSmem<V> &sm, int b, int cnt, int shift, uint32_t gb, int64_t base,
-                                                    uint32_t *s_gofs, uint32_t *s_warp, uint32_t *__restrict__ keys_out,
-                                                    V *__restrict__ vals_out)
-{
-    constexpr int kPerWarp = kOsTile / kOsWarps;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint32_t lt = lanemask_lt();
-    // stable warp-private ranking: warp w owns the contiguous slice
-    // [w * 256, (w + 1) * 256) and keeps running per-digit counts
-    uint32_t k[kOsItems], rk[kOsItems];
-    V v[kOsItems];
-    auto rank = [&](auto full_tag) {
-        constexpr bool FULL = decltype(full_tag)::value;   // no bounds checks on full tiles
-        uint32_t peers[kOsItems];
-#pragma unroll
-        for (int j = 0; j < kOsItems; j++) {
-            const int i = wid * kPerWarp + j * 32 + lane;
-            k[j] = sm.in_k[b][i];
-            if constexpr (IDX_IN)
-                v[j] = make_uint2((uint32_t)(base + i), reinterpret_cast<const uint32_t *>(sm.in_v[b])[i]);
-            else
-                v[j] = sm.in_v[b][i];
-            const bool ok = FULL || i < cnt;
-            if constexpr (MATCH_ANY)
-                peers[j] = __match_any_sync(0xffffffffu, ok ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane);
-            else if constexpr (FULL)
-                peers[j] = match_digit8((k[j] >> shift) & 0xFFu);
-            else
-                peers[j] = match_digit8((k[j] >> shift) & 0xFFu) & __ballot_sync(0xffffffffu, ok);
-        }
-#pragma unroll
-        for (int j = 0; j < kOsItems; j++) {
-            const bool ok = FULL || wid * kPerWarp + j * 32 + lane < cnt;
-            const uint32_t d = (k[j] >> shift) & 0xFFu;
-            const uint32_t r = __popc(peers[j] & lt);
-            const uint32_t prev = ok ? sm.wcnt[wid][d] : 0u;
-            __syncwarp();
-            if (ok && r == 0) sm.wcnt[wid][d] = (uint16_t)(prev + __popc(peers[j]));
-            __syncwarp();
-            rk[j] = prev + r;
-        }
-    };
-    if (cnt == kOsTile)
-        rank(std::true_type{});
-    else
-        rank(std::false_type{});
-    __syncthreads();
-    // thread = digit: its per-warp counts, the tile-local digit start (block scan), then
-    // wcnt[w][d] = digit start + exclusive prefix over warps (the scatter base of warp w)
-    uint32_t wc[kOsWarps];
-    uint32_t tot = 0;
-    if (tid < 256) {
-#pragma unroll
-        for (int w = 0; w < kOsWarps; w++) {
-            wc[w] = sm.wcnt[w][tid];
-            tot += wc[w];
-        }
-    }
-    {
-        uint32_t total;
-        const uint32_t ds = block_excl_scan<kOsThreads>(tid < 256 ? tot : 0u, s_warp, total);
-        if (tid < 256) {
-            uint32_t run = ds;
-#pragma unroll
-            for (int w = 0; w < kOsWarps; w++) {
-                sm.wcnt[w][tid] = (uint16_t)run;
-                run += wc[w];
-            }
-            s_gofs[tid] = gb - ds;   // output index = s_gofs[d] + tile position (mod 2^32)
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kOsItems; j++) {
-        if (wid * kPerWarp + j * 32 + lane < cnt) {
-            const uint32_t d = (k[j] >> shift) & 0xFFu;
-            const uint32_t pos = sm.wcnt[wid][d] + rk[j];
-            sm.in_k[b][pos] = k[j];
-            sm.in_v[b][pos] = v[j];
-        }
-    }
-    __syncthreads();
-    // coalesced write-out: consecutive positions of one digit are contiguous in the output
-#pragma unroll 4
-    for (int i = tid; i < cnt; i += kOsThreads) {
-        const uint32_t key = sm.in_k[b][i];
-        const uint32_t dst = s_gofs[(key >> shift) & 0xFFu] + (uint32_t)i;
-        keys_out[dst] = key;
-        vals_out[dst] = sm.in_v[b][i];
-    }
-    return tot;
-}
-
 // MATCH_ANY: rank with match.any (fast when a warp holds few distinct digits,
 // e.g. the block sort's high byte: screen rows follow depth order) instead of
 // the constant-cost 8-ballot match.
@@ -427,13 +327,14 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
                                                               int64_t ntiles_max, unsigned long long *tk_next,
                                                               unsigned long long *tk_done)
 {
+    constexpr int kPerWarp = kOsTile / kOsWarps;
     extern __shared__ __align__(128) uint4 s_dyn4[];
     OsSmem<V> &sm = *reinterpret_cast<OsSmem<V> *>(s_dyn4);
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_gofs[256];     // global scatter base - tile-local start of each digit
     __shared__ uint32_t s_warp[32];
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host);
     const int64_t ntiles = (n + kOsTile - 1) / kOsTile;
     auto issue = [&](int64_t t, int b) {
@@ -459,6 +360,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
     int64_t tile = s_tile;
     uint32_t phase0 = 0, phase1 = 0;
     int b = 0;
+    const uint32_t lt = lanemask_lt();
     while (tile < ntiles) {
         __syncthreads();   // buffer b^1 (previous tile) fully written out; s_tile read by all
         if (tid == 0) {   // the next tile's ticket and its TMA load, one tile ahead
@@ -479,7 +381,89 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
         }
         __syncthreads();
 
-        os_rank_scatter<V, MATCH_ANY, IDX_IN>(sm, b, cnt, shift, gb, base, s_gofs, s_warp, keys_out, vals_out);
+        // stable warp-private ranking: warp w owns the contiguous slice
+        // [w * 256, (w + 1) * 256) and keeps running per-digit counts
+        uint32_t k[kOsItems], rk[kOsItems];
+        V v[kOsItems];
+        auto rank = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;   // no bounds checks on full tiles
+            uint32_t peers[kOsItems];
+#pragma unroll
+            for (int j = 0; j < kOsItems; j++) {
+                const int i = wid * kPerWarp + j * 32 + lane;
+                k[j] = sm.in_k[b][i];
+                if constexpr (IDX_IN)
+                    v[j] = make_uint2((uint32_t)(base + i), reinterpret_cast<const uint32_t *>(sm.in_v[b])[i]);
+                else
+                    v[j] = sm.in_v[b][i];
+                const bool ok = FULL || i < cnt;
+                if constexpr (MATCH_ANY)
+                    peers[j] = __match_any_sync(0xffffffffu, ok ? ((k[j] >> shift) & 0xFFu) : 256u + (uint32_t)lane);
+                else if constexpr (FULL)
+                    peers[j] = match_digit8((k[j] >> shift) & 0xFFu);
+                else
+                    peers[j] = match_digit8((k[j] >> shift) & 0xFFu) & __ballot_sync(0xffffffffu, ok);
+            }
+#pragma unroll
+            for (int j = 0; j < kOsItems; j++) {
+                const bool ok = FULL || wid * kPerWarp + j * 32 + lane < cnt;
+                const uint32_t d = (k[j] >> shift) & 0xFFu;
+                const uint32_t r = __popc(peers[j] & lt);
+                const uint32_t prev = ok ? sm.wcnt[wid][d] : 0u;
+                __syncwarp();
+                if (ok && r == 0) sm.wcnt[wid][d] = (uint16_t)(prev + __popc(peers[j]));
+                __syncwarp();
+                rk[j] = prev + r;
+            }
+        };
+        if (cnt == kOsTile)
+            rank(std::true_type{});
+        else
+            rank(std::false_type{});
+        __syncthreads();
+        // thread = digit: its per-warp counts, the tile-local digit start (block scan), then
+        // wcnt[w][d] = digit start + exclusive prefix over warps (the scatter base of warp w)
+        uint32_t wc[kOsWarps];
+        uint32_t tot = 0;
+        if (tid < 256) {
+#pragma unroll
+            for (int w = 0; w < kOsWarps; w++) {
+                wc[w] = sm.wcnt[w][tid];
+                tot += wc[w];
+            }
+        }
+        {
+            uint32_t total;
+            const uint32_t ds = block_excl_scan<kOsThreads>(tid < 256 ? tot : 0u, s_warp, total);
+            if (tid < 256) {
+                uint32_t run = ds;
+#pragma unroll
+                for (int w = 0; w < kOsWarps; w++) {
+                    sm.wcnt[w][tid] = (uint16_t)run;
+                    run += wc[w];
+                }
+                s_gofs[tid] = gb - ds;   // output index = s_gofs[d] + tile position (mod 2^32)
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kOsItems; j++) {
+            if (wid * kPerWarp + j * 32 + lane < cnt) {
+                const uint32_t d = (k[j] >> shift) & 0xFFu;
+                const uint32_t pos = sm.wcnt[wid][d] + rk[j];
+                sm.in_k[b][pos] = k[j];
+                sm.in_v[b][pos] = v[j];
+            }
+        }
+        __syncthreads();
+        // coalesced write-out: consecutive positions of one digit are contiguous in the output
+#pragma unroll 4
+        for (int i = tid; i < cnt; i += kOsThreads) {
+            const uint32_t key = sm.in_k[b][i];
+            const uint32_t dst = s_gofs[(key >> shift) & 0xFFu] + (uint32_t)i;
+            keys_out[dst] = key;
+            vals_out[dst] = sm.in_v[b][i];
+        }
         // generic-proxy writes to buffer b above; its next refill is a TMA (async-proxy) write
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         b ^= 1;
@@ -653,206 +637,145 @@ __device__ __forceinline__ uint32_t block_count(int x0, int x1, int y0, int y1)
     return (uint32_t)((x1 / 8 - x0 / 8 + 1) * (y1 / 4 - y0 / 4 + 1));
 }
 
-// ---------------------------------------------------------------------------
-// Block entries generated straight into the block sort's first pass (frame path).
-//
-// The depth-ordered passed splats are cut into groups of kSplitGroup; a group's
-// block entries (each splat's blocks row-major, splats in depth order) are the
-// sort's "tile" for the first 8-bit digit of the block id.  k_bentry_hist
-// generates each group's entries and histograms that digit into the digit-major
-// count matrix; one exclusive scan gives every (digit, group) output base;
-// k_bentry_split generates the group's entries again, 4096 at a time, into the
-// shared staging tile of the radix downsweep and ranks / scatters them exactly as
-// k_radix_down does (os_rank_scatter), digit bases running across the group's
-// sub-tiles.  The emission order and the stable pass are those of the separate
-// emission + first radix pass it replaces (bit-identical lists), without writing
-// the 8-byte entries to HBM and reading them back twice.
-// ---------------------------------------------------------------------------
-constexpr int kSplitBig = 32;   // splats with more block entries are generated by the whole CTA
-struct SplitGroup {
-    uint32_t off[kSplitGroup + 1];   // exclusive entry offsets within the group (+ the group's total)
-    uint2 win[kSplitGroup];          // clamped pixel window: x0 | x1 << 16, y0 | y1 << 16
-    uint32_t idx[kSplitGroup];       // survivor index (the entry value)
-    uint32_t big[kSplitGroup];       // group-local indices of splats with > kSplitBig entries
-    uint32_t n_big;
-};
-static_assert(kSplitGroup == 2 * kOsThreads, "two consecutive splats per thread");
-
-// entry r (row-major over the splat's blocks) of a splat with pixel window w:
-// key = block id << 10 | block-relative window (the emission's encoding)
-__device__ __forceinline__ uint32_t split_key(uint2 w, uint32_t ry, uint32_t rx, int n_tx)
+__device__ __forceinline__ uint32_t bentry_count(uint2 v, const sc_window *wins, int width, int height)
 {
-    const int x0 = (int)(w.x & 0xFFFFu), x1 = (int)(w.x >> 16), y0 = (int)(w.y & 0xFFFFu), y1 = (int)(w.y >> 16);
-    const int bx = (x0 >> 3) + (int)rx, by = (y0 >> 2) + (int)ry;
-    const int rx0 = max(x0 - 8 * bx, 0), rx1 = min(x1 - 8 * bx, 7), ry0 = max(y0 - 4 * by, 0), ry1 = min(y1 - 4 * by, 3);
-    const uint32_t id = (uint32_t)((((by >> 2) * n_tx + (bx >> 1)) << 3) + (by & 3) * 2 + (bx & 1));
-    return (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
+    int x0, x1, y0, y1;
+    return unpack_window(v.y, v.x, wins, width, height, x0, x1, y0, y1) ? block_count(x0, x1, y0, y1) : 0u;
 }
-__device__ __forceinline__ uint32_t split_nbx(uint2 w) { return ((w.x >> 16) >> 3) - ((w.x & 0xFFFFu) >> 3) + 1u; }
 
-// windows, entry counts, offsets and the big-splat list of group g (ends with a barrier);
-// returns the group's entry total
-__device__ uint32_t split_load_group(SplitGroup &G, const uint2 *__restrict__ pv, const sc_window *wins, int64_t n,
-                                     int64_t g, int width, int height, uint32_t *s_warp)
+// Emission tiles: kEmitTile consecutive passed splats (depth order) per CTA
+// iteration, warp w owning the contiguous kEmitPerWarp splats [w * 512, w * 512
+// + 512) of the tile.  Pass 1 writes per-(tile, warp) entry totals, one
+// exclusive scan turns them into output bases, pass 2 emits (every warp on its
+// own, no CTA barrier): no per-splat count array round trip through HBM.
+constexpr int kEmitThreads = 256;
+constexpr int kEmitTile = 4096;
+constexpr int kEmitPerWarp = kEmitTile / (kEmitThreads / 32);
+
+// pass 1: the entry total of every (tile, warp) range of kEmitPerWarp splats
+__global__ void __launch_bounds__(kEmitThreads) k_bentry_tiles(const uint2 *__restrict__ pv, const sc_window *wins,
+                                                               const unsigned long long *n_dev, int64_t n_host,
+                                                               int64_t ntiles_max, int width, int height,
+                                                               uint32_t *warp_tot)
 {
-    const int tid = threadIdx.x;
-    if (tid == 0) G.n_big = 0;
-    uint32_t c[2] = {0u, 0u};
-    const int64_t k0 = g * kSplitGroup + 2 * tid;
-    uint2 v[2] = {make_uint2(0u, kWinEmpty), make_uint2(0u, kWinEmpty)};
-    if (k0 + 1 < n) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(pv + k0));
-        v[0] = make_uint2(q.x, q.y);
-        v[1] = make_uint2(q.z, q.w);
-    } else if (k0 < n) {
-        v[0] = __ldg(pv + k0);
-    }
-#pragma unroll
-    for (int q = 0; q < 2; q++) {
-        int x0, x1, y0, y1;
-        uint2 w = make_uint2(0u, 0u);
-        if (unpack_window(v[q].y, v[q].x, wins, width, height, x0, x1, y0, y1)) {
-            c[q] = block_count(x0, x1, y0, y1);
-            w = make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
+    const int64_t n = dev_count(n_dev, n_host);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t = blockIdx.x; t < ntiles_max; t += gridDim.x) {
+        const int64_t wbase = t * kEmitTile + (int64_t)wid * kEmitPerWarp;
+        uint32_t c = 0;
+        if (wbase < n) {
+#pragma unroll 4
+            for (int r = 0; r < kEmitPerWarp / 32; r++) {
+                const int64_t k = wbase + r * 32 + lane;
+                if (k < n) c += bentry_count(__ldg(pv + k), wins, width, height);
+            }
         }
-        G.win[2 * tid + q] = w;
-        G.idx[2 * tid + q] = v[q].x;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) warp_tot[t * (kEmitThreads / 32) + wid] = c;
     }
-    uint32_t total;
-    const uint32_t ex = block_excl_scan<kOsThreads>(c[0] + c[1], s_warp, total);   // (its barriers order n_big = 0)
-    G.off[2 * tid] = ex;
-    G.off[2 * tid + 1] = ex + c[0];
-    if (tid == kOsThreads - 1) G.off[kSplitGroup] = total;
+}
+
+// one warp: the (contiguous) entries of 32 consecutive passed splats, starting
+// at output obase; returns their total
+__device__ __forceinline__ uint32_t emit_group(uint2 cv, bool valid, uint32_t obase, const sc_window *wins, int width,
+                                               int height, int n_tx, uint32_t *ekey, uint32_t *eval, int lane)
+{
+    // Warp-cooperative, load-balanced: lane l produces output o = step + l; the
+    // owning splat is found by an upper-bound search over the warp's exclusive
+    // counts (5 shuffles).  Splats covering thousands of blocks (close to the
+    // camera) do not serialise one thread, and the stores are coalesced.
+    int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
+    uint32_t sv = 0, cnt = 0;
+    if (valid) {
+        sv = cv.x;
+        if (unpack_window(cv.y, cv.x, wins, width, height, x0, x1, y0, y1)) cnt = block_count(x0, x1, y0, y1);
+    }
+    uint32_t incl = cnt;
 #pragma unroll
-    for (int q = 0; q < 2; q++)
-        if (c[q] > (uint32_t)kSplitBig) G.big[atomicAdd(&G.n_big, 1u)] = (uint32_t)(2 * tid + q);
-    __syncthreads();
+    for (int s = 1; s < 32; s <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, s);
+        if (lane >= s) incl += y;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (__reduce_max_sync(0xffffffffu, cnt) <= 16u) {
+        // small splats (the common case): each lane writes its own entries, row by row;
+        // the warp's outputs are one contiguous range, so the stores stay within a few lines
+        uint32_t o = obase + excl;
+        if (cnt) {
+            for (int by = y0 / 4; by <= y1 / 4; by++) {
+                const int ry0 = max(y0 - 4 * by, 0), ry1 = min(y1 - 4 * by, 3);
+                const uint32_t row = (uint32_t)(((by >> 2) * n_tx) * 8 + (by & 3) * 2);
+                for (int bx = x0 / 8; bx <= x1 / 8; bx++) {
+                    const int rx0 = max(x0 - 8 * bx, 0), rx1 = min(x1 - 8 * bx, 7);
+                    const uint32_t id = row + (uint32_t)((bx >> 1) * 8 + (bx & 1));
+                    ekey[o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
+                    eval[o] = sv;
+                    o++;
+                }
+            }
+        }
+        return total;
+    }
+    for (uint32_t o0 = 0; o0 < total; o0 += 32) {
+        const uint32_t o = o0 + lane;
+        int s = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, excl, s + step);
+            if (e <= o) s += step;
+        }
+        const uint32_t li = o - __shfl_sync(0xffffffffu, excl, s);
+        const int X0 = __shfl_sync(0xffffffffu, x0, s), X1 = __shfl_sync(0xffffffffu, x1, s);
+        const int Y0 = __shfl_sync(0xffffffffu, y0, s), Y1 = __shfl_sync(0xffffffffu, y1, s);
+        const uint32_t v = __shfl_sync(0xffffffffu, sv, s);
+        if (o < total) {
+            const int w = X1 / 8 - X0 / 8 + 1;
+            // li / w without an integer division (li < 2^24: one correction step is exact)
+            int qy = (int)((float)li * __frcp_rn((float)w));
+            int rx = (int)li - qy * w;
+            if (rx < 0) { qy--; rx += w; } else if (rx >= w) { qy++; rx -= w; }
+            const int bx = X0 / 8 + rx, by = Y0 / 4 + qy;
+            const int rx0 = max(X0 - 8 * bx, 0), rx1 = min(X1 - 8 * bx, 7);
+            const int ry0 = max(Y0 - 4 * by, 0), ry1 = min(Y1 - 4 * by, 3);
+            const uint32_t id = (uint32_t)(((by >> 2) * n_tx + (bx >> 1)) * 8 + (by & 3) * 2 + (bx & 1));
+            ekey[obase + o] = (id << kCodeBits) | (uint32_t)(rx0 | (rx1 << 3) | (ry0 << 6) | (ry1 << 8));
+            eval[obase + o] = v;
+        }
+    }
     return total;
 }
 
-// calls f(position in the group, key, survivor index) for every entry of the group in
-// [t0, t1): the small splats by their own thread, the big ones by the whole CTA
-template <typename F>
-__device__ __forceinline__ void split_generate(const SplitGroup &G, uint32_t t0, uint32_t t1, int n_tx, F &&f)
+__global__ void __launch_bounds__(kEmitThreads) k_bentry_emit(const uint2 *__restrict__ pv, const sc_window *wins,
+                                                              const uint32_t *warp_off, const unsigned long long *n_dev,
+                                                              int64_t n_host, int width, int height, int n_tx,
+                                                              uint32_t *ekey, uint32_t *eval,
+                                                              const unsigned long long *e_total,
+                                                              unsigned long long *e_eff, int64_t cap_e,
+                                                              sc_frame_stats *stats)
 {
-    const int tid = threadIdx.x;
-#pragma unroll
-    for (int q = 0; q < 2; q++) {
-        const int i = 2 * tid + q;
-        const uint32_t o = G.off[i], c = G.off[i + 1] - o;
-        if (c == 0u || c > (uint32_t)kSplitBig) continue;
-        const uint32_t r0 = (o > t0 ? o : t0) - o, r1 = min(o + c, t1);
-        if (o + r0 >= r1) continue;
-        const uint2 w = G.win[i];
-        const uint32_t nbx = split_nbx(w), sv = G.idx[i];
-        uint32_t ry = r0 / nbx, rx = r0 - ry * nbx;
-        for (uint32_t p = o + r0; p < r1; p++) {
-            f(p, split_key(w, ry, rx, n_tx), sv);
-            if (++rx == nbx) {
-                rx = 0;
-                ry++;
-            }
-        }
-    }
-    for (uint32_t b = 0; b < G.n_big; b++) {
-        const int i = (int)G.big[b];
-        const uint32_t o = G.off[i], c = G.off[i + 1] - o;
-        const uint32_t p0 = o > t0 ? o : t0, p1 = min(o + c, t1);
-        const uint2 w = G.win[i];
-        const uint32_t nbx = split_nbx(w), sv = G.idx[i];
-        for (uint32_t p = p0 + (uint32_t)tid; p < p1; p += kOsThreads) {
-            const uint32_t r = p - o, ry = r / nbx;
-            f(p, split_key(w, ry, r - ry * nbx, n_tx), sv);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kOsThreads) k_bentry_hist(const uint2 *__restrict__ pv, const sc_window *wins,
-                                                           const unsigned long long *n_dev, int64_t n_host,
-                                                           int64_t ngroups_max, int width, int height, int n_tx,
-                                                           uint32_t *counts, unsigned long long *tk_next,
-                                                           unsigned long long *tk_done)
-{
-    __shared__ SplitGroup G;
-    __shared__ uint32_t h[kOsWarps][256];
-    __shared__ uint32_t s_warp[32];
-    __shared__ int64_t s_g;
-    const int tid = threadIdx.x, wid = tid >> 5;
-    const int64_t n = dev_count(n_dev, n_host);
-    for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&h[0][0])[i] = 0;
-    for (;;) {
-        if (tid == 0) s_g = (int64_t)atomicAdd(tk_next, 1ull);
-        __syncthreads();
-        const int64_t g = s_g;
-        if (g >= ngroups_max) break;
-        if (g * kSplitGroup < n) {
-            const uint32_t total = split_load_group(G, pv, wins, n, g, width, height, s_warp);
-            uint32_t *hw = h[wid];
-            split_generate(G, 0u, total, n_tx, [&](uint32_t, uint32_t key, uint32_t) {
-                atomicAdd(&hw[(key >> kCodeBits) & 0xFFu], 1u);
-            });
-            __syncthreads();
-        }
-        // digit-major column g (empty groups write zeros: the scan runs over the whole matrix)
-        if (tid < 256) {
-            uint32_t c = 0;
-#pragma unroll
-            for (int w = 0; w < kOsWarps; w++) {
-                c += h[w][tid];
-                h[w][tid] = 0;
-            }
-            counts[(int64_t)tid * ngroups_max + g] = c;
-        }
-        __syncthreads();
-    }
-    if (tid == 0) ticket_release(tk_next, tk_done);
-}
-
-__global__ void __launch_bounds__(kOsThreads, 2) k_bentry_split(
-    const uint2 *__restrict__ pv, const sc_window *wins, const unsigned long long *n_dev, int64_t n_host,
-    int64_t ngroups_max, int width, int height, int n_tx, const uint32_t *__restrict__ bases,
-    uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, const unsigned long long *e_total,
-    unsigned long long *e_eff, int64_t cap_e, sc_frame_stats *stats, unsigned long long *tk_next,
-    unsigned long long *tk_done)
-{
-    extern __shared__ __align__(128) uint4 s_dyn4[];
-    OsSmem<uint32_t> &sm = *reinterpret_cast<OsSmem<uint32_t> *>(s_dyn4);
-    __shared__ SplitGroup G;
-    __shared__ uint32_t s_gofs[256], s_run[256], s_warp[32];
-    __shared__ int64_t s_g;
-    const int tid = threadIdx.x;
     const int64_t n = dev_count(n_dev, n_host);
     const bool over = (int64_t)*e_total > cap_e;
-    if (blockIdx.x == 0 && tid == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         *e_eff = over ? 0ull : *e_total;
         stats->block_entries = (int64_t)*e_total;
         if (over) atomicOr((unsigned long long *)&stats->overflow, 2ull);
     }
-    if (over) return;   // (no CTA took a ticket: the counters stay zero)
-    for (;;) {
-        if (tid == 0) s_g = (int64_t)atomicAdd(tk_next, 1ull);
-        __syncthreads();
-        const int64_t g = s_g;
-        if (g >= ngroups_max) break;
-        if (g * kSplitGroup >= n) break;   // later tickets are past the passed splats too
-        const uint32_t total = split_load_group(G, pv, wins, n, g, width, height, s_warp);
-        if (tid < 256) s_run[tid] = bases[(int64_t)tid * ngroups_max + g];
-        for (uint32_t t0 = 0; t0 < total; t0 += kOsTile) {
-            const int cnt = (int)min((uint32_t)kOsTile, total - t0);
-            for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&sm.wcnt[0][0])[i] = 0;
-            split_generate(G, t0, t0 + (uint32_t)cnt, n_tx, [&](uint32_t p, uint32_t key, uint32_t sv) {
-                sm.in_k[0][p - t0] = key;
-                sm.in_v[0][p - t0] = sv;
-            });
-            __syncthreads();
-            const uint32_t gb = tid < 256 ? s_run[tid] : 0u;
-            const uint32_t tot = os_rank_scatter<uint32_t, false, false>(sm, 0, cnt, kCodeBits, gb, 0, s_gofs, s_warp,
-                                                                          keys_out, vals_out);
-            if (tid < 256) s_run[tid] = gb + tot;
-            __syncthreads();   // the tile is written out before the next sub-tile is generated into it
+    if (over) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t ntiles = (n + kEmitTile - 1) / kEmitTile;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        // this warp's range of the tile and its output base (scan of the (tile, warp) totals)
+        const int64_t wbase = t * kEmitTile + (int64_t)wid * kEmitPerWarp;
+        uint32_t o = warp_off[t * (kEmitThreads / 32) + wid];
+        for (int r = 0; r < kEmitPerWarp / 32; r++) {
+            const int64_t g0 = wbase + r * 32;
+            if (g0 >= n) break;
+            const int64_t k = g0 + lane;
+            const uint2 cv = k < n ? __ldg(pv + k) : make_uint2(0u, kWinEmpty);
+            o += emit_group(cv, k < n, o, wins, width, height, n_tx, ekey, eval, lane);
         }
     }
-    if (tid == 0) ticket_release(tk_next, tk_done);
 }
 
 // boff[b] = first entry with block id >= b, for b in [0, n_blocks]: one thread
@@ -919,30 +842,22 @@ cudaError_t launch_bin(const Ws &ws, const sc_scene &scene, const sc_survivor *s
         SC_LAUNCH(k_extract_order, grid_for(n_max, 256), 256, 0, st, pv_s, p_dev, n_max, dbg_order);
     uint32_t *ek = nullptr, *ev = nullptr;
     if (blocks) {
-        // group histograms of the block id's low byte -> (digit, group) bases -> entries generated
-        // and scattered by that byte in one kernel; then the remaining id bits
-        const int64_t ngroups = std::max<int64_t>(1, (n_max + kSplitGroup - 1) / kSplitGroup);
-        const int nsm = sm_count_sort();
-        SC_LAUNCH(k_bentry_hist, (int)std::min<int64_t>(ngroups, (int64_t)nsm * 4), kOsThreads, 0, st, pv_s, wins, p_dev,
-                  n_max, ngroups, cam.width, cam.height, ws.n_tx, ws.rs_counts, &ws.ctr->rs_next, &ws.ctr->rs_done);
-        e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ngroups, ws.scan_part, &ws.ctr->entries, nullptr, st);
+        // per-(tile, warp) entry totals (free key buffer) -> output bases -> emission
+        const int64_t etiles = std::max<int64_t>(1, (n_max + kEmitTile - 1) / kEmitTile);
+        const int egrid = (int)std::min<int64_t>(etiles, (int64_t)sm_count_sort() * 8);
+        uint32_t *wtot = key_free;   // etiles x 8 words <= max(capS, 4096)
+        SC_LAUNCH(k_bentry_tiles, egrid, kEmitThreads, 0, st, pv_s, wins, p_dev, n_max, etiles, cam.width, cam.height,
+                  wtot);
+        e = scan_excl(wtot, wtot, nullptr, etiles * (kEmitThreads / 32), ws.scan_part, &ws.ctr->entries, nullptr, st);
         if (e != cudaSuccess) return e;
-        e = smem_attr_once(reinterpret_cast<const void *>(k_bentry_split), (int)sizeof(OsSmem<uint32_t>));
-        if (e != cudaSuccess) return e;
-        SC_LAUNCH(k_bentry_split, (int)std::min<int64_t>(ngroups, (int64_t)nsm * 2), kOsThreads,
-                  sizeof(OsSmem<uint32_t>), st, pv_s, wins, p_dev, n_max, ngroups, cam.width, cam.height, ws.n_tx,
-                  ws.rs_counts, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats,
-                  &ws.ctr->rs_next, &ws.ctr->rs_done);
+        SC_LAUNCH(k_bentry_emit, egrid, kEmitThreads, 0, st, pv_s, wins, wtot, p_dev, n_max, cam.width,
+                  cam.height, ws.n_tx, ws.ekey_a, ws.eval_a, &ws.ctr->entries, &ws.ctr->entries_eff, ws.capE, stats);
         const int64_t n_blocks = 8 * ws.n_tiles;
-        ek = ws.ekey_a;
-        ev = ws.eval_a;
-        // remaining passes (block-id high byte ~ screen rows, which follow depth order): few
-        // distinct digits per warp, match.any ranks them faster than the ballot match
-        if (bits_for(n_blocks) > 8) {
-            e = radix_sort<uint32_t>(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE,
-                                     kCodeBits + 8, kCodeBits + bits_for(n_blocks), ws, &ek, &ev, st, true);
-            if (e != cudaSuccess) return e;
-        }
+        // last pass (block-id high byte ~ screen rows, which follow depth order): few distinct
+        // digits per warp, match.any ranks them faster than the ballot match
+        e = radix_sort<uint32_t>(ws.ekey_a, ws.eval_a, ws.ekey_b, ws.eval_b, &ws.ctr->entries_eff, ws.capE, kCodeBits,
+                                 kCodeBits + bits_for(n_blocks), ws, &ek, &ev, st, true);
+        if (e != cudaSuccess) return e;
         SC_LAUNCH(k_block_offsets, (int)((n_blocks + 1 + 255) / 256), 256, 0, st, ek, &ws.ctr->entries_eff, ws.capE,
                   n_blocks, ws.boff);
         if (order_out) *order_out = nullptr;

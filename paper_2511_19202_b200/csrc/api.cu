@@ -328,7 +328,7 @@ int frame_tail(const sc_scene *scene, const sc_camera *cam, const sc_opts *opts,
     }
     if (opts->record_contributions && w.capS > 0)
         SC_TRY(cudaMemsetAsync(out->contrib_max, 0, 4 * (size_t)w.capS, st), "memset contrib_max");
-    const sc::BlendLists lists{w.boff, entries, bkeys, nullptr, true, &w.ctr->blend_next};
+    const sc::BlendLists lists{w.boff, entries, bkeys, nullptr, true, w.ctr};
     SC_TRY(sc::launch_blend(w.splats, lists, *cam, *opts, *out, w.capS, w.task_order, st), "blend");
     SC_TRY(mark(4), "event");
     if (opts->record_contributions)

@@ -836,6 +836,52 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t *off, int64_
     }
 }
 
+// Frame path: the same LPT order over the (tile, block) lists, built by many CTAs
+// (the single-CTA k_tile_order was ~80 us on the frame's critical path): a bucket
+// histogram, then every list takes a slot in its bucket from an atomic cursor (the
+// order inside a bucket is arbitrary; each list's result does not depend on it).
+__device__ __forceinline__ uint32_t list_bucket(const uint32_t *off, int64_t t)
+{
+    const uint32_t c = off[t + 1] - off[t];
+    return c ? 32 - __clz(c) : 0;
+}
+
+__global__ void k_order_hist(const uint32_t *__restrict__ off, int64_t base, int64_t n, unsigned int *hist)
+{
+    __shared__ unsigned int h[33];
+    if (threadIdx.x < 33) h[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&h[list_bucket(off, base + t)], 1u);
+    __syncthreads();
+    if (threadIdx.x < 33 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void k_order_scatter(const uint32_t *__restrict__ off, int64_t base, int64_t n, const unsigned int *hist,
+                                unsigned int *cursor, uint32_t *order, unsigned long long *n_long, int long_log2)
+{
+    __shared__ unsigned int s_base[33];
+    if (threadIdx.x == 0) {
+        unsigned int run = 0;
+        for (int b = 32; b >= 0; b--) {   // heavier buckets first
+            s_base[b] = run;
+            run += hist[b];
+        }
+        if (blockIdx.x == 0 && n_long) *n_long = long_log2 >= 0 && long_log2 < 32 ? s_base[long_log2] : 0;
+    }
+    __syncthreads();
+    for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x; t0 < n; t0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = t0 + threadIdx.x;
+        const uint32_t b = t < n ? list_bucket(off, base + t) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        uint32_t slot = 0;
+        if (b != 0xFFFFFFFFu && (int)(threadIdx.x & 31) == leader) slot = atomicAdd(&cursor[b], __popc(peers));
+        slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(peers & lanemask_lt());
+        if (b != 0xFFFFFFFFu) order[s_base[b] + slot] = (uint32_t)(base + t);
+    }
+}
+
 __global__ void k_count_used(const float *cmax, const unsigned long long *n_dev, int64_t n_host,
                              sc_frame_stats *stats)
 {
@@ -876,7 +922,7 @@ static cudaError_t blend_impl(const sc_splat *splats, const BlendLists &lists, c
 #ifndef SC_BLEND_PERSIST
 #define SC_BLEND_PERSIST 1
 #endif
-    if (SC_BLEND_PERSIST && lists.blocks && task_order && lists.ticket) {
+    if (SC_BLEND_PERSIST && lists.blocks && task_order && lists.ctr) {
         // frame path: persistent warps over the (tile, block) lists, longest first
         cudaError_t e = smem_attr_once(reinterpret_cast<const void *>(k_blend_blocks<REC>), kSmem);
         if (e != cudaSuccess) return e;
@@ -892,11 +938,15 @@ static cudaError_t blend_impl(const sc_splat *splats, const BlendLists &lists, c
         }
         const int64_t n_tasks = 8 * n_tiles;
         // ticket[0]: next short list (per warp), [1]: next long list (per CTA), [2]: number of long lists
-        SC_LAUNCH(k_tile_order, 1, 1024, 0, st, lists.offsets, 8 * tile_base, n_tasks, 1, task_order,
-                  lists.ticket + 2, REC ? -1 : long_list_log2());
+        unsigned long long *ticket = &lists.ctr->blend_next;   // [0] short lists, [1] long lists, [2] n_long
+        unsigned int *hist = lists.ctr->order_hist, *cursor = lists.ctr->order_cursor;
+        const int ogrid = (int)std::max<int64_t>(1, std::min<int64_t>((n_tasks + 255) / 256, (int64_t)sm_count()));
+        SC_LAUNCH(k_order_hist, ogrid, 256, 0, st, lists.offsets, 8 * tile_base, n_tasks, hist);
+        SC_LAUNCH(k_order_scatter, ogrid, 256, 0, st, lists.offsets, 8 * tile_base, n_tasks, hist, cursor, task_order,
+                  ticket + 2, REC ? -1 : long_list_log2());
         const int grid = (int)std::min<int64_t>((n_tasks + kBlendWarps - 1) / kBlendWarps, (int64_t)sm_count() * cps);
         SC_LAUNCH(k_blend_blocks<REC>, grid, kBlendWarps * 32, kSmem, st, splats, n_splats, lists.offsets, lists.vals,
-                  lists.keys, task_order, n_tasks, lists.ticket, cam.width, cam.height, n_tx,
+                  lists.keys, task_order, n_tasks, ticket, cam.width, cam.height, n_tx,
                   (float)opts.stop_transmittance, (float)opts.background[0], (float)opts.background[1],
                   (float)opts.background[2], out.image, out.trans,
                   out.contrib_sum, out.contrib_max);

@@ -88,6 +88,8 @@ struct Counters {
     unsigned long long blend_next;     // persistent blend warps: next short (tile, block) list of the LPT order
     unsigned long long blend_long_next;   // ... next long list (one CTA each)
     unsigned long long blend_n_long;      // ... number of long lists at the head of the order (k_tile_order)
+    unsigned int order_hist[33];          // LPT buckets of the (tile, block) lists (k_order_hist)
+    unsigned int order_cursor[33];        // ... slots handed out per bucket (k_order_scatter)
 };
 
 // Workspace carve-out (all offsets 256-byte aligned), see api.cu:carve().
@@ -260,7 +262,7 @@ struct BlendLists {
     const uint32_t *keys;
     const sc_window *wins;   // tile lists only: windows to clip per warp block
     bool blocks;
-    unsigned long long *ticket;   // block lists: Counters::blend_next (3 consecutive u64, zeroed per frame), else NULL
+    Counters *ctr;   // block lists: the frame's counters (blend tickets, list order; zeroed per frame), else NULL
 };
 cudaError_t launch_blend(const sc_splat *splats, const BlendLists &lists, const sc_camera &cam, const sc_opts &opts,
                          const sc_frame_out &out, int64_t n_splats, uint32_t *task_order, cudaStream_t st);

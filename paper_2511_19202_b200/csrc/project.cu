@@ -55,8 +55,11 @@ __device__ __forceinline__ float fdot3(float a0, float a1, float a2, float b0, f
 // kProjExact: all-f64 reference path, over `list` when it is given.
 enum { kProjMixed = 0, kProjFast = 1, kProjExact = 2 };
 
+#ifndef SC_PROJ_CPS
+#define SC_PROJ_CPS 2
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) k_project(
+__global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
     sc_scene scene, const sc_survivor *surv, const unsigned long long *n_dev, int64_t n_host, sc_camera cam,
     sc_opts opts, sc_splat *splats, sc_window *wins, double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
     double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr, uint32_t *list)
@@ -469,7 +472,7 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
     if (n_max <= 0) return cudaSuccess;
     const int nsm = sm_count();
 #ifndef SC_PROJ_GRID
-#define SC_PROJ_GRID 8
+#define SC_PROJ_GRID 2   // one wave of resident CTAs (2 per SM): no partial last wave
 #endif
     const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * SC_PROJ_GRID);
     if (opts.exact_projection) {

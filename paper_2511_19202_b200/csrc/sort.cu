@@ -768,11 +768,14 @@ __global__ void __launch_bounds__(kEmitThreads) k_bentry_emit(const uint2 *__res
         // this warp's range of the tile and its output base (scan of the (tile, warp) totals)
         const int64_t wbase = t * kEmitTile + (int64_t)wid * kEmitPerWarp;
         uint32_t o = warp_off[t * (kEmitThreads / 32) + wid];
+        // the next group's pairs are loaded while this group is emitted
+        uint2 cv_next = wbase + lane < n ? __ldg(pv + wbase + lane) : make_uint2(0u, kWinEmpty);
         for (int r = 0; r < kEmitPerWarp / 32; r++) {
             const int64_t g0 = wbase + r * 32;
             if (g0 >= n) break;
             const int64_t k = g0 + lane;
-            const uint2 cv = k < n ? __ldg(pv + k) : make_uint2(0u, kWinEmpty);
+            const uint2 cv = cv_next;
+            if (r + 1 < kEmitPerWarp / 32 && k + 32 < n) cv_next = __ldg(pv + k + 32);
             o += emit_group(cv, k < n, o, wins, width, height, n_tx, ekey, eval, lane);
         }
     }

@@ -34,5 +34,8 @@ torch.cuda.synchronize()
 t1 = time.perf_counter()
 gc.enable()
 d = np.diff(np.array([t0] + ts)) * 1e3
+caps = {k: (w.cap_s, w.cap_e) for k, w in r.workspaces.items()}
+top = np.argsort(-d)[:4]
 print(f"F={F}: {len(seq) / (t1 - t0):.1f} FPS, frame gaps ms p50 {np.percentile(d, 50):.2f} p90 {np.percentile(d, 90):.2f} "
-      f"max {d.max():.2f}, host busy {1e3 * ((t1 - t0) - r.path_wait_s) / len(seq):.2f} ms/frame", flush=True)
+      f"max {d.max():.2f} (frames {top.tolist()}: {np.round(d[top], 1).tolist()}), "
+      f"host busy {1e3 * ((t1 - t0) - r.path_wait_s) / len(seq):.2f} ms/frame, workspaces {caps}", flush=True)

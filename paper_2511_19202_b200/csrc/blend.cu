@@ -90,6 +90,15 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane)
     return x;
 }
 
+// e^x for x in [0, ln 255 + 1] (power - p_min once the window test passed): the same
+// ex2.approx as __expf, without its denormal-result range fix-up (never taken here)
+__device__ __forceinline__ float exp_nonneg(float x)
+{
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x * 1.4426950408889634f));
+    return r;
+}
+
 __device__ __forceinline__ int lo16(uint32_t w) { return (int)(int16_t)(w & 0xFFFFu); }
 __device__ __forceinline__ int hi16(uint32_t w) { return (int)(int16_t)(w >> 16); }
 
@@ -178,7 +187,7 @@ __device__ __forceinline__ void pixel_entry_parallel(const WalkCtx &c, const flo
         const float dx = qx - g.x, dy = qy - g.y;
         const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
         if (!(power > 0.0f || power < p.y)) {
-            alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
+            alpha = fminf(0.99f, exp_nonneg(power - p.y) * (1.0f / 255.0f));
             const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
             const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);
             cr = __low2float(rg);
@@ -248,7 +257,7 @@ __device__ __forceinline__ void blend_stage(const WalkCtx &c, const float4 *grp,
             const float power = -(g.z * dx * dx + p.x * dy * dy) - g.w * dx * dy;
             if (!(power > 0.0f || power < p.y)) {
                 // opacity * e^power == e^(power - p_min) / 255
-                const float alpha = fminf(0.99f, __expf(power - p.y) * (1.0f / 255.0f));
+                const float alpha = fminf(0.99f, exp_nonneg(power - p.y) * (1.0f / 255.0f));
                 const float contrib = alpha * a.T;
                 const __half2 rg = *reinterpret_cast<const __half2 *>(&p.z);
                 const __half2 bx = *reinterpret_cast<const __half2 *>(&p.w);

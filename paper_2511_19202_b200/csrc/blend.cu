@@ -511,6 +511,8 @@ struct CoopSmem {
     float4 fin[32];                         // (T, r, g, b) of pixels retired by a segment re-composite
     uint32_t cnt[2][kBlendWarps];           // stream step: hits per warp (double-buffered by step parity)
     uint32_t ticket[2];
+    uint32_t mask_x[64];                    // code_mask by table: column byte of (x0 | x1 << 3)
+    uint32_t mask_y[16];                    // ... and row selector of (y0 | y1 << 2): mask = x * y
 };
 static_assert(sizeof(CoopSmem) <= kBlendWarps * kWarpSmem, "the CTA layout reuses the per-warp queues' bytes");
 static_assert(kCoopQ >= 2 * kCoopChunk + kCoopStep, "queue holds two chunks plus one stream step");
@@ -561,7 +563,8 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
             uint32_t fp[4], bal[4], nw = 0;
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-                fp[j] = (int64_t)va[j] < c.n_splats ? code_mask(ka[j] & 0x3FFu) & alive : 0u;
+                // (padding past the list end carries kEmptyCode: an empty mask)
+                fp[j] = s.mask_x[ka[j] & 63u] * s.mask_y[(ka[j] >> 6) & 15u] & alive;
                 bal[j] = __ballot_sync(0xffffffffu, fp[j] != 0u);
                 nw += __popc(bal[j]);
             }
@@ -710,6 +713,10 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
     const int64_t n_coop = (int64_t)*reinterpret_cast<volatile unsigned long long *>(ticket + 2);
     if (n_coop > 0) {
         CoopSmem &s = *reinterpret_cast<CoopSmem *>(s_dyn);
+        // code_mask(c) = cols(x0, x1) * rows(y0, y1): cols = code_mask(c & 63) (row 0 only), rows = code_mask of
+        // the row bits with x0 = x1 = 0 (column 0 only)
+        if (threadIdx.x < 64) s.mask_x[threadIdx.x] = code_mask(threadIdx.x);
+        if (threadIdx.x < 16) s.mask_y[threadIdx.x] = code_mask(threadIdx.x << 6);
         for (int it = 0;; it++) {
             if (threadIdx.x == 0) s.ticket[it & 1] = (uint32_t)atomicAdd(ticket + 1, 1ull);
             __syncthreads();

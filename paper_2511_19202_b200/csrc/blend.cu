@@ -43,6 +43,8 @@ namespace sc {
 // [entries, 32-entry slots walked, (entry, warp) hits, pixel evaluations, max warp cycles, warp iterations, 0, 0]
 constexpr int kDbgTiles = 32400;
 __device__ unsigned long long g_blend_dbg[kDbgTiles * 8];
+// per (tile, block) list of the frame path: [entries, entries streamed before the walk stopped]
+__device__ unsigned int g_blend_used[kDbgTiles * 8 * 2];
 #endif
 
 constexpr int kBlendWarps = 8;           // warps per CTA (one 16x16 tile)
@@ -159,7 +161,7 @@ struct PixAcc {
 };
 
 #ifdef SC_BLEND_STATS
-struct WalkStats { unsigned long long slots, hits, evals, iters; };
+struct WalkStats { unsigned long long slots, hits, evals, iters, meta; };
 #define SC_WS_PARAM , WalkStats &d
 #define SC_WS_ARG , d
 #else
@@ -305,6 +307,9 @@ __device__ __forceinline__ void blend_stage(const WalkCtx &c, const float4 *grp,
 __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint32_t end, PixAcc &a SC_WS_PARAM)
 {
     const int lane = c.lane;
+#ifdef SC_BLEND_STATS
+    d.meta = 0;
+#endif
     if (__all_sync(0xffffffffu, a.done) || start >= end) return;
     const uint32_t lt = lanemask_lt();
     // meta of stream step [base, base + 128): entry base + 32 j + lane in (v[j], k[j])
@@ -408,6 +413,9 @@ __device__ __forceinline__ void walk_list(const WalkCtx &c, uint32_t start, uint
     }
     cp_async_wait<0>();
     __syncwarp();
+#ifdef SC_BLEND_STATS
+    d.meta = min(mbase, end) - start;
+#endif
 }
 
 // Frame path: one CTA per 16x16 tile, warp w = 8x4 block w, walking its own
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
     c.stage = reinterpret_cast<uint2 *>(wbase + kHQBytesW);
     c.recs = reinterpret_cast<float4 *>(wbase + kHQBytesW + kStageMetaBytesW);
 #ifdef SC_BLEND_STATS
-    WalkStats d{0, 0, 0, 0};
+    WalkStats d{0, 0, 0, 0, 0};
     const long long d_t0 = clock64();
 #endif
     const int cta = (int)blockIdx.x / ngroups;
@@ -673,6 +681,9 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
     }
     cp_async_wait<0>();
     __syncwarp();
+#ifdef SC_BLEND_STATS
+    d.meta = min(mbase, end) - start;
+#endif
 }
 
 // Frame path, persistent: every warp repeatedly takes the next (16x16 tile, 8x4
@@ -707,7 +718,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
     c.stage = reinterpret_cast<uint2 *>(wbase + kHQBytesW);
     c.recs = reinterpret_cast<float4 *>(wbase + kHQBytesW + kStageMetaBytesW);
 #ifdef SC_BLEND_STATS
-    WalkStats d{0, 0, 0, 0};
+    WalkStats d{0, 0, 0, 0, 0};
 #endif
     // phase 1: the long lists at the head of the LPT order, one CTA each
     const int64_t n_coop = (int64_t)*reinterpret_cast<volatile unsigned long long *>(ticket + 2);
@@ -736,6 +747,12 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
             PixAcc a{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, !inside};
             bool retired_here = false;
             coop_list(c, s, wid, __ldg(boff + blk), __ldg(boff + blk + 1), a, retired_here SC_WS_ARG);
+#ifdef SC_BLEND_STATS
+            if (threadIdx.x == 0 && blk < kDbgTiles * 8) {
+                g_blend_used[2 * blk] = __ldg(boff + blk + 1) - __ldg(boff + blk);
+                g_blend_used[2 * blk + 1] = (unsigned int)d.meta;
+            }
+#endif
             __syncthreads();   // s.fin complete
             if (wid == 0 && inside) {
                 if (retired_here) {
@@ -772,6 +789,12 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
         c.fpy = (float)py;
         PixAcc a{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, !inside};
         walk_list(c, __ldg(boff + blk), __ldg(boff + blk + 1), a SC_WS_ARG);
+#ifdef SC_BLEND_STATS
+        if (lane == 0 && blk < kDbgTiles * 8) {
+            g_blend_used[2 * blk] = __ldg(boff + blk + 1) - __ldg(boff + blk);
+            g_blend_used[2 * blk + 1] = (unsigned int)d.meta;
+        }
+#endif
         if (inside) {
             const int64_t p = (int64_t)py * width + px;
             image[3 * p + 0] = a.cr + a.T * bg_r;
@@ -1027,6 +1050,14 @@ extern "C" __attribute__((visibility("default"))) int sc_debug_blend_stats(unsig
     if (cudaGetSymbolAddress(&p, sc::g_blend_dbg) != cudaSuccess) return 2;
     if (reset) return cudaMemset(p, 0, sizeof(sc::g_blend_dbg)) == cudaSuccess ? 0 : 2;
     const size_t bytes = sizeof(unsigned long long) * 8 * (size_t)std::min<int64_t>(n_tiles, sc::kDbgTiles);
+    return cudaMemcpy(host, p, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
+}
+// [n_blocks][2] = (list length, entries streamed before the walk stopped) of the last frame
+extern "C" __attribute__((visibility("default"))) int sc_debug_blend_used(unsigned int *host, int64_t n_blocks)
+{
+    void *p = nullptr;
+    if (cudaGetSymbolAddress(&p, sc::g_blend_used) != cudaSuccess) return 2;
+    const size_t bytes = sizeof(unsigned int) * 2 * (size_t)std::min<int64_t>(n_blocks, 8 * sc::kDbgTiles);
     return cudaMemcpy(host, p, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
 #endif

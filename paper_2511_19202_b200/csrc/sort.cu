@@ -237,69 +237,68 @@ __device__ __forceinline__ void ticket_release(unsigned long long *next, unsigne
     }
 }
 
-// Upsweep: warp-private shared histograms (plain shared atomics, no ranking),
-// keys loaded 4 per thread per load (uint4, streaming).
-// A ticket covers kUpTiles consecutive tiles whose keys are all loaded up front
-// (kUpTiles x 2 x 16 B per thread in flight), then histogrammed tile by tile.
-constexpr int kUpTiles = 4;
-__global__ void __launch_bounds__(kOsThreads) k_radix_up(const uint32_t *__restrict__ keys,
-                                                         const unsigned long long *n_dev, int64_t n_host, int shift,
-                                                         uint32_t *counts, int64_t ntiles_max,
-                                                         unsigned long long *tk_next, unsigned long long *tk_done)
+// Upsweep, warp per tile: a warp takes a whole 4096-key tile from the ticket,
+// histograms it into its private shared counters and writes the tile's 256
+// counts itself -- no CTA barrier per tile (a CTA-cooperative upsweep spent its
+// time in two barriers per tile: 90 vs ~60 us per depth pass, far view).
+constexpr int kUpwBatch = 4;   // uint4 loads per lane per batch (double-buffered)
+__global__ void __launch_bounds__(kOsThreads, 2) k_radix_up(const uint32_t *__restrict__ keys,
+                                                             const unsigned long long *n_dev, int64_t n_host,
+                                                             int shift, uint32_t *counts, int64_t ntiles_max,
+                                                             unsigned long long *tk_next, unsigned long long *tk_done)
 {
     __shared__ uint32_t h[kOsWarps][256];
-    __shared__ int64_t s_t;
-    const int tid = threadIdx.x, wid = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host);
-    constexpr int kQ = kOsItems / 4;   // uint4 loads per thread per tile
-    for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&h[0][0])[i] = 0;
+    uint32_t *hw = h[wid];
+#pragma unroll
+    for (int q = 0; q < 8; q++) hw[lane + 32 * q] = 0;
+    __syncwarp();
+    constexpr int kBatches = kOsTile / (32 * 4 * kUpwBatch);
     for (;;) {
-        if (tid == 0) s_t = (int64_t)atomicAdd(tk_next, 1ull) * kUpTiles;
-        __syncthreads();
-        const int64_t t0 = s_t;
-        if (t0 >= ntiles_max) break;
-        uint4 kv[kUpTiles][kQ];
+        unsigned long long tt = 0;
+        if (lane == 0) tt = atomicAdd(tk_next, 1ull);
+        const int64_t t = (int64_t)__shfl_sync(0xffffffffu, tt, 0);
+        if (t >= ntiles_max) break;
+        const int64_t base = t * kOsTile;
+        if (base + kOsTile <= n) {
+            uint4 ka[kUpwBatch], kb[kUpwBatch];
+            auto load = [&](int bi, uint4 *dst) {
 #pragma unroll
-        for (int u = 0; u < kUpTiles; u++)
+                for (int q = 0; q < kUpwBatch; q++)
+                    dst[q] = __ldcs(reinterpret_cast<const uint4 *>(keys + base) + (bi * kUpwBatch + q) * 32 + lane);
+            };
+            auto count = [&](const uint4 *src) {
 #pragma unroll
-            for (int q = 0; q < kQ; q++) {
-                const int64_t i = (t0 + u) * kOsTile + 4 * (q * kOsThreads + tid);   // 4 consecutive keys
-                kv[u][q] = i + 4 <= n ? __ldcs(reinterpret_cast<const uint4 *>(keys + i))
-                                      : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-            }
-        uint32_t *hw = h[wid];
-#pragma unroll
-        for (int u = 0; u < kUpTiles; u++) {
-            const int64_t t = t0 + u;
-            if (t >= ntiles_max) break;
-            const int64_t base = t * kOsTile;
-#pragma unroll
-            for (int q = 0; q < kQ; q++) {
-                const int64_t i = base + 4 * (q * kOsThreads + tid);
-                if (i + 4 <= n) {
-                    const uint4 k = kv[u][q];
-                    atomicAdd(&hw[(k.x >> shift) & 0xFFu], 1u);
-                    atomicAdd(&hw[(k.y >> shift) & 0xFFu], 1u);
-                    atomicAdd(&hw[(k.z >> shift) & 0xFFu], 1u);
-                    atomicAdd(&hw[(k.w >> shift) & 0xFFu], 1u);
-                } else {
-                    for (int64_t e = i; e < n && e < i + 4; e++) atomicAdd(&hw[(keys[e] >> shift) & 0xFFu], 1u);
+                for (int q = 0; q < kUpwBatch; q++) {
+                    atomicAdd(&hw[(src[q].x >> shift) & 0xFFu], 1u);
+                    atomicAdd(&hw[(src[q].y >> shift) & 0xFFu], 1u);
+                    atomicAdd(&hw[(src[q].z >> shift) & 0xFFu], 1u);
+                    atomicAdd(&hw[(src[q].w >> shift) & 0xFFu], 1u);
                 }
+            };
+            load(0, ka);
+#pragma unroll 1
+            for (int bi = 0; bi < kBatches; bi += 2) {
+                load(bi + 1, kb);
+                count(ka);
+                if (bi + 2 < kBatches) load(bi + 2, ka);
+                count(kb);
             }
-            __syncthreads();
-            // digit-major: the matrix's exclusive scan is every (digit, tile) base; empty tiles write zeros
-            if (tid < 256) {
-                uint32_t c = 0;
-#pragma unroll
-                for (int w = 0; w < kOsWarps; w++) {
-                    c += h[w][tid];
-                    h[w][tid] = 0;
-                }
-                counts[(int64_t)tid * ntiles_max + t] = c;
-            }
-            __syncthreads();
+        } else {
+            for (int64_t e = base + lane; e < n && e < base + kOsTile; e += 32) atomicAdd(&hw[(keys[e] >> shift) & 0xFFu], 1u);
         }
+        __syncwarp();
+        // digit-major: the matrix's exclusive scan is every (digit, tile) base; empty tiles write zeros
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int d = lane + 32 * q;
+            counts[(int64_t)d * ntiles_max + t] = hw[d];
+            hw[d] = 0;
+        }
+        __syncwarp();
     }
+    __syncthreads();
     if (tid == 0) ticket_release(tk_next, tk_done);
 }
 
@@ -317,6 +316,10 @@ struct OsSmem {
 // IDX_IN (first depth pass of the frame path, V = uint2): the input values are the
 // packed pixel windows alone (u32, the projection writes no index) and the output
 // value is (input position = survivor index, window).
+#ifndef SC_RADIX_WUNROLL
+#define SC_RADIX_WUNROLL 1
+#endif
+constexpr int kRadixWUnroll = SC_RADIX_WUNROLL;
 template <typename V, bool MATCH_ANY, bool IDX_IN = false>
 __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__restrict__ keys_in,
                                                               const V *__restrict__ vals_in,
@@ -332,7 +335,6 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
     OsSmem<V> &sm = *reinterpret_cast<OsSmem<V> *>(s_dyn4);
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_gofs[256];     // global scatter base - tile-local start of each digit
-    __shared__ uint32_t s_warp[32];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host);
@@ -349,6 +351,8 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
                          (c * (uint32_t)sizeof(V) + 15u) & ~15u);
     };
     __shared__ int64_t s_tile;
+    __shared__ uint32_t s_dsum[256 / 32];   // per-warp digit totals of the scan phase
+    for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&sm.wcnt[0][0])[i] = 0;
     if (tid == 0) {
         os_mbar_init(&s_bar[0]);
         os_mbar_init(&s_bar[1]);
@@ -367,7 +371,6 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
             s_tile = (int64_t)atomicAdd(tk_next, 1ull);
             if (s_tile < ntiles) issue(s_tile, b ^ 1);
         }
-        for (int i = tid; i < kOsWarps * 256; i += kOsThreads) (&sm.wcnt[0][0])[i] = 0;
         uint32_t gb = 0;
         if (tid < 256) gb = bases[(int64_t)tid * ntiles_max + tile];
         const int64_t base = tile * kOsTile;
@@ -379,7 +382,8 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
             os_mbar_wait(&s_bar[1], phase1);
             phase1 ^= 1u;
         }
-        __syncthreads();
+        // (no barrier: every thread observed the TMA's mbarrier itself, and the warp counters
+        // were zeroed before the loop-top barrier)
 
         // stable warp-private ranking: warp w owns the contiguous slice
         // [w * 256, (w + 1) * 256) and keeps running per-digit counts
@@ -433,8 +437,22 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
             }
         }
         {
-            uint32_t total;
-            const uint32_t ds = block_excl_scan<kOsThreads>(tid < 256 ? tot : 0u, s_warp, total);
+            // exclusive scan over the 256 digits: warp scans, one barrier, each thread adds the
+            // totals of the warps before its own (<= 7 broadcast reads)
+            uint32_t ds = 0;
+            if (tid < 256) {
+                uint32_t x = tot;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (lane == 31) s_dsum[wid] = x;
+                ds = x - tot;
+            }
+            __syncthreads();
+            if (tid < 256)
+                for (int w = 0; w < wid; w++) ds += s_dsum[w];
             if (tid < 256) {
                 uint32_t run = ds;
 #pragma unroll
@@ -457,13 +475,17 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
         }
         __syncthreads();
         // coalesced write-out: consecutive positions of one digit are contiguous in the output
-#pragma unroll 4
+        // (not unrolled: bursts of unrolled loads then stores ran 3 % slower per pass)
+#pragma unroll kRadixWUnroll
         for (int i = tid; i < cnt; i += kOsThreads) {
             const uint32_t key = sm.in_k[b][i];
             const uint32_t dst = s_gofs[(key >> shift) & 0xFFu] + (uint32_t)i;
             keys_out[dst] = key;
             vals_out[dst] = sm.in_v[b][i];
         }
+        // the next tile's warp counters (the write-out does not read them; the loop-top
+        // barrier orders this before the next ranking)
+        for (int i = tid; i < kOsWarps * 256 / 8; i += kOsThreads) reinterpret_cast<uint4 *>(&sm.wcnt[0][0])[i] = make_uint4(0, 0, 0, 0);
         // generic-proxy writes to buffer b above; its next refill is a TMA (async-proxy) write
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         b ^= 1;
@@ -502,9 +524,8 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
     V *vi = va, *vo = vb;
     for (int p = 0; p < npass; p++) {
         const int shift = bit_lo + 8 * p;
-        SC_LAUNCH(k_radix_up, (int)std::min<int64_t>((ntiles + kUpTiles - 1) / kUpTiles, (int64_t)nsm * 4), kOsThreads, 0,
-                  st, ki, n_dev, n_max,
-                  shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
+        SC_LAUNCH(k_radix_up, (int)std::min<int64_t>((ntiles + kOsWarps - 1) / kOsWarps, (int64_t)nsm * 2),
+                  kOsThreads, 0, st, ki, n_dev, n_max, shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
         e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;
 #ifndef SC_RADIX_CPS
@@ -653,6 +674,7 @@ constexpr int kEmitTile = 4096;
 constexpr int kEmitPerWarp = kEmitTile / (kEmitThreads / 32);
 
 // pass 1: the entry total of every (tile, warp) range of kEmitPerWarp splats
+
 __global__ void __launch_bounds__(kEmitThreads) k_bentry_tiles(const uint2 *__restrict__ pv, const sc_window *wins,
                                                                const unsigned long long *n_dev, int64_t n_host,
                                                                int64_t ntiles_max, int width, int height,

@@ -53,7 +53,9 @@ __device__ __forceinline__ float fdot3(float a0, float a1, float a2, float b0, f
 //            and projected afterwards by the exact kernel (frame path: keeps this
 //            kernel small enough for 4 CTAs per SM);
 // kProjExact: all-f64 reference path, over `list` when it is given.
-enum { kProjMixed = 0, kProjFast = 1, kProjExact = 2 };
+// kProjFrame: kProjFast inside the frame path (keys written; no stage-API outputs, no
+//            exact depth range: compile-time, not pointer tests)
+enum { kProjMixed = 0, kProjFast = 1, kProjExact = 2, kProjFrame = 3 };
 
 #ifndef SC_PROJ_CPS
 #define SC_PROJ_CPS 2
@@ -66,17 +68,22 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
 {
     // frame path: depth keys quantised over the instance spheres' depth range (k_prep)
     const double key_dmin = keys ? ctr->key_dmin : 0.0, key_scale = keys ? ctr->key_scale : 0.0;
+    constexpr bool kDefer = MODE == kProjFast || MODE == kProjFrame;   // f32 only, ambiguous splats deferred
+    if constexpr (MODE == kProjFrame) {
+        depth64 = nullptr; rect = nullptr; dbg_f64 = nullptr; dbg_rect = nullptr; dbg_flags = nullptr;
+    }
     const int64_t n_surv = n_dev ? min((int64_t)*n_dev, n_host) : n_host;
     const bool from_list = MODE == kProjExact && list != nullptr;
     const int64_t n = from_list ? (int64_t)ctr->proj_deferred : n_surv;
     const double lim_x = 1.3 * cam.tan_x, lim_y = 1.3 * cam.tan_y;
+    const float lim_xf = (float)lim_x, lim_yf = (float)lim_y;
     const double focal = cam.focal;
     const int ts = opts.tile_size;
     const int tsh = (ts & (ts - 1)) == 0 ? __ffs(ts) - 1 : -1;   // log2 of a power-of-two tile size
     const int n_tx = (cam.width + ts - 1) / ts;
     const Band band = band_of(opts, cam.height, ts);
     unsigned long long n_passed = 0, n_skipped = 0, dmin_inv = 0, dmax_bits = 0, n_tentries = 0, n_exact = 0;
-    const bool fast = MODE == kProjFast || (MODE == kProjMixed && opts.exact_projection == 0);
+    const bool fast = kDefer || (MODE == kProjMixed && opts.exact_projection == 0);
     // camera rotation in f32 for the f32 covariance path (loop invariant)
     const float clip_f = opts.radius_clip > 0.0 ? (float)opts.radius_clip : 0.0f;
     const float pos_x = (float)cam.pos[0], pos_y = (float)cam.pos[1], pos_z = (float)cam.pos[2];
@@ -122,8 +129,6 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
         bool fast_done = false;
         if (tz > cam.near_) {
             const double txz = tx / tz, tyz = ty / tz;
-            const double ctxz = fmin(fmax(txz, -lim_x), lim_x);
-            const double ctyz = fmin(fmax(tyz, -lim_y), lim_y);
             mx = focal * txz + (double)(cam.width - 1) / 2.0;
             my = focal * tyz + (double)(cam.height - 1) / 2.0;
             const double *R = cam.rot;
@@ -136,7 +141,9 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
                 // The radius is taken from f32 only when the whole interval of lambda
                 // gives the same ceil(3 sqrt(lambda)); else the f64 path below runs.
                 const float fz = (float)focal / (float)tz;
-                const float cx = (float)ctxz, cy = (float)ctyz;
+                // (float) of the f64 clamp below == the f32 clamp of (float) txz (rounding is monotone)
+                const float cx = fminf(fmaxf((float)txz, -lim_xf), lim_xf);
+                const float cy = fminf(fmaxf((float)tyz, -lim_yf), lim_yf);
                 const float j00 = fz * fmaf(-cx, r6, r0), j01 = fz * fmaf(-cx, r7, r1), j02 = fz * fmaf(-cx, r8, r2);
                 const float j10 = fz * fmaf(-cy, r6, r3), j11 = fz * fmaf(-cy, r7, r4), j12 = fz * fmaf(-cy, r8, r5);
                 const float qn = rsqrtf(fmaf(qf.x, qf.x, fdot3(qf.y, qf.z, qf.w, qf.y, qf.z, qf.w)));
@@ -201,16 +208,18 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
                     f_sc = fc + err;
                 }
             }
-            if constexpr (MODE == kProjFast) {
+            if constexpr (kDefer) {
                 if (!fast_done) {   // ambiguous: the exact kernel projects this splat afterwards
                     list[atomicAdd(&ctr->proj_deferred, 1ull)] = (uint32_t)k;
                     n_exact++;
                     continue;
                 }
             }
-            if (MODE != kProjFast && !fast_done) {
+            if (!kDefer && !fast_done) {
                 if (fast) n_exact++;
                 const double fz = focal / tz;
+                const double ctxz = fmin(fmax(txz, -lim_x), lim_x);
+                const double ctyz = fmin(fmax(tyz, -lim_y), lim_y);
                 const double j00 = fz * R[0] - fz * ctxz * R[6];
                 const double j01 = fz * R[1] - fz * ctxz * R[7];
                 const double j02 = fz * R[2] - fz * ctxz * R[8];
@@ -297,9 +306,11 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
         n_passed += passed;
         if (passed) {
             n_tentries += (unsigned long long)((tx1 - tx0) * (ty1 - ty0));   // reference tile entries
-            const unsigned long long bits = (unsigned long long)__double_as_longlong(tz);
-            dmin_inv = max(dmin_inv, ~bits);
-            dmax_bits = max(dmax_bits, bits);
+            if constexpr (MODE != kProjFrame) {   // the stage API's key range (k_depth_keys)
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(tz);
+                dmin_inv = max(dmin_inv, ~bits);
+                dmax_bits = max(dmax_bits, bits);
+            }
         }
 
         // --- colour (sc/raster.py:198-226) and opacity (sc/asset.py:44-51) ---
@@ -421,7 +432,8 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
             // monotone non-decreasing in tz (clamped subtraction, positive scale, floor): equal keys are
             // re-ordered by (tz, index) in the tie-fix; non-passed splats sink to the end
             constexpr double kTop = 4294967040.0;
-            keys[k] = passed ? (uint32_t)fmin(floor(fmax(tz - key_dmin, 0.0) * key_scale), kTop) : 0xFFFFFFFFu;
+            // (cvt.rmi.u32.f64 clamps to [0, 2^32 - 1]: floor(max(x, 0)) in one conversion)
+            keys[k] = passed ? min(__double2uint_rd((tz - key_dmin) * key_scale), (uint32_t)kTop) : 0xFFFFFFFFu;
             reinterpret_cast<uint32_t *>(pv)[k] = packed;   // the first depth pass adds the index (= k)
         }
         if (rect) rect[k] = make_ushort4((unsigned short)tx0, (unsigned short)tx1, (unsigned short)ty0, (unsigned short)ty1);
@@ -479,8 +491,12 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
         SC_LAUNCH(k_project<kProjExact>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
                   depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, nullptr);
     } else if (defer_list && ctr) {   // lean f32 kernel, then the exact kernel over the deferred splats
-        SC_LAUNCH(k_project<kProjFast>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
-                  depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
+        if (keys && !depth64 && !rect && !dbg_f64 && !dbg_rect && !dbg_flags)   // the frame path
+            SC_LAUNCH(k_project<kProjFrame>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats,
+                      wins, depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
+        else
+            SC_LAUNCH(k_project<kProjFast>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats,
+                      wins, depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
         SC_LAUNCH(k_project<kProjExact>, nsm, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins, depth64,
                   rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
     } else {

@@ -37,6 +37,14 @@ __device__ __forceinline__ float sqrt_approx(float x)
     return r;
 }
 
+// rcp.approx (rel. error < 2^-23): the f32 conic only (tolerance-checked, never a decision)
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // floor / ceil of an f64 value as int32, saturating (cvt.rmi / cvt.rpi clamp to the int range)
 __device__ __forceinline__ int ifloor(double v) { return __double2int_rd(v); }
 __device__ __forceinline__ int iceil(double v) { return __double2int_ru(v); }
@@ -176,13 +184,14 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
                 constexpr float kEps = 5.9604645e-08f, K = 64.0f;
                 const float err = K * kEps * nn + 4.0f * kEps * fabsf(dil);
                 const float hd = 0.5f * (fa - fc);
-                const float lam = 0.5f * (fa + fc) + sqrtf(hd * hd + fb * fb);
+                // sqrt.approx (rel. error < 2^-22 = 4 eps) stays inside the 16 eps slack of lo / hi
+                const float lam = 0.5f * (fa + fc) + sqrt_approx(fmaf(hd, hd, fb * fb));
                 const float lo = fmaxf(lam * (1.0f - 16.0f * kEps) - 2.0f * err, 0.0f);
                 const float hi = lam * (1.0f + 16.0f * kEps) + 2.0f * err;
                 // radius = ceil(3 sqrt(lambda)) is the same integer rc for every lambda in [lo, hi] iff
                 // (rc - 1)^2 < 9 lo and 9 hi <= rc^2 (squares exact in f32 below 4096; 9 x rounded
                 // with margin): one square root instead of one per interval end
-                const float rc = ceilf(3.0f * sqrtf(lam));
+                const float rc = ceilf(3.0f * sqrt_approx(lam));   // any rc: the test below validates it
                 const bool r_ok = rc >= 1.0f && rc <= 4000.0f && (rc - 1.0f) * (rc - 1.0f) < 9.0f * lo * (1.0f - 8.0f * kEps) &&
                                   9.0f * hi * (1.0f + 8.0f * kEps) <= rc * rc;
                 const float rlo = r_ok ? rc : 0.0f, rhi = r_ok ? rc : -1.0f;
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
                     fast_done = true;
                     radius = (double)rlo;
                     f_det = fdet;
-                    const float inv = 1.0f / fdet;
+                    const float inv = rcp_approx(fdet);   // fdet > 1e-12: a normal positive number
                     f_ha = 0.5f * (fc * inv);
                     f_b = -fb * inv;
                     f_hc = 0.5f * (fa * inv);

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
                 // generous: ~40 dependent roundings, f32 exp, f32 quaternion product).
                 // The radius is taken from f32 only when the whole interval of lambda
                 // gives the same ceil(3 sqrt(lambda)); else the f64 path below runs.
-                const float fz = (float)focal / (float)tz;
+                const float fz = (float)focal * rcp_approx((float)tz);   // <= 5 eps (K below has +8 for it)
                 // (float) of the f64 clamp below == the f32 clamp of (float) txz (rounding is monotone)
                 const float cx = fminf(fmaxf((float)txz, -lim_xf), lim_xf);
                 const float cy = fminf(fmaxf((float)tyz, -lim_yf), lim_yf);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
                 // s0 + s1 + s2 (rotation invariant; 1e-3 slack for the f32 rotation's norm)
                 const float jn = fdot3(j00, j01, j02, j00, j01, j02) + fdot3(j10, j11, j12, j10, j11, j12);
                 const float nn = 2.002f * (s0 + s1 + s2) * jn;
-                constexpr float kEps = 5.9604645e-08f, K = 64.0f;
+                constexpr float kEps = 5.9604645e-08f, K = 72.0f;
                 const float err = K * kEps * nn + 4.0f * kEps * fabsf(dil);
                 const float hd = 0.5f * (fa - fc);
                 // sqrt.approx (rel. error < 2^-22 = 4 eps) stays inside the 16 eps slack of lo / hi

@@ -65,11 +65,18 @@ __device__ __forceinline__ float fdot3(float a0, float a1, float a2, float b0, f
 //            exact depth range: compile-time, not pointer tests)
 enum { kProjMixed = 0, kProjFast = 1, kProjExact = 2, kProjFrame = 3 };
 
+// frame-path kernel: 128-thread CTAs, 5 per SM (<= 102 registers: 96, no spills): 20 warps
+// per SM; 256 x 2 (123 registers) gave 16, 128 x 6 (80 registers) spills (A/B: -1.3 % /
+// +0.5 % frame).  The stage-API / exact instances keep their registers (no spills).
 #ifndef SC_PROJ_CPS
-#define SC_PROJ_CPS 2
+#define SC_PROJ_CPS 5
 #endif
+#ifndef SC_PROJ_THREADS
+#define SC_PROJ_THREADS 128
+#endif
+constexpr int kProjThreads = SC_PROJ_THREADS;
 template <int MODE>
-__global__ void __launch_bounds__(256, SC_PROJ_CPS) k_project(
+__global__ void __launch_bounds__(kProjThreads, MODE == kProjFrame ? SC_PROJ_CPS : 2) k_project(
     sc_scene scene, const sc_survivor *surv, const unsigned long long *n_dev, int64_t n_host, sc_camera cam,
     sc_opts opts, sc_splat *splats, sc_window *wins, double *depth64, ushort4 *rect, uint32_t *keys, uint2 *pv,
     double *dbg_f64, int32_t *dbg_rect, uint8_t *dbg_flags, sc_frame_stats *stats, Counters *ctr, uint32_t *list)
@@ -493,23 +500,23 @@ cudaError_t launch_project(const sc_scene &scene, const sc_survivor *surv, const
     if (n_max <= 0) return cudaSuccess;
     const int nsm = sm_count();
 #ifndef SC_PROJ_GRID
-#define SC_PROJ_GRID 2   // one wave of resident CTAs (2 per SM): no partial last wave
+#define SC_PROJ_GRID SC_PROJ_CPS   // one wave of resident CTAs: no partial last wave
 #endif
-    const int64_t blocks = std::min<int64_t>((n_max + 255) / 256, (int64_t)nsm * SC_PROJ_GRID);
+    const int64_t blocks = std::min<int64_t>((n_max + kProjThreads - 1) / kProjThreads, (int64_t)nsm * SC_PROJ_GRID);
     if (opts.exact_projection) {
-        SC_LAUNCH(k_project<kProjExact>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
+        SC_LAUNCH(k_project<kProjExact>, (int)blocks, kProjThreads, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
                   depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, nullptr);
     } else if (defer_list && ctr) {   // lean f32 kernel, then the exact kernel over the deferred splats
         if (keys && !depth64 && !rect && !dbg_f64 && !dbg_rect && !dbg_flags)   // the frame path
-            SC_LAUNCH(k_project<kProjFrame>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats,
+            SC_LAUNCH(k_project<kProjFrame>, (int)blocks, kProjThreads, 0, st, scene, surv, n_dev, n_max, cam, opts, splats,
                       wins, depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
         else
-            SC_LAUNCH(k_project<kProjFast>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats,
+            SC_LAUNCH(k_project<kProjFast>, (int)blocks, kProjThreads, 0, st, scene, surv, n_dev, n_max, cam, opts, splats,
                       wins, depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
-        SC_LAUNCH(k_project<kProjExact>, nsm, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins, depth64,
+        SC_LAUNCH(k_project<kProjExact>, nsm, kProjThreads, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins, depth64,
                   rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, defer_list);
     } else {
-        SC_LAUNCH(k_project<kProjMixed>, (int)blocks, 256, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
+        SC_LAUNCH(k_project<kProjMixed>, (int)blocks, kProjThreads, 0, st, scene, surv, n_dev, n_max, cam, opts, splats, wins,
                   depth64, rect, keys, pv, dbg_f64, dbg_rect, dbg_flags, stats, ctr, nullptr);
     }
     return cudaGetLastError();

@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
     mlp_setup(sm, tid);
     uint32_t phase = 0;
     int loaded_model = -1;
-    unsigned long long n_pass = 0, n_query = 0, n_cull = 0;
+    uint32_t n_pass = 0, n_query = 0, n_cull = 0;   // per thread (< 2^32 pairs each)
     const unsigned long long total = ws.ctr->total_chunks;
     const double cxp = (double)(cam.width - 1) / 2.0, cyp = (double)(cam.height - 1) / 2.0;
     const int ts = opts.tile_size;
@@ -303,19 +303,21 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
             __syncthreads();
         }
         const int64_t j0 = (int64_t)(chunk - s_fr.chunk_begin) * kChunk;
-        const int64_t j1 = min(j0 + (int64_t)kChunk, s_as.count);
-        const uint32_t inst_id = s_inst;
+        // pairs of the chunk: gaussians gbase + [0, nloc) of the asset (32-bit offsets in the loop)
+        const int nloc = (int)(min(j0 + (int64_t)kChunk, s_as.count) - j0);
+        const int64_t gbase = s_as.offset + j0;
+        const float4 *mo_c = reinterpret_cast<const float4 *>(scene.mean_opa) + gbase;
+        const uint4 *ft_c = reinterpret_cast<const uint4 *>(scene.features) + gbase;
 
         for (int t = 0; t < kCullTilesPerChunk; t++) {
-            const int64_t jt = j0 + (int64_t)t * kCullThreads;
-            if (jt >= j1) break;
-            const int64_t j = jt + tid;
-            const bool active = j < j1;
+            const int jt = t * kCullThreads;
+            if (jt >= nloc) break;
+            const int jl = jt + tid;   // pair offset in the chunk
+            const bool active = jl < nloc;
             bool pass = false, queried = false;
             uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
             if (active) {
-                const int64_t g = s_as.offset + j;
-                const float4 mo = __ldg(reinterpret_cast<const float4 *>(scene.mean_opa) + g);
+                const float4 mo = __ldg(mo_c + jl);
                 // the f32 instanced mean (B2), only needed by the exact per-pair tests
                 const bool need_mean = !s_fr.inside || (model >= 0 && s_fr.gate < 0);
                 const float3 mw = need_mean ? inst_mean(s_in, mo.x, mo.y, mo.z) : make_float3(0.f, 0.f, 0.f);
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
                     pass = true;   // k_prep: the whole instance sphere passes
                 } else {
                     // exact per-pair test on the f32 instanced mean (B3), f64 as the oracle
-                    const float smax = __ldg(scene.scale_smax + 4 * g + 3);
+                    const float smax = __ldg(scene.scale_smax + 4 * (gbase + jl) + 3);
                     double tx, ty, tz;
                     cam_xyz(cam, mw.x, mw.y, mw.z, tx, ty, tz);
                     if (opts.frustum_mode == SC_FRUSTUM_OFF) {
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
                         const float ims = (float)s_as.inv_mean_scale;
                         lo = make_uint4(pack_h2(mo.x * ims, mo.y * ims), pack_h2(mo.z * ims, px * rinv),
                                         pack_h2(py * rinv, pz * rinv), pack_h2(dn, s_fr.fwd_local[0]));
-                        const uint4 feat = __ldg(reinterpret_cast<const uint4 *>(scene.features) + g);
+                        const uint4 feat = __ldg(ft_c + jl);
                         hi = make_uint4(pack_h2(s_fr.fwd_local[1], s_fr.fwd_local[2]), feat.x, feat.y, feat.z);
                     }
                 }
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
             n_cull += (pass && !keep);
             // warp-local ordered compaction: segment (t, w) of the chunk, no CTA barrier
             const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-            if (keep) s_surv[t * kCullThreads + wid * 32 + __popc(bal & lanemask_lt())] = (uint16_t)(j - j0);
+            if (keep) s_surv[t * kCullThreads + wid * 32 + __popc(bal & lanemask_lt())] = (uint16_t)jl;
             if (lane == 0) s_wcnt[t * kCullWarps + wid] = __popc(bal);
         }
         // chunk order = (tile, warp)-major: scan the 32 segment counts (one warp)
@@ -420,15 +422,13 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
         }
     }
     // stats
-    for (int o = 16; o > 0; o >>= 1) {
-        n_pass += __shfl_down_sync(0xffffffffu, n_pass, o);
-        n_query += __shfl_down_sync(0xffffffffu, n_query, o);
-        n_cull += __shfl_down_sync(0xffffffffu, n_cull, o);
-    }
+    n_pass = __reduce_add_sync(0xffffffffu, n_pass);
+    n_query = __reduce_add_sync(0xffffffffu, n_query);
+    n_cull = __reduce_add_sync(0xffffffffu, n_cull);
     if (lane == 0) {
-        if (n_pass) atomicAdd((unsigned long long *)&stats->frustum_passed, n_pass);
-        if (n_query) atomicAdd((unsigned long long *)&stats->mlp_queried, n_query);
-        if (n_cull) atomicAdd((unsigned long long *)&stats->mlp_culled, n_cull);
+        if (n_pass) atomicAdd((unsigned long long *)&stats->frustum_passed, (unsigned long long)n_pass);
+        if (n_query) atomicAdd((unsigned long long *)&stats->mlp_queried, (unsigned long long)n_query);
+        if (n_cull) atomicAdd((unsigned long long *)&stats->mlp_culled, (unsigned long long)n_cull);
     }
     mlp_teardown(sm, tid);
 }

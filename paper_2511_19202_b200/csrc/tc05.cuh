@@ -213,6 +213,27 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b)
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
+#ifndef SC_MLP_FFMA2
+#define SC_MLP_FFMA2 1
+#endif
+// packed f32 pair in one 64-bit register (f32x2 arithmetic, sm_100)
+__device__ __forceinline__ uint64_t pack_f2(float a, float b)
+{
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void unpack_f2(uint64_t r, float &a, float &b)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c)
+{
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+
 // Runs the three layers for the tile whose inputs are in sm.a1 if any thread
 // passes `pred` (the first barrier doubles as that vote); returns whether it
 // ran, the logit of this thread's row in *logit.  Must be called by all 128
@@ -265,6 +286,23 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
     mbar_wait(&sm.bar, phase);
     phase ^= 1u;
     tc_fence_after();
+#if SC_MLP_FFMA2
+    // layer 3 as two interleaved partial sums on packed f32x2 FMAs (FFMA2: half the FMA issue)
+    uint64_t acc = pack_f2(sm.b3, 0.0f);
+#pragma unroll
+    for (int half = 0; half < 2; half++) {
+        tmem_ld16(sm.tmem_base + lane_sel + 16 * half, v);
+#pragma unroll
+        for (int n4 = 0; n4 < 4; n4++) {
+            const float4 w = reinterpret_cast<const float4 *>(sm.w3)[4 * half + n4];
+            acc = ffma2(pack_f2(fmaxf(v[4 * n4], 0.0f), fmaxf(v[4 * n4 + 1], 0.0f)), pack_f2(w.x, w.y), acc);
+            acc = ffma2(pack_f2(fmaxf(v[4 * n4 + 2], 0.0f), fmaxf(v[4 * n4 + 3], 0.0f)), pack_f2(w.z, w.w), acc);
+        }
+    }
+    float l0, l1;
+    unpack_f2(acc, l0, l1);
+    const float logit = l0 + l1;
+#else
     float logit = sm.b3;
 #pragma unroll
     for (int half = 0; half < 2; half++) {
@@ -278,6 +316,7 @@ __device__ __forceinline__ bool mlp_tile(MlpSmem &sm, int tid, uint32_t &phase, 
             logit += fmaxf(v[4 * n4 + 3], 0.0f) * w.w;
         }
     }
+#endif
     tc_fence_before();
     *logit_out = logit;
     return true;

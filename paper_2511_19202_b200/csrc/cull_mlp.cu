@@ -250,6 +250,10 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
     __shared__ sc_instance_rec s_in;
     __shared__ sc_asset_rec s_as;
     __shared__ InstFrame s_fr;
+    // the chunk's MLP-input constants, one broadcast 16-byte load each per pair: (s, cam_local),
+    // (dn_a, dn_b, 1 / mean_scale, fwd_local[0]), fp16x2 (fwd_local[1], fwd_local[2])
+    __shared__ float4 s_fc[2];
+    __shared__ uint32_t s_fwd12;
     __shared__ uint16_t s_surv[kChunk];   // survivors of the chunk: offset from the chunk start
     constexpr int kCullWarps = kCullThreads / 32;
     static_assert(kCullTilesPerChunk * kCullWarps == 32, "one warp scans the chunk's segment counts");
@@ -293,7 +297,13 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
             const uint32_t *ga = reinterpret_cast<const uint32_t *>(scene.assets + asset);
             uint32_t *sa = reinterpret_cast<uint32_t *>(&s_as);
             for (int w = lane; w < (int)(sizeof(sc_asset_rec) / 4); w += 32) sa[w] = ga[w];
-            if (lane == 0) s_inst = (uint32_t)lo;
+            __syncwarp();
+            if (lane == 0) {
+                s_inst = (uint32_t)lo;
+                s_fc[0] = make_float4(s_fr.s, s_fr.cam_local[0], s_fr.cam_local[1], s_fr.cam_local[2]);
+                s_fc[1] = make_float4(s_fr.dn_a, s_fr.dn_b, (float)s_as.inv_mean_scale, s_fr.fwd_local[0]);
+                s_fwd12 = pack_h2(s_fr.fwd_local[1], s_fr.fwd_local[2]);
+            }
         }
         __syncthreads();
         const int model = (opts.use_mlp && s_as.model >= 0) ? s_as.model : -1;
@@ -363,18 +373,19 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
                     if (queried) {
                         // MLP inputs in the instance frame, f32 (they are rounded to fp16):
                         // R^T (m' - c) = s m + R^T (t - c)
-                        const float px = fmaf(s_fr.s, mo.x, s_fr.cam_local[0]);
-                        const float py = fmaf(s_fr.s, mo.y, s_fr.cam_local[1]);
-                        const float pz = fmaf(s_fr.s, mo.z, s_fr.cam_local[2]);
+                        const float4 fa = s_fc[0], fb = s_fc[1];
+                        const float px = fmaf(fa.x, mo.x, fa.y);
+                        const float py = fmaf(fa.x, mo.y, fa.z);
+                        const float pz = fmaf(fa.x, mo.z, fa.w);
                         const float d2 = fmaf(px, px, fmaf(py, py, pz * pz));
                         const float rinv = rsqrtf(d2);
                         const float d_r = d2 * rinv;
-                        const float dn = fminf(fmaxf(fmaf(d_r, s_fr.dn_a, s_fr.dn_b), -1.0f), 1.0f);
-                        const float ims = (float)s_as.inv_mean_scale;
+                        const float dn = fminf(fmaxf(fmaf(d_r, fb.x, fb.y), -1.0f), 1.0f);
+                        const float ims = fb.z;
                         lo = make_uint4(pack_h2(mo.x * ims, mo.y * ims), pack_h2(mo.z * ims, px * rinv),
-                                        pack_h2(py * rinv, pz * rinv), pack_h2(dn, s_fr.fwd_local[0]));
+                                        pack_h2(py * rinv, pz * rinv), pack_h2(dn, fb.w));
                         const uint4 feat = __ldg(ft_c + jl);
-                        hi = make_uint4(pack_h2(s_fr.fwd_local[1], s_fr.fwd_local[2]), feat.x, feat.y, feat.z);
+                        hi = make_uint4(s_fwd12, feat.x, feat.y, feat.z);
                     }
                 }
             }

@@ -769,6 +769,9 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
                 trans[p] = a.T;
             }
         }
+        // every warp has read the last ticket before any warp's phase-2 queues (which reuse
+        // these bytes) are written (racecheck: a WAR on s.ticket without this barrier)
+        __syncthreads();
     }
     // phase 2: the remaining lists, one warp each
     for (;;) {

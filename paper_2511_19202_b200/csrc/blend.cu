@@ -641,7 +641,8 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
         if (__any_sync(0xffffffffu, fp != 0u)) blend_stage(c, s.recs[wid][slot], m.x, fp, loc SC_WS_ARG);
         s.seg[wid][lane] = make_float4(loc.T, loc.cr, loc.cg, loc.cb);
         __syncthreads();
-        // 4. combine the segments in list order (every warp, identical results)
+        // 4. combine the segments in list order (every warp, identical T and retirements; the
+        // colour only in warp 0, which writes the pixels)
         int rw = -1;
         float tin = 0.0f;
         if (!a.done) {
@@ -654,9 +655,11 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
                     tin = a.T;
                     break;
                 }
-                a.cr += a.T * g.y;
-                a.cg += a.T * g.z;
-                a.cb += a.T * g.w;
+                if (wid == 0) {
+                    a.cr += a.T * g.y;
+                    a.cg += a.T * g.z;
+                    a.cb += a.T * g.w;
+                }
                 a.T = tn;
             }
         }
@@ -670,7 +673,7 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
             const float qx = __shfl_sync(0xffffffffu, c.fpx, pl), qy = __shfl_sync(0xffffffffu, c.fpy, pl);
             float sr, sg, sb, sc, T_out;
             pixel_entry_parallel(c, s.recs[wid][slot], cov, T_in, qx, qy, m.x, sr, sg, sb, sc, T_out);
-            if (lane == pl) s.fin[pl] = make_float4(T_out, a.cr + sr, a.cg + sg, a.cb + sb);
+            if (lane == pl) s.fin[pl] = make_float4(T_out, sr, sg, sb);   // warp 0 adds its colour
         }
         if (rw >= 0) {
             a.done = true;
@@ -755,12 +758,12 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
 #endif
             __syncthreads();   // s.fin complete
             if (wid == 0 && inside) {
-                if (retired_here) {
+                if (retired_here) {   // warp 0's colour stopped before the retiring segment
                     const float4 f = s.fin[lane];
                     a.T = f.x;
-                    a.cr = f.y;
-                    a.cg = f.z;
-                    a.cb = f.w;
+                    a.cr += f.y;
+                    a.cg += f.z;
+                    a.cb += f.w;
                 }
                 const int64_t p = (int64_t)py * width + px;
                 image[3 * p + 0] = a.cr + a.T * bg_r;

@@ -10,7 +10,10 @@ namespace sc {
 
 constexpr int kTile = 16;              // blend CTA tile edge (frame path; 8 warps of 8x4 pixel blocks)
 constexpr int kCullThreads = 128;      // one MLP row per thread (tcgen05 M = 128)
-constexpr int kCullTilesPerChunk = 8;  // chunk = 1024 (instance, gaussian) pairs
+#ifndef SC_CULL_TILES
+#define SC_CULL_TILES 8
+#endif
+constexpr int kCullTilesPerChunk = SC_CULL_TILES;  // chunk = 1024 (instance, gaussian) pairs
 constexpr int kChunk = kCullThreads * kCullTilesPerChunk;
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;

@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
     __shared__ uint32_t s_fwd12;
     __shared__ uint16_t s_surv[kChunk];   // survivors of the chunk: offset from the chunk start
     constexpr int kCullWarps = kCullThreads / 32;
-    static_assert(kCullTilesPerChunk * kCullWarps == 32, "one warp scans the chunk's segment counts");
+    constexpr int kSegs = kCullTilesPerChunk * kCullWarps, kSegPerLane = kSegs / 32;
+    static_assert(kSegs % 32 == 0 && kChunk <= 65536, "one warp scans the chunk's segment counts; u16 offsets");
     __shared__ uint32_t s_wcnt[kCullTilesPerChunk * kCullWarps];   // survivors per (tile, warp) segment
     __shared__ uint32_t s_segoff[kCullTilesPerChunk * kCullWarps];
     __shared__ uint32_t s_chunk, s_inst, s_nc;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
         __syncthreads();
         const uint32_t chunk = s_chunk;
         if (chunk >= total) break;
-        if (tid < kCullTilesPerChunk * kCullWarps) s_wcnt[tid] = 0;   // tiles past the chunk end stay empty
+        for (int q = tid; q < kSegs; q += kCullThreads) s_wcnt[q] = 0;   // tiles past the chunk end stay empty
         if (wid == 0) {
             // the chunk's instance (k_chunk_map), then the warp copies the instance, its asset
             // and its frame records word by word (two load latencies)
@@ -406,15 +407,25 @@ __global__ void __launch_bounds__(kCullThreads, SC_CULL_CPS) k_cull(sc_scene sce
         }
         // chunk order = (tile, warp)-major: scan the 32 segment counts (one warp)
         __syncthreads();
-        if (wid == 0) {
-            const uint32_t c = s_wcnt[lane];
-            uint32_t x = c;
+        if (wid == 0) {   // lane: segments [kSegPerLane lane, kSegPerLane (lane + 1))
+            uint32_t c[kSegPerLane], sum = 0;
+#pragma unroll
+            for (int q = 0; q < kSegPerLane; q++) {
+                c[q] = s_wcnt[kSegPerLane * lane + q];
+                sum += c[q];
+            }
+            uint32_t x = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            s_segoff[lane] = x - c;
+            uint32_t run = x - sum;
+#pragma unroll
+            for (int q = 0; q < kSegPerLane; q++) {
+                s_segoff[kSegPerLane * lane + q] = run;
+                run += c[q];
+            }
             if (lane == 31) s_nc = x;
         }
         __syncthreads();

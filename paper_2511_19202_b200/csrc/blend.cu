@@ -648,14 +648,14 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
         if (!a.done) {
 #pragma unroll
             for (int w = 0; w < kBlendWarps; w++) {
-                const float4 g = s.seg[w][lane];
-                const float tn = a.T * g.x;
+                const float tn = a.T * s.seg[w][lane].x;   // (a 4-byte read outside warp 0)
                 if (tn < c.stop_t) {
                     rw = w;
                     tin = a.T;
                     break;
                 }
                 if (wid == 0) {
+                    const float4 g = s.seg[w][lane];
                     a.cr += a.T * g.y;
                     a.cg += a.T * g.z;
                     a.cb += a.T * g.w;

@@ -391,7 +391,7 @@ def main():
     # ---------------- e2e through the public API ----------------
     e2e = None
     if not args.no_e2e:
-        ke = args.e2e_steps or max(K, 60)   # >= 60 frames: one host hiccup weighs little
+        ke = args.e2e_steps or max(K, 240)   # >= 240 frames (~2 s): a 50 ms host hiccup weighs ~2 %
         wl.scene._device = r            # the public API reuses this scene's uploaded copy
         pkg.render_composed(wl.scene, cams[rank % ncam])
         torch.cuda.synchronize()

@@ -163,8 +163,15 @@ cudaError_t scan_excl(const uint32_t *in, uint32_t *out, const unsigned long lon
 //              block sort's last pass), staging in shared memory, digit-run
 //              coalesced write-out.
 // ---------------------------------------------------------------------------
-constexpr int kOsThreads = 512;
-constexpr int kOsItems = 8;
+// 4096-key tiles, 256 threads x 16 keys, 2 CTAs per SM (~120 registers): 8 warps share each
+// tile barrier (512 x 8 keys: 16 warps, 64 registers, 3 % slower sort; 128 threads cannot
+// hold the one-thread-per-digit scan phase)
+#ifndef SC_RADIX_THREADS
+#define SC_RADIX_THREADS 256
+#endif
+constexpr int kOsThreads = SC_RADIX_THREADS;
+constexpr int kOsItems = 4096 / SC_RADIX_THREADS;
+static_assert(kOsThreads >= 256, "the scan phase has one thread per digit");
 constexpr int kOsTile = kOsThreads * kOsItems;
 constexpr int kOsWarps = kOsThreads / 32;
 static_assert(kOsTile == kRadixTile, "matrix sizing in api.cu assumes kRadixTile keys per tile");
@@ -242,12 +249,16 @@ __device__ __forceinline__ void ticket_release(unsigned long long *next, unsigne
 // counts itself -- no CTA barrier per tile (a CTA-cooperative upsweep spent its
 // time in two barriers per tile: 90 vs ~60 us per depth pass, far view).
 constexpr int kUpwBatch = 4;   // uint4 loads per lane per batch (double-buffered)
-__global__ void __launch_bounds__(kOsThreads, 2) k_radix_up(const uint32_t *__restrict__ keys,
+#ifndef SC_UP_THREADS
+#define SC_UP_THREADS 256
+#endif
+constexpr int kUpThreads = SC_UP_THREADS, kUpWarps = kUpThreads / 32;   // upsweep: warp per tile
+__global__ void __launch_bounds__(kUpThreads, 2) k_radix_up(const uint32_t *__restrict__ keys,
                                                              const unsigned long long *n_dev, int64_t n_host,
                                                              int shift, uint32_t *counts, int64_t ntiles_max,
                                                              unsigned long long *tk_next, unsigned long long *tk_done)
 {
-    __shared__ uint32_t h[kOsWarps][256];
+    __shared__ uint32_t h[kUpWarps][256];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host);
     uint32_t *hw = h[wid];
@@ -524,8 +535,8 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
     V *vi = va, *vo = vb;
     for (int p = 0; p < npass; p++) {
         const int shift = bit_lo + 8 * p;
-        SC_LAUNCH(k_radix_up, (int)std::min<int64_t>((ntiles + kOsWarps - 1) / kOsWarps, (int64_t)nsm * 2),
-                  kOsThreads, 0, st, ki, n_dev, n_max, shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
+        SC_LAUNCH(k_radix_up, (int)std::min<int64_t>((ntiles + kUpWarps - 1) / kUpWarps, (int64_t)nsm * 2),
+                  kUpThreads, 0, st, ki, n_dev, n_max, shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
         e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;
 #ifndef SC_RADIX_CPS

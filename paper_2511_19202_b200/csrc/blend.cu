@@ -47,7 +47,13 @@ __device__ unsigned long long g_blend_dbg[kDbgTiles * 8];
 __device__ unsigned int g_blend_used[kDbgTiles * 8 * 2];
 #endif
 
-constexpr int kBlendWarps = 8;           // warps per CTA (one 16x16 tile)
+#ifndef SC_BLEND_WARPS
+#define SC_BLEND_WARPS 4
+#endif
+// warps per CTA: 4 (a CTA walk splits each 32-hit x 4 chunk over 4 warps; 8 warps spent 18 % of
+// their stall samples at the chunk barriers waiting for the slowest segment: blend -18 %; 2 warps
+// leave the long lists too few warps)
+constexpr int kBlendWarps = SC_BLEND_WARPS;
 constexpr int kG = 32;                   // hits per record stage
 constexpr int kStep = 128;               // meta entries per stream step (4 per lane)
 constexpr int kHQ = 256;                 // hit queue capacity (>= kG + kStep)
@@ -508,7 +514,8 @@ __global__ void __launch_bounds__(kBlendWarps * 32) k_blend(const sc_splat *__re
 #ifndef SC_COOP_LOG2
 #define SC_COOP_LOG2 10
 #endif
-constexpr int kCoopQ = 2048;                     // CTA hit queue (ring; >= 2 chunks + one stream step)
+constexpr int pow2_at_least(int x) { return x <= 1 ? 1 : 2 * pow2_at_least((x + 1) / 2); }
+constexpr int kCoopQ = pow2_at_least(2 * kBlendWarps * kG + kBlendWarps * kStep);   // CTA hit queue (ring: 2 chunks + one stream step)
 constexpr int kCoopChunk = kBlendWarps * kG;     // 256 hits per chunk, 32 per warp
 constexpr int kCoopStep = kBlendWarps * kStep;   // 1024 meta entries per CTA stream step
 struct CoopSmem {
@@ -697,7 +704,7 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
 // ~17 % warps active).  Per list the walk is the same as k_blend's, so images
 // are bit-identical.
 template <int REC>
-__global__ void __launch_bounds__(kBlendWarps * 32, 4) k_blend_blocks(
+__global__ void __launch_bounds__(kBlendWarps * 32, 32 / kBlendWarps) k_blend_blocks(
     const sc_splat *__restrict__ splats, int64_t n_splats, const uint32_t *__restrict__ boff,
     const uint32_t *__restrict__ vals, const uint32_t *__restrict__ keys, const uint32_t *__restrict__ task_order,
     int64_t n_tasks, unsigned long long *ticket, int width, int height, int n_tx, float stop_t, float bg_r,

@@ -704,7 +704,10 @@ __device__ void coop_list(const WalkCtx &c, CoopSmem &s, int wid, uint32_t start
 // ~17 % warps active).  Per list the walk is the same as k_blend's, so images
 // are bit-identical.
 template <int REC>
-__global__ void __launch_bounds__(kBlendWarps * 32, 32 / kBlendWarps) k_blend_blocks(
+#ifndef SC_BLEND_CPS
+#define SC_BLEND_CPS 6   // 72 registers, no spills (7 CTAs fit); 8 per SM at 64 spilled: -0.2 %
+#endif
+__global__ void __launch_bounds__(kBlendWarps * 32, SC_BLEND_CPS) k_blend_blocks(
     const sc_splat *__restrict__ splats, int64_t n_splats, const uint32_t *__restrict__ boff,
     const uint32_t *__restrict__ vals, const uint32_t *__restrict__ keys, const uint32_t *__restrict__ task_order,
     int64_t n_tasks, unsigned long long *ticket, int width, int height, int n_tx, float stop_t, float bg_r,

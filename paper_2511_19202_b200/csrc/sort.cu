@@ -248,7 +248,10 @@ __device__ __forceinline__ void ticket_release(unsigned long long *next, unsigne
 // histograms it into its private shared counters and writes the tile's 256
 // counts itself -- no CTA barrier per tile (a CTA-cooperative upsweep spent its
 // time in two barriers per tile: 90 vs ~60 us per depth pass, far view).
-constexpr int kUpwBatch = 4;   // uint4 loads per lane per batch (double-buffered)
+#ifndef SC_UPW_BATCH
+#define SC_UPW_BATCH 4
+#endif
+constexpr int kUpwBatch = SC_UPW_BATCH;   // uint4 loads per lane per batch (double-buffered)
 #ifndef SC_UP_THREADS
 #define SC_UP_THREADS 256
 #endif

@@ -88,6 +88,7 @@ struct Counters {
     // CTA to finish resets them), so a sweep sharing the GPU with another stream's
     // kernels does not wait on CTAs that are not resident yet
     unsigned long long rs_next, rs_done;
+    unsigned long long rs_scan_n;      // radix pass: 256 x this frame's tiles (the count matrix's length)
     unsigned long long blend_next;     // persistent blend warps: next short (tile, block) list of the LPT order
     unsigned long long blend_long_next;   // ... next long list (one CTA each)
     unsigned long long blend_n_long;      // ... number of long lists at the head of the order (k_tile_order)

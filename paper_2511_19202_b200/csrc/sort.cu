@@ -258,12 +258,17 @@ constexpr int kUpwBatch = SC_UPW_BATCH;   // uint4 loads per lane per batch (dou
 constexpr int kUpThreads = SC_UP_THREADS, kUpWarps = kUpThreads / 32;   // upsweep: warp per tile
 __global__ void __launch_bounds__(kUpThreads, 2) k_radix_up(const uint32_t *__restrict__ keys,
                                                              const unsigned long long *n_dev, int64_t n_host,
-                                                             int shift, uint32_t *counts, int64_t ntiles_max,
+                                                             int shift, uint32_t *counts,
+                                                             unsigned long long *scan_n,
                                                              unsigned long long *tk_next, unsigned long long *tk_done)
 {
     __shared__ uint32_t h[kUpWarps][256];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host);
+    // the count matrix is [256][tiles of this frame] (not of the capacity): the scan and the
+    // downsweep use the same device-side tile count
+    const int64_t ntiles = (n + kOsTile - 1) / kOsTile;
+    if (blockIdx.x == 0 && tid == 0) *scan_n = 256ull * (unsigned long long)ntiles;
     uint32_t *hw = h[wid];
 #pragma unroll
     for (int q = 0; q < 8; q++) hw[lane + 32 * q] = 0;
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(kUpThreads, 2) k_radix_up(const uint32_t *__re
         unsigned long long tt = 0;
         if (lane == 0) tt = atomicAdd(tk_next, 1ull);
         const int64_t t = (int64_t)__shfl_sync(0xffffffffu, tt, 0);
-        if (t >= ntiles_max) break;
+        if (t >= ntiles) break;
         const int64_t base = t * kOsTile;
         if (base + kOsTile <= n) {
             uint4 ka[kUpwBatch], kb[kUpwBatch];
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(kUpThreads, 2) k_radix_up(const uint32_t *__re
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int d = lane + 32 * q;
-            counts[(int64_t)d * ntiles_max + t] = hw[d];
+            counts[(int64_t)d * ntiles + t] = hw[d];
             hw[d] = 0;
         }
         __syncwarp();
@@ -341,7 +346,8 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
                                                               V *__restrict__ vals_out,
                                                               const unsigned long long *n_dev, int64_t n_host,
                                                               int shift, const uint32_t *__restrict__ bases,
-                                                              int64_t ntiles_max, unsigned long long *tk_next,
+                                                              int64_t /* capacity tiles (unused) */,
+                                                              unsigned long long *tk_next,
                                                               unsigned long long *tk_done)
 {
     constexpr int kPerWarp = kOsTile / kOsWarps;
@@ -386,7 +392,7 @@ __global__ void __launch_bounds__(kOsThreads, 2) k_radix_down(const uint32_t *__
             if (s_tile < ntiles) issue(s_tile, b ^ 1);
         }
         uint32_t gb = 0;
-        if (tid < 256) gb = bases[(int64_t)tid * ntiles_max + tile];
+        if (tid < 256) gb = bases[(int64_t)tid * ntiles + tile];   // (matrix stride: this frame's tiles)
         const int64_t base = tile * kOsTile;
         const int cnt = (int)std::min<int64_t>(kOsTile, n - base);
         if (b == 0) {
@@ -539,8 +545,9 @@ static cudaError_t radix_sort(uint32_t *ka, V *va, uint32_t *kb, V *vb, const un
     for (int p = 0; p < npass; p++) {
         const int shift = bit_lo + 8 * p;
         SC_LAUNCH(k_radix_up, (int)std::min<int64_t>((ntiles + kUpWarps - 1) / kUpWarps, (int64_t)nsm * 2),
-                  kUpThreads, 0, st, ki, n_dev, n_max, shift, ws.rs_counts, ntiles, &ws.ctr->rs_next, &ws.ctr->rs_done);
-        e = scan_excl(ws.rs_counts, ws.rs_counts, nullptr, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
+                  kUpThreads, 0, st, ki, n_dev, n_max, shift, ws.rs_counts, &ws.ctr->rs_scan_n, &ws.ctr->rs_next,
+                  &ws.ctr->rs_done);
+        e = scan_excl(ws.rs_counts, ws.rs_counts, &ws.ctr->rs_scan_n, 256 * ntiles, ws.scan_part, nullptr, nullptr, st);
         if (e != cudaSuccess) return e;
 #ifndef SC_RADIX_CPS
 #define SC_RADIX_CPS 2

@@ -512,6 +512,31 @@ def test_workspace_regrows_on_overflow():
     assert torch.equal(got.image, ref.image)
 
 
+def test_small_view_in_large_workspace():
+    """A view with fewer survivors / entries than the workspace was sized for (the
+    largest view of a path, as in bench.py): the radix count matrices follow the
+    frame's own tile counts, so its order, block lists and image equal a render in
+    a workspace sized for that view alone."""
+    import torch
+
+    from paper_2511_19202_b200.scene import RenderOptions, Renderer
+    from paper_2511_19202_b200.workloads import config3
+
+    wl = config3(n_per=5_000, n_instances=100, width=320, height=180)
+    near, far = wl.cameras[0], wl.cameras[2]
+    shared = Renderer(wl.scene)
+    shared.render(far, RenderOptions(), to_host=False)            # sizes the workspace for the far view
+    fresh = Renderer(wl.scene)
+    _a, sa, da = shared.render(near, RenderOptions(), to_host=False, debug=True)
+    key = Renderer.ws_key(near)
+    assert shared.workspaces[key].cap_s > 2 * sa.instantiated     # sized for the far view: 2.5x the near survivors
+    _b, sb, db = fresh.render(near, RenderOptions(), to_host=False, debug=True)
+    assert sa.instantiated == sb.instantiated and sa.passed == sb.passed and sa.block_entries == sb.block_entries
+    for k in ("order", "block_offsets", "block_entries", "block_codes"):
+        np.testing.assert_array_equal(da[k], db[k], err_msg=k)
+    assert torch.equal(_a.image, _b.image) and torch.equal(_a.trans, _b.trans)
+
+
 @pytest.mark.parametrize("cam_i", [0, 2])
 def test_record_contributions_composed(cam_i):
     """§8f rank 1 on a composed scene: per-splat max contribution, per-pixel
